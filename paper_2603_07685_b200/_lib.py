@@ -1,0 +1,78 @@
+"""ctypes binding of the C-ABI library ``libmoe_b200.so`` (include/moe_b200.h).
+
+There is no fallback: if the library is missing or fails to load, every product
+call raises. Device pointers are passed as integers (``tensor.data_ptr()``), the
+stream as the raw ``cudaStream_t`` of torch's current stream.
+"""
+from __future__ import annotations
+
+import ctypes
+from ctypes import c_float, c_int, c_int64, c_void_p
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libmoe_b200.so"
+
+# Status codes (include/moe_b200.h, csrc/common.cuh)
+OK, ERR_INVALID_ARG, ERR_NONFINITE, ERR_TOPK, ERR_CUDA, ERR_UNSUPPORTED, ERR_WORKSPACE = range(7)
+_STATUS_NAMES = {
+    ERR_INVALID_ARG: "invalid argument",
+    ERR_NONFINITE: "router logits are not finite",
+    ERR_TOPK: "top_k exceeds num_experts",
+    ERR_CUDA: "CUDA error",
+    ERR_UNSUPPORTED: "unsupported configuration",
+    ERR_WORKSPACE: "workspace too small",
+}
+
+P = c_void_p
+I = c_int
+L = c_int64
+F = c_float
+
+# name -> argtypes (all return int status)
+SIGNATURES: dict[str, list] = {
+    # grouped GEMM (csrc/grouped_gemm.cu)
+    "moe_gg_fc1_fwd": [P, P, I, I, I, I, P, P, P, P, P, P],
+    "moe_gg_fc2_fwd": [P, P, I, I, I, I, P, P, P, P],
+    "moe_gg_fc2_dgrad": [P, P, P, I, I, I, I, P, P, P, P, P, P],
+    "moe_gg_fc1_dgrad": [P, P, I, I, I, I, P, P, P, P],
+    "moe_gg_wgrad": [P, P, I, I, I, I, P, P, P],
+    "moe_gg_gemm_f32": [P, P, I, I, I, I, P, P, P, P],
+}
+
+_lib = None
+
+
+class MoEKernelError(RuntimeError):
+    pass
+
+
+def load():
+    """Load the library (once). Raises if it is not built: no CPU fallback exists."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise MoEKernelError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2603_07685_b200.build` "
+            "(or __graft_entry__.build()); there is no CPU fallback")
+    lib = ctypes.CDLL(str(LIB_PATH))
+    for name, argtypes in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = c_int
+    _lib = lib
+    return lib
+
+
+def exported_symbols() -> list[str]:
+    return list(SIGNATURES)
+
+
+def check(status: int, what: str) -> None:
+    if status != OK:
+        raise MoEKernelError(f"{what} failed: {_STATUS_NAMES.get(status, status)} (status {status})")
+
+
+def call(name: str, *args) -> None:
+    lib = load()
+    check(getattr(lib, name)(*args), name)

@@ -1,0 +1,605 @@
+// Grouped GEMM for the MoE expert FFN on sm_100a: tcgen05.mma (bf16 in, fp32 in TMEM),
+// TMA-fed 4-stage shared-memory ring, double-buffered TMEM accumulators, persistent
+// warp-specialised CTAs (warp 0 = TMA producer, warp 1 = MMA issuer, warps 2-5 = epilogue).
+//
+// Oracle it replaces: the per-expert numpy GEMMs of expert_activation / expert_forward
+// (reference pkg/src/moelab/routing.py:59-68) and the GEMMs implied by the backward of
+// combine_standard / combine_mem_efficient (routing.py:189-223).
+//
+// Two grouping modes, both driven by DEVICE-resident group metadata (no host sync):
+//   grouped-M (fwd, dgrad): C[rows, N] = A[rows, K] * B_e^T where the expert-major
+//     permuted activations are padded per expert to 128-row blocks, so every 128-row
+//     M tile belongs to exactly one expert (block_expert[] says which).
+//   grouped-K (wgrad): C_e[M, N] = sum_{r in rows(e)} A[r, :M]^T B[r, :N] with the
+//     reduction over the expert's (128-aligned, zero-padded) token rows.
+//
+// Epilogues (fused): plain bf16 store, fp32 store, SwiGLU (silu(gate)*up, optional
+// per-row routing-prob scale for the memory-efficient combine), dSwiGLU (recompute
+// phi from the saved pre-activation, optional prob scale + per-row dprob partials).
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace moe {
+namespace gg {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
+constexpr int STAGES = 4;
+constexpr int UMMA_K = 16;
+constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
+constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
+constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr int TMEM_COLS = 512;  // 2 accumulator stages x 256 fp32 columns
+constexpr int NUM_THREADS = 192;
+constexpr int BAND_M = 16;  // raster: 16 m-blocks share each swept n-block (L2 reuse)
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+enum Epi : int { EPI_BF16 = 0, EPI_SWIGLU = 1, EPI_DSWIGLU = 2, EPI_F32 = 3 };
+
+struct Params {
+  // grouped-M
+  const int* num_m_blocks;  // device scalar
+  const int* block_expert;  // [max_m_blocks]
+  int max_m_blocks;
+  // grouped-K
+  const int* expert_offsets;  // [E+1], multiples of 128
+  int num_experts;
+  int M;  // grouped-K: output rows per expert
+  int N;  // output columns (per expert), multiple of 256
+  int K;  // grouped-M: reduction length, multiple of 64
+  // epilogue operands
+  void* out;
+  long long ldo;
+  long long out_expert_stride;
+  void* out2;
+  long long ldo2;
+  const __nv_bfloat16* aux;
+  long long ld_aux;
+  const float* row_scale;
+  float* row_partial;
+  int ld_partial;
+};
+
+struct Tile {
+  int expert, m0, n0, k_begin, num_kb;
+};
+
+template <bool GROUPED_K>
+__device__ __forceinline__ void decode_tile(const Params& p, int t, int num_mb, Tile& tl) {
+  const int nb_count = p.N / BN;
+  if constexpr (!GROUPED_K) {
+    const int band = t / (BAND_M * nb_count);
+    const int rem = t - band * BAND_M * nb_count;
+    const int mb0 = band * BAND_M;
+    const int rows = min(BAND_M, num_mb - mb0);
+    const int nb = rem / rows;
+    const int mb = mb0 + (rem - nb * rows);
+    tl.expert = __ldg(p.block_expert + mb);
+    tl.m0 = mb * BM;
+    tl.n0 = nb * BN;
+    tl.k_begin = 0;
+    tl.num_kb = p.K / BK;
+  } else {
+    const int mb_count = p.M / BM;
+    const int per_e = mb_count * nb_count;
+    const int e = t / per_e;
+    const int rem = t - e * per_e;
+    const int mb = rem / nb_count;
+    const int nb = rem - mb * nb_count;
+    tl.expert = e;
+    tl.m0 = mb * BM;
+    tl.n0 = nb * BN;
+    const int r0 = __ldg(p.expert_offsets + e);
+    const int r1 = __ldg(p.expert_offsets + e + 1);
+    tl.k_begin = r0;
+    tl.num_kb = (r1 - r0) / BK;
+  }
+}
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+
+template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                        const __grid_constant__ CUtensorMap tmap_b, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + STAGES * A_STAGE_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 4);
+    }
+    fence_mbar_init();
+    fence_async_shared();
+  }
+  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  int num_tiles;
+  int num_mb = 0;
+  if constexpr (!GROUPED_K) {
+    num_mb = *p.num_m_blocks;
+    num_tiles = num_mb * (p.N / BN);
+  } else {
+    num_tiles = p.num_experts * (p.M / BM) * (p.N / BN);
+  }
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        Tile tl;
+        decode_tile<GROUPED_K>(p, t, num_mb, tl);
+        for (int kb = 0; kb < tl.num_kb; ++kb) {
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full_bar[s], STAGE_BYTES);
+          uint8_t* sa = smem_a + s * A_STAGE_BYTES;
+          uint8_t* sb = smem_b + s * B_STAGE_BYTES;
+          const int k = tl.k_begin + kb * BK;
+          if constexpr (!A_MN) {
+            tma_load_2d(sa, &tmap_a, &full_bar[s], k, tl.m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_2d(sa + j * (64 * BK * 2), &tmap_a, &full_bar[s], tl.m0 + 64 * j, k);
+          }
+          if constexpr (!B_MN) {
+            tma_load_2d(sb, &tmap_b, &full_bar[s], k, tl.expert * p.N + tl.n0);
+          } else {
+            const int krow = GROUPED_K ? k : tl.expert * p.K + k;
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(sb + j * (64 * BK * 2), &tmap_b, &full_bar[s], tl.n0 + 64 * j, krow);
+          }
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (single thread) =====================
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t acc_ph = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        Tile tl;
+        decode_tile<GROUPED_K>(p, t, num_mb, tl);
+        if (tl.num_kb == 0) continue;
+        mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < tl.num_kb; ++kb) {
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(smem_a + s * A_STAGE_BYTES);
+          const uint32_t b_base = smem_u32(smem_b + s * B_STAGE_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+            const uint64_t adesc =
+                A_MN ? make_sdesc_sw128(a_base + kk * (UMMA_K * 128), 64 * BK * 2, 1024)
+                     : make_sdesc_sw128(a_base + kk * (UMMA_K * 2), 16, 1024);
+            const uint64_t bdesc =
+                B_MN ? make_sdesc_sw128(b_base + kk * (UMMA_K * 128), 64 * BK * 2, 1024)
+                     : make_sdesc_sw128(b_base + kk * (UMMA_K * 2), 16, 1024);
+            umma_bf16(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[s]);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        umma_commit(&tfull_bar[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_ph ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===================== epilogue (warps 2..5, one TMEM lane quarter each) ==========
+    const int q = warp & 3;
+    const int row_local = q * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      Tile tl;
+      decode_tile<GROUPED_K>(p, t, num_mb, tl);
+      const long long row = tl.m0 + row_local;
+      if (tl.num_kb == 0) {
+        // Expert with no rows: its weight gradient is exactly zero.
+        if constexpr (EPI == EPI_BF16) {
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) +
+                             tl.expert * p.out_expert_stride + row * p.ldo + tl.n0;
+          const int4 z = make_int4(0, 0, 0, 0);
+#pragma unroll 4
+          for (int c = 0; c < BN / 8; ++c) reinterpret_cast<int4*>(o)[c] = z;
+        } else if constexpr (EPI == EPI_F32) {
+          float* o = reinterpret_cast<float*>(p.out) + tl.expert * p.out_expert_stride +
+                     row * p.ldo + tl.n0;
+          const int4 z = make_int4(0, 0, 0, 0);
+#pragma unroll 4
+          for (int c = 0; c < BN / 4; ++c) reinterpret_cast<int4*>(o)[c] = z;
+        }
+        continue;
+      }
+      mbar_wait(&tfull_bar[acc], acc_ph);
+      tc_fence_after();
+      const uint32_t t_base = tmem_base + lane_off + acc * BN;
+
+      if constexpr (EPI == EPI_BF16 || EPI == EPI_F32) {
+        const long long ebase = GROUPED_K ? tl.expert * p.out_expert_stride : 0;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_base + c * 32, r);
+          tmem_ld_wait();
+          if constexpr (EPI == EPI_BF16) {
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + ebase + row * p.ldo +
+                               tl.n0 + c * 32;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              int4 w;
+              w.x = pack_bf16x2(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1]));
+              w.y = pack_bf16x2(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3]));
+              w.z = pack_bf16x2(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5]));
+              w.w = pack_bf16x2(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
+              reinterpret_cast<int4*>(o)[v] = w;
+            }
+          } else {
+            float* o = reinterpret_cast<float*>(p.out) + ebase + row * p.ldo + tl.n0 + c * 32;
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+              reinterpret_cast<int4*>(o)[v] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2],
+                                                        r[4 * v + 3]);
+          }
+        }
+      } else if constexpr (EPI == EPI_SWIGLU) {
+        // Tile columns [0,128) = gate rows, [128,256) = up rows of the interleaved W1.
+        const float scale = p.row_scale ? __ldg(p.row_scale + row) : 1.0f;
+        __nv_bfloat16* pre = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo + tl.n0;
+        __nv_bfloat16* act =
+            reinterpret_cast<__nv_bfloat16*>(p.out2) + row * p.ldo2 + (tl.n0 >> 1);
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t g[32], u[32];
+          tmem_ld_32x32b_x32(t_base + c * 32, g);
+          tmem_ld_32x32b_x32(t_base + 128 + c * 32, u);
+          tmem_ld_wait();
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            int4 wg, wu, wa;
+            uint32_t* pg = reinterpret_cast<uint32_t*>(&wg);
+            uint32_t* pu = reinterpret_cast<uint32_t*>(&wu);
+            uint32_t* pa = reinterpret_cast<uint32_t*>(&wa);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int i = 8 * v + 2 * j;
+              const float g0 = __uint_as_float(g[i]), g1 = __uint_as_float(g[i + 1]);
+              const float u0 = __uint_as_float(u[i]), u1 = __uint_as_float(u[i + 1]);
+              pg[j] = pack_bf16x2(g0, g1);
+              pu[j] = pack_bf16x2(u0, u1);
+              pa[j] = pack_bf16x2(silu_f(g0) * u0 * scale, silu_f(g1) * u1 * scale);
+            }
+            reinterpret_cast<int4*>(pre + c * 32)[v] = wg;
+            reinterpret_cast<int4*>(pre + 128 + c * 32)[v] = wu;
+            reinterpret_cast<int4*>(act + c * 32)[v] = wa;
+          }
+        }
+      } else if constexpr (EPI == EPI_DSWIGLU) {
+        // Accumulator = dL/d(act) (or dL/d(p*act) for the mem-efficient combine) for
+        // columns [n0, n0+256) of the m-wide activation. Recompute phi from preact.
+        const float scale = p.row_scale ? __ldg(p.row_scale + row) : 1.0f;
+        float dp_acc = 0.0f;
+        const __nv_bfloat16* pre_row = p.aux + row * p.ld_aux;
+        __nv_bfloat16* dpre_row = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_base + c * 32, r);
+          const int j0 = tl.n0 + c * 32;
+          const long long pos = (long long)(j0 >> 7) * 256 + (j0 & 127);
+          int4 gv[4], uv[4];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            gv[v] = reinterpret_cast<const int4*>(pre_row + pos)[v];
+            uv[v] = reinterpret_cast<const int4*>(pre_row + pos + 128)[v];
+          }
+          tmem_ld_wait();
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            int4 wg, wu;
+            uint32_t* pg = reinterpret_cast<uint32_t*>(&wg);
+            uint32_t* pu = reinterpret_cast<uint32_t*>(&wu);
+            const uint32_t* sg = reinterpret_cast<const uint32_t*>(&gv[v]);
+            const uint32_t* su = reinterpret_cast<const uint32_t*>(&uv[v]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 gg = unpack_bf16x2(sg[j]);
+              const float2 uu = unpack_bf16x2(su[j]);
+              const int i = 8 * v + 2 * j;
+              const float a0 = __uint_as_float(r[i]), a1 = __uint_as_float(r[i + 1]);
+              const float s0 = 1.0f / (1.0f + __expf(-gg.x));
+              const float s1 = 1.0f / (1.0f + __expf(-gg.y));
+              const float si0 = gg.x * s0, si1 = gg.y * s1;
+              dp_acc += a0 * si0 * uu.x + a1 * si1 * uu.y;
+              const float da0 = a0 * scale, da1 = a1 * scale;
+              const float dg0 = da0 * uu.x * s0 * (1.0f + gg.x * (1.0f - s0));
+              const float dg1 = da1 * uu.y * s1 * (1.0f + gg.y * (1.0f - s1));
+              pg[j] = pack_bf16x2(dg0, dg1);
+              pu[j] = pack_bf16x2(da0 * si0, da1 * si1);
+            }
+            reinterpret_cast<int4*>(dpre_row + pos)[v] = wg;
+            reinterpret_cast<int4*>(dpre_row + pos + 128)[v] = wu;
+          }
+        }
+        if (p.row_partial) p.row_partial[row * p.ld_partial + tl.n0 / BN] = dp_acc;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_ph ^= 1;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor [outer, inner] with row stride `ld` elements, 128B-swizzled boxes.
+static int make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
+                     uint64_t ld, uint32_t box_inner, uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return kErrCuda;
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * 2) & 15)) return kErrInvalidArg;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? kOk : kErrCuda;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI>
+static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int max_tiles,
+                  cudaStream_t stream) {
+  auto kern = grouped_gemm_kernel<A_MN, B_MN, GROUPED_K, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    MOE_CUDA_CHECK(
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    attr_set = true;
+  }
+  if (max_tiles <= 0) return kOk;
+  const int grid = max_tiles < num_sms() ? max_tiles : num_sms();
+  kern<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ta, tb, p);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+static Params base_params() {
+  Params p{};
+  return p;
+}
+
+}  // namespace gg
+}  // namespace moe
+
+using namespace moe;
+using namespace moe::gg;
+
+extern "C" {
+
+// fc1 forward + SwiGLU.  xp[rows, h] (expert-major, 128-row padded), w1[E, 2m, h] with
+// gate/up interleaved in 128-row blocks.  Writes preact[rows, 2m] (interleaved) and
+// act[rows, m] = silu(gate) * up (* row_prob[row] when row_prob != NULL).
+int moe_gg_fc1_fwd(const void* xp, const void* w1, int max_rows, int h, int m, int num_experts,
+                   const int* block_expert, const int* num_m_blocks, const float* row_prob,
+                   void* preact, void* act, void* stream) {
+  if (h % BK || (2 * m) % BN || max_rows % BM) return kErrInvalidArg;
+  CUtensorMap ta, tb;
+  int st;
+  if ((st = make_tmap(&ta, xp, h, max_rows, h, BK, BM))) return st;
+  if ((st = make_tmap(&tb, w1, h, (uint64_t)num_experts * 2 * m, h, BK, BN))) return st;
+  Params p = base_params();
+  p.num_m_blocks = num_m_blocks;
+  p.block_expert = block_expert;
+  p.max_m_blocks = max_rows / BM;
+  p.num_experts = num_experts;
+  p.N = 2 * m;
+  p.K = h;
+  p.out = preact;
+  p.ldo = 2 * m;
+  p.out2 = act;
+  p.ldo2 = m;
+  p.row_scale = row_prob;
+  return launch<false, false, false, EPI_SWIGLU>(ta, tb, p, p.max_m_blocks * (p.N / BN),
+                                                 static_cast<cudaStream_t>(stream));
+}
+
+// fc2 forward: out[rows, h] = act[rows, m] * w2_e^T, w2[E, h, m].
+int moe_gg_fc2_fwd(const void* act, const void* w2, int max_rows, int m, int h, int num_experts,
+                   const int* block_expert, const int* num_m_blocks, void* out, void* stream) {
+  if (m % BK || h % BN || max_rows % BM) return kErrInvalidArg;
+  CUtensorMap ta, tb;
+  int st;
+  if ((st = make_tmap(&ta, act, m, max_rows, m, BK, BM))) return st;
+  if ((st = make_tmap(&tb, w2, m, (uint64_t)num_experts * h, m, BK, BN))) return st;
+  Params p = base_params();
+  p.num_m_blocks = num_m_blocks;
+  p.block_expert = block_expert;
+  p.max_m_blocks = max_rows / BM;
+  p.num_experts = num_experts;
+  p.N = h;
+  p.K = m;
+  p.out = out;
+  p.ldo = h;
+  return launch<false, false, false, EPI_BF16>(ta, tb, p, p.max_m_blocks * (p.N / BN),
+                                               static_cast<cudaStream_t>(stream));
+}
+
+// fc2 data-gradient fused with the SwiGLU backward.
+//   G[rows, m] = dout[rows, h] * w2_e  (w2[E, h, m] read MN-major)
+//   da = G * row_prob (mem-efficient) or G (standard); dprob_partial[row, m/256] = <G, act>
+//   d_preact (interleaved like preact) = [da * u * s(g)(1+g(1-s(g))), da * silu(g)]
+int moe_gg_fc2_dgrad(const void* dout, const void* w2, const void* preact, int max_rows, int h,
+                     int m, int num_experts, const int* block_expert, const int* num_m_blocks,
+                     const float* row_prob, void* d_preact, float* dprob_partial, void* stream) {
+  if (h % BK || m % BN || max_rows % BM) return kErrInvalidArg;
+  CUtensorMap ta, tb;
+  int st;
+  if ((st = make_tmap(&ta, dout, h, max_rows, h, BK, BM))) return st;
+  if ((st = make_tmap(&tb, w2, m, (uint64_t)num_experts * h, m, 64, BK))) return st;
+  Params p = base_params();
+  p.num_m_blocks = num_m_blocks;
+  p.block_expert = block_expert;
+  p.max_m_blocks = max_rows / BM;
+  p.num_experts = num_experts;
+  p.N = m;
+  p.K = h;
+  p.out = d_preact;
+  p.ldo = 2 * m;
+  p.aux = static_cast<const __nv_bfloat16*>(preact);
+  p.ld_aux = 2 * m;
+  p.row_scale = row_prob;
+  p.row_partial = dprob_partial;
+  p.ld_partial = m / BN;
+  return launch<false, true, false, EPI_DSWIGLU>(ta, tb, p, p.max_m_blocks * (p.N / BN),
+                                                 static_cast<cudaStream_t>(stream));
+}
+
+// fc1 data-gradient: dxp[rows, h] = d_preact[rows, 2m] * w1_e  (w1[E, 2m, h] read MN-major).
+int moe_gg_fc1_dgrad(const void* d_preact, const void* w1, int max_rows, int m, int h,
+                     int num_experts, const int* block_expert, const int* num_m_blocks,
+                     void* dxp, void* stream) {
+  if ((2 * m) % BK || h % BN || max_rows % BM) return kErrInvalidArg;
+  CUtensorMap ta, tb;
+  int st;
+  if ((st = make_tmap(&ta, d_preact, 2 * m, max_rows, 2 * m, BK, BM))) return st;
+  if ((st = make_tmap(&tb, w1, h, (uint64_t)num_experts * 2 * m, h, 64, BK))) return st;
+  Params p = base_params();
+  p.num_m_blocks = num_m_blocks;
+  p.block_expert = block_expert;
+  p.max_m_blocks = max_rows / BM;
+  p.num_experts = num_experts;
+  p.N = h;
+  p.K = 2 * m;
+  p.out = dxp;
+  p.ldo = h;
+  return launch<false, true, false, EPI_BF16>(ta, tb, p, p.max_m_blocks * (p.N / BN),
+                                              static_cast<cudaStream_t>(stream));
+}
+
+// Weight gradient with the reduction over each expert's token rows:
+//   dw[e, M, N] = sum_{r in [off[e], off[e+1])} a[r, 0:M]^T b[r, 0:N]
+// a[rows, M], b[rows, N] row-major (read MN-major); off[] multiples of 128.
+int moe_gg_wgrad(const void* a, const void* b, int max_rows, int M, int N, int num_experts,
+                 const int* expert_offsets, void* dw, void* stream) {
+  if (M % BM || N % BN || max_rows % BK) return kErrInvalidArg;
+  CUtensorMap ta, tb;
+  int st;
+  if ((st = make_tmap(&ta, a, M, max_rows, M, 64, BK))) return st;
+  if ((st = make_tmap(&tb, b, N, max_rows, N, 64, BK))) return st;
+  Params p = base_params();
+  p.expert_offsets = expert_offsets;
+  p.num_experts = num_experts;
+  p.M = M;
+  p.N = N;
+  p.out = dw;
+  p.ldo = N;
+  p.out_expert_stride = (long long)M * N;
+  return launch<true, true, true, EPI_BF16>(ta, tb, p, num_experts * (M / BM) * (N / BN),
+                                            static_cast<cudaStream_t>(stream));
+}
+
+// Plain grouped-M GEMM with fp32 output (router logits / tests): out[rows, N] = a * b_e^T.
+int moe_gg_gemm_f32(const void* a, const void* b, int max_rows, int K, int N, int num_experts,
+                    const int* block_expert, const int* num_m_blocks, float* out, void* stream) {
+  if (K % BK || N % BN || max_rows % BM) return kErrInvalidArg;
+  CUtensorMap ta, tb;
+  int st;
+  if ((st = make_tmap(&ta, a, K, max_rows, K, BK, BM))) return st;
+  if ((st = make_tmap(&tb, b, K, (uint64_t)num_experts * N, K, BK, BN))) return st;
+  Params p = base_params();
+  p.num_m_blocks = num_m_blocks;
+  p.block_expert = block_expert;
+  p.max_m_blocks = max_rows / BM;
+  p.num_experts = num_experts;
+  p.N = N;
+  p.K = K;
+  p.out = out;
+  p.ldo = N;
+  return launch<false, false, false, EPI_F32>(ta, tb, p, p.max_m_blocks * (p.N / BN),
+                                              static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,169 @@
+"""tcgen05 grouped GEMM vs a plain torch fp32 reference (per expert)."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2603_07685_b200 import gemm  # noqa: E402
+
+
+def _layout(counts, device):
+    """Padded expert-major layout metadata for given per-expert row counts."""
+    offs = [0]
+    block_expert = []
+    for e, c in enumerate(counts):
+        nb = (c + 127) // 128
+        block_expert += [e] * nb
+        offs.append(offs[-1] + nb * 128)
+    rows = offs[-1]
+    max_rows = rows + 256  # slack: buffers sized by an upper bound
+    be = torch.zeros(max_rows // 128, dtype=torch.int32)
+    be[: len(block_expert)] = torch.tensor(block_expert, dtype=torch.int32)
+    return (torch.tensor(offs, dtype=torch.int32, device=device), be.to(device),
+            torch.tensor([len(block_expert)], dtype=torch.int32, device=device), rows, max_rows)
+
+
+def _rows(counts, offs_host, width, device, gen):
+    x = torch.zeros((offs_host[-1] + 256, width), dtype=torch.bfloat16, device=device)
+    for e, c in enumerate(counts):
+        x[offs_host[e]: offs_host[e] + c] = torch.randn((c, width), generator=gen).to(device, torch.bfloat16)
+    return x
+
+
+def _relerr(a, b):
+    return ((a.float() - b.float()).norm() / b.float().norm().clamp_min(1e-30)).item()
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return torch.device("cuda:0")
+
+
+COUNTS = [200, 0, 333, 128, 1]
+
+
+def test_fc2_fwd_plain(dev):
+    g = torch.Generator().manual_seed(0)
+    E, m, h = len(COUNTS), 256, 512
+    offs, be, nmb, rows, max_rows = _layout(COUNTS, dev)
+    oh = offs.tolist()
+    act = _rows(COUNTS, oh, m, dev, g)
+    w2 = (torch.randn((E, h, m), generator=g) / m ** 0.5).to(dev, torch.bfloat16)
+    out = gemm.fc2_fwd(act, w2, be, nmb)
+    torch.cuda.synchronize()
+    for e, c in enumerate(COUNTS):
+        ref = act[oh[e]: oh[e] + c].float() @ w2[e].float().T
+        got = out[oh[e]: oh[e] + c]
+        if c:
+            assert _relerr(got, ref) < 1e-2, e
+    # padding rows are zero in, zero out
+    assert out[oh[0] + COUNTS[0]: oh[1]].abs().max().item() == 0
+
+
+def test_fc1_fwd_swiglu(dev):
+    g = torch.Generator().manual_seed(1)
+    E, m, h = len(COUNTS), 384, 256
+    offs, be, nmb, rows, max_rows = _layout(COUNTS, dev)
+    oh = offs.tolist()
+    xp = _rows(COUNTS, oh, h, dev, g)
+    gate = (torch.randn((E, m, h), generator=g) / h ** 0.5).to(dev, torch.bfloat16)
+    up = (torch.randn((E, m, h), generator=g) / h ** 0.5).to(dev, torch.bfloat16)
+    w1 = gemm.interleave_gate_up(gate, up)
+    prob = torch.rand((xp.shape[0],), generator=g).to(dev)
+    for rp in (None, prob):
+        preact, act = gemm.fc1_fwd(xp, w1, be, nmb, row_prob=rp)
+        torch.cuda.synchronize()
+        gp, upre = gemm.deinterleave_cols(preact)
+        for e, c in enumerate(COUNTS):
+            if not c:
+                continue
+            xs = xp[oh[e]: oh[e] + c].float()
+            rg = xs @ gate[e].float().T
+            ru = xs @ up[e].float().T
+            ra = torch.nn.functional.silu(rg) * ru
+            if rp is not None:
+                ra = ra * rp[oh[e]: oh[e] + c, None]
+            assert _relerr(gp[oh[e]: oh[e] + c], rg) < 1e-2
+            assert _relerr(upre[oh[e]: oh[e] + c], ru) < 1e-2
+            assert _relerr(act[oh[e]: oh[e] + c], ra) < 1e-2
+
+
+def test_fc2_dgrad_dswiglu(dev):
+    g = torch.Generator().manual_seed(2)
+    E, m, h = len(COUNTS), 512, 256
+    offs, be, nmb, rows, max_rows = _layout(COUNTS, dev)
+    oh = offs.tolist()
+    dout = _rows(COUNTS, oh, h, dev, g)
+    preact = _rows(COUNTS, oh, 2 * m, dev, g)
+    w2 = (torch.randn((E, h, m), generator=g) / m ** 0.5).to(dev, torch.bfloat16)
+    prob = torch.rand((dout.shape[0],), generator=g).to(dev)
+    for rp in (None, prob):
+        dpre, part = gemm.fc2_dgrad(dout, w2, preact, be, nmb, row_prob=rp, want_dprob=True)
+        torch.cuda.synchronize()
+        dg, du = gemm.deinterleave_cols(dpre)
+        pg, pu = gemm.deinterleave_cols(preact)
+        for e, c in enumerate(COUNTS):
+            if not c:
+                continue
+            sl = slice(oh[e], oh[e] + c)
+            G = dout[sl].float() @ w2[e].float()
+            gg, uu = pg[sl].float(), pu[sl].float()
+            s = torch.sigmoid(gg)
+            a = gg * s * uu
+            da = G * (rp[sl, None] if rp is not None else 1.0)
+            rdg = da * uu * s * (1 + gg * (1 - s))
+            rdu = da * gg * s
+            assert _relerr(dg[sl], rdg) < 1e-2
+            assert _relerr(du[sl], rdu) < 1e-2
+            rdp = (G * a).sum(1)
+            assert _relerr(part[sl].sum(1), rdp) < 1e-3
+
+
+def test_fc1_dgrad(dev):
+    g = torch.Generator().manual_seed(3)
+    E, m, h = len(COUNTS), 256, 512
+    offs, be, nmb, rows, max_rows = _layout(COUNTS, dev)
+    oh = offs.tolist()
+    dpre = _rows(COUNTS, oh, 2 * m, dev, g)
+    w1 = (torch.randn((E, 2 * m, h), generator=g) / h ** 0.5).to(dev, torch.bfloat16)
+    dx = gemm.fc1_dgrad(dpre, w1, be, nmb)
+    torch.cuda.synchronize()
+    for e, c in enumerate(COUNTS):
+        if c:
+            sl = slice(oh[e], oh[e] + c)
+            assert _relerr(dx[sl], dpre[sl].float() @ w1[e].float()) < 1e-2
+
+
+def test_wgrad(dev):
+    g = torch.Generator().manual_seed(4)
+    E, M, N = len(COUNTS), 256, 512
+    offs, be, nmb, rows, max_rows = _layout(COUNTS, dev)
+    oh = offs.tolist()
+    a = _rows(COUNTS, oh, M, dev, g)
+    b = _rows(COUNTS, oh, N, dev, g)
+    dw = gemm.wgrad(a, b, offs, E)
+    torch.cuda.synchronize()
+    for e, c in enumerate(COUNTS):
+        sl = slice(oh[e], oh[e + 1])
+        ref = a[sl].float().T @ b[sl].float()
+        if c == 0:
+            assert dw[e].abs().max().item() == 0
+        else:
+            assert _relerr(dw[e], ref) < 1e-2, e
+
+
+def test_gemm_f32_large_k(dev):
+    g = torch.Generator().manual_seed(5)
+    counts = [1000, 2000]
+    E, K, N = 2, 4096, 256
+    offs, be, nmb, rows, max_rows = _layout(counts, dev)
+    oh = offs.tolist()
+    a = _rows(counts, oh, K, dev, g)
+    b = (torch.randn((E, N, K), generator=g) / K ** 0.5).to(dev, torch.bfloat16)
+    out = gemm.gemm_f32(a, b, be, nmb)
+    torch.cuda.synchronize()
+    for e, c in enumerate(counts):
+        sl = slice(oh[e], oh[e] + c)
+        assert _relerr(out[sl], a[sl].float() @ b[e].float().T) < 1e-4
