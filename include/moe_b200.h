@@ -1,0 +1,117 @@
+/*
+ * moe_b200.h — C ABI of libmoe_b200.so, the B200-native (sm_100a) MoE-layer hot path.
+ *
+ * The reference (arxiv 2603.07685's `moelab`) exposes this path only as the Python
+ * function API of pkg/src/moelab/routing.py; it has no native interface. Each entry point
+ * below names the reference function(s) whose computation it replaces (file:line, relative
+ * to the reference's pkg/src/moelab/). The Python shim paper_2603_07685_b200/routing.py
+ * re-exposes the reference names on top of these calls.
+ *
+ * Conventions
+ *   - Every function returns an int status: 0 ok, 1 invalid argument, 2 non-finite
+ *     logits, 3 top_k > num_experts, 4 CUDA error, 5 unsupported, 6 workspace too small.
+ *   - All pointers are DEVICE pointers unless noted; `stream` is a cudaStream_t. Work is
+ *     enqueued on `stream` with no host synchronisation and no allocation: dynamic sizes
+ *     (per-expert counts, padded offsets, number of active row blocks) live in device
+ *     arrays produced by earlier calls; the host passes only static upper bounds.
+ *   - bf16 = __nv_bfloat16 (2 bytes), row-major, rows 16-byte aligned.
+ *   - "Padded plan": token copies grouped expert-major, ascending token index within an
+ *     expert, each expert block starting at a multiple of 128 rows (the GEMM M tile);
+ *     rows [off_pad[e] + eff[e], off_pad[e+1]) are zero. The oracle's compact row_id_map
+ *     is each block's first eff[e] rows (moe_permute_compact_map).
+ *   - W1 is stacked [E, 2m, h] with gate/up rows interleaved in 128-row blocks
+ *     (rows [256j, 256j+128) = gate rows [128j, 128j+128), the next 128 = up rows);
+ *     W2 is [E, h, m]. This is the oracle's per-expert out x in layout (routing.py:46-48).
+ */
+#ifndef MOE_B200_H_
+#define MOE_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ router
+ * replaces route() routing.py:71-108 (score :85-91, bias on scores :95, stable top-k with
+ * lowest-index ties :96-101, unnormalised probs :102, counts :106) and aux_loss()
+ * routing.py:111-120. The logits GEMM x @ W_r (routing.py:79) runs on moe_gg_gemm_f32. */
+int moe_router_num_partials(int T);
+int moe_router_topk(const float* logits, int ld, int T, int E, int K, int score_fn,
+                    const float* sel_bias, int* topk_idx, float* topk_prob, float* scores_out,
+                    int* counts, float* score_partials, int* status, void* stream);
+int moe_router_finalize(const int* counts, const float* score_partials, int T, int K, int E,
+                        float coeff, float* aux_out, float* aux_grad, float* mean_scores,
+                        void* stream);
+/* replaces aux_loss_grad_wr() routing.py:123-137 (generalised: combine + aux terms, softmax
+ * and sigma/sum-sigma Jacobians). Writes bf16 dlogits [T, ldd]. */
+int moe_router_bwd(const float* logits, int ld, int T, int E, int K, int score_fn,
+                   const int* topk_idx, const float* dprob, const float* aux_grad,
+                   void* dlogits, int ldd, void* stream);
+/* W_r [h,E] bf16 -> W_r^T zero-padded [Epad,h] and/or W_r zero-padded [h,Epad] */
+int moe_stage_router_weight(const void* w, int h, int E, int Epad, void* wt_pad, void* w_pad,
+                            void* stream);
+int moe_reduce_groups_f32(const float* in, int G, int rows, int cols_in, int cols_out,
+                          float* out, void* stream);
+
+/* ------------------------------------------------------------------ permutation
+ * replaces permute() routing.py:149-168, _expert_slices() :180-186, effective_counts()
+ * :33-39, apply_capacity() :226-247 (capacity >= 0; pad = drop-and-pad). */
+long long moe_permute_workspace_ints(int T, int K, int E);
+int moe_permute_plan(const int* topk_idx, const float* topk_prob, int T, int K, int E,
+                     int capacity, int pad, const int* phantom, int max_rows, int* meta,
+                     int* off_pad, int* off_c,
+                     int* kept, int* eff, int* counts, int* block_expert, int* inv_map,
+                     int* row_src, float* row_prob, int* workspace, int* status, void* stream);
+int moe_permute_compact_map(const int* meta, const int* off_c, const int* off_pad, int E,
+                            const int* row_src, long long* row_id_map, int* compact_to_pad,
+                            int max_compact, void* stream);
+int moe_permute_gather(const void* x, int T, int K, int h, const int* inv_map,
+                       const int* row_src, const int* meta, void* xp, void* stream);
+int moe_zero_pad_rows(const int* meta, const int* row_src, int h, void* rows, void* stream);
+int moe_gather_rows(const void* in, int h, const int* map, const int* n_dev, int n_host,
+                    void* out, void* stream);
+
+/* ------------------------------------------------------------------ combine
+ * replaces unpermute_sum() routing.py:171-177, the prob multiply + unpermute of
+ * combine_standard() :197-201, the scatter of combine_mem_efficient() :219-222 and the
+ * residual fallback of moe_output_with_residual() :259-261. */
+int moe_combine(const void* rows, int T, int K, int h, const int* inv_map,
+                const float* weights, const void* resid, const void* extra,
+                const void* extra2, void* out, void* stream);
+int moe_combine_bwd(const void* dy, const void* o_rows, int T, int K, int h,
+                    const int* inv_map, const float* prob, void* d_rows, float* dprob,
+                    void* stream);
+int moe_dprob_from_partials(const int* inv_map, long long n, const float* partial, int ldp,
+                            float* dprob, void* stream);
+
+/* ------------------------------------------------------------------ grouped GEMM (tcgen05)
+ * replaces expert_activation()/expert_forward() routing.py:59-68 per expert block and the
+ * corresponding backward GEMMs. */
+int moe_gg_fc1_fwd(const void* xp, const void* w1, int a_rows, int max_rows, int h, int m,
+                   int num_experts, const int* block_expert, const int* num_m_blocks,
+                   const float* row_prob, void* preact, void* act, void* stream);
+int moe_gg_fc2_fwd(const void* act, const void* w2, int a_rows, int max_rows, int m, int h,
+                   int num_experts, const int* block_expert, const int* num_m_blocks,
+                   void* out, void* stream);
+int moe_gg_fc2_dgrad(const void* dout, const void* w2, const void* preact, int a_rows,
+                     int max_rows, int h, int m, int num_experts, const int* block_expert,
+                     const int* num_m_blocks, const float* row_prob, void* d_preact,
+                     float* dprob_partial, void* stream);
+int moe_gg_fc1_dgrad(const void* d_preact, const void* w1, int a_rows, int max_rows, int m,
+                     int h,
+                     int num_experts, const int* block_expert, const int* num_m_blocks,
+                     void* dxp, void* stream);
+int moe_gg_wgrad(const void* a, const void* b, int max_rows, int M, int N, int num_experts,
+                 const int* expert_offsets, void* dw, void* stream);
+int moe_gg_wgrad_f32(const void* a, const void* b, int max_rows, int M, int N,
+                     int num_groups, const int* offsets, float* dw, void* stream);
+int moe_gg_gemm_f32(const void* a, const void* b, int a_rows, int max_rows, int K, int N,
+                    int num_experts, const int* block_expert, const int* num_m_blocks,
+                    float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MOE_B200_H_ */

@@ -30,13 +30,34 @@ F = c_float
 
 # name -> argtypes (all return int status)
 SIGNATURES: dict[str, list] = {
+    # router (csrc/router.cu, csrc/util.cu)
+    "moe_router_topk": [P, I, I, I, I, I, P, P, P, P, P, P, P, P],
+    "moe_router_finalize": [P, P, I, I, I, F, P, P, P, P],
+    "moe_router_bwd": [P, I, I, I, I, I, P, P, P, P, I, P],
+    "moe_stage_router_weight": [P, I, I, I, P, P, P],
+    "moe_reduce_groups_f32": [P, I, I, I, I, P, P],
+    # permutation / combine (csrc/permute.cu)
+    "moe_permute_plan": [P, P, I, I, I, I, I, P, I, P, P, P, P, P, P, P, P, P, P, P, P, P],
+    "moe_permute_compact_map": [P, P, P, I, P, P, P, I, P],
+    "moe_permute_gather": [P, I, I, I, P, P, P, P, P],
+    "moe_zero_pad_rows": [P, P, I, P, P],
+    "moe_gather_rows": [P, I, P, P, I, P, P],
+    "moe_combine": [P, I, I, I, P, P, P, P, P, P, P],
+    "moe_combine_bwd": [P, P, I, I, I, P, P, P, P, P],
+    "moe_dprob_from_partials": [P, L, P, I, P, P],
     # grouped GEMM (csrc/grouped_gemm.cu)
-    "moe_gg_fc1_fwd": [P, P, I, I, I, I, P, P, P, P, P, P],
-    "moe_gg_fc2_fwd": [P, P, I, I, I, I, P, P, P, P],
-    "moe_gg_fc2_dgrad": [P, P, P, I, I, I, I, P, P, P, P, P, P],
-    "moe_gg_fc1_dgrad": [P, P, I, I, I, I, P, P, P, P],
+    "moe_gg_fc1_fwd": [P, P, I, I, I, I, I, P, P, P, P, P, P],
+    "moe_gg_fc2_fwd": [P, P, I, I, I, I, I, P, P, P, P],
+    "moe_gg_fc2_dgrad": [P, P, P, I, I, I, I, I, P, P, P, P, P, P],
+    "moe_gg_fc1_dgrad": [P, P, I, I, I, I, I, P, P, P, P],
     "moe_gg_wgrad": [P, P, I, I, I, I, P, P, P],
-    "moe_gg_gemm_f32": [P, P, I, I, I, I, P, P, P, P],
+    "moe_gg_wgrad_f32": [P, P, I, I, I, I, P, P, P],
+    "moe_gg_gemm_f32": [P, P, I, I, I, I, I, P, P, P, P],
+}
+# non-status query functions: name -> (argtypes, restype)
+QUERIES: dict[str, tuple] = {
+    "moe_router_num_partials": ([I], c_int),
+    "moe_permute_workspace_ints": ([I, I, I], c_int64),
 }
 
 _lib = None
@@ -60,12 +81,20 @@ def load():
         fn = getattr(lib, name)
         fn.argtypes = argtypes
         fn.restype = c_int
+    for name, (argtypes, restype) in QUERIES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = restype
     _lib = lib
     return lib
 
 
 def exported_symbols() -> list[str]:
-    return list(SIGNATURES)
+    return list(SIGNATURES) + list(QUERIES)
+
+
+def query(name: str, *args):
+    return getattr(load(), name)(*args)
 
 
 def check(status: int, what: str) -> None:

@@ -462,13 +462,15 @@ extern "C" {
 // fc1 forward + SwiGLU.  xp[rows, h] (expert-major, 128-row padded), w1[E, 2m, h] with
 // gate/up interleaved in 128-row blocks.  Writes preact[rows, 2m] (interleaved) and
 // act[rows, m] = silu(gate) * up (* row_prob[row] when row_prob != NULL).
-int moe_gg_fc1_fwd(const void* xp, const void* w1, int max_rows, int h, int m, int num_experts,
-                   const int* block_expert, const int* num_m_blocks, const float* row_prob,
-                   void* preact, void* act, void* stream) {
-  if (h % BK || (2 * m) % BN || max_rows % BM) return kErrInvalidArg;
+// a_rows: physical rows of xp (TMA bound; rows beyond read as zero), max_rows: rows of the
+// output buffers (multiple of 128).
+int moe_gg_fc1_fwd(const void* xp, const void* w1, int a_rows, int max_rows, int h, int m,
+                   int num_experts, const int* block_expert, const int* num_m_blocks,
+                   const float* row_prob, void* preact, void* act, void* stream) {
+  if (h % BK || (2 * m) % BN || max_rows % BM || a_rows > max_rows) return kErrInvalidArg;
   CUtensorMap ta, tb;
   int st;
-  if ((st = make_tmap(&ta, xp, h, max_rows, h, BK, BM))) return st;
+  if ((st = make_tmap(&ta, xp, h, a_rows, h, BK, BM))) return st;
   if ((st = make_tmap(&tb, w1, h, (uint64_t)num_experts * 2 * m, h, BK, BN))) return st;
   Params p = base_params();
   p.num_m_blocks = num_m_blocks;
@@ -487,12 +489,13 @@ int moe_gg_fc1_fwd(const void* xp, const void* w1, int max_rows, int h, int m, i
 }
 
 // fc2 forward: out[rows, h] = act[rows, m] * w2_e^T, w2[E, h, m].
-int moe_gg_fc2_fwd(const void* act, const void* w2, int max_rows, int m, int h, int num_experts,
-                   const int* block_expert, const int* num_m_blocks, void* out, void* stream) {
-  if (m % BK || h % BN || max_rows % BM) return kErrInvalidArg;
+int moe_gg_fc2_fwd(const void* act, const void* w2, int a_rows, int max_rows, int m, int h,
+                   int num_experts, const int* block_expert, const int* num_m_blocks, void* out,
+                   void* stream) {
+  if (m % BK || h % BN || max_rows % BM || a_rows > max_rows) return kErrInvalidArg;
   CUtensorMap ta, tb;
   int st;
-  if ((st = make_tmap(&ta, act, m, max_rows, m, BK, BM))) return st;
+  if ((st = make_tmap(&ta, act, m, a_rows, m, BK, BM))) return st;
   if ((st = make_tmap(&tb, w2, m, (uint64_t)num_experts * h, m, BK, BN))) return st;
   Params p = base_params();
   p.num_m_blocks = num_m_blocks;
@@ -511,13 +514,14 @@ int moe_gg_fc2_fwd(const void* act, const void* w2, int max_rows, int m, int h, 
 //   G[rows, m] = dout[rows, h] * w2_e  (w2[E, h, m] read MN-major)
 //   da = G * row_prob (mem-efficient) or G (standard); dprob_partial[row, m/256] = <G, act>
 //   d_preact (interleaved like preact) = [da * u * s(g)(1+g(1-s(g))), da * silu(g)]
-int moe_gg_fc2_dgrad(const void* dout, const void* w2, const void* preact, int max_rows, int h,
-                     int m, int num_experts, const int* block_expert, const int* num_m_blocks,
-                     const float* row_prob, void* d_preact, float* dprob_partial, void* stream) {
-  if (h % BK || m % BN || max_rows % BM) return kErrInvalidArg;
+int moe_gg_fc2_dgrad(const void* dout, const void* w2, const void* preact, int a_rows,
+                     int max_rows, int h, int m, int num_experts, const int* block_expert,
+                     const int* num_m_blocks, const float* row_prob, void* d_preact,
+                     float* dprob_partial, void* stream) {
+  if (h % BK || m % BN || max_rows % BM || a_rows > max_rows) return kErrInvalidArg;
   CUtensorMap ta, tb;
   int st;
-  if ((st = make_tmap(&ta, dout, h, max_rows, h, BK, BM))) return st;
+  if ((st = make_tmap(&ta, dout, h, a_rows, h, BK, BM))) return st;
   if ((st = make_tmap(&tb, w2, m, (uint64_t)num_experts * h, m, 64, BK))) return st;
   Params p = base_params();
   p.num_m_blocks = num_m_blocks;
@@ -538,13 +542,13 @@ int moe_gg_fc2_dgrad(const void* dout, const void* w2, const void* preact, int m
 }
 
 // fc1 data-gradient: dxp[rows, h] = d_preact[rows, 2m] * w1_e  (w1[E, 2m, h] read MN-major).
-int moe_gg_fc1_dgrad(const void* d_preact, const void* w1, int max_rows, int m, int h,
-                     int num_experts, const int* block_expert, const int* num_m_blocks,
+int moe_gg_fc1_dgrad(const void* d_preact, const void* w1, int a_rows, int max_rows, int m,
+                     int h, int num_experts, const int* block_expert, const int* num_m_blocks,
                      void* dxp, void* stream) {
-  if ((2 * m) % BK || h % BN || max_rows % BM) return kErrInvalidArg;
+  if ((2 * m) % BK || h % BN || max_rows % BM || a_rows > max_rows) return kErrInvalidArg;
   CUtensorMap ta, tb;
   int st;
-  if ((st = make_tmap(&ta, d_preact, 2 * m, max_rows, 2 * m, BK, BM))) return st;
+  if ((st = make_tmap(&ta, d_preact, 2 * m, a_rows, 2 * m, BK, BM))) return st;
   if ((st = make_tmap(&tb, w1, h, (uint64_t)num_experts * 2 * m, h, 64, BK))) return st;
   Params p = base_params();
   p.num_m_blocks = num_m_blocks;
@@ -564,7 +568,7 @@ int moe_gg_fc1_dgrad(const void* d_preact, const void* w1, int max_rows, int m, 
 // a[rows, M], b[rows, N] row-major (read MN-major); off[] multiples of 128.
 int moe_gg_wgrad(const void* a, const void* b, int max_rows, int M, int N, int num_experts,
                  const int* expert_offsets, void* dw, void* stream) {
-  if (M % BM || N % BN || max_rows % BK) return kErrInvalidArg;
+  if (M % BM || N % BN) return kErrInvalidArg;
   CUtensorMap ta, tb;
   int st;
   if ((st = make_tmap(&ta, a, M, max_rows, M, 64, BK))) return st;
@@ -581,13 +585,37 @@ int moe_gg_wgrad(const void* a, const void* b, int max_rows, int M, int N, int n
                                             static_cast<cudaStream_t>(stream));
 }
 
-// Plain grouped-M GEMM with fp32 output (router logits / tests): out[rows, N] = a * b_e^T.
-int moe_gg_gemm_f32(const void* a, const void* b, int max_rows, int K, int N, int num_experts,
-                    const int* block_expert, const int* num_m_blocks, float* out, void* stream) {
-  if (K % BK || N % BN || max_rows % BM) return kErrInvalidArg;
+// Same as moe_gg_wgrad with fp32 output (split-K partials of the router weight gradient:
+// "experts" are token chunks). Rows beyond max_rows read as zero (TMA OOB fill), so offsets
+// may run to the next multiple of 64 past the last valid row.
+int moe_gg_wgrad_f32(const void* a, const void* b, int max_rows, int M, int N, int num_groups,
+                     const int* offsets, float* dw, void* stream) {
+  if (M % BM || N % BN) return kErrInvalidArg;
   CUtensorMap ta, tb;
   int st;
-  if ((st = make_tmap(&ta, a, K, max_rows, K, BK, BM))) return st;
+  if ((st = make_tmap(&ta, a, M, max_rows, M, 64, BK))) return st;
+  if ((st = make_tmap(&tb, b, N, max_rows, N, 64, BK))) return st;
+  Params p = base_params();
+  p.expert_offsets = offsets;
+  p.num_experts = num_groups;
+  p.M = M;
+  p.N = N;
+  p.out = dw;
+  p.ldo = N;
+  p.out_expert_stride = (long long)M * N;
+  return launch<true, true, true, EPI_F32>(ta, tb, p, num_groups * (M / BM) * (N / BN),
+                                           static_cast<cudaStream_t>(stream));
+}
+
+// Plain grouped-M GEMM with fp32 output (router logits / tests): out[rows, N] = a * b_e^T.
+// a_rows: physical rows of a (TMA bound); max_rows: rows of out (multiple of 128).
+int moe_gg_gemm_f32(const void* a, const void* b, int a_rows, int max_rows, int K, int N,
+                    int num_experts, const int* block_expert, const int* num_m_blocks, float* out,
+                    void* stream) {
+  if (K % BK || N % BN || max_rows % BM || a_rows > max_rows) return kErrInvalidArg;
+  CUtensorMap ta, tb;
+  int st;
+  if ((st = make_tmap(&ta, a, K, a_rows, K, BK, BM))) return st;
   if ((st = make_tmap(&tb, b, K, (uint64_t)num_experts * N, K, BK, BN))) return st;
   Params p = base_params();
   p.num_m_blocks = num_m_blocks;

@@ -54,58 +54,67 @@ def deinterleave_cols(preact: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]
     return v[:, :, 0].reshape(r, m), v[:, :, 1].reshape(r, m)
 
 
-def fc1_fwd(xp, w1, block_expert, num_m_blocks, row_prob=None, preact=None, act=None):
-    rows, h = xp.shape
+def fc1_fwd(xp, w1, block_expert, num_m_blocks, row_prob=None, preact=None, act=None,
+            max_rows=None):
+    a_rows, h = xp.shape
+    rows = a_rows if max_rows is None else max_rows
     e, m2, _ = w1.shape
     m = m2 // 2
     if preact is None:
         preact = torch.empty((rows, m2), dtype=torch.bfloat16, device=xp.device)
     if act is None:
         act = torch.empty((rows, m), dtype=torch.bfloat16, device=xp.device)
-    _lib.call("moe_gg_fc1_fwd", xp.data_ptr(), w1.data_ptr(), rows, h, m, e,
+    _lib.call("moe_gg_fc1_fwd", xp.data_ptr(), w1.data_ptr(), a_rows, rows, h, m, e,
               block_expert.data_ptr(), num_m_blocks.data_ptr(), _ptr(row_prob),
               preact.data_ptr(), act.data_ptr(), _stream())
     return preact, act
 
 
-def fc2_fwd(act, w2, block_expert, num_m_blocks, out=None):
-    rows, m = act.shape
+def fc2_fwd(act, w2, block_expert, num_m_blocks, out=None, max_rows=None):
+    a_rows, m = act.shape
+    rows = a_rows if max_rows is None else max_rows
     e, h, _ = w2.shape
     if out is None:
         out = torch.empty((rows, h), dtype=torch.bfloat16, device=act.device)
-    _lib.call("moe_gg_fc2_fwd", act.data_ptr(), w2.data_ptr(), rows, m, h, e,
+    _lib.call("moe_gg_fc2_fwd", act.data_ptr(), w2.data_ptr(), a_rows, rows, m, h, e,
               block_expert.data_ptr(), num_m_blocks.data_ptr(), out.data_ptr(), _stream())
     return out
 
 
 def fc2_dgrad(dout, w2, preact, block_expert, num_m_blocks, row_prob=None, want_dprob=False,
-              d_preact=None):
-    rows, h = dout.shape
+              d_preact=None, max_rows=None):
+    a_rows, h = dout.shape
+    rows = a_rows if max_rows is None else max_rows
     e, _, m = w2.shape
     if d_preact is None:
         d_preact = torch.empty((rows, 2 * m), dtype=torch.bfloat16, device=dout.device)
     part = None
     if want_dprob:
         part = torch.empty((rows, m // 256), dtype=torch.float32, device=dout.device)
-    _lib.call("moe_gg_fc2_dgrad", dout.data_ptr(), w2.data_ptr(), preact.data_ptr(), rows, h, m,
-              e, block_expert.data_ptr(), num_m_blocks.data_ptr(), _ptr(row_prob),
+    _lib.call("moe_gg_fc2_dgrad", dout.data_ptr(), w2.data_ptr(), preact.data_ptr(), a_rows, rows,
+              h, m, e, block_expert.data_ptr(), num_m_blocks.data_ptr(), _ptr(row_prob),
               d_preact.data_ptr(), _ptr(part), _stream())
     return d_preact, part
 
 
-def fc1_dgrad(d_preact, w1, block_expert, num_m_blocks, out=None):
-    rows, m2 = d_preact.shape
+def fc1_dgrad(d_preact, w1, block_expert, num_m_blocks, out=None, max_rows=None):
+    a_rows, m2 = d_preact.shape
+    rows = a_rows if max_rows is None else max_rows
     e, _, h = w1.shape
     if out is None:
         out = torch.empty((rows, h), dtype=torch.bfloat16, device=d_preact.device)
-    _lib.call("moe_gg_fc1_dgrad", d_preact.data_ptr(), w1.data_ptr(), rows, m2 // 2, h, e,
+    _lib.call("moe_gg_fc1_dgrad", d_preact.data_ptr(), w1.data_ptr(), a_rows, rows, m2 // 2, h, e,
               block_expert.data_ptr(), num_m_blocks.data_ptr(), out.data_ptr(), _stream())
     return out
 
 
-def wgrad(a, b, expert_offsets, num_experts, out=None):
-    """out[e] = a[rows_e]^T @ b[rows_e] for each expert's padded row range."""
+def wgrad(a, b, expert_offsets, num_experts, out=None, max_rows=None):
+    """out[e] = a[rows_e]^T @ b[rows_e] for each expert's padded row range.
+
+    max_rows bounds the rows TMA reads from both operands (beyond it: zeros)."""
     rows, M = a.shape
+    if max_rows is not None:
+        rows = max_rows
     _, N = b.shape
     if out is None:
         out = torch.empty((num_experts, M, N), dtype=torch.bfloat16, device=a.device)
@@ -114,11 +123,24 @@ def wgrad(a, b, expert_offsets, num_experts, out=None):
     return out
 
 
-def gemm_f32(a, b, block_expert, num_m_blocks, out=None):
-    rows, K = a.shape
+def gemm_f32(a, b, block_expert, num_m_blocks, out=None, max_rows=None):
+    a_rows, K = a.shape
+    rows = a_rows if max_rows is None else max_rows
     e, N, _ = b.shape
     if out is None:
         out = torch.empty((rows, N), dtype=torch.float32, device=a.device)
-    _lib.call("moe_gg_gemm_f32", a.data_ptr(), b.data_ptr(), rows, K, N, e,
+    _lib.call("moe_gg_gemm_f32", a.data_ptr(), b.data_ptr(), a_rows, rows, K, N, e,
               block_expert.data_ptr(), num_m_blocks.data_ptr(), out.data_ptr(), _stream())
+    return out
+
+
+def wgrad_f32(a, b, offsets, num_groups, max_rows=None, out=None):
+    """Split-K fp32 partials: out[g] = a[off[g]:off[g+1]]^T @ b[...] (rows >= max_rows read 0)."""
+    a_rows, M = a.shape
+    _, N = b.shape
+    rows = a_rows if max_rows is None else max_rows
+    if out is None:
+        out = torch.empty((num_groups, M, N), dtype=torch.float32, device=a.device)
+    _lib.call("moe_gg_wgrad_f32", a.data_ptr(), b.data_ptr(), rows, M, N, num_groups,
+              offsets.data_ptr(), out.data_ptr(), _stream())
     return out

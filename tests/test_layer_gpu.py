@@ -1,0 +1,157 @@
+"""MoE layer fwd+bwd on the GPU vs the CPU oracle (oracle/routing_ref.py + backward_ref.py).
+
+Parity contract (BASELINE.md §2 targets):
+  * routing indices, counts, drops and the permutation row_id_map: bit-exact. The
+    decision is compared at the logits boundary: the oracle routes the GPU's fp32
+    logits with W_r = I (the reference's own test idiom, test_routing.py:25-29).
+  * outputs: relative Frobenius error <= 1e-2; gradients <= 2e-2 (bf16 storage,
+    fp32 accumulate; emulated floor 3.9e-3).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import backward_ref as B
+from oracle import routing_ref as R
+
+pytestmark = pytest.mark.gpu
+
+from paper_2603_07685_b200 import gemm, ops  # noqa: E402
+from paper_2603_07685_b200.layer import MoEConfig, moe_forward  # noqa: E402
+
+Y_TOL = 1e-2
+G_TOL = 2e-2
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return torch.device("cuda:0")
+
+
+def relfro(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def make(cfg: MoEConfig, T, seed, dev):
+    g = torch.Generator().manual_seed(seed)
+    h, m, e = cfg.hidden, cfg.ffn_hidden, cfg.num_experts
+    bf = lambda t: t.to(torch.bfloat16)  # noqa: E731
+    x = bf(torch.randn((T, h), generator=g))
+    w_r = bf(torch.randn((h, e), generator=g) * h ** -0.5)
+    up = bf(torch.randn((e, m, h), generator=g) * h ** -0.5)
+    w2 = bf(torch.randn((e, h, m), generator=g) * m ** -0.5)
+    gate = bf(torch.randn((e, m, h), generator=g) * h ** -0.5)
+    dy = bf(torch.randn((T, h), generator=torch.Generator().manual_seed(seed + 1)))
+    shared = None
+    if cfg.shared_ffn_hidden:
+        ms = cfg.shared_ffn_hidden
+        shared = (bf(torch.randn((1, ms, h), generator=g) * h ** -0.5),
+                  bf(torch.randn((1, ms, h), generator=g) * h ** -0.5),
+                  bf(torch.randn((1, h, ms), generator=g) * ms ** -0.5))
+    return x, w_r, gate, up, w2, dy, shared
+
+
+def f64(t):
+    return t.detach().double().cpu().numpy()
+
+
+def run_case(cfg: MoEConfig, T, seed, dev):
+    x, w_r, gate, up, w2, dy, shared = make(cfg, T, seed, dev)
+    xd = x.to(dev).requires_grad_(True)
+    w_rd = w_r.to(dev).requires_grad_(True)
+    w1d = gemm.interleave_gate_up(gate.to(dev), up.to(dev)).requires_grad_(True)
+    w2d = w2.to(dev).requires_grad_(True)
+    w1s = w2s = None
+    if shared is not None:
+        w1s = gemm.interleave_gate_up(shared[0].to(dev), shared[1].to(dev)).requires_grad_(True)
+        w2s = shared[2].to(dev).requires_grad_(True)
+    y, aux = moe_forward(xd, w_rd, w1d, w2d, cfg, None, w1s, w2s)
+    loss = (y.float() * dy.to(dev).float()).sum() + aux
+    loss.backward()
+    torch.cuda.synchronize()
+
+    # the decision at the logits boundary
+    r = ops.router_forward(x.to(dev), w_r.to(dev), cfg.top_k, cfg.score, None, cfg.aux_loss_coeff)
+    cap = cfg.capacity(T)
+    plan = ops.build_plan(r.topk_idx, r.topk_prob, cfg.num_experts, cap, cfg.pad_to_capacity)
+    rmap_gpu, _ = ops.compact_row_id_map(plan)
+    logits = f64(r.logits[:T, :cfg.num_experts])
+    dec = R.route(logits, np.eye(cfg.num_experts), score=cfg.score, top_k=cfg.top_k)
+    gpu_map = np.zeros((T, cfg.num_experts), dtype=bool)
+    np.put_along_axis(gpu_map, r.topk_idx.long().cpu().numpy(), True, axis=1)
+    assert np.array_equal(gpu_map, dec.routing_map), "routing indices differ"
+    assert np.all(np.diff(r.topk_idx.cpu().numpy(), axis=1) > 0), "topk not ascending"
+    assert np.array_equal(r.counts.cpu().numpy(), dec.counts)
+    if cap >= 0:
+        dec = R.apply_capacity(dec, cfg.capacity_factor, pad=cfg.pad_to_capacity)
+    _, rmap_ref = R.permute(np.zeros((T, 1)), dec)
+    assert np.array_equal(rmap_gpu.cpu().numpy(), rmap_ref), "row_id_map differs"
+    np.testing.assert_allclose(r.topk_prob.cpu().numpy(),
+                               np.take_along_axis(dec.probs, r.topk_idx.long().cpu().numpy(), 1),
+                               rtol=1e-5, atol=1e-7)
+    # logits vs fp64 GEMM of the same bf16 values
+    assert relfro(logits, f64(x) @ f64(w_r)) < 1e-5
+
+    params = R.ExpertParams(w1=list(f64(up)), w2=list(f64(w2)), gate=list(f64(gate)))
+    variant = "mem_efficient" if cfg.mem_efficient else "standard"
+    ref = B.moe_forward_backward(f64(x), f64(w_r), params, f64(dy), score=cfg.score,
+                                 top_k=cfg.top_k, coeff=cfg.aux_loss_coeff, variant=variant,
+                                 decision=dec)
+    y_ref, dx_ref = ref["y"], ref["dx"]
+    if shared is not None:
+        sp = R.ExpertParams(w1=[f64(shared[1][0])], w2=[f64(shared[2][0])],
+                            gate=[f64(shared[0][0])])
+        ys = R.expert_forward(sp, 0, f64(x))
+        y_ref = y_ref + ys
+        rs = B.moe_forward_backward(f64(x), np.zeros((cfg.hidden, 1)), sp, f64(dy),
+                                    top_k=1, coeff=0.0)
+        dx_ref = dx_ref + rs["dx"]
+        dgs, dus = gemm.split_gate_up(w1s.grad)
+        assert relfro(f64(dgs[0]), rs["dgate"][0]) < G_TOL
+        assert relfro(f64(dus[0]), rs["dw1"][0]) < G_TOL
+        assert relfro(f64(w2s.grad[0]), rs["dw2"][0]) < G_TOL
+    assert relfro(f64(y), y_ref) < Y_TOL
+    assert abs(float(aux) - ref["aux"]) <= 1e-4 * max(abs(ref["aux"]), 1e-6)
+    assert relfro(f64(xd.grad), dx_ref) < G_TOL
+    assert relfro(f64(w_rd.grad), ref["dw_r"]) < G_TOL
+    dg, du = gemm.split_gate_up(w1d.grad)
+    for e in range(cfg.num_experts):
+        if dec.effective_counts()[e] == 0:
+            continue
+        assert relfro(f64(dg[e]), ref["dgate"][e]) < G_TOL, e
+        assert relfro(f64(du[e]), ref["dw1"][e]) < G_TOL, e
+        assert relfro(f64(w2d.grad[e]), ref["dw2"][e]) < G_TOL, e
+
+
+def test_softmax_standard_dropless(dev):
+    run_case(MoEConfig(8, 2, 256, 512, aux_loss_coeff=1e-2), 512, 0, dev)
+
+
+def test_softmax_mem_efficient(dev):
+    run_case(MoEConfig(8, 2, 256, 512, aux_loss_coeff=1e-2, mem_efficient=True), 384, 1, dev)
+
+
+def test_sigmoid_many_experts(dev):
+    run_case(MoEConfig(32, 4, 256, 256, score="sigmoid", aux_loss_coeff=1e-2), 640, 2, dev)
+
+
+def test_capacity_drop_and_pad(dev):
+    run_case(MoEConfig(8, 2, 256, 256, aux_loss_coeff=1e-2, capacity_factor=0.5,
+                       pad_to_capacity=True), 512, 3, dev)
+
+
+def test_capacity_drop_no_pad_ragged_tokens(dev):
+    run_case(MoEConfig(8, 2, 256, 256, capacity_factor=0.6), 300, 4, dev)
+
+
+def test_shared_expert_sigmoid(dev):
+    run_case(MoEConfig(16, 4, 256, 256, score="sigmoid", aux_loss_coeff=1e-2,
+                       shared_ffn_hidden=256), 256, 5, dev)
+
+
+def test_experts_128_top8(dev):
+    run_case(MoEConfig(128, 8, 256, 256, aux_loss_coeff=1e-2), 1024, 6, dev)
