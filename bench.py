@@ -1,0 +1,428 @@
+#!/usr/bin/env python
+"""Benchmark: MoE layer fwd+bwd tokens/s & grouped-GEMM TFLOPS on B200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config mixtral]
+    python bench.py --impl reference ...      # the reference CPU path (oracle port)
+
+N>1 is launched by torchrun (one rank per GPU, NCCL): expert parallelism over the
+N ranks with T tokens per GPU (weak scaling). One step = router -> permute ->
+grouped-GEMM SwiGLU experts -> combine forward + the full backward, on one batch of
+synthetic tokens already resident in HBM. Prints ONE JSON line on rank 0.
+
+The ``e2e`` number repeats the step through the public layer API with the step's
+inputs (x, dY) copied from pinned host memory and the loss read back every step.
+The ``cpu_baseline`` (rank 0, N=1) times the oracle port (oracle/backward_ref.py,
+numpy fp32, all host threads) on a bounded token sample of the same layer.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # BASELINE.json configs[1]: the metric's workload (fits one GPU at EP=1)
+    "mixtral": dict(E=8, K=2, h=4096, m=14336, T=16384, score="softmax",
+                    name="Mixtral-8x7B-shape MoE layer"),
+    "qwen3": dict(E=128, K=8, h=4096, m=1536, T=32768, score="softmax",
+                  name="Qwen3-235B-shape MoE layer"),
+    "deepseek": dict(E=256, K=8, h=7168, m=2048, T=4096, score="sigmoid", shared=2048,
+                     name="DeepSeek-V3-shape MoE layer (+1 shared expert)"),
+    "capacity": dict(E=8, K=2, h=4096, m=14336, T=16384, score="softmax", cf=1.0, pad=True,
+                     name="Mixtral-shape, capacity factor 1.0 drop-and-pad"),
+    "tiny": dict(E=8, K=2, h=256, m=512, T=4096, score="softmax", name="tiny MoE layer"),
+}
+AUX_COEFF = 1e-2
+METRIC = "MoE layer fwd+bwd tokens/s & grouped-GEMM TFLOPS at 1/2/4/8 B200 (EP)"
+
+
+def flops_per_token(c) -> float:
+    """Algorithmic fwd+bwd FLOPs per token: 18*K*h*m routed, 18*h*m_s shared,
+    6*h*E router."""
+    return 18.0 * c["K"] * c["h"] * c["m"] + 18.0 * c["h"] * c.get("shared", 0) + 6.0 * c["h"] * c["E"]
+
+
+def gemm_flops_per_token(c) -> float:
+    return 18.0 * c["K"] * c["h"] * c["m"] + 18.0 * c["h"] * c.get("shared", 0)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+def cpu_baseline(c, sample_tokens: int, threads: int, reps: int = 1) -> dict:
+    """Oracle port (numpy fp32) fwd+bwd of the same layer on `sample_tokens` tokens."""
+    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
+    import numpy as np
+
+    from oracle import backward_ref as B
+    from oracle import routing_ref as R
+
+    rng = np.random.default_rng(0)
+    h, m, e, k = c["h"], c["m"], c["E"], c["K"]
+    f32 = np.float32
+    x = rng.standard_normal((sample_tokens, h), dtype=f32)
+    w_r = (rng.standard_normal((h, e), dtype=f32) * h ** -0.5).astype(f32)
+    # one expert's weights shared by reference across all experts: identical FLOPs and
+    # memory traffic per expert, without generating E x 3 x m x h random numbers.
+    up = (rng.standard_normal((m, h), dtype=f32) * h ** -0.5).astype(f32)
+    gate = (rng.standard_normal((m, h), dtype=f32) * h ** -0.5).astype(f32)
+    w2 = (rng.standard_normal((h, m), dtype=f32) * m ** -0.5).astype(f32)
+    params = R.ExpertParams(w1=[up] * e, w2=[w2] * e, gate=[gate] * e)
+    dy = rng.standard_normal((sample_tokens, h), dtype=f32)
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        B.moe_forward_backward(x, w_r, params, dy, score=c["score"], top_k=k, coeff=AUX_COEFF)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return {"value": sample_tokens / best, "unit": "tokens/s", "cores": threads,
+            "kind": "port", "seconds": best,
+            "sample": (f"{sample_tokens} tokens of the {c['name']} (E={e},K={k},h={h},m={m}), "
+                       f"fwd+bwd, oracle/backward_ref.py numpy fp32, best of {reps}")}
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu(args, c) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_07685_b200 import _lib, gemm
+    from paper_2603_07685_b200.layer import MoEConfig, moe_forward
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = world
+    T, E, K, h, m = c["T"], c["E"], c["K"], c["h"], c["m"]
+    if E % n:
+        raise SystemExit(f"E={E} not divisible by {n} ranks")
+    cfg = MoEConfig(E, K, h, m, score=c["score"], aux_loss_coeff=AUX_COEFF,
+                    capacity_factor=c.get("cf"), pad_to_capacity=c.get("pad", False),
+                    shared_ffn_hidden=c.get("shared", 0))
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    bf = torch.bfloat16
+    x = torch.randn((T, h), device=dev, generator=g).to(bf)
+    dy = torch.randn((T, h), device=dev, generator=g).to(bf)
+    gw = torch.Generator(device=dev).manual_seed(99)  # weights identical on every rank
+    w_r = (torch.randn((h, E), device=dev, generator=gw) * h ** -0.5).to(bf).requires_grad_()
+    if c.get("skew"):
+        pass
+    e_loc = E // n
+    w1 = (torch.randn((e_loc, 2 * m, h), device=dev, generator=g) * h ** -0.5).to(bf)
+    w2 = (torch.randn((e_loc, h, m), device=dev, generator=g) * m ** -0.5).to(bf)
+    w1.requires_grad_()
+    w2.requires_grad_()
+    w1s = w2s = None
+    if c.get("shared"):
+        ms = c["shared"]
+        w1s = (torch.randn((1, 2 * ms, h), device=dev, generator=g) * h ** -0.5).to(bf)
+        w2s = (torch.randn((1, h, ms), device=dev, generator=g) * ms ** -0.5).to(bf)
+        w1s.requires_grad_()
+        w2s.requires_grad_()
+    params = [w_r, w1, w2] + ([w1s, w2s] if w1s is not None else [])
+
+    if n > 1:
+        from paper_2603_07685_b200.dispatcher import EPGroup, moe_forward_ep
+
+        ep = EPGroup(dist.group.WORLD)
+
+        def layer(xx):
+            return moe_forward_ep(xx, w_r, w1, w2, cfg, ep, None, w1s, w2s)
+    else:
+        def layer(xx):
+            return moe_forward(xx, w_r, w1, w2, cfg, None, w1s, w2s)
+
+    def step(xx, dyy):
+        for p in params:
+            p.grad = None
+        xx = xx.detach().requires_grad_(True)
+        y, aux = layer(xx)
+        torch.autograd.backward([y, aux], [dyy, torch.ones_like(aux)])
+        return y, aux
+
+    def barrier():
+        if n > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # nvidia-smi start-up contends with the driver: start sampling before the warm-up and
+    # wait for its first sample so the timed region only sees the steady 100 ms polling.
+    clocks = ClockSampler()
+    if rank == 0:
+        clocks.start()
+        t_wait = time.time()
+        while not clocks.lines and time.time() - t_wait < 10:
+            time.sleep(0.05)
+    for _ in range(args.warmup):
+        step(x, dy)
+    barrier()
+
+    # ---- timed region: device-resident inputs ------------------------------------
+    if rank == 0:
+        clocks.lines.clear()
+    _lib.stats.launches = 0
+    _lib.stats.timing = True
+    _lib.stats.events = []
+    barrier()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record()
+    for _ in range(args.steps):
+        step(x, dy)
+    t_end.record()
+    barrier()
+    _lib.stats.timing = False
+    launches = _lib.stats.launches
+    ms_total = t_start.elapsed_time(t_end)
+    ev = _lib.stats.events
+    gemm_ms = sum(s.elapsed_time(e) for nm, s, e in ev if nm.startswith("moe_gg_"))
+    per_kernel: dict[str, list] = {}
+    for nm, s, e in ev:
+        per_kernel.setdefault(nm, []).append(s.elapsed_time(e))
+    clk = clocks.stop() if rank == 0 else None
+
+    t_tensor = torch.tensor([ms_total, gemm_ms], dtype=torch.float64, device=dev)
+    if n > 1:
+        dist.all_reduce(t_tensor, op=dist.ReduceOp.MAX)
+    ms_total, gemm_ms_max = t_tensor.tolist()
+    ms_step = ms_total / args.steps
+    tokens = T * n
+    value = tokens / (ms_step / 1e3)
+
+    # ---- e2e: host buffers through the public API ----------------------------------
+    x_host = x.cpu().pin_memory()
+    dy_host = dy.cpu().pin_memory()
+    loss_host = torch.empty((), dtype=torch.float32).pin_memory()
+    xd = torch.empty_like(x)
+    dyd = torch.empty_like(dy)
+
+    def e2e_step():
+        xd.copy_(x_host, non_blocking=True)
+        dyd.copy_(dy_host, non_blocking=True)
+        y, aux = step(xd, dyd)
+        loss_host.copy_(aux.detach(), non_blocking=True)
+
+    e2e_step()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record()
+    barrier()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+    if n > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
+
+    if rank == 0:
+        peaks = {}
+        pk = ROOT / "MEASURED_PEAKS.json"
+        if pk.exists():
+            peaks = json.loads(pk.read_text())
+        # the GEMMs run back to back inside a long step under the 1 kW cap: sustained peak
+        peak_tf = peaks.get("bf16_tflops_sustained", 1400.0)
+        peak_src = ("measured sustained cuBLAS bf16 (MEASURED_PEAKS.json bf16_tflops_sustained)"
+                    if peaks else "fallback ~1.4 PF sustained (B200_PROFILING.md)")
+        gemm_flops_step = gemm_flops_per_token(c) * T  # per rank
+        gemm_tflops = gemm_flops_step * args.steps / (gemm_ms / 1e3) / 1e12 if gemm_ms else None
+        gemm_launches = sum(len(v) for k_, v in per_kernel.items() if k_.startswith("moe_gg_"))
+        out = {
+            "metric": METRIC,
+            "value": round(value, 1),
+            "unit": "tokens/s",
+            "n_gpus": n,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic (seeded N(0,1) tokens, N(0,1/fan_in) random-init weights)",
+            "config": {
+                "workload": f"{c['name']}: E={E}, top-{K}, h={h}, ffn={m}, {T} tokens/GPU, "
+                            f"{c['score']} router, aux coeff {AUX_COEFF}"
+                            + (f", shared expert {c['shared']}" if c.get("shared") else "")
+                            + (f", capacity factor {c['cf']} pad" if c.get("cf") else ", dropless"),
+                "global_batch": tokens,
+                "tokens_per_gpu": T,
+                "parallelism": f"ep{n}",
+                "l2": "inputs larger than L2 (x alone is "
+                      f"{T * h * 2 / 1e6:.0f} MB; expert weights {E * 3 * h * m * 2 / 1e9:.2f} GB)",
+            },
+            "grouped_gemm_tflops": round(gemm_tflops, 1) if gemm_tflops else None,
+            "layer_tflops": round(flops_per_token(c) * tokens / (ms_step / 1e3) / 1e12 / n, 1),
+            "roofline": {
+                "bound": "tensor",
+                "kernel": "grouped GEMM (all tcgen05 launches: fc1/fc2 fwd, dgrad, wgrad)",
+                "achieved": round(gemm_tflops, 1) if gemm_tflops else None,
+                "peak": peak_tf,
+                "peak_source": peak_src,
+                "unit": "TFLOP/s",
+                "frac": round(gemm_tflops / peak_tf, 4) if gemm_tflops else None,
+                "traffic": None,
+                "algorithmic": f"18*K*h*m FLOP/token = {gemm_flops_per_token(c) / 1e9:.3f} "
+                               "GFLOP/token (fwd 6, dgrad 6, wgrad 6)",
+                "gemm_share_of_step": round(gemm_ms / args.steps / ms_step, 4) if gemm_ms else None,
+            },
+            "e2e": {
+                "value": round(tokens / (e2e_ms / 1e3), 1),
+                "unit": "tokens/s",
+                "ms_per_step": round(e2e_ms, 4),
+                "h2d_bytes_per_step": int(x.numel() * 2 + dy.numel() * 2),
+                "d2h_bytes_per_step": 4,
+            },
+            "gpu_launches": launches,
+            "gpu_launches_per_step": launches / args.steps,
+            "gemm_launches": gemm_launches,
+            "kernel_ms_per_step": {k_: round(sum(v) / args.steps, 4) for k_, v in
+                                   sorted(per_kernel.items(), key=lambda kv: -sum(kv[1]))},
+            "clocks": clk,
+        }
+        if n == 1 and not args.no_cpu_baseline:
+            thr = cpu_threads()
+            out["cpu_baseline"] = cpu_baseline(c, args.cpu_sample_tokens, thr)
+        print(json.dumps(out), flush=True)
+    if n > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args, c) -> None:
+    """Reference arm: the reference CPU path (oracle port of pkg/src/moelab/routing.py plus
+    the restated backward) on the host cores, all threads, bounded sample per step."""
+    rank = int(os.environ.get("RANK", "0"))
+    n = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if rank != 0:
+        return
+    thr = cpu_threads()
+    times = []
+    base = None
+    for i in range(args.warmup + args.steps):
+        b = cpu_baseline(c, args.cpu_sample_tokens, thr)
+        if i >= args.warmup:
+            times.append(b["seconds"])
+            base = b
+    sec = statistics.mean(times)
+    value = args.cpu_sample_tokens / sec
+    out = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "tokens/s",
+        "n_gpus": n,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(sec * 1e3, 2),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "fp32",
+        "data": "synthetic",
+        "config": {"workload": f"{c['name']}: E={c['E']}, top-{c['K']}, h={c['h']}, "
+                               f"ffn={c['m']}, CPU sample of {args.cpu_sample_tokens} tokens",
+                   "parallelism": "host CPU (all threads)"},
+        "cpu_baseline": {**{k: base[k] for k in ("cores", "kind", "sample")},
+                         "value": round(value, 2), "unit": "tokens/s"},
+        "e2e": {"value": round(value, 2), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample-tokens", type=int, default=1024)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    c = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, c)
+    else:
+        run_gpu(args, c)
+
+
+if __name__ == "__main__":
+    main()

@@ -102,6 +102,34 @@ def check(status: int, what: str) -> None:
         raise MoEKernelError(f"{what} failed: {_STATUS_NAMES.get(status, status)} (status {status})")
 
 
+# kernels of ours launched by one call of each entry point (cudaMemsetAsync not counted)
+KERNELS_PER_CALL = {name: 1 for name in SIGNATURES}
+KERNELS_PER_CALL.update({"moe_permute_plan": 5, "moe_permute_gather": 2})
+
+
+class _Stats:
+    """Launch counter + optional per-call CUDA-event timing (bench.py instrumentation)."""
+
+    launches = 0
+    timing = False
+    events: list = []  # (name, start_event, end_event)
+
+
+stats = _Stats()
+
+
 def call(name: str, *args) -> None:
     lib = load()
-    check(getattr(lib, name)(*args), name)
+    fn = getattr(lib, name)
+    if stats.timing:
+        import torch
+
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        st = fn(*args)
+        e.record()
+        stats.events.append((name, s, e))
+    else:
+        st = fn(*args)
+    check(st, name)
+    stats.launches += KERNELS_PER_CALL.get(name, 1)

@@ -100,8 +100,7 @@ class _MoEFunction(torch.autograd.Function):
             t = x.shape[0]
             d_pre_s, _ = gemm.fc2_dgrad(dy, w2s, pre_s, be, nmb, max_rows=rows)
             dx_shared = gemm.fc1_dgrad(d_pre_s, w1s, be, nmb)
-            offs = torch.zeros((2,), dtype=torch.int32, device=x.device)
-            offs[1] = ops.ceil_to(t, 64)
+            offs = torch.arange(2, dtype=torch.int32, device=x.device) * ops.ceil_to(t, 64)
             # rows >= t read as zero (TMA bound = t)
             dw2s = gemm.wgrad(dy, act_s, offs, 1, max_rows=t)
             dw1s = gemm.wgrad(d_pre_s, x, offs, 1, max_rows=t)

@@ -123,9 +123,10 @@ def router_backward(x: torch.Tensor, w_r_pad: torch.Tensor, r: RouterOut, dprob:
     # dW_r = x^T dl : split-K over token chunks (multiples of 64 rows), fixed-order reduce
     splits = max(1, min(num_splits, -(-t // 64)))
     chunk = ceil_to(-(-t // splits), 64)
+    # chunk * splits >= ceil64(t), so the clamp makes the last offset exactly ceil64(t);
+    # built on the device (no host->device scalar copy, hence no stream sync)
     offs_t = (torch.arange(splits + 1, dtype=torch.int32, device=dev) * chunk).clamp_(
         max=ceil_to(t, 64))
-    offs_t[-1] = ceil_to(t, 64)
     parts = gemm.wgrad_f32(x, dl, offs_t, splits, max_rows=t)
     dw = torch.empty((h, e), dtype=torch.float32, device=dev)
     _lib.call("moe_reduce_groups_f32", parts.data_ptr(), splits, h, epad, e, dw.data_ptr(),
