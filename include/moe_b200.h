@@ -59,10 +59,15 @@ int moe_reduce_groups_f32(const float* in, int G, int rows, int cols_in, int col
  * :33-39, apply_capacity() :226-247 (capacity >= 0; pad = drop-and-pad). */
 long long moe_permute_workspace_ints(int T, int K, int E);
 int moe_permute_plan(const int* topk_idx, const float* topk_prob, int T, int K, int E,
-                     int capacity, int pad, const int* phantom, int max_rows, int* meta,
-                     int* off_pad, int* off_c,
-                     int* kept, int* eff, int* counts, int* block_expert, int* inv_map,
-                     int* row_src, float* row_prob, int* workspace, int* status, void* stream);
+                     int capacity, const int* cap_e, int pad, const int* phantom, int align,
+                     int max_rows, int* meta, int* off_pad, int* off_c, int* kept, int* eff,
+                     int* counts, int* block_expert, int* inv_map, int* row_src,
+                     float* row_prob, int* workspace, int* status, void* stream);
+/* Expert-parallel receive-side regroup maps (all-to-all layout <-> local padded plan);
+ * capacity under EP keeps the lowest GLOBAL token indices (apply_capacity :240-243 on
+ * the global batch) via the per-expert cap_e of moe_permute_plan. */
+int moe_ep_regroup_map(const int* table, int n, int el, int rows_pad, int* map_pad,
+                       int* map_recv, void* stream);
 int moe_permute_compact_map(const int* meta, const int* off_c, const int* off_pad, int E,
                             const int* row_src, long long* row_id_map, int* compact_to_pad,
                             int max_compact, void* stream);

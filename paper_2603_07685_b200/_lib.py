@@ -37,7 +37,9 @@ SIGNATURES: dict[str, list] = {
     "moe_stage_router_weight": [P, I, I, I, P, P, P],
     "moe_reduce_groups_f32": [P, I, I, I, I, P, P],
     # permutation / combine (csrc/permute.cu)
-    "moe_permute_plan": [P, P, I, I, I, I, I, P, I, P, P, P, P, P, P, P, P, P, P, P, P, P],
+    "moe_permute_plan": [P, P, I, I, I, I, P, I, P, I, I, P, P, P, P, P, P, P, P, P, P, P, P,
+                         P],
+    "moe_ep_regroup_map": [P, I, I, I, P, P, P],
     "moe_permute_compact_map": [P, P, P, I, P, P, P, I, P],
     "moe_permute_gather": [P, I, I, I, P, P, P, P, P],
     "moe_zero_pad_rows": [P, P, I, P, P],

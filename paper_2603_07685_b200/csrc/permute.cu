@@ -82,8 +82,9 @@ __global__ void scan_kernel(const int* __restrict__ hist, int W, int E, int* __r
 // P3: block offsets. capacity < 0 = dropless. meta layout (int32):
 //   [0] num_m_blocks  [1] total padded rows  [2] total compact rows (sum eff)
 //   off_pad[E+1], off_c[E+1], kept[E], eff[E]
-__global__ void offsets_kernel(const int* __restrict__ count, int E, int capacity, int pad,
-                               const int* __restrict__ phantom, int max_rows,
+__global__ void offsets_kernel(const int* __restrict__ count, int E, int capacity,
+                               const int* __restrict__ cap_e, int pad,
+                               const int* __restrict__ phantom, int align, int max_rows,
                                int* __restrict__ meta, int* __restrict__ off_pad,
                                int* __restrict__ off_c, int* __restrict__ kept,
                                int* __restrict__ eff, int* __restrict__ block_expert,
@@ -93,10 +94,12 @@ __global__ void offsets_kernel(const int* __restrict__ count, int E, int capacit
   int kp = 0, ef = 0, pd = 0;
   if (e < E) {
     const int c = count[e];
-    kp = capacity < 0 ? c : min(c, capacity);
+    // per-expert capacity (EP global-position drops) or a uniform one
+    const int cap = cap_e ? cap_e[e] : capacity;
+    kp = cap < 0 ? c : min(c, cap);
     // phantom rows: explicit (routing_map_pad, routing.py:312-325) or capacity pad (:244-246)
-    ef = phantom ? kp + phantom[e] : ((capacity >= 0 && pad) ? capacity : kp);
-    pd = ceil_div_i(ef, ALIGN) * ALIGN;
+    ef = phantom ? kp + phantom[e] : ((cap >= 0 && pad) ? cap : kp);
+    pd = ceil_div_i(ef, align) * align;
     kept[e] = kp;
     eff[e] = ef;
   }
@@ -121,12 +124,12 @@ __global__ void offsets_kernel(const int* __restrict__ count, int E, int capacit
     off_c[0] = 0;
     const int tot = s_pad[E - 1];
     if (tot > max_rows) atomicOr(status, 2);
-    meta[0] = min(tot, max_rows) / ALIGN;
+    meta[0] = align == ALIGN ? min(tot, max_rows) / ALIGN : 0;
     meta[1] = tot;
     meta[2] = s_c[E - 1];
   }
   __syncthreads();
-  if (e < E) {
+  if (e < E && block_expert && align == ALIGN) {
     const int b0 = (e ? s_pad[e - 1] : 0) / ALIGN;
     const int b1 = min(s_pad[e], max_rows) / ALIGN;
     for (int b = b0; b < b1; ++b) block_expert[b] = e;
@@ -136,8 +139,9 @@ __global__ void offsets_kernel(const int* __restrict__ count, int E, int capacit
 // P4: destination of every (token, k) selection + per-row source token and prob.
 __global__ void assign_kernel(const int* __restrict__ topk_idx, const float* __restrict__ topk_prob,
                               const int* __restrict__ rank, const int* __restrict__ base, int T,
-                              int K, int E, int capacity, const int* __restrict__ off_pad,
-                              int max_rows, int* __restrict__ inv_map, int* __restrict__ row_src,
+                              int K, int E, int capacity, const int* __restrict__ cap_e,
+                              const int* __restrict__ off_pad, int max_rows,
+                              int* __restrict__ inv_map, int* __restrict__ row_src,
                               float* __restrict__ row_prob) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long long)T * K) return;
@@ -149,7 +153,8 @@ __global__ void assign_kernel(const int* __restrict__ topk_idx, const float* __r
   }
   const int pos = base[(long long)(t >> 5) * E + e] + rank[i];
   int dest = -1;
-  if (capacity < 0 || pos < capacity) {
+  const int cap = cap_e ? cap_e[e] : capacity;
+  if (cap < 0 || pos < cap) {
     dest = off_pad[e] + pos;
     if (dest < max_rows) {
       row_src[dest] = t;
@@ -453,17 +458,23 @@ long long moe_permute_workspace_ints(int T, int K, int E) {
   return 2 * W * E + (long long)T * K;
 }
 
-// Build the padded dispatch plan from top-k indices (device only, no host sync).
-//   capacity: -1 dropless, else per-expert capacity C (drop-and-pad if pad != 0)
+// Build the dispatch plan from top-k indices (device only, no host sync).
+//   capacity: -1 dropless, else uniform per-expert capacity C; cap_e (nullable) overrides it
+//             per expert (EP: C_global minus lower ranks' counts); pad != 0: drop-and-pad
+//   phantom (nullable): explicit extra zero rows per expert (routing_map_pad)
+//   align: 128 = padded plan for the grouped GEMM, 1 = compact (EP send buffer)
 //   outputs: meta[3], off_pad[E+1], off_c[E+1], kept[E], eff[E], counts[E],
-//            block_expert[max_rows/128], inv_map[T,K], row_src[max_rows], row_prob[max_rows]
+//            block_expert[max_rows/128] (nullable), inv_map[T,K], row_src[max_rows],
+//            row_prob[max_rows] (nullable)
 //   status bit 1: plan exceeded max_rows (rows beyond are dropped; caller must size buffers)
 int moe_permute_plan(const int* topk_idx, const float* topk_prob, int T, int K, int E,
-                     int capacity, int pad, const int* phantom, int max_rows, int* meta,
-                     int* off_pad, int* off_c,
-                     int* kept, int* eff, int* counts, int* block_expert, int* inv_map,
-                     int* row_src, float* row_prob, int* workspace, int* status, void* stream) {
-  if (E < 1 || E > 1024 || K < 1 || K > 32 || max_rows % ALIGN) return kErrInvalidArg;
+                     int capacity, const int* cap_e, int pad, const int* phantom, int align,
+                     int max_rows, int* meta, int* off_pad, int* off_c, int* kept, int* eff,
+                     int* counts, int* block_expert, int* inv_map, int* row_src,
+                     float* row_prob, int* workspace, int* status, void* stream) {
+  if (E < 1 || E > 1024 || K < 1 || K > 32) return kErrInvalidArg;
+  if (align != 1 && align != ALIGN) return kErrInvalidArg;
+  if (align == ALIGN && max_rows % ALIGN) return kErrInvalidArg;
   auto st = static_cast<cudaStream_t>(stream);
   const int W = ceil_div_i(T > 0 ? T : 1, 32);
   int* hist = workspace;
@@ -483,18 +494,72 @@ int moe_permute_plan(const int* topk_idx, const float* topk_prob, int T, int K, 
   }
   int threads = 32;
   while (threads < E) threads <<= 1;
-  offsets_kernel<<<1, threads, 0, st>>>(counts, E, capacity, pad, phantom, max_rows, meta,
-                                        off_pad, off_c, kept, eff, block_expert, status);
+  offsets_kernel<<<1, threads, 0, st>>>(counts, E, capacity, cap_e, pad, phantom, align,
+                                        max_rows, meta, off_pad, off_c, kept, eff, block_expert,
+                                        status);
   MOE_LAUNCH_CHECK();
   if (T > 0) {
     const long long n = (long long)T * K;
     assign_kernel<<<(int)ceil_div_ll(n, 256), 256, 0, st>>>(topk_idx, topk_prob, rank, base, T, K,
-                                                           E, capacity, off_pad, max_rows,
+                                                           E, capacity, cap_e, off_pad, max_rows,
                                                            inv_map, row_src, row_prob);
     MOE_LAUNCH_CHECK();
   }
-  pad_rows_kernel<<<sms() * 4, 256, 0, st>>>(meta, block_expert, off_pad, kept, row_src,
-                                              row_prob);
+  if (align == ALIGN && block_expert) {
+    pad_rows_kernel<<<sms() * 4, 256, 0, st>>>(meta, block_expert, off_pad, kept, row_src,
+                                                row_prob);
+    MOE_LAUNCH_CHECK();
+  }
+  return kOk;
+}
+
+// ---------------------------------------------------------------------------- EP regroup
+// Map between the all-to-all receive layout [src rank][local expert][rows] and the local
+// padded plan [local expert][src rank rows | phantom | pad].  Host-built table (int32):
+//   kept[n*el] (rows src s sends for local expert e), recv_off[n*el] (row offset of chunk
+//   (s,e) in the receive buffer), off_pad[el+1], real[el] (= sum_s kept[s][e]).
+// map_pad[r] = receive row feeding padded row r, or -1 (phantom / padding: zero row);
+// map_recv[i] = padded row of receive row i.
+__global__ void regroup_map_kernel(const int* __restrict__ tab, int n, int el, int rows_pad,
+                                   int* __restrict__ map_pad, int* __restrict__ map_recv) {
+  const int* kept = tab;
+  const int* recv_off = tab + n * el;
+  const int* off_pad = recv_off + n * el;
+  const int* real = off_pad + el + 1;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows_pad;
+       r += gridDim.x * blockDim.x) {
+    int lo = 0, hi = el - 1;  // last e with off_pad[e] <= r
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (off_pad[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    const int e = lo;
+    const int j = r - off_pad[e];
+    int src_row = -1;
+    if (j < real[e]) {
+      int acc = 0;
+      for (int s = 0; s < n; ++s) {
+        const int k = kept[s * el + e];
+        if (j < acc + k) {
+          src_row = recv_off[s * el + e] + (j - acc);
+          break;
+        }
+        acc += k;
+      }
+    }
+    map_pad[r] = src_row;
+    if (src_row >= 0 && map_recv) map_recv[src_row] = r;
+  }
+}
+
+int moe_ep_regroup_map(const int* table, int n, int el, int rows_pad, int* map_pad,
+                       int* map_recv, void* stream) {
+  if (n < 1 || el < 1) return kErrInvalidArg;
+  if (rows_pad <= 0) return kOk;
+  regroup_map_kernel<<<ceil_div_i(rows_pad, 256) < sms() * 8 ? ceil_div_i(rows_pad, 256)
+                                                              : sms() * 8,
+                       256, 0, static_cast<cudaStream_t>(stream)>>>(table, n, el, rows_pad,
+                                                                    map_pad, map_recv);
   MOE_LAUNCH_CHECK();
   return kOk;
 }

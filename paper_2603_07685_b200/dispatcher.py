@@ -1,0 +1,289 @@
+"""Expert-parallel (EP) token dispatcher: experts shard over the ranks of one box and
+tokens move by NCCL all-to-all over NVLink (Megatron's all-to-all dispatcher,
+PAPER.md:204-211; the reference models only its bytes, pkg/src/moelab/perf.py:62-70).
+
+Placement follows the reference convention: expert e lives on rank e // (E / EP)
+(planners.py:299, tests/test_perf.py:27-33); the EP group is all ranks of the box
+(tests/test_folding.py:41-45).
+
+Per forward:
+  1. local router on this rank's T tokens;
+  2. ONE all-gather of [counts | mean scores] (2E floats per rank): sizes every
+     exchange, gives the global aux loss (the global aux != mean of per-rank aux), and
+     the per-rank prefix that reproduces the oracle's GLOBAL-position capacity drops
+     (keep slot j of expert e on rank r iff sum_{r'<r} counts[r',e] + j < C_global);
+  3. local permute into the compact expert-major send buffer (expert-major order is
+     already destination-rank order);
+  4. NCCL all_to_all_single -> receive layout [src rank][local expert];
+  5. regroup into the local 128-row padded plan (phantom rows created here, on the
+     expert's home rank) -> the same tcgen05 grouped GEMMs as EP = 1;
+  6. reverse regroup + all_to_all_single back, combine on the source rank.
+The backward mirrors it (dY dispatch, dX combine). The only host synchronisation is
+the D2H copy of the gathered [EP, 2E] statistics in step 2 (sync-free dispatch is the
+SURVEY §8(f) "next" item 2).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib, gemm, ops
+from .layer import MoEConfig, shared_expert_backward, shared_expert_forward
+
+
+class EPGroup:
+    def __init__(self, group=None):
+        self.group = group if group is not None else dist.group.WORLD
+        self.n = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+
+
+@dataclass
+class EPHostPlan:
+    """Host-side exchange plan computed identically on every rank from counts_all."""
+
+    n: int
+    rank: int
+    el: int                    # local experts
+    kept: np.ndarray           # [n, E] rows rank s sends for expert e (after capacity)
+    cap_local: np.ndarray | None  # [E] this rank's per-expert capacity (None = dropless)
+    send_splits: list          # rows to each destination rank
+    recv_splits: list          # rows from each source rank
+    table: np.ndarray          # int32 regroup table (moe_ep_regroup_map)
+    off_pad: np.ndarray        # [el+1] local padded offsets
+    block_expert: np.ndarray   # [rows_pad/128]
+    rows_pad: int
+    real: np.ndarray           # [el] real (non-phantom) rows per local expert
+    eff: np.ndarray            # [el] real + phantom
+
+
+def _excl_cumsum(a, axis=-1):
+    c = np.cumsum(a, axis=axis)
+    return c - a
+
+
+def ep_host_plan(counts_all: np.ndarray, rank: int, capacity: int = -1,
+                 pad: bool = False, align: int = ops.ALIGN) -> EPHostPlan:
+    """Exchange plan from the all-gathered per-rank expert counts [n, E].
+
+    capacity: global per-expert capacity C (apply_capacity() on the global batch,
+    routing.py:226-247), -1 = dropless. pad: phantom rows fill each expert to C.
+    """
+    counts_all = np.asarray(counts_all, dtype=np.int64)
+    n, E = counts_all.shape
+    el = E // n
+    if capacity < 0:
+        kept = counts_all.copy()
+        cap_local = None
+    else:
+        prefix = _excl_cumsum(counts_all, axis=0)  # tokens of lower ranks (lower global index)
+        kept = np.clip(capacity - prefix, 0, counts_all)
+        cap_local = np.maximum(capacity - prefix[rank], 0)
+    send_splits = [int(kept[rank, d * el:(d + 1) * el].sum()) for d in range(n)]
+    mine = slice(rank * el, (rank + 1) * el)
+    kept_mine = kept[:, mine]                                   # [n, el]
+    recv_splits = [int(v) for v in kept_mine.sum(axis=1)]
+    recv_base = _excl_cumsum(np.asarray(recv_splits, dtype=np.int64))
+    recv_off = recv_base[:, None] + _excl_cumsum(kept_mine, axis=1)   # [n, el]
+    real = kept_mine.sum(axis=0)
+    phantom = np.zeros(el, dtype=np.int64)
+    if capacity >= 0 and pad:
+        phantom = capacity - np.minimum(counts_all[:, mine].sum(axis=0), capacity)
+    eff = real + phantom
+    padded = -(-eff // align) * align
+    off_pad = np.concatenate([[0], np.cumsum(padded)]).astype(np.int64)
+    rows_pad = int(off_pad[-1])
+    block_expert = np.repeat(np.arange(el), padded // align) if align == ops.ALIGN else (
+        np.zeros(0, dtype=np.int64))
+    table = np.concatenate([kept_mine.ravel(), recv_off.ravel(), off_pad, real]).astype(np.int32)
+    return EPHostPlan(n, rank, el, kept, cap_local, send_splits, recv_splits, table, off_pad,
+                      block_expert, rows_pad, real, eff)
+
+
+def regroup_maps_numpy(hp: EPHostPlan):
+    """numpy restatement of csrc/permute.cu regroup_map_kernel (CPU tests)."""
+    n, el = hp.n, hp.el
+    kept = hp.table[: n * el].reshape(n, el)
+    recv_off = hp.table[n * el: 2 * n * el].reshape(n, el)
+    map_pad = np.full(hp.rows_pad, -1, dtype=np.int64)
+    total_recv = int(sum(hp.recv_splits))
+    map_recv = np.full(total_recv, -1, dtype=np.int64)
+    for e in range(el):
+        j = 0
+        for s in range(n):
+            for q in range(int(kept[s, e])):
+                r = int(hp.off_pad[e]) + j
+                map_pad[r] = int(recv_off[s, e]) + q
+                map_recv[map_pad[r]] = r
+                j += 1
+    return map_pad, map_recv
+
+
+def global_aux(counts_all, mean_scores_all, T, K, coeff):
+    """aux_loss (routing.py:111-120) of the GLOBAL batch and d aux / d s_te (all ranks)."""
+    counts = counts_all.sum(axis=0).astype(np.float64)
+    n, E = counts_all.shape
+    f = counts / max(n * T * K, 1)
+    P = mean_scores_all.astype(np.float64).mean(axis=0)  # equal T per rank
+    aux = coeff * E * float(np.dot(f, P))
+    aux_grad = coeff * E * f / max(n * T, 1)
+    return aux, aux_grad
+
+
+class _Exchange:
+    """Device-side state of one forward's exchange (kept for the backward)."""
+
+    def __init__(self, hp: EPHostPlan, dev):
+        self.hp = hp
+        tab = torch.from_numpy(np.concatenate([
+            hp.table, hp.block_expert.astype(np.int32), np.array([hp.rows_pad // ops.ALIGN],
+                                                                 dtype=np.int32)]))
+        tab = tab.pin_memory().to(dev, non_blocking=True)
+        nt = hp.table.size
+        self.table = tab[:nt]
+        n, el = hp.n, hp.el
+        self.off_pad = self.table[2 * n * el: 2 * n * el + el + 1]
+        self.block_expert = tab[nt: nt + hp.block_expert.size]
+        self.num_m_blocks = tab[nt + hp.block_expert.size:]
+        self.rows_alloc = max(hp.rows_pad, ops.ALIGN)
+        self.total_recv = int(sum(hp.recv_splits))
+        self.total_send = int(sum(hp.send_splits))
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.map_pad = torch.empty((self.rows_alloc,), **i32)
+        self.map_recv = torch.empty((max(self.total_recv, 1),), **i32)
+        if hp.rows_pad:
+            _lib.call("moe_ep_regroup_map", self.table.data_ptr(), n, el, hp.rows_pad,
+                      self.map_pad.data_ptr(), self.map_recv.data_ptr(),
+                      torch.cuda.current_stream().cuda_stream)
+
+    def a2a(self, send, forward: bool, group):
+        """forward: send layout -> receive layout; else the reverse."""
+        hp = self.hp
+        out_rows = self.total_recv if forward else self.total_send
+        out = torch.empty((out_rows,) + tuple(send.shape[1:]), dtype=send.dtype,
+                          device=send.device)
+        dist.all_to_all_single(out, send, hp.recv_splits if forward else hp.send_splits,
+                               hp.send_splits if forward else hp.recv_splits, group=group)
+        return out
+
+    def to_padded(self, recv):
+        out = torch.empty((self.rows_alloc, recv.shape[1]), dtype=recv.dtype, device=recv.device)
+        src = recv if recv.shape[0] else torch.zeros((1, recv.shape[1]), dtype=recv.dtype,
+                                                     device=recv.device)
+        ops.gather_rows(src, self.map_pad, n=self.rows_alloc, out=out)
+        return out
+
+    def from_padded(self, rows):
+        out = torch.empty((self.total_recv, rows.shape[1]), dtype=rows.dtype, device=rows.device)
+        if self.total_recv:
+            ops.gather_rows(rows, self.map_recv, n=self.total_recv, out=out)
+        return out
+
+
+class _MoEEPFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w_r, w1, w2, sel_bias, w1s, w2s, cfg: MoEConfig, ep: EPGroup):
+        t, h = x.shape
+        E, K = cfg.num_experts, cfg.top_k
+        n = ep.n
+        dev = x.device
+        w_r_t, w_r_pad = ops.stage_router_weight(w_r)
+        r = ops.router_forward(x, w_r, K, cfg.score, sel_bias, 0.0, w_r_t=w_r_t)
+        stats = torch.cat([r.counts.float(), r.mean_scores])
+        gathered = torch.empty((n, 2 * E), dtype=torch.float32, device=dev)
+        dist.all_gather_into_tensor(gathered, stats, group=ep.group)
+        g = gathered.cpu().numpy()  # the one host sync of the EP forward
+        counts_all = np.rint(g[:, :E]).astype(np.int64)
+        cap = cfg.capacity(n * t)  # global capacity on the global batch
+        hp = ep_host_plan(counts_all, ep.rank, cap, cfg.pad_to_capacity)
+        aux_v, aux_g = global_aux(counts_all, g[:, E:], t, K, cfg.aux_loss_coeff)
+        small = torch.from_numpy(np.concatenate([[aux_v], aux_g]).astype(np.float32))
+        small = small.pin_memory().to(dev, non_blocking=True)
+        aux = small[0].clone()
+        r.aux_grad = small[1:]
+        cap_e = None
+        if hp.cap_local is not None:
+            cap_e = torch.from_numpy(hp.cap_local.astype(np.int32)).pin_memory().to(
+                dev, non_blocking=True)
+        xc = _Exchange(hp, dev)
+        splan = ops.build_plan(r.topk_idx, r.topk_prob, E, -1, False, cap_e=cap_e, compact=True)
+        send = ops.permute_gather(x, splan, out=torch.empty((max(xc.total_send, 1), h),
+                                                            dtype=x.dtype, device=dev))
+        recv = xc.a2a(send[: xc.total_send], True, ep.group)
+        xp = xc.to_padded(recv)
+        row_prob = None
+        if cfg.mem_efficient:
+            prob_recv = xc.a2a(splan.row_prob[: xc.total_send].contiguous(), True, ep.group)
+            mp = xc.map_pad.long()
+            row_prob = torch.where(mp >= 0, prob_recv[mp.clamp(min=0)] if xc.total_recv else
+                                   torch.zeros_like(mp, dtype=torch.float32),
+                                   torch.zeros((), device=dev)).float().contiguous()
+        preact, act = gemm.fc1_fwd(xp, w1, xc.block_expert, xc.num_m_blocks, row_prob)
+        o = gemm.fc2_fwd(act, w2, xc.block_expert, xc.num_m_blocks)
+        o_local = xc.a2a(xc.from_padded(o), False, ep.group)
+        shared = shared_expert_forward(x, w1s, w2s) if w1s is not None else None
+        y = ops.combine(o_local, splan, None if cfg.mem_efficient else r.topk_prob,
+                        resid=x if cap >= 0 else None,
+                        extra=shared[-1] if shared is not None else None)
+        ctx.cfg, ctx.ep, ctx.r, ctx.splan, ctx.xc, ctx.cap = cfg, ep, r, splan, xc, cap
+        ctx.row_prob = row_prob
+        ctx.shared = shared[:-1] if shared is not None else None
+        ctx.save_for_backward(x, w_r_pad, w1, w2, xp, preact, act, o_local, w1s, w2s)
+        return y, aux
+
+    @staticmethod
+    def backward(ctx, dy, daux):
+        cfg, ep, r, splan, xc = ctx.cfg, ctx.ep, ctx.r, ctx.splan, ctx.xc
+        x, w_r_pad, w1, w2, xp, preact, act, o_local, w1s, w2s = ctx.saved_tensors
+        dev = x.device
+        h = x.shape[1]
+        el = xc.hp.el
+        dy = dy.contiguous()
+        d_send = torch.empty((max(xc.total_send, 1), h), dtype=dy.dtype, device=dev)
+        if cfg.mem_efficient:
+            d_send, _ = ops.combine_backward(dy, splan, None, None, d_rows=d_send)
+        else:
+            d_send, dprob = ops.combine_backward(dy, splan, o_local, r.topk_prob, d_rows=d_send)
+        d_o = xc.to_padded(xc.a2a(d_send[: xc.total_send], True, ep.group))
+        if cfg.mem_efficient:
+            d_pre, part = gemm.fc2_dgrad(d_o, w2, preact, xc.block_expert, xc.num_m_blocks,
+                                         row_prob=ctx.row_prob, want_dprob=True)
+            dp_pad = part.sum(dim=1)
+            dp_recv = dp_pad[xc.map_recv.long()] if xc.total_recv else dp_pad[:0]
+            dp_send = xc.a2a(dp_recv.contiguous(), False, ep.group)
+            inv = splan.inv_map.long()
+            dprob = torch.where(inv >= 0, dp_send[inv.clamp(min=0)] if xc.total_send else
+                                torch.zeros_like(inv, dtype=torch.float32),
+                                torch.zeros((), device=dev)).float().contiguous()
+        else:
+            d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, xc.block_expert, xc.num_m_blocks)
+        dw2 = gemm.wgrad(d_o, act, xc.off_pad, el)
+        dxp = gemm.fc1_dgrad(d_pre, w1, xc.block_expert, xc.num_m_blocks)
+        dw1 = gemm.wgrad(d_pre, xp, xc.off_pad, el)
+        dxp_local = xc.a2a(xc.from_padded(dxp), False, ep.group)
+        aux_scale = None if daux is None else daux.float()
+        dw_r, dx_router = ops.router_backward(x, w_r_pad, r, dprob, cfg.score,
+                                              aux_scale=aux_scale)
+        dx_shared = dw1s = dw2s = None
+        if ctx.shared is not None:
+            dx_shared, dw1s, dw2s = shared_expert_backward(x, dy, w1s, w2s, ctx.shared)
+        dx = ops.combine(dxp_local, splan, None, resid=dy if ctx.cap >= 0 else None,
+                         extra=dx_router, extra2=dx_shared)
+        return (dx, dw_r.to(torch.bfloat16), dw1, dw2, None, dw1s, dw2s, None, None)
+
+
+def moe_forward_ep(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
+                   selection_bias=None, w1_shared=None, w2_shared=None):
+    """EP MoE layer: w1_local [E/EP, 2m, h], w2_local [E/EP, h, m] are this rank's experts
+    (global experts [rank*E/EP, (rank+1)*E/EP)). Returns (y [T,h], global aux).
+
+    The router weight gradient returned is this rank's partial sum over its own tokens;
+    W_r is replicated, so its all-reduce belongs to the data-parallel gradient sync.
+    """
+    if cfg.num_experts % ep.n:
+        raise ValueError(f"num_experts {cfg.num_experts} not divisible by EP {ep.n}")
+    return _MoEEPFunction.apply(x, w_r, w1_local, w2_local, selection_bias, w1_shared,
+                                w2_shared, cfg, ep)

@@ -56,21 +56,14 @@ class _MoEFunction(torch.autograd.Function):
         row_prob = plan.row_prob if cfg.mem_efficient else None
         preact, act = gemm.fc1_fwd(xp, w1, plan.block_expert, plan.num_m_blocks, row_prob)
         o = gemm.fc2_fwd(act, w2, plan.block_expert, plan.num_m_blocks)
-        shared = None
-        if w1s is not None:
-            rows = ops.ceil_to(max(t, 1), ops.ALIGN)
-            nmb = torch.full((1,), rows // ops.ALIGN, dtype=torch.int32, device=x.device)
-            be = torch.zeros((rows // ops.ALIGN,), dtype=torch.int32, device=x.device)
-            pre_s, act_s = gemm.fc1_fwd(x, w1s, be, nmb, max_rows=rows)
-            o_s = gemm.fc2_fwd(act_s, w2s, be, nmb)
-            shared = (pre_s, act_s, nmb, be, rows)
+        shared = shared_expert_forward(x, w1s, w2s) if w1s is not None else None
         y = ops.combine(o, plan, None if cfg.mem_efficient else r.topk_prob,
                         resid=x if cap >= 0 else None,
-                        extra=o_s if shared is not None else None)
+                        extra=shared[-1] if shared is not None else None)
         ctx.cfg = cfg
         ctx.plan = plan
         ctx.r = r
-        ctx.shared = shared
+        ctx.shared = shared[:-1] if shared is not None else None
         ctx.save_for_backward(x, w_r_pad, w1, w2, xp, preact, act, o, w1s, w2s)
         return y, r.aux
 
@@ -96,18 +89,35 @@ class _MoEFunction(torch.autograd.Function):
                                               aux_scale=aux_scale)
         dx_shared = dw1s = dw2s = None
         if ctx.shared is not None:
-            pre_s, act_s, nmb, be, rows = ctx.shared
-            t = x.shape[0]
-            d_pre_s, _ = gemm.fc2_dgrad(dy, w2s, pre_s, be, nmb, max_rows=rows)
-            dx_shared = gemm.fc1_dgrad(d_pre_s, w1s, be, nmb)
-            offs = torch.arange(2, dtype=torch.int32, device=x.device) * ops.ceil_to(t, 64)
-            # rows >= t read as zero (TMA bound = t)
-            dw2s = gemm.wgrad(dy, act_s, offs, 1, max_rows=t)
-            dw1s = gemm.wgrad(d_pre_s, x, offs, 1, max_rows=t)
+            dx_shared, dw1s, dw2s = shared_expert_backward(x, dy, w1s, w2s, ctx.shared)
         cap = cfg.capacity(x.shape[0])
         dx = ops.combine(dxp, plan, None, resid=dy if cap >= 0 else None, extra=dx_router,
                          extra2=dx_shared)
         return (dx, dw_r.to(torch.bfloat16), dw1, dw2, None, dw1s, dw2s, None)
+
+
+def shared_expert_forward(x, w1s, w2s):
+    """DeepSeek shared expert (latent_moe_forward's shared term, routing.py:276-278): a dense
+    SwiGLU MLP on every token, run as a 1-group grouped GEMM. Returns saved state + output."""
+    t = x.shape[0]
+    rows = ops.ceil_to(max(t, 1), ops.ALIGN)
+    nmb = torch.full((1,), rows // ops.ALIGN, dtype=torch.int32, device=x.device)
+    be = torch.zeros((rows // ops.ALIGN,), dtype=torch.int32, device=x.device)
+    pre_s, act_s = gemm.fc1_fwd(x, w1s, be, nmb, max_rows=rows)
+    o_s = gemm.fc2_fwd(act_s, w2s, be, nmb)
+    return pre_s, act_s, nmb, be, rows, o_s
+
+
+def shared_expert_backward(x, dy, w1s, w2s, saved):
+    pre_s, act_s, nmb, be, rows = saved
+    t = x.shape[0]
+    d_pre_s, _ = gemm.fc2_dgrad(dy, w2s, pre_s, be, nmb, max_rows=rows)
+    dx_s = gemm.fc1_dgrad(d_pre_s, w1s, be, nmb)
+    offs = torch.arange(2, dtype=torch.int32, device=x.device) * ops.ceil_to(t, 64)
+    # rows >= t read as zero (TMA bound = t)
+    dw2s = gemm.wgrad(dy, act_s, offs, 1, max_rows=t)
+    dw1s = gemm.wgrad(d_pre_s, x, offs, 1, max_rows=t)
+    return dx_s, dw1s, dw2s
 
 
 def moe_forward(x, w_r, w1, w2, cfg: MoEConfig, selection_bias=None, w1_shared=None,

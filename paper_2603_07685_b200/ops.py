@@ -180,13 +180,18 @@ def plan_max_rows(T: int, K: int, E: int, capacity: int = -1, pad: bool = False)
 
 def build_plan(topk_idx: torch.Tensor, topk_prob: torch.Tensor | None, E: int,
                capacity: int = -1, pad: bool = False, max_rows: int | None = None,
-               phantom: torch.Tensor | None = None, phantom_max: int = 0) -> Plan:
+               phantom: torch.Tensor | None = None, phantom_max: int = 0,
+               cap_e: torch.Tensor | None = None, compact: bool = False) -> Plan:
     """phantom: optional device int32 [E] extra zero rows per expert (routing_map_pad);
-    phantom_max bounds it for buffer sizing."""
+    phantom_max bounds it for buffer sizing. cap_e: optional device int32 [E] per-expert
+    capacity (EP global-position drops). compact: no 128-row alignment (EP send layout)."""
     t, k = topk_idx.shape
     dev = topk_idx.device
     if max_rows is None:
-        max_rows = plan_max_rows(t, k, E, capacity, pad) + ceil_to(E * phantom_max, ALIGN)
+        if compact:
+            max_rows = max(t * k, 1)
+        else:
+            max_rows = plan_max_rows(t, k, E, capacity, pad) + ceil_to(E * phantom_max, ALIGN)
     i32 = dict(dtype=torch.int32, device=dev)
     meta = torch.empty((3,), **i32)
     off_pad = torch.empty((E + 1,), **i32)
@@ -194,17 +199,18 @@ def build_plan(topk_idx: torch.Tensor, topk_prob: torch.Tensor | None, E: int,
     kept = torch.empty((E,), **i32)
     eff = torch.empty((E,), **i32)
     counts = torch.empty((E,), **i32)
-    block_expert = torch.empty((max_rows // ALIGN,), **i32)
+    block_expert = None if compact else torch.empty((max_rows // ALIGN,), **i32)
     inv_map = torch.empty((t, k), **i32)
     row_src = torch.empty((max_rows,), **i32)
     row_prob = torch.empty((max_rows,), dtype=torch.float32, device=dev)
     ws = torch.empty((max(int(_lib.query("moe_permute_workspace_ints", t, k, E)), 1),), **i32)
     status = torch.empty((1,), **i32)
     _lib.call("moe_permute_plan", topk_idx.data_ptr(), _p(topk_prob), t, k, E, int(capacity),
-              int(bool(pad)), _p(phantom), max_rows, meta.data_ptr(), off_pad.data_ptr(), off_c.data_ptr(),
-              kept.data_ptr(), eff.data_ptr(), counts.data_ptr(), block_expert.data_ptr(),
-              inv_map.data_ptr(), row_src.data_ptr(), row_prob.data_ptr(), ws.data_ptr(),
-              status.data_ptr(), _stream())
+              _p(cap_e), int(bool(pad)), _p(phantom), 1 if compact else ALIGN, max_rows,
+              meta.data_ptr(), off_pad.data_ptr(), off_c.data_ptr(), kept.data_ptr(),
+              eff.data_ptr(), counts.data_ptr(), _p(block_expert), inv_map.data_ptr(),
+              row_src.data_ptr(), row_prob.data_ptr(), ws.data_ptr(), status.data_ptr(),
+              _stream())
     return Plan(t, k, E, int(capacity), bool(pad), max_rows, meta, off_pad, off_c, kept, eff,
                 counts, block_expert, inv_map, row_src, row_prob, status)
 

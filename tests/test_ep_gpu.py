@@ -1,0 +1,144 @@
+"""EP layer on N GPUs (NCCL) vs the single-process GLOBAL oracle.
+
+Each rank owns tokens [r*T, (r+1)*T) of one global batch and experts
+[r*E/N, (r+1)*E/N). The oracle runs the whole layer on the global batch (decision taken
+from the GPUs' own fp32 logits, i.e. parity at the logits boundary); every rank checks
+its slice of y and dX, its experts' dW1/dW2, the all-reduced dW_r and the global aux.
+Skipped unless >= 2 GPUs are visible (gpurun --gpus 2|4).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "dropless_softmax": dict(E=8, K=2, h=256, m=256, T=256, score="softmax", cf=None, pad=False),
+    "capacity_pad": dict(E=8, K=2, h=256, m=256, T=256, score="softmax", cf=1.0, pad=True,
+                         skew=True),
+    "sigmoid_many": dict(E=16, K=4, h=256, m=256, T=192, score="sigmoid", cf=None, pad=False),
+    "mem_efficient": dict(E=8, K=2, h=256, m=256, T=128, score="softmax", cf=None, pad=False,
+                          mem=True),
+}
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, case, q):
+    try:
+        import torch.distributed as dist
+
+        from oracle import backward_ref as B
+        from oracle import routing_ref as R
+        from paper_2603_07685_b200 import gemm, ops
+        from paper_2603_07685_b200.dispatcher import EPGroup, moe_forward_ep
+        from paper_2603_07685_b200.layer import MoEConfig
+
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(rank)
+        dev = torch.device("cuda", rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+        E, K, h, m, T = case["E"], case["K"], case["h"], case["m"], case["T"]
+        cfg = MoEConfig(E, K, h, m, score=case["score"], aux_loss_coeff=1e-2,
+                        capacity_factor=case["cf"], pad_to_capacity=case["pad"],
+                        mem_efficient=case.get("mem", False))
+        g = torch.Generator().manual_seed(11)
+        bf = torch.bfloat16
+        x_g = torch.randn((world * T, h), generator=g).to(bf)
+        w_r = (torch.randn((h, E), generator=g) * h ** -0.5)
+        if case.get("skew"):
+            # push routing towards low expert ids (capacity drops on the global batch)
+            x_g = (x_g.float() + torch.linspace(1.0, 0.0, h)[None, :] * 0.5).to(bf)
+            w_r[:, 0] += 0.05
+        w_r = w_r.to(bf)
+        up = (torch.randn((E, m, h), generator=g) * h ** -0.5).to(bf)
+        gate = (torch.randn((E, m, h), generator=g) * h ** -0.5).to(bf)
+        w2 = (torch.randn((E, h, m), generator=g) * m ** -0.5).to(bf)
+        dy_g = torch.randn((world * T, h), generator=g).to(bf)
+        el = E // world
+        mine = slice(rank * el, (rank + 1) * el)
+        sl = slice(rank * T, (rank + 1) * T)
+
+        x = x_g[sl].to(dev).requires_grad_(True)
+        w_rd = w_r.to(dev).requires_grad_(True)
+        w1d = gemm.interleave_gate_up(gate[mine].to(dev), up[mine].to(dev)).requires_grad_(True)
+        w2d = w2[mine].to(dev).contiguous().requires_grad_(True)
+        ep = EPGroup()
+        y, aux = moe_forward_ep(x, w_rd, w1d, w2d, cfg, ep)
+        torch.autograd.backward([y, aux], [dy_g[sl].to(dev), torch.ones_like(aux)])
+        dwr = w_rd.grad.float().clone()
+        dist.all_reduce(dwr)
+        # global decision from the GPUs' own logits
+        r = ops.router_forward(x.detach(), w_rd.detach(), K, cfg.score)
+        lg = r.logits[:T, :E].contiguous()
+        lg_all = torch.empty((world * T, E), dtype=torch.float32, device=dev)
+        dist.all_gather_into_tensor(lg_all, lg)
+        torch.cuda.synchronize()
+
+        f64 = lambda t: t.detach().double().cpu().numpy()  # noqa: E731
+        dec = R.route(f64(lg_all), np.eye(E), score=cfg.score, top_k=K)
+        if cfg.capacity_factor is not None:
+            dec = R.apply_capacity(dec, cfg.capacity_factor, pad=cfg.pad_to_capacity)
+        params = R.ExpertParams(w1=list(f64(up)), w2=list(f64(w2)), gate=list(f64(gate)))
+        ref = B.moe_forward_backward(f64(x_g), f64(w_r), params, f64(dy_g), score=cfg.score,
+                                     top_k=K, coeff=1e-2, decision=dec,
+                                     variant="mem_efficient" if cfg.mem_efficient else "standard")
+
+        def rel(a, b):
+            return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+        errs = {
+            "y": rel(f64(y), ref["y"][sl]),
+            "dx": rel(f64(x.grad), ref["dx"][sl]),
+            "dwr": rel(f64(dwr), ref["dw_r"]),
+        }
+        dg, du = gemm.split_gate_up(w1d.grad)
+        for j in range(el):
+            e = rank * el + j
+            if dec.effective_counts()[e] == 0:
+                continue
+            errs[f"dgate{e}"] = rel(f64(dg[j]), ref["dgate"][e])
+            errs[f"dup{e}"] = rel(f64(du[j]), ref["dw1"][e])
+            errs[f"dw2_{e}"] = rel(f64(w2d.grad[j]), ref["dw2"][e])
+        aux_err = abs(float(aux.detach()) - ref["aux"]) / max(abs(ref["aux"]), 1e-9)
+        bad = {k: v for k, v in errs.items() if v > (1e-2 if k == "y" else 2e-2)}
+        if aux_err > 1e-4:
+            bad["aux"] = aux_err
+        q.put((rank, "ok" if not bad else f"errors {bad}"))
+        dist.destroy_process_group()
+    except Exception as exc:  # pragma: no cover
+        import traceback
+
+        q.put((rank, traceback.format_exc() + repr(exc)))
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_ep_layer_matches_global_oracle(name):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(torch.cuda.device_count(), 8)
+    while CASES[name]["E"] % world:
+        world -= 1
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES[name], q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, msg in res:
+        assert msg == "ok", f"rank {rank}: {msg}"
