@@ -1,0 +1,474 @@
+"""Drop-in GPU implementation of the reference's ``moelab.routing`` function API.
+
+Same function names, argument meaning and error behaviour as reference
+pkg/src/moelab/routing.py (ValueError "finite" :80-81, "top_k ... exceeds" :83-84,
+"unknown score function" :93, "step must be > 0" :143-144, "capacity_factor must be > 0"
+:232-233, "not divisible" :295-296, "multiple must be >= 1" / "insufficient filler
+capacity" :316-324; NotImplementedError for the sigmoid aux gradient :131-132).
+
+Differences that are properties of the device path, not of the API:
+  * compute runs in bf16 with fp32 accumulation on the sm_100a kernels (BASELINE.json
+    north star); numpy inputs are rounded to bf16 once, results come back as numpy
+    float64 (torch inputs return CUDA tensors);
+  * routing parity is defined at the logits boundary: selections equal the reference
+    applied to the logits the device computed (bit-exact, lowest-index ties);
+  * any shape works: hidden / ffn dims are zero-padded to the GEMM tile multiples and
+    sliced back (exact: zero rows and columns contribute nothing). Ungated experts
+    (routing.py:64, silu(x W1^T)) run on the SwiGLU kernel with the "up" operand
+    replaced by a constant-one feature (act = silu(z) * 1, exact).
+
+There is no CPU fallback: without libmoe_b200.so every call raises.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import torch
+
+from . import _lib, gemm, ops
+
+_DEV = None
+
+
+def _dev():
+    global _DEV
+    if _DEV is None:
+        if not torch.cuda.is_available():
+            raise _lib.MoEKernelError("paper_2603_07685_b200 needs a CUDA device (no CPU fallback)")
+        _DEV = torch.device("cuda", torch.cuda.current_device())
+    return _DEV
+
+
+def _is_np(a):
+    return not isinstance(a, torch.Tensor)
+
+
+def _t(a, dtype=torch.bfloat16):
+    """numpy / torch -> contiguous CUDA tensor of `dtype`."""
+    if isinstance(a, torch.Tensor):
+        return a.to(device=_dev(), dtype=dtype).contiguous()
+    return torch.as_tensor(np.asarray(a), device=_dev()).to(dtype).contiguous()
+
+
+def _out(t, like_numpy):
+    if not like_numpy or t is None:
+        return t
+    if t.dtype == torch.bool:
+        return t.cpu().numpy()
+    if t.dtype in (torch.int32, torch.int64):
+        return t.cpu().numpy().astype(np.int64)
+    return t.detach().double().cpu().numpy()
+
+
+def _ceil(a, b):
+    return -(-a // b) * b
+
+
+def _pad2(t, rows=None, cols=None):
+    r = t.shape[0] if rows is None else rows
+    c = t.shape[1] if cols is None else cols
+    if (r, c) == tuple(t.shape):
+        return t.contiguous()
+    out = torch.zeros((r, c), dtype=t.dtype, device=t.device)
+    out[: t.shape[0], : t.shape[1]] = t
+    return out
+
+
+# ----------------------------------------------------------------------------- types
+
+@dataclass(frozen=True)
+class RoutingDecision:
+    """routing.py:16-39. Dense fields as in the reference (CUDA tensors, or numpy when the
+    router was called with numpy); the compact device selection rides along privately."""
+
+    probs: object
+    routing_map: object
+    counts: object
+    scores: object
+    dropped: object = None
+    phantom_rows: object = None
+    _topk_idx: torch.Tensor | None = field(default=None, repr=False, compare=False)
+    _topk_prob: torch.Tensor | None = field(default=None, repr=False, compare=False)
+    _logits: torch.Tensor | None = field(default=None, repr=False, compare=False)
+
+    @property
+    def num_tokens(self) -> int:
+        return self.routing_map.shape[0]
+
+    @property
+    def num_experts(self) -> int:
+        return self.routing_map.shape[1]
+
+    def effective_counts(self):
+        """routing.py:33-39"""
+        m = _t(self.routing_map, torch.bool)
+        if self.dropped is not None:
+            m = m & ~_t(self.dropped, torch.bool)
+        c = m.sum(0).to(torch.int64)
+        if self.phantom_rows is not None:
+            c = c + _t(self.phantom_rows, torch.int64)
+        return _out(c, _is_np(self.routing_map))
+
+
+@dataclass(frozen=True)
+class ExpertParams:
+    """routing.py:42-52: per-expert w1 ("up" / ungated) [m,h], w2 [h,m], gate [m,h]."""
+
+    w1: list
+    w2: list
+    gate: list | None = None
+
+    @property
+    def num_experts(self) -> int:
+        return len(self.w1)
+
+
+# ----------------------------------------------------------------------------- router
+
+def route(hidden, w_r, score: str = "softmax", top_k: int = 1, selection_bias=None):
+    """routing.py:71-108 on the device (tcgen05 logits GEMM + warp-per-token top-k)."""
+    if score not in ops.SCORE_FN:
+        raise ValueError(f"unknown score function {score!r}")
+    np_io = _is_np(hidden)
+    x = _t(hidden)
+    w = _t(w_r)
+    t, h = x.shape
+    e = w.shape[1]
+    if top_k > e:
+        raise ValueError(f"top_k={top_k} exceeds num_experts={e}")
+    hp = _ceil(max(h, 1), 64)
+    x = _pad2(x, cols=hp)
+    w = _pad2(w, rows=hp)
+    bias = None if selection_bias is None else _t(selection_bias, torch.float32)
+    r = ops.router_forward(x, w, top_k, score, bias, 0.0, want_scores=True)
+    if int(r.status.item()) & 1:
+        raise ValueError("router logits are not finite")
+    idx = r.topk_idx.long()
+    rmap = torch.zeros((t, e), dtype=torch.bool, device=x.device)
+    rmap.scatter_(1, idx, True)
+    probs = torch.zeros((t, e), dtype=torch.float32, device=x.device)
+    probs.scatter_(1, idx, r.topk_prob)
+    return RoutingDecision(_out(probs, np_io), _out(rmap, np_io), _out(r.counts, np_io),
+                           _out(r.scores, np_io), None, None, r.topk_idx, r.topk_prob,
+                           r.logits[:t, :e])
+
+
+def aux_loss(decision: RoutingDecision, coeff: float) -> float:
+    """routing.py:111-120: coeff * E * sum_i f_i P_i, f = counts / sum(map)."""
+    rm = _t(decision.routing_map, torch.bool)
+    total = max(int(rm.sum().item()), 1)
+    f = _t(decision.counts, torch.float64) / total
+    p = _t(decision.scores, torch.float64).mean(0)
+    return float(coeff * decision.num_experts * torch.dot(f, p).item())
+
+
+def aux_loss_grad_wr(hidden, w_r, top_k: int, coeff: float, score: str = "softmax"):
+    """routing.py:123-137: d aux / d W_r (f constant) via moe_router_bwd + split-K wgrad."""
+    if score != "softmax":
+        raise NotImplementedError("analytic gradient implemented for softmax scoring")
+    np_io = _is_np(hidden)
+    x = _t(hidden)
+    w = _t(w_r)
+    t, h = x.shape
+    e = w.shape[1]
+    hp = _ceil(max(h, 1), 256)
+    x = _pad2(x, cols=hp)
+    w = _pad2(w, rows=hp)
+    wt, wpad = ops.stage_router_weight(w)
+    r = ops.router_forward(x, w, top_k, score, None, coeff, w_r_t=wt)
+    dprob = torch.zeros((t, top_k), dtype=torch.float32, device=x.device)
+    dw, _ = ops.router_backward(x, wpad, r, dprob, score, aux_scale=1.0)
+    return _out(dw[:h], np_io)
+
+
+def auxfree_bias_update(counts, bias, step: float):
+    """routing.py:140-146"""
+    if step <= 0:
+        raise ValueError("step must be > 0")
+    np_io = _is_np(bias)
+    c = _t(counts, torch.float64)
+    b = _t(bias, torch.float64)
+    return _out(b + step * torch.sign(c.mean() - c), np_io)
+
+
+# ----------------------------------------------------------------------------- selection
+
+def _selection(decision: RoutingDecision):
+    """(topk_idx int32 [T,Kmax] ascending, -1 padded; per-selection prob fp32) of the
+    KEPT selections (routing_map & ~dropped)."""
+    rm = _t(decision.routing_map, torch.bool)
+    keep = rm if decision.dropped is None else rm & ~_t(decision.dropped, torch.bool)
+    t, e = keep.shape
+    kmax = max(int(keep.sum(1).max().item()) if t else 0, 1)
+    ar = torch.arange(e, device=keep.device).expand(t, e)
+    key = torch.where(keep, ar, torch.full_like(ar, e))
+    srt, _ = torch.sort(key, dim=1)
+    idx = srt[:, :kmax]
+    valid = idx < e
+    prob = torch.gather(_t(decision.probs, torch.float32), 1, idx.clamp(max=e - 1))
+    idx = torch.where(valid, idx, torch.full_like(idx, -1)).to(torch.int32).contiguous()
+    prob = torch.where(valid, prob, torch.zeros_like(prob)).contiguous()
+    return idx, prob
+
+
+def _plan(decision: RoutingDecision):
+    idx, prob = _selection(decision)
+    phantom = None
+    pmax = 0
+    if decision.phantom_rows is not None:
+        phantom = _t(decision.phantom_rows, torch.int32)
+        pmax = int(phantom.max().item()) if phantom.numel() else 0
+    return ops.build_plan(idx, prob, decision.num_experts, -1, False, phantom=phantom,
+                          phantom_max=pmax), prob
+
+
+def expert_capacity(capacity_factor: float, tokens: int, top_k: int, num_experts: int) -> int:
+    """routing.py:250-251"""
+    return -(-int(round(capacity_factor * tokens * top_k)) // num_experts)
+
+
+def apply_capacity(decision: RoutingDecision, capacity_factor: float, pad: bool = False):
+    """routing.py:226-247: keep the first C selections of each expert by token index."""
+    if capacity_factor <= 0:
+        raise ValueError("capacity_factor must be > 0")
+    np_io = _is_np(decision.routing_map)
+    rm = _t(decision.routing_map, torch.bool)
+    t, e = rm.shape
+    k = int(round(int(rm.sum().item()) / max(t, 1)))
+    cap = expert_capacity(capacity_factor, t, k, e)
+    idx, prob = _selection(replace(decision, dropped=None))
+    plan = ops.build_plan(idx, prob, e, cap, pad)
+    dropped_sel = (plan.inv_map < 0) & (idx >= 0)
+    dropped = torch.zeros((t, e), dtype=torch.bool, device=rm.device)
+    if t:
+        dropped.scatter_(1, idx.long().clamp(min=0), dropped_sel)
+    phantom = None
+    if pad:
+        phantom = (cap - torch.clamp(rm.sum(0), max=cap)).to(torch.int64)
+    return replace(decision, dropped=_out(dropped, np_io),
+                   phantom_rows=_out(phantom, np_io) if pad else None)
+
+
+def routing_map_pad(decision: RoutingDecision, multiple: int, num_filler_tokens=None):
+    """routing.py:312-325 (uses raw routing_map counts; replaces phantom_rows)."""
+    if multiple < 1:
+        raise ValueError("multiple must be >= 1")
+    np_io = _is_np(decision.routing_map)
+    counts = _t(decision.routing_map, torch.bool).sum(0).to(torch.int64)
+    needed = (-counts) % multiple
+    mx = int(needed.max().item()) if needed.numel() else 0
+    if num_filler_tokens is not None and mx > num_filler_tokens:
+        raise ValueError(f"insufficient filler capacity: need {mx} rows per "
+                         f"expert, have {num_filler_tokens}")
+    return replace(decision, phantom_rows=_out(needed, np_io))
+
+
+# ----------------------------------------------------------------------------- permutation
+
+def permute(tokens, decision: RoutingDecision):
+    """routing.py:149-168 -> (rows, row_id_map int64, -1 for phantom rows)."""
+    np_io = _is_np(tokens)
+    x = _t(tokens)
+    h = x.shape[1]
+    x = _pad2(x, cols=_ceil(max(h, 1), 8))
+    plan, _ = _plan(decision)
+    rmap, _ = ops.compact_row_id_map(plan)
+    rows = ops.gather_rows(x, rmap.to(torch.int32)) if rmap.numel() else x[:0]
+    return _out(rows[:, :h], np_io), _out(rmap, np_io)
+
+
+def unpermute_sum(rows, row_id_map, num_tokens: int):
+    """routing.py:171-177: out[src] += rows[r], rows of a token summed in row order."""
+    np_io = _is_np(rows)
+    r = _t(rows)
+    h = r.shape[1]
+    r = _pad2(r, cols=_ceil(max(h, 1), 8))
+    m = _t(row_id_map, torch.int64)
+    out = torch.empty((num_tokens, r.shape[1]), dtype=torch.bfloat16, device=r.device)
+    real = m >= 0
+    cnt = torch.bincount(m[real], minlength=num_tokens) if num_tokens else m[:0]
+    kmax = max(int(cnt.max().item()) if cnt.numel() else 0, 1)
+    inv = torch.full((num_tokens, kmax), -1, dtype=torch.int32, device=r.device)
+    if real.any():
+        rows_idx = torch.nonzero(real).squeeze(1)
+        src = m[rows_idx]
+        order = torch.argsort(src, stable=True)  # row order within a token preserved
+        src_s, rows_s = src[order], rows_idx[order]
+        start = torch.cumsum(cnt, 0) - cnt
+        slot = torch.arange(src_s.numel(), device=r.device) - start[src_s]
+        inv[src_s, slot] = rows_s.to(torch.int32)
+    if num_tokens:
+        _lib.call("moe_combine", r.data_ptr(), num_tokens, kmax, r.shape[1], inv.data_ptr(),
+                  None, None, None, None, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    return _out(out[:, :h], np_io)
+
+
+# ----------------------------------------------------------------------------- experts
+
+class _Stacked:
+    """ExpertParams -> stacked, zero-padded device weights for the grouped GEMM."""
+
+    def __init__(self, params: ExpertParams, h_in: int):
+        e = params.num_experts
+        w1 = [_t(w) for w in params.w1]
+        w2 = [_t(w) for w in params.w2]
+        m = w1[0].shape[0]
+        self.gated = params.gate is not None
+        self.h_in, self.m = h_in, m
+        self.h_out = w2[0].shape[0]
+        # ungated: one extra input feature fixed at 1 feeds the "up" half -> act = silu(z)
+        self.hp = _ceil(h_in + (0 if self.gated else 1), 256)
+        self.hop = _ceil(self.h_out, 256)
+        self.mp = _ceil(m, 256)
+        dev = w1[0].device
+        gate = torch.zeros((e, self.mp, self.hp), dtype=torch.bfloat16, device=dev)
+        up = torch.zeros_like(gate)
+        w2p = torch.zeros((e, self.hop, self.mp), dtype=torch.bfloat16, device=dev)
+        for i in range(e):
+            if self.gated:
+                gate[i, :m, :h_in] = _t(params.gate[i])
+                up[i, :m, :h_in] = w1[i]
+            else:
+                gate[i, :m, :h_in] = w1[i]
+                up[i, :m, h_in] = 1.0
+            w2p[i, : self.h_out, :m] = w2[i]
+        self.w1 = gemm.interleave_gate_up(gate, up)
+        self.w2 = w2p
+
+    def pad_x(self, x):
+        xp = _pad2(x, cols=self.hp)
+        if not self.gated:
+            xp[:, self.h_in] = 1.0
+        return xp
+
+
+def _experts_padded(xp_rows, st: _Stacked, plan, row_prob=None):
+    """fc1+SwiGLU then fc2 on a padded plan -> expert output rows [max_rows, hop]."""
+    _, act = gemm.fc1_fwd(xp_rows, st.w1, plan.block_expert, plan.num_m_blocks, row_prob)
+    return gemm.fc2_fwd(act, st.w2, plan.block_expert, plan.num_m_blocks)
+
+
+def _dense_plan(t, dev):
+    rows = max(_ceil(t, 128), 128)
+    nmb = torch.full((1,), rows // 128, dtype=torch.int32, device=dev)
+    be = torch.zeros((rows // 128,), dtype=torch.int32, device=dev)
+    return rows, nmb, be
+
+
+def expert_activation(params: ExpertParams, expert: int, x_rows):
+    """routing.py:59-64 on the device."""
+    np_io = _is_np(x_rows)
+    x = _t(x_rows)
+    st = _Stacked(ExpertParams([params.w1[expert]], [params.w2[expert]],
+                               None if params.gate is None else [params.gate[expert]]),
+                  x.shape[1])
+    rows, nmb, be = _dense_plan(x.shape[0], x.device)
+    _, act = gemm.fc1_fwd(st.pad_x(x), st.w1, be, nmb, max_rows=rows)
+    return _out(act[: x.shape[0], : st.m], np_io)
+
+
+def expert_forward(params: ExpertParams, expert: int, x_rows):
+    """routing.py:67-68 on the device."""
+    np_io = _is_np(x_rows)
+    x = _t(x_rows)
+    st = _Stacked(ExpertParams([params.w1[expert]], [params.w2[expert]],
+                               None if params.gate is None else [params.gate[expert]]),
+                  x.shape[1])
+    rows, nmb, be = _dense_plan(x.shape[0], x.device)
+    _, act = gemm.fc1_fwd(st.pad_x(x), st.w1, be, nmb, max_rows=rows)
+    out = gemm.fc2_fwd(act, st.w2, be, nmb)
+    return _out(out[: x.shape[0], : st.h_out], np_io)
+
+
+def silu(x):
+    """routing.py:55-56 (elementwise; API helper, not on the layer hot path)."""
+    np_io = _is_np(x)
+    return _out(torch.nn.functional.silu(_t(x, torch.float32)), np_io)
+
+
+def _combine(tokens, decision: RoutingDecision, params: ExpertParams, mem_efficient: bool,
+             residual: bool):
+    np_io = _is_np(tokens)
+    x = _t(tokens)
+    t = x.shape[0]
+    st = _Stacked(params, x.shape[1])
+    plan, prob = _plan(decision)
+    xp = ops.permute_gather(st.pad_x(x), plan)
+    o = _experts_padded(xp, st, plan, plan.row_prob if mem_efficient else None)
+    resid = None
+    if residual and decision.dropped is not None:
+        resid = _pad2(x, cols=st.hop)
+    y = ops.combine(o, plan, None if mem_efficient else prob, resid=resid)
+    return _out(y[:t, : st.h_out], np_io)
+
+
+def combine_standard(tokens, decision: RoutingDecision, params: ExpertParams):
+    """routing.py:189-201"""
+    return _combine(tokens, decision, params, False, False)
+
+
+def combine_mem_efficient(tokens, decision: RoutingDecision, params: ExpertParams):
+    """routing.py:204-223"""
+    return _combine(tokens, decision, params, True, False)
+
+
+def moe_output_with_residual(tokens, decision: RoutingDecision, params: ExpertParams):
+    """routing.py:254-262: fully dropped tokens pass through on the residual path."""
+    return _combine(tokens, decision, params, False, True)
+
+
+def _linear(a, w):
+    """a [T,K] @ w[N,K]^T on the grouped GEMM (1 group), any shape (zero-padded)."""
+    t, k = a.shape
+    n = w.shape[0]
+    kp, np_ = _ceil(max(k, 1), 64), _ceil(max(n, 1), 256)
+    rows, nmb, be = _dense_plan(t, a.device)
+    out = gemm.fc2_fwd(_pad2(a, cols=kp), _pad2(w, rows=np_, cols=kp)[None], be, nmb,
+                       max_rows=rows)
+    return out[:t, :n]
+
+
+def latent_moe_forward(x, w_down, w_up, experts: ExpertParams, decision: RoutingDecision,
+                       shared: ExpertParams | None = None):
+    """routing.py:265-279: W_up (sum_i p_i E_i(W_down x)) + sum_j E_j_shared(x)."""
+    np_io = _is_np(x)
+    xd = _t(x)
+    latent = _linear(xd, _t(w_down))
+    routed = _t(combine_standard(latent, decision, experts))
+    out = _linear(routed, _t(w_up)).float()
+    if shared is not None:
+        for j in range(shared.num_experts):
+            out = out + _t(expert_forward(shared, j, xd), torch.float32)
+    return _out(out, np_io)
+
+
+def upcycle(dense_w1, dense_w2, granularity: int, duplication: int, dense_gate=None):
+    """routing.py:282-309 (initialisation-time weight surgery, done with tensor ops)."""
+    np_io = _is_np(dense_w1)
+    inter, h = dense_w1.shape
+    if inter % granularity != 0:
+        raise ValueError(f"intermediate dim {inter} not divisible by granularity {granularity}")
+    shard = inter // granularity
+    n = granularity * duplication
+    f = (lambda a: np.asarray(a)) if np_io else (lambda a: a)
+    w1 = [f(dense_w1)[g * shard:(g + 1) * shard].copy() if np_io else
+          dense_w1[g * shard:(g + 1) * shard].clone() for _ in range(duplication)
+          for g in range(granularity)]
+    w2 = [f(dense_w2)[:, g * shard:(g + 1) * shard] * n for _ in range(duplication)
+          for g in range(granularity)]
+    gates = None
+    if dense_gate is not None:
+        gates = [f(dense_gate)[g * shard:(g + 1) * shard].copy() if np_io else
+                 dense_gate[g * shard:(g + 1) * shard].clone() for _ in range(duplication)
+                 for g in range(granularity)]
+    w_r = np.zeros((h, n)) if np_io else torch.zeros((h, n), dtype=dense_w1.dtype,
+                                                      device=dense_w1.device)
+    return ExpertParams(w1=w1, w2=w2, gate=gates), w_r
+
+
+def a2a_send_volume(tokens: int, top_k: int, hidden: int, ep: int, width: float = 2.0) -> float:
+    """perf.py:62-70: per-GPU bytes of one all-to-all (the EP dispatcher's byte model)."""
+    if ep < 1:
+        raise ValueError("ep must be >= 1")
+    return tokens * top_k * hidden * width * (ep - 1) / ep
