@@ -92,21 +92,23 @@ int moe_dprob_from_partials(const int* inv_map, long long n, const float* partia
 
 /* ------------------------------------------------------------------ grouped GEMM (tcgen05)
  * replaces expert_activation()/expert_forward() routing.py:59-68 per expert block and the
- * corresponding backward GEMMs. */
+ * corresponding backward GEMMs. flags bit 0 (grouped-M calls): the plan's
+ * expert blocks are 256-row aligned -> CTA-pair engine (UMMA 256x256, cta_group::2). The
+ * weight-gradient calls pick the pair engine by themselves whenever M % 256 == 0. */
 int moe_gg_fc1_fwd(const void* xp, const void* w1, int a_rows, int max_rows, int h, int m,
                    int num_experts, const int* block_expert, const int* num_m_blocks,
-                   const float* row_prob, void* preact, void* act, void* stream);
+                   const float* row_prob, void* preact, void* act, int flags, void* stream);
 int moe_gg_fc2_fwd(const void* act, const void* w2, int a_rows, int max_rows, int m, int h,
                    int num_experts, const int* block_expert, const int* num_m_blocks,
-                   void* out, void* stream);
+                   void* out, int flags, void* stream);
 int moe_gg_fc2_dgrad(const void* dout, const void* w2, const void* preact, int a_rows,
                      int max_rows, int h, int m, int num_experts, const int* block_expert,
                      const int* num_m_blocks, const float* row_prob, void* d_preact,
-                     float* dprob_partial, void* stream);
+                     float* dprob_partial, int flags, void* stream);
 int moe_gg_fc1_dgrad(const void* d_preact, const void* w1, int a_rows, int max_rows, int m,
                      int h,
                      int num_experts, const int* block_expert, const int* num_m_blocks,
-                     void* dxp, void* stream);
+                     void* dxp, int flags, void* stream);
 int moe_gg_wgrad(const void* a, const void* b, int max_rows, int M, int N, int num_experts,
                  const int* expert_offsets, void* dw, void* stream);
 int moe_gg_wgrad_f32(const void* a, const void* b, int max_rows, int M, int N,

@@ -48,10 +48,10 @@ SIGNATURES: dict[str, list] = {
     "moe_combine_bwd": [P, P, I, I, I, P, P, P, P, P],
     "moe_dprob_from_partials": [P, L, P, I, P, P],
     # grouped GEMM (csrc/grouped_gemm.cu)
-    "moe_gg_fc1_fwd": [P, P, I, I, I, I, I, P, P, P, P, P, P],
-    "moe_gg_fc2_fwd": [P, P, I, I, I, I, I, P, P, P, P],
-    "moe_gg_fc2_dgrad": [P, P, P, I, I, I, I, I, P, P, P, P, P, P],
-    "moe_gg_fc1_dgrad": [P, P, I, I, I, I, I, P, P, P, P],
+    "moe_gg_fc1_fwd": [P, P, I, I, I, I, I, P, P, P, P, P, I, P],
+    "moe_gg_fc2_fwd": [P, P, I, I, I, I, I, P, P, P, I, P],
+    "moe_gg_fc2_dgrad": [P, P, P, I, I, I, I, I, P, P, P, P, P, I, P],
+    "moe_gg_fc1_dgrad": [P, P, I, I, I, I, I, P, P, P, I, P],
     "moe_gg_wgrad": [P, P, I, I, I, I, P, P, P],
     "moe_gg_wgrad_f32": [P, P, I, I, I, I, P, P, P],
     "moe_gg_gemm_f32": [P, P, I, I, I, I, I, P, P, P, P],

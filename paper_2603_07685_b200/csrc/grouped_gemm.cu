@@ -1,6 +1,13 @@
 // Grouped GEMM for the MoE expert FFN on sm_100a: tcgen05.mma (bf16 in, fp32 in TMEM),
-// TMA-fed 4-stage shared-memory ring, double-buffered TMEM accumulators, persistent
+// TMA-fed shared-memory ring, double-buffered TMEM accumulators, persistent
 // warp-specialised CTAs (warp 0 = TMA producer, warp 1 = MMA issuer, warps 2-5 = epilogue).
+//
+// Two tile engines, selected per call:
+//   CG = 1: one CTA per 128x256 tile (UMMA 128x256x16, cta_group::1), 4 x 48 KB stages.
+//   CG = 2: an SM pair (thread-block cluster of 2) per 256x256 tile (UMMA 256x256x16,
+//           cta_group::2): each CTA stages its 128 rows of A and HALF of B, so the shared-
+//           memory operand traffic per SM drops from 48 KB to 32 KB per k-block; the leader
+//           CTA issues the MMAs and multicasts completion to both CTAs; 6 x 32 KB stages.
 //
 // Oracle it replaces: the per-expert numpy GEMMs of expert_activation / expert_forward
 // (reference pkg/src/moelab/routing.py:59-68) and the GEMMs implied by the backward of
@@ -8,10 +15,10 @@
 //
 // Two grouping modes, both driven by DEVICE-resident group metadata (no host sync):
 //   grouped-M (fwd, dgrad): C[rows, N] = A[rows, K] * B_e^T where the expert-major
-//     permuted activations are padded per expert to 128-row blocks, so every 128-row
-//     M tile belongs to exactly one expert (block_expert[] says which).
+//     permuted activations are padded per expert to 128-row (CG=1) or 256-row (CG=2)
+//     blocks, so every M tile belongs to exactly one expert (block_expert[] says which).
 //   grouped-K (wgrad): C_e[M, N] = sum_{r in rows(e)} A[r, :M]^T B[r, :N] with the
-//     reduction over the expert's (128-aligned, zero-padded) token rows.
+//     reduction over the expert's (zero-padded) token rows.
 //
 // Epilogues (fused): plain bf16 store, fp32 store, SwiGLU (silu(gate)*up, optional
 // per-row routing-prob scale for the memory-efficient combine), dSwiGLU (recompute
@@ -25,28 +32,33 @@
 namespace moe {
 namespace gg {
 
-constexpr int BM = 128;
-constexpr int BN = 256;
-constexpr int BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
-constexpr int STAGES = 4;
+constexpr int BM = 128;  // rows per CTA
+constexpr int BN = 256;  // output columns per tile
+constexpr int BK = 64;   // 64 bf16 = 128 B = one SWIZZLE_128B row
 constexpr int UMMA_K = 16;
-constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
-constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
-constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int TMEM_COLS = 512;  // 2 accumulator stages x 256 fp32 columns
 constexpr int NUM_THREADS = 192;
-constexpr int BAND_M = 16;  // raster: 16 m-blocks share each swept n-block (L2 reuse)
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int BAND_M = 16;  // raster: 16 M units share each swept n-block (L2 reuse)
+
+template <int CG>
+struct Cfg {
+  static constexpr int A_STAGE = BM * BK * 2;           // this CTA's 128 rows of A
+  static constexpr int B_ROWS = BN / CG;                // rows of the B tile this CTA stages
+  static constexpr int B_STAGE = B_ROWS * BK * 2;
+  static constexpr int STAGE = A_STAGE + B_STAGE;
+  static constexpr int STAGES = CG == 1 ? 4 : 6;
+  static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+};
 
 enum Epi : int { EPI_BF16 = 0, EPI_SWIGLU = 1, EPI_DSWIGLU = 2, EPI_F32 = 3 };
 
 struct Params {
   // grouped-M
-  const int* num_m_blocks;  // device scalar
+  const int* num_m_blocks;  // device scalar: active 128-row blocks
   const int* block_expert;  // [max_m_blocks]
   int max_m_blocks;
   // grouped-K
-  const int* expert_offsets;  // [E+1], multiples of 128
+  const int* expert_offsets;  // [E+1], multiples of 64
   int num_experts;
   int M;  // grouped-K: output rows per expert
   int N;  // output columns (per expert), multiple of 256
@@ -68,30 +80,32 @@ struct Tile {
   int expert, m0, n0, k_begin, num_kb;
 };
 
-template <bool GROUPED_K>
-__device__ __forceinline__ void decode_tile(const Params& p, int t, int num_mb, Tile& tl) {
+// Tile t of the cluster-level schedule; m0 is THIS CTA's first row (rank selects the half).
+template <bool GROUPED_K, int CG>
+__device__ __forceinline__ void decode_tile(const Params& p, int t, int num_units, int rank,
+                                            Tile& tl) {
   const int nb_count = p.N / BN;
   if constexpr (!GROUPED_K) {
     const int band = t / (BAND_M * nb_count);
     const int rem = t - band * BAND_M * nb_count;
-    const int mb0 = band * BAND_M;
-    const int rows = min(BAND_M, num_mb - mb0);
+    const int u0 = band * BAND_M;
+    const int rows = min(BAND_M, num_units - u0);
     const int nb = rem / rows;
-    const int mb = mb0 + (rem - nb * rows);
-    tl.expert = __ldg(p.block_expert + mb);
-    tl.m0 = mb * BM;
+    const int u = u0 + (rem - nb * rows);
+    tl.expert = __ldg(p.block_expert + u * CG);
+    tl.m0 = u * (BM * CG) + rank * BM;
     tl.n0 = nb * BN;
     tl.k_begin = 0;
     tl.num_kb = p.K / BK;
   } else {
-    const int mb_count = p.M / BM;
-    const int per_e = mb_count * nb_count;
+    const int mu_count = p.M / (BM * CG);
+    const int per_e = mu_count * nb_count;
     const int e = t / per_e;
     const int rem = t - e * per_e;
-    const int mb = rem / nb_count;
-    const int nb = rem - mb * nb_count;
+    const int mu = rem / nb_count;
+    const int nb = rem - mu * nb_count;
     tl.expert = e;
-    tl.m0 = mb * BM;
+    tl.m0 = mu * (BM * CG) + rank * BM;
     tl.n0 = nb * BN;
     const int r0 = __ldg(p.expert_offsets + e);
     const int r1 = __ldg(p.expert_offsets + e + 1);
@@ -102,83 +116,153 @@ __device__ __forceinline__ void decode_tile(const Params& p, int t, int num_mb, 
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
 
-template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI>
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+// TMA load whose completion bytes land on the LEADER CTA's mbarrier (pair mode).
+__device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const void* tmap,
+                                                 uint64_t* bar, int x, int y) {
+  const uint32_t bar_leader = smem_u32(bar) & 0xFEFFFFFFu;  // peer bit cleared -> CTA 0
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_leader), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Commit to the same-offset mbarrier in both CTAs of the pair.
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], m;\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+// Arrive on the leader CTA's copy of an mbarrier.
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, 0;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                         const __grid_constant__ CUtensorMap tmap_b, const Params p) {
+  using C = Cfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* smem_a = smem;
-  uint8_t* smem_b = smem + STAGES * A_STAGE_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty_bar = full_bar + STAGES;
-  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint8_t* smem_b = smem + C::STAGES * C::A_STAGE;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty_bar = full_bar + C::STAGES;
+  uint64_t* tfull_bar = empty_bar + C::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
   const int warp = warp_id();
   const int lane = lane_id();
+  const int rank = CG == 2 ? static_cast<int>(cluster_rank()) : 0;
+  const bool leader = rank == 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 4);
+      mbar_init(&tempty_bar[s], 4 * CG);
     }
     fence_mbar_init();
     fence_async_shared();
   }
-  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (CG == 1) {
+      tmem_alloc<TMEM_COLS>(tmem_slot);
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) {
+    cluster_sync_all();
+  } else {
+    __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   int num_tiles;
-  int num_mb = 0;
+  int num_units = 0;
   if constexpr (!GROUPED_K) {
-    num_mb = *p.num_m_blocks;
-    num_tiles = num_mb * (p.N / BN);
+    num_units = *p.num_m_blocks / CG;
+    num_tiles = num_units * (p.N / BN);
   } else {
-    num_tiles = p.num_experts * (p.M / BM) * (p.N / BN);
+    num_tiles = p.num_experts * (p.M / (BM * CG)) * (p.N / BN);
   }
+  const int first = blockIdx.x / CG;
+  const int stride = gridDim.x / CG;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (each CTA stages its own halves) ===============
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = first; t < num_tiles; t += stride) {
         Tile tl;
-        decode_tile<GROUPED_K>(p, t, num_mb, tl);
+        decode_tile<GROUPED_K, CG>(p, t, num_units, rank, tl);
         for (int kb = 0; kb < tl.num_kb; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full_bar[s], STAGE_BYTES);
-          uint8_t* sa = smem_a + s * A_STAGE_BYTES;
-          uint8_t* sb = smem_b + s * B_STAGE_BYTES;
+          if (leader) mbar_arrive_expect_tx(&full_bar[s], C::STAGE * CG);
+          uint8_t* sa = smem_a + s * C::A_STAGE;
+          uint8_t* sb = smem_b + s * C::B_STAGE;
           const int k = tl.k_begin + kb * BK;
+          auto load = [&](void* dst, const CUtensorMap* tm, int x, int y) {
+            if constexpr (CG == 1)
+              tma_load_2d(dst, tm, &full_bar[s], x, y);
+            else
+              tma_load_2d_pair(dst, tm, &full_bar[s], x, y);
+          };
           if constexpr (!A_MN) {
-            tma_load_2d(sa, &tmap_a, &full_bar[s], k, tl.m0);
+            load(sa, &tmap_a, k, tl.m0);
           } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j)
-              tma_load_2d(sa + j * (64 * BK * 2), &tmap_a, &full_bar[s], tl.m0 + 64 * j, k);
+            for (int j = 0; j < BM / 64; ++j) load(sa + j * (64 * BK * 2), &tmap_a, tl.m0 + 64 * j, k);
           }
+          const int nb0 = tl.n0 + rank * C::B_ROWS;
           if constexpr (!B_MN) {
-            tma_load_2d(sb, &tmap_b, &full_bar[s], k, tl.expert * p.N + tl.n0);
+            load(sb, &tmap_b, k, tl.expert * p.N + nb0);
           } else {
             const int krow = GROUPED_K ? k : tl.expert * p.K + k;
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(sb + j * (64 * BK * 2), &tmap_b, &full_bar[s], tl.n0 + 64 * j, krow);
+            for (int j = 0; j < C::B_ROWS / 64; ++j)
+              load(sb + j * (64 * BK * 2), &tmap_b, nb0 + 64 * j, krow);
           }
-          if (++s == STAGES) {
+          if (++s == C::STAGES) {
             s = 0;
             ph ^= 1;
           }
@@ -186,16 +270,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer (single thread) =====================
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+    // ===================== MMA issuer (single thread of the leader CTA) =================
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = make_idesc_bf16(BM * CG, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
       uint32_t acc_ph = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = first; t < num_tiles; t += stride) {
         Tile tl;
-        decode_tile<GROUPED_K>(p, t, num_mb, tl);
+        decode_tile<GROUPED_K, CG>(p, t, num_units, rank, tl);
         if (tl.num_kb == 0) continue;
         mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
         tc_fence_after();
@@ -203,8 +287,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < tl.num_kb; ++kb) {
           mbar_wait(&full_bar[s], ph);
           tc_fence_after();
-          const uint32_t a_base = smem_u32(smem_a + s * A_STAGE_BYTES);
-          const uint32_t b_base = smem_u32(smem_b + s * B_STAGE_BYTES);
+          const uint32_t a_base = smem_u32(smem_a + s * C::A_STAGE);
+          const uint32_t b_base = smem_u32(smem_b + s * C::B_STAGE);
 #pragma unroll
           for (int kk = 0; kk < BK / UMMA_K; ++kk) {
             const uint64_t adesc =
@@ -213,15 +297,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t bdesc =
                 B_MN ? make_sdesc_sw128(b_base + kk * (UMMA_K * 128), 64 * BK * 2, 1024)
                      : make_sdesc_sw128(b_base + kk * (UMMA_K * 2), 16, 1024);
-            umma_bf16(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
+            if constexpr (CG == 1)
+              umma_bf16(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
+            else
+              umma_bf16_pair(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
           }
-          umma_commit(&empty_bar[s]);
-          if (++s == STAGES) {
+          if constexpr (CG == 1)
+            umma_commit(&empty_bar[s]);
+          else
+            umma_commit_pair(&empty_bar[s]);
+          if (++s == C::STAGES) {
             s = 0;
             ph ^= 1;
           }
         }
-        umma_commit(&tfull_bar[acc]);
+        if constexpr (CG == 1)
+          umma_commit(&tfull_bar[acc]);
+        else
+          umma_commit_pair(&tfull_bar[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_ph ^= 1;
@@ -235,9 +328,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     int acc = 0;
     uint32_t acc_ph = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int t = first; t < num_tiles; t += stride) {
       Tile tl;
-      decode_tile<GROUPED_K>(p, t, num_mb, tl);
+      decode_tile<GROUPED_K, CG>(p, t, num_units, rank, tl);
       const long long row = tl.m0 + row_local;
       if (tl.num_kb == 0) {
         // Expert with no rows: its weight gradient is exactly zero.
@@ -370,7 +463,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 1)
+          mbar_arrive(&tempty_bar[acc]);
+        else
+          mbar_arrive_leader(&tempty_bar[acc]);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_ph ^= 1;
@@ -379,10 +477,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) {
+    cluster_sync_all();
+  } else {
+    __syncthreads();
+  }
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<TMEM_COLS>(tmem_base);
+    if constexpr (CG == 1) {
+      tmem_dealloc<TMEM_COLS>(tmem_base);
+    } else {
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(TMEM_COLS)
+                   : "memory");
+    }
   }
 }
 
@@ -429,26 +537,52 @@ static int num_sms() {
   return n;
 }
 
-template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI>
-static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int max_tiles,
-                  cudaStream_t stream) {
-  auto kern = grouped_gemm_kernel<A_MN, B_MN, GROUPED_K, EPI>;
+template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI, int CG>
+static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
+                     int max_tiles, cudaStream_t stream) {
+  auto kern = grouped_gemm_kernel<A_MN, B_MN, GROUPED_K, EPI, CG>;
   static bool attr_set = false;
   if (!attr_set) {
-    MOE_CUDA_CHECK(
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    MOE_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        Cfg<CG>::SMEM));
     attr_set = true;
   }
   if (max_tiles <= 0) return kOk;
-  const int grid = max_tiles < num_sms() ? max_tiles : num_sms();
-  kern<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ta, tb, p);
-  MOE_LAUNCH_CHECK();
+  int grid = max_tiles * CG < num_sms() ? max_tiles * CG : num_sms();
+  grid -= grid % CG;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = Cfg<CG>::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MOE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
   return kOk;
 }
 
-static Params base_params() {
-  Params p{};
-  return p;
+// flags bit 0: CTA-pair engine (grouped-M: expert blocks 256-row aligned).
+constexpr int kFlagPair = 1;
+
+// Builds tensor maps for the chosen engine and launches. a_inner/a_outer/b_* describe the
+// 2-D global views; a/b K-major (box {64, rows}) or MN-major (box {64, 64}).
+template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI>
+static int run(const void* a, uint64_t a_inner, uint64_t a_outer, const void* b,
+               uint64_t b_inner, uint64_t b_outer, Params p, int units_m, int pair,
+               cudaStream_t stream) {
+  CUtensorMap ta, tb;
+  int st;
+  const int cg = pair ? 2 : 1;
+  if ((st = make_tmap(&ta, a, a_inner, a_outer, a_inner, 64, A_MN ? BK : BM))) return st;
+  if ((st = make_tmap(&tb, b, b_inner, b_outer, b_inner, 64, B_MN ? BK : BN / cg))) return st;
+  const int nb = p.N / BN;
+  if (pair) return launch_cg<A_MN, B_MN, GROUPED_K, EPI, 2>(ta, tb, p, (units_m / 2) * nb, stream);
+  return launch_cg<A_MN, B_MN, GROUPED_K, EPI, 1>(ta, tb, p, units_m * nb, stream);
 }
 
 }  // namespace gg
@@ -459,20 +593,18 @@ using namespace moe::gg;
 
 extern "C" {
 
-// fc1 forward + SwiGLU.  xp[rows, h] (expert-major, 128-row padded), w1[E, 2m, h] with
+// fc1 forward + SwiGLU.  xp[rows, h] (expert-major, padded plan), w1[E, 2m, h] with
 // gate/up interleaved in 128-row blocks.  Writes preact[rows, 2m] (interleaved) and
 // act[rows, m] = silu(gate) * up (* row_prob[row] when row_prob != NULL).
 // a_rows: physical rows of xp (TMA bound; rows beyond read as zero), max_rows: rows of the
-// output buffers (multiple of 128).
+// output buffers (multiple of 128; of 256 with the pair flag).
 int moe_gg_fc1_fwd(const void* xp, const void* w1, int a_rows, int max_rows, int h, int m,
                    int num_experts, const int* block_expert, const int* num_m_blocks,
-                   const float* row_prob, void* preact, void* act, void* stream) {
-  if (h % BK || (2 * m) % BN || max_rows % BM || a_rows > max_rows) return kErrInvalidArg;
-  CUtensorMap ta, tb;
-  int st;
-  if ((st = make_tmap(&ta, xp, h, a_rows, h, BK, BM))) return st;
-  if ((st = make_tmap(&tb, w1, h, (uint64_t)num_experts * 2 * m, h, BK, BN))) return st;
-  Params p = base_params();
+                   const float* row_prob, void* preact, void* act, int flags, void* stream) {
+  const int pair = flags & kFlagPair;
+  if (h % BK || (2 * m) % BN || max_rows % (BM * (pair ? 2 : 1)) || a_rows > max_rows)
+    return kErrInvalidArg;
+  Params p{};
   p.num_m_blocks = num_m_blocks;
   p.block_expert = block_expert;
   p.max_m_blocks = max_rows / BM;
@@ -484,20 +616,19 @@ int moe_gg_fc1_fwd(const void* xp, const void* w1, int a_rows, int max_rows, int
   p.out2 = act;
   p.ldo2 = m;
   p.row_scale = row_prob;
-  return launch<false, false, false, EPI_SWIGLU>(ta, tb, p, p.max_m_blocks * (p.N / BN),
-                                                 static_cast<cudaStream_t>(stream));
+  return run<false, false, false, EPI_SWIGLU>(xp, h, a_rows, w1, h, (uint64_t)num_experts * 2 * m,
+                                              p, p.max_m_blocks, pair,
+                                              static_cast<cudaStream_t>(stream));
 }
 
 // fc2 forward: out[rows, h] = act[rows, m] * w2_e^T, w2[E, h, m].
 int moe_gg_fc2_fwd(const void* act, const void* w2, int a_rows, int max_rows, int m, int h,
                    int num_experts, const int* block_expert, const int* num_m_blocks, void* out,
-                   void* stream) {
-  if (m % BK || h % BN || max_rows % BM || a_rows > max_rows) return kErrInvalidArg;
-  CUtensorMap ta, tb;
-  int st;
-  if ((st = make_tmap(&ta, act, m, a_rows, m, BK, BM))) return st;
-  if ((st = make_tmap(&tb, w2, m, (uint64_t)num_experts * h, m, BK, BN))) return st;
-  Params p = base_params();
+                   int flags, void* stream) {
+  const int pair = flags & kFlagPair;
+  if (m % BK || h % BN || max_rows % (BM * (pair ? 2 : 1)) || a_rows > max_rows)
+    return kErrInvalidArg;
+  Params p{};
   p.num_m_blocks = num_m_blocks;
   p.block_expert = block_expert;
   p.max_m_blocks = max_rows / BM;
@@ -506,8 +637,9 @@ int moe_gg_fc2_fwd(const void* act, const void* w2, int a_rows, int max_rows, in
   p.K = m;
   p.out = out;
   p.ldo = h;
-  return launch<false, false, false, EPI_BF16>(ta, tb, p, p.max_m_blocks * (p.N / BN),
-                                               static_cast<cudaStream_t>(stream));
+  return run<false, false, false, EPI_BF16>(act, m, a_rows, w2, m, (uint64_t)num_experts * h, p,
+                                            p.max_m_blocks, pair,
+                                            static_cast<cudaStream_t>(stream));
 }
 
 // fc2 data-gradient fused with the SwiGLU backward.
@@ -517,13 +649,11 @@ int moe_gg_fc2_fwd(const void* act, const void* w2, int a_rows, int max_rows, in
 int moe_gg_fc2_dgrad(const void* dout, const void* w2, const void* preact, int a_rows,
                      int max_rows, int h, int m, int num_experts, const int* block_expert,
                      const int* num_m_blocks, const float* row_prob, void* d_preact,
-                     float* dprob_partial, void* stream) {
-  if (h % BK || m % BN || max_rows % BM || a_rows > max_rows) return kErrInvalidArg;
-  CUtensorMap ta, tb;
-  int st;
-  if ((st = make_tmap(&ta, dout, h, a_rows, h, BK, BM))) return st;
-  if ((st = make_tmap(&tb, w2, m, (uint64_t)num_experts * h, m, 64, BK))) return st;
-  Params p = base_params();
+                     float* dprob_partial, int flags, void* stream) {
+  const int pair = flags & kFlagPair;
+  if (h % BK || m % BN || max_rows % (BM * (pair ? 2 : 1)) || a_rows > max_rows)
+    return kErrInvalidArg;
+  Params p{};
   p.num_m_blocks = num_m_blocks;
   p.block_expert = block_expert;
   p.max_m_blocks = max_rows / BM;
@@ -537,20 +667,19 @@ int moe_gg_fc2_dgrad(const void* dout, const void* w2, const void* preact, int a
   p.row_scale = row_prob;
   p.row_partial = dprob_partial;
   p.ld_partial = m / BN;
-  return launch<false, true, false, EPI_DSWIGLU>(ta, tb, p, p.max_m_blocks * (p.N / BN),
-                                                 static_cast<cudaStream_t>(stream));
+  return run<false, true, false, EPI_DSWIGLU>(dout, h, a_rows, w2, m, (uint64_t)num_experts * h,
+                                              p, p.max_m_blocks, pair,
+                                              static_cast<cudaStream_t>(stream));
 }
 
 // fc1 data-gradient: dxp[rows, h] = d_preact[rows, 2m] * w1_e  (w1[E, 2m, h] read MN-major).
 int moe_gg_fc1_dgrad(const void* d_preact, const void* w1, int a_rows, int max_rows, int m,
                      int h, int num_experts, const int* block_expert, const int* num_m_blocks,
-                     void* dxp, void* stream) {
-  if ((2 * m) % BK || h % BN || max_rows % BM || a_rows > max_rows) return kErrInvalidArg;
-  CUtensorMap ta, tb;
-  int st;
-  if ((st = make_tmap(&ta, d_preact, 2 * m, a_rows, 2 * m, BK, BM))) return st;
-  if ((st = make_tmap(&tb, w1, h, (uint64_t)num_experts * 2 * m, h, 64, BK))) return st;
-  Params p = base_params();
+                     void* dxp, int flags, void* stream) {
+  const int pair = flags & kFlagPair;
+  if ((2 * m) % BK || h % BN || max_rows % (BM * (pair ? 2 : 1)) || a_rows > max_rows)
+    return kErrInvalidArg;
+  Params p{};
   p.num_m_blocks = num_m_blocks;
   p.block_expert = block_expert;
   p.max_m_blocks = max_rows / BM;
@@ -559,21 +688,19 @@ int moe_gg_fc1_dgrad(const void* d_preact, const void* w1, int a_rows, int max_r
   p.K = 2 * m;
   p.out = dxp;
   p.ldo = h;
-  return launch<false, true, false, EPI_BF16>(ta, tb, p, p.max_m_blocks * (p.N / BN),
-                                              static_cast<cudaStream_t>(stream));
+  return run<false, true, false, EPI_BF16>(d_preact, 2 * m, a_rows, w1, h,
+                                           (uint64_t)num_experts * 2 * m, p, p.max_m_blocks,
+                                           pair, static_cast<cudaStream_t>(stream));
 }
 
 // Weight gradient with the reduction over each expert's token rows:
 //   dw[e, M, N] = sum_{r in [off[e], off[e+1])} a[r, 0:M]^T b[r, 0:N]
-// a[rows, M], b[rows, N] row-major (read MN-major); off[] multiples of 128.
+// a[rows, M], b[rows, N] row-major (read MN-major); off[] multiples of 64; rows >= max_rows
+// read as zero. Uses the CTA-pair engine whenever M % 256 == 0.
 int moe_gg_wgrad(const void* a, const void* b, int max_rows, int M, int N, int num_experts,
                  const int* expert_offsets, void* dw, void* stream) {
   if (M % BM || N % BN) return kErrInvalidArg;
-  CUtensorMap ta, tb;
-  int st;
-  if ((st = make_tmap(&ta, a, M, max_rows, M, 64, BK))) return st;
-  if ((st = make_tmap(&tb, b, N, max_rows, N, 64, BK))) return st;
-  Params p = base_params();
+  Params p{};
   p.expert_offsets = expert_offsets;
   p.num_experts = num_experts;
   p.M = M;
@@ -581,21 +708,18 @@ int moe_gg_wgrad(const void* a, const void* b, int max_rows, int M, int N, int n
   p.out = dw;
   p.ldo = N;
   p.out_expert_stride = (long long)M * N;
-  return launch<true, true, true, EPI_BF16>(ta, tb, p, num_experts * (M / BM) * (N / BN),
-                                            static_cast<cudaStream_t>(stream));
+  const int pair = (M % (2 * BM)) == 0;
+  return run<true, true, true, EPI_BF16>(a, M, max_rows, b, N, max_rows, p,
+                                         num_experts * (M / BM), pair,
+                                         static_cast<cudaStream_t>(stream));
 }
 
 // Same as moe_gg_wgrad with fp32 output (split-K partials of the router weight gradient:
-// "experts" are token chunks). Rows beyond max_rows read as zero (TMA OOB fill), so offsets
-// may run to the next multiple of 64 past the last valid row.
+// "experts" are token chunks).
 int moe_gg_wgrad_f32(const void* a, const void* b, int max_rows, int M, int N, int num_groups,
                      const int* offsets, float* dw, void* stream) {
   if (M % BM || N % BN) return kErrInvalidArg;
-  CUtensorMap ta, tb;
-  int st;
-  if ((st = make_tmap(&ta, a, M, max_rows, M, 64, BK))) return st;
-  if ((st = make_tmap(&tb, b, N, max_rows, N, 64, BK))) return st;
-  Params p = base_params();
+  Params p{};
   p.expert_offsets = offsets;
   p.num_experts = num_groups;
   p.M = M;
@@ -603,8 +727,10 @@ int moe_gg_wgrad_f32(const void* a, const void* b, int max_rows, int M, int N, i
   p.out = dw;
   p.ldo = N;
   p.out_expert_stride = (long long)M * N;
-  return launch<true, true, true, EPI_F32>(ta, tb, p, num_groups * (M / BM) * (N / BN),
-                                           static_cast<cudaStream_t>(stream));
+  const int pair = (M % (2 * BM)) == 0;
+  return run<true, true, true, EPI_F32>(a, M, max_rows, b, N, max_rows, p,
+                                        num_groups * (M / BM), pair,
+                                        static_cast<cudaStream_t>(stream));
 }
 
 // Plain grouped-M GEMM with fp32 output (router logits / tests): out[rows, N] = a * b_e^T.
@@ -613,11 +739,7 @@ int moe_gg_gemm_f32(const void* a, const void* b, int a_rows, int max_rows, int 
                     int num_experts, const int* block_expert, const int* num_m_blocks, float* out,
                     void* stream) {
   if (K % BK || N % BN || max_rows % BM || a_rows > max_rows) return kErrInvalidArg;
-  CUtensorMap ta, tb;
-  int st;
-  if ((st = make_tmap(&ta, a, K, a_rows, K, BK, BM))) return st;
-  if ((st = make_tmap(&tb, b, K, (uint64_t)num_experts * N, K, BK, BN))) return st;
-  Params p = base_params();
+  Params p{};
   p.num_m_blocks = num_m_blocks;
   p.block_expert = block_expert;
   p.max_m_blocks = max_rows / BM;
@@ -626,8 +748,8 @@ int moe_gg_gemm_f32(const void* a, const void* b, int a_rows, int max_rows, int 
   p.K = K;
   p.out = out;
   p.ldo = N;
-  return launch<false, false, false, EPI_F32>(ta, tb, p, p.max_m_blocks * (p.N / BN),
-                                              static_cast<cudaStream_t>(stream));
+  return run<false, false, false, EPI_F32>(a, K, a_rows, b, K, (uint64_t)num_experts * N, p,
+                                           p.max_m_blocks, 0, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -124,12 +124,12 @@ __global__ void offsets_kernel(const int* __restrict__ count, int E, int capacit
     off_c[0] = 0;
     const int tot = s_pad[E - 1];
     if (tot > max_rows) atomicOr(status, 2);
-    meta[0] = align == ALIGN ? min(tot, max_rows) / ALIGN : 0;
+    meta[0] = align >= ALIGN ? min(tot, max_rows) / ALIGN : 0;
     meta[1] = tot;
     meta[2] = s_c[E - 1];
   }
   __syncthreads();
-  if (e < E && block_expert && align == ALIGN) {
+  if (e < E && block_expert && align >= ALIGN) {
     const int b0 = (e ? s_pad[e - 1] : 0) / ALIGN;
     const int b1 = min(s_pad[e], max_rows) / ALIGN;
     for (int b = b0; b < b1; ++b) block_expert[b] = e;
@@ -473,8 +473,8 @@ int moe_permute_plan(const int* topk_idx, const float* topk_prob, int T, int K, 
                      int* counts, int* block_expert, int* inv_map, int* row_src,
                      float* row_prob, int* workspace, int* status, void* stream) {
   if (E < 1 || E > 1024 || K < 1 || K > 32) return kErrInvalidArg;
-  if (align != 1 && align != ALIGN) return kErrInvalidArg;
-  if (align == ALIGN && max_rows % ALIGN) return kErrInvalidArg;
+  if (align != 1 && align != ALIGN && align != 2 * ALIGN) return kErrInvalidArg;
+  if (align >= ALIGN && max_rows % align) return kErrInvalidArg;
   auto st = static_cast<cudaStream_t>(stream);
   const int W = ceil_div_i(T > 0 ? T : 1, 32);
   int* hist = workspace;
@@ -505,7 +505,7 @@ int moe_permute_plan(const int* topk_idx, const float* topk_prob, int T, int K, 
                                                            inv_map, row_src, row_prob);
     MOE_LAUNCH_CHECK();
   }
-  if (align == ALIGN && block_expert) {
+  if (align >= ALIGN && block_expert) {
     pad_rows_kernel<<<sms() * 4, 256, 0, st>>>(meta, block_expert, off_pad, kept, row_src,
                                                 row_prob);
     MOE_LAUNCH_CHECK();

@@ -96,7 +96,8 @@ def ep_host_plan(counts_all: np.ndarray, rank: int, capacity: int = -1,
     padded = -(-eff // align) * align
     off_pad = np.concatenate([[0], np.cumsum(padded)]).astype(np.int64)
     rows_pad = int(off_pad[-1])
-    block_expert = np.repeat(np.arange(el), padded // align) if align == ops.ALIGN else (
+    # one entry per 128-row GEMM block (also for 256-row aligned plans)
+    block_expert = np.repeat(np.arange(el), padded // ops.ALIGN) if align >= ops.ALIGN else (
         np.zeros(0, dtype=np.int64))
     table = np.concatenate([kept_mine.ravel(), recv_off.ravel(), off_pad, real]).astype(np.int32)
     return EPHostPlan(n, rank, el, kept, cap_local, send_splits, recv_splits, table, off_pad,
@@ -148,7 +149,7 @@ class _Exchange:
         self.off_pad = self.table[2 * n * el: 2 * n * el + el + 1]
         self.block_expert = tab[nt: nt + hp.block_expert.size]
         self.num_m_blocks = tab[nt + hp.block_expert.size:]
-        self.rows_alloc = max(hp.rows_pad, ops.ALIGN)
+        self.rows_alloc = max(hp.rows_pad, 2 * ops.ALIGN)
         self.total_recv = int(sum(hp.recv_splits))
         self.total_send = int(sum(hp.send_splits))
         i32 = dict(dtype=torch.int32, device=dev)
@@ -198,7 +199,9 @@ class _MoEEPFunction(torch.autograd.Function):
         g = gathered.cpu().numpy()  # the one host sync of the EP forward
         counts_all = np.rint(g[:, :E]).astype(np.int64)
         cap = cfg.capacity(n * t)  # global capacity on the global batch
-        hp = ep_host_plan(counts_all, ep.rank, cap, cfg.pad_to_capacity)
+        align = ops.pick_align(n * t, K, E)
+        hp = ep_host_plan(counts_all, ep.rank, cap, cfg.pad_to_capacity, align)
+        pair = align == 2 * ops.ALIGN
         aux_v, aux_g = global_aux(counts_all, g[:, E:], t, K, cfg.aux_loss_coeff)
         small = torch.from_numpy(np.concatenate([[aux_v], aux_g]).astype(np.float32))
         small = small.pin_memory().to(dev, non_blocking=True)
@@ -221,8 +224,9 @@ class _MoEEPFunction(torch.autograd.Function):
             row_prob = torch.where(mp >= 0, prob_recv[mp.clamp(min=0)] if xc.total_recv else
                                    torch.zeros_like(mp, dtype=torch.float32),
                                    torch.zeros((), device=dev)).float().contiguous()
-        preact, act = gemm.fc1_fwd(xp, w1, xc.block_expert, xc.num_m_blocks, row_prob)
-        o = gemm.fc2_fwd(act, w2, xc.block_expert, xc.num_m_blocks)
+        preact, act = gemm.fc1_fwd(xp, w1, xc.block_expert, xc.num_m_blocks, row_prob,
+                                   pair=pair)
+        o = gemm.fc2_fwd(act, w2, xc.block_expert, xc.num_m_blocks, pair=pair)
         o_local = xc.a2a(xc.from_padded(o), False, ep.group)
         shared = shared_expert_forward(x, w1s, w2s) if w1s is not None else None
         y = ops.combine(o_local, splan, None if cfg.mem_efficient else r.topk_prob,
@@ -230,6 +234,7 @@ class _MoEEPFunction(torch.autograd.Function):
                         extra=shared[-1] if shared is not None else None)
         ctx.cfg, ctx.ep, ctx.r, ctx.splan, ctx.xc, ctx.cap = cfg, ep, r, splan, xc, cap
         ctx.row_prob = row_prob
+        ctx.pair = pair
         ctx.shared = shared[:-1] if shared is not None else None
         ctx.save_for_backward(x, w_r_pad, w1, w2, xp, preact, act, o_local, w1s, w2s)
         return y, aux
@@ -250,7 +255,7 @@ class _MoEEPFunction(torch.autograd.Function):
         d_o = xc.to_padded(xc.a2a(d_send[: xc.total_send], True, ep.group))
         if cfg.mem_efficient:
             d_pre, part = gemm.fc2_dgrad(d_o, w2, preact, xc.block_expert, xc.num_m_blocks,
-                                         row_prob=ctx.row_prob, want_dprob=True)
+                                         row_prob=ctx.row_prob, want_dprob=True, pair=ctx.pair)
             dp_pad = part.sum(dim=1)
             dp_recv = dp_pad[xc.map_recv.long()] if xc.total_recv else dp_pad[:0]
             dp_send = xc.a2a(dp_recv.contiguous(), False, ep.group)
@@ -259,9 +264,10 @@ class _MoEEPFunction(torch.autograd.Function):
                                 torch.zeros_like(inv, dtype=torch.float32),
                                 torch.zeros((), device=dev)).float().contiguous()
         else:
-            d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, xc.block_expert, xc.num_m_blocks)
+            d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, xc.block_expert, xc.num_m_blocks,
+                                      pair=ctx.pair)
         dw2 = gemm.wgrad(d_o, act, xc.off_pad, el)
-        dxp = gemm.fc1_dgrad(d_pre, w1, xc.block_expert, xc.num_m_blocks)
+        dxp = gemm.fc1_dgrad(d_pre, w1, xc.block_expert, xc.num_m_blocks, pair=ctx.pair)
         dw1 = gemm.wgrad(d_pre, xp, xc.off_pad, el)
         dxp_local = xc.a2a(xc.from_padded(dxp), False, ep.group)
         aux_scale = None if daux is None else daux.float()

@@ -55,7 +55,7 @@ def deinterleave_cols(preact: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]
 
 
 def fc1_fwd(xp, w1, block_expert, num_m_blocks, row_prob=None, preact=None, act=None,
-            max_rows=None):
+            max_rows=None, pair=False):
     a_rows, h = xp.shape
     rows = a_rows if max_rows is None else max_rows
     e, m2, _ = w1.shape
@@ -66,23 +66,24 @@ def fc1_fwd(xp, w1, block_expert, num_m_blocks, row_prob=None, preact=None, act=
         act = torch.empty((rows, m), dtype=torch.bfloat16, device=xp.device)
     _lib.call("moe_gg_fc1_fwd", xp.data_ptr(), w1.data_ptr(), a_rows, rows, h, m, e,
               block_expert.data_ptr(), num_m_blocks.data_ptr(), _ptr(row_prob),
-              preact.data_ptr(), act.data_ptr(), _stream())
+              preact.data_ptr(), act.data_ptr(), int(pair), _stream())
     return preact, act
 
 
-def fc2_fwd(act, w2, block_expert, num_m_blocks, out=None, max_rows=None):
+def fc2_fwd(act, w2, block_expert, num_m_blocks, out=None, max_rows=None, pair=False):
     a_rows, m = act.shape
     rows = a_rows if max_rows is None else max_rows
     e, h, _ = w2.shape
     if out is None:
         out = torch.empty((rows, h), dtype=torch.bfloat16, device=act.device)
     _lib.call("moe_gg_fc2_fwd", act.data_ptr(), w2.data_ptr(), a_rows, rows, m, h, e,
-              block_expert.data_ptr(), num_m_blocks.data_ptr(), out.data_ptr(), _stream())
+              block_expert.data_ptr(), num_m_blocks.data_ptr(), out.data_ptr(), int(pair),
+              _stream())
     return out
 
 
 def fc2_dgrad(dout, w2, preact, block_expert, num_m_blocks, row_prob=None, want_dprob=False,
-              d_preact=None, max_rows=None):
+              d_preact=None, max_rows=None, pair=False):
     a_rows, h = dout.shape
     rows = a_rows if max_rows is None else max_rows
     e, _, m = w2.shape
@@ -93,18 +94,19 @@ def fc2_dgrad(dout, w2, preact, block_expert, num_m_blocks, row_prob=None, want_
         part = torch.empty((rows, m // 256), dtype=torch.float32, device=dout.device)
     _lib.call("moe_gg_fc2_dgrad", dout.data_ptr(), w2.data_ptr(), preact.data_ptr(), a_rows, rows,
               h, m, e, block_expert.data_ptr(), num_m_blocks.data_ptr(), _ptr(row_prob),
-              d_preact.data_ptr(), _ptr(part), _stream())
+              d_preact.data_ptr(), _ptr(part), int(pair), _stream())
     return d_preact, part
 
 
-def fc1_dgrad(d_preact, w1, block_expert, num_m_blocks, out=None, max_rows=None):
+def fc1_dgrad(d_preact, w1, block_expert, num_m_blocks, out=None, max_rows=None, pair=False):
     a_rows, m2 = d_preact.shape
     rows = a_rows if max_rows is None else max_rows
     e, _, h = w1.shape
     if out is None:
         out = torch.empty((rows, h), dtype=torch.bfloat16, device=d_preact.device)
     _lib.call("moe_gg_fc1_dgrad", d_preact.data_ptr(), w1.data_ptr(), a_rows, rows, m2 // 2, h, e,
-              block_expert.data_ptr(), num_m_blocks.data_ptr(), out.data_ptr(), _stream())
+              block_expert.data_ptr(), num_m_blocks.data_ptr(), out.data_ptr(), int(pair),
+              _stream())
     return out
 
 
@@ -130,7 +132,8 @@ def gemm_f32(a, b, block_expert, num_m_blocks, out=None, max_rows=None):
     if out is None:
         out = torch.empty((rows, N), dtype=torch.float32, device=a.device)
     _lib.call("moe_gg_gemm_f32", a.data_ptr(), b.data_ptr(), a_rows, rows, K, N, e,
-              block_expert.data_ptr(), num_m_blocks.data_ptr(), out.data_ptr(), _stream())
+              block_expert.data_ptr(), num_m_blocks.data_ptr(), out.data_ptr(), int(pair),
+              _stream())
     return out
 
 

@@ -51,11 +51,13 @@ class _MoEFunction(torch.autograd.Function):
         r = ops.router_forward(x, w_r, cfg.top_k, cfg.score, sel_bias, cfg.aux_loss_coeff,
                                w_r_t=w_r_t)
         cap = cfg.capacity(t)
-        plan = ops.build_plan(r.topk_idx, r.topk_prob, e, cap, cfg.pad_to_capacity)
+        plan = ops.build_plan(r.topk_idx, r.topk_prob, e, cap, cfg.pad_to_capacity,
+                              align=ops.pick_align(t, cfg.top_k, e))
         xp = ops.permute_gather(x, plan)
         row_prob = plan.row_prob if cfg.mem_efficient else None
-        preact, act = gemm.fc1_fwd(xp, w1, plan.block_expert, plan.num_m_blocks, row_prob)
-        o = gemm.fc2_fwd(act, w2, plan.block_expert, plan.num_m_blocks)
+        preact, act = gemm.fc1_fwd(xp, w1, plan.block_expert, plan.num_m_blocks, row_prob,
+                                   pair=plan.pair)
+        o = gemm.fc2_fwd(act, w2, plan.block_expert, plan.num_m_blocks, pair=plan.pair)
         shared = shared_expert_forward(x, w1s, w2s) if w1s is not None else None
         y = ops.combine(o, plan, None if cfg.mem_efficient else r.topk_prob,
                         resid=x if cap >= 0 else None,
@@ -76,13 +78,15 @@ class _MoEFunction(torch.autograd.Function):
         if cfg.mem_efficient:
             d_o, _ = ops.combine_backward(dy, plan, None, None)
             d_pre, part = gemm.fc2_dgrad(d_o, w2, preact, plan.block_expert, plan.num_m_blocks,
-                                         row_prob=plan.row_prob, want_dprob=True)
+                                         row_prob=plan.row_prob, want_dprob=True,
+                                         pair=plan.pair)
             dprob = ops.dprob_from_partials(plan, part)
         else:
             d_o, dprob = ops.combine_backward(dy, plan, o, r.topk_prob)
-            d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, plan.block_expert, plan.num_m_blocks)
+            d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, plan.block_expert, plan.num_m_blocks,
+                                      pair=plan.pair)
         dw2 = gemm.wgrad(d_o, act, plan.off_pad, e)
-        dxp = gemm.fc1_dgrad(d_pre, w1, plan.block_expert, plan.num_m_blocks)
+        dxp = gemm.fc1_dgrad(d_pre, w1, plan.block_expert, plan.num_m_blocks, pair=plan.pair)
         dw1 = gemm.wgrad(d_pre, xp, plan.off_pad, e)
         aux_scale = None if daux is None else daux.float()
         dw_r, dx_router = ops.router_backward(x, w_r_pad, r, dprob, cfg.score,

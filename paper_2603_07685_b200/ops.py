@@ -161,27 +161,40 @@ class Plan:
     row_src: torch.Tensor       # [max_rows] source token or -1
     row_prob: torch.Tensor      # [max_rows] fp32
     status: torch.Tensor        # [1] bit1 = overflow of max_rows
+    align: int = ALIGN          # expert block alignment (256: CTA-pair GEMM engine)
 
     @property
     def num_m_blocks(self) -> torch.Tensor:
         return self.meta[0:1]
 
+    @property
+    def pair(self) -> bool:
+        return self.align == 2 * ALIGN
 
-def plan_max_rows(T: int, K: int, E: int, capacity: int = -1, pad: bool = False) -> int:
+
+def plan_max_rows(T: int, K: int, E: int, capacity: int = -1, pad: bool = False,
+                  align: int = ALIGN) -> int:
     """Static upper bound of the padded plan's rows (buffer sizing, no host sync)."""
     if capacity < 0:
-        bound = T * K + E * (ALIGN - 1)
+        bound = T * K + E * (align - 1)
     elif pad:
-        bound = E * ceil_to(capacity, ALIGN)
+        bound = E * ceil_to(capacity, align)
     else:
-        bound = min(T * K, E * capacity) + E * (ALIGN - 1)
-    return max(ceil_to(bound, ALIGN), ALIGN)
+        bound = min(T * K, E * capacity) + E * (align - 1)
+    return max(ceil_to(bound, align), align)
+
+
+def pick_align(T: int, K: int, E: int) -> int:
+    """256-row expert blocks (CTA-pair GEMM engine) when experts are large enough that the
+    extra padding is negligible; 128 otherwise (e.g. DeepSeek-shape at EP=1, ~128 rows)."""
+    return 2 * ALIGN if T * K >= 8 * 2 * ALIGN * E else ALIGN
 
 
 def build_plan(topk_idx: torch.Tensor, topk_prob: torch.Tensor | None, E: int,
                capacity: int = -1, pad: bool = False, max_rows: int | None = None,
                phantom: torch.Tensor | None = None, phantom_max: int = 0,
-               cap_e: torch.Tensor | None = None, compact: bool = False) -> Plan:
+               cap_e: torch.Tensor | None = None, compact: bool = False,
+               align: int = ALIGN) -> Plan:
     """phantom: optional device int32 [E] extra zero rows per expert (routing_map_pad);
     phantom_max bounds it for buffer sizing. cap_e: optional device int32 [E] per-expert
     capacity (EP global-position drops). compact: no 128-row alignment (EP send layout)."""
@@ -191,7 +204,8 @@ def build_plan(topk_idx: torch.Tensor, topk_prob: torch.Tensor | None, E: int,
         if compact:
             max_rows = max(t * k, 1)
         else:
-            max_rows = plan_max_rows(t, k, E, capacity, pad) + ceil_to(E * phantom_max, ALIGN)
+            max_rows = (plan_max_rows(t, k, E, capacity, pad, align)
+                        + ceil_to(E * phantom_max, align))
     i32 = dict(dtype=torch.int32, device=dev)
     meta = torch.empty((3,), **i32)
     off_pad = torch.empty((E + 1,), **i32)
@@ -206,13 +220,14 @@ def build_plan(topk_idx: torch.Tensor, topk_prob: torch.Tensor | None, E: int,
     ws = torch.empty((max(int(_lib.query("moe_permute_workspace_ints", t, k, E)), 1),), **i32)
     status = torch.empty((1,), **i32)
     _lib.call("moe_permute_plan", topk_idx.data_ptr(), _p(topk_prob), t, k, E, int(capacity),
-              _p(cap_e), int(bool(pad)), _p(phantom), 1 if compact else ALIGN, max_rows,
+              _p(cap_e), int(bool(pad)), _p(phantom), 1 if compact else align, max_rows,
               meta.data_ptr(), off_pad.data_ptr(), off_c.data_ptr(), kept.data_ptr(),
               eff.data_ptr(), counts.data_ptr(), _p(block_expert), inv_map.data_ptr(),
               row_src.data_ptr(), row_prob.data_ptr(), ws.data_ptr(), status.data_ptr(),
               _stream())
     return Plan(t, k, E, int(capacity), bool(pad), max_rows, meta, off_pad, off_c, kept, eff,
-                counts, block_expert, inv_map, row_src, row_prob, status)
+                counts, block_expert, inv_map, row_src, row_prob, status,
+                1 if compact else align)
 
 
 def compact_row_id_map(plan: Plan, n_compact: int | None = None):

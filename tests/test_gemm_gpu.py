@@ -7,16 +7,19 @@ pytestmark = pytest.mark.gpu
 from paper_2603_07685_b200 import gemm  # noqa: E402
 
 
+ALIGN = 128  # set per test by the `pair` fixture (256 for the CTA-pair engine)
+
+
 def _layout(counts, device):
     """Padded expert-major layout metadata for given per-expert row counts."""
     offs = [0]
     block_expert = []
     for e, c in enumerate(counts):
-        nb = (c + 127) // 128
+        nb = (c + ALIGN - 1) // ALIGN * (ALIGN // 128)
         block_expert += [e] * nb
         offs.append(offs[-1] + nb * 128)
     rows = offs[-1]
-    max_rows = rows + 256  # slack: buffers sized by an upper bound
+    max_rows = rows + 512  # slack: buffers sized by an upper bound
     be = torch.zeros(max_rows // 128, dtype=torch.int32)
     be[: len(block_expert)] = torch.tensor(block_expert, dtype=torch.int32)
     return (torch.tensor(offs, dtype=torch.int32, device=device), be.to(device),
@@ -24,7 +27,7 @@ def _layout(counts, device):
 
 
 def _rows(counts, offs_host, width, device, gen):
-    x = torch.zeros((offs_host[-1] + 256, width), dtype=torch.bfloat16, device=device)
+    x = torch.zeros((offs_host[-1] + 512, width), dtype=torch.bfloat16, device=device)
     for e, c in enumerate(counts):
         x[offs_host[e]: offs_host[e] + c] = torch.randn((c, width), generator=gen).to(device, torch.bfloat16)
     return x
@@ -41,17 +44,25 @@ def dev():
     return torch.device("cuda:0")
 
 
+@pytest.fixture(params=[False, True], ids=["cta1", "cta_pair"])
+def pair(request):
+    global ALIGN
+    ALIGN = 256 if request.param else 128
+    yield request.param
+    ALIGN = 128
+
+
 COUNTS = [200, 0, 333, 128, 1]
 
 
-def test_fc2_fwd_plain(dev):
+def test_fc2_fwd_plain(dev, pair):
     g = torch.Generator().manual_seed(0)
     E, m, h = len(COUNTS), 256, 512
     offs, be, nmb, rows, max_rows = _layout(COUNTS, dev)
     oh = offs.tolist()
     act = _rows(COUNTS, oh, m, dev, g)
     w2 = (torch.randn((E, h, m), generator=g) / m ** 0.5).to(dev, torch.bfloat16)
-    out = gemm.fc2_fwd(act, w2, be, nmb)
+    out = gemm.fc2_fwd(act, w2, be, nmb, pair=pair)
     torch.cuda.synchronize()
     for e, c in enumerate(COUNTS):
         ref = act[oh[e]: oh[e] + c].float() @ w2[e].float().T
@@ -62,7 +73,7 @@ def test_fc2_fwd_plain(dev):
     assert out[oh[0] + COUNTS[0]: oh[1]].abs().max().item() == 0
 
 
-def test_fc1_fwd_swiglu(dev):
+def test_fc1_fwd_swiglu(dev, pair):
     g = torch.Generator().manual_seed(1)
     E, m, h = len(COUNTS), 384, 256
     offs, be, nmb, rows, max_rows = _layout(COUNTS, dev)
@@ -73,7 +84,7 @@ def test_fc1_fwd_swiglu(dev):
     w1 = gemm.interleave_gate_up(gate, up)
     prob = torch.rand((xp.shape[0],), generator=g).to(dev)
     for rp in (None, prob):
-        preact, act = gemm.fc1_fwd(xp, w1, be, nmb, row_prob=rp)
+        preact, act = gemm.fc1_fwd(xp, w1, be, nmb, row_prob=rp, pair=pair)
         torch.cuda.synchronize()
         gp, upre = gemm.deinterleave_cols(preact)
         for e, c in enumerate(COUNTS):
@@ -90,7 +101,7 @@ def test_fc1_fwd_swiglu(dev):
             assert _relerr(act[oh[e]: oh[e] + c], ra) < 1e-2
 
 
-def test_fc2_dgrad_dswiglu(dev):
+def test_fc2_dgrad_dswiglu(dev, pair):
     g = torch.Generator().manual_seed(2)
     E, m, h = len(COUNTS), 512, 256
     offs, be, nmb, rows, max_rows = _layout(COUNTS, dev)
@@ -100,7 +111,8 @@ def test_fc2_dgrad_dswiglu(dev):
     w2 = (torch.randn((E, h, m), generator=g) / m ** 0.5).to(dev, torch.bfloat16)
     prob = torch.rand((dout.shape[0],), generator=g).to(dev)
     for rp in (None, prob):
-        dpre, part = gemm.fc2_dgrad(dout, w2, preact, be, nmb, row_prob=rp, want_dprob=True)
+        dpre, part = gemm.fc2_dgrad(dout, w2, preact, be, nmb, row_prob=rp, want_dprob=True,
+                                     pair=pair)
         torch.cuda.synchronize()
         dg, du = gemm.deinterleave_cols(dpre)
         pg, pu = gemm.deinterleave_cols(preact)
@@ -121,14 +133,14 @@ def test_fc2_dgrad_dswiglu(dev):
             assert _relerr(part[sl].sum(1), rdp) < 1e-3
 
 
-def test_fc1_dgrad(dev):
+def test_fc1_dgrad(dev, pair):
     g = torch.Generator().manual_seed(3)
     E, m, h = len(COUNTS), 256, 512
     offs, be, nmb, rows, max_rows = _layout(COUNTS, dev)
     oh = offs.tolist()
     dpre = _rows(COUNTS, oh, 2 * m, dev, g)
     w1 = (torch.randn((E, 2 * m, h), generator=g) / h ** 0.5).to(dev, torch.bfloat16)
-    dx = gemm.fc1_dgrad(dpre, w1, be, nmb)
+    dx = gemm.fc1_dgrad(dpre, w1, be, nmb, pair=pair)
     torch.cuda.synchronize()
     for e, c in enumerate(COUNTS):
         if c:
@@ -136,9 +148,9 @@ def test_fc1_dgrad(dev):
             assert _relerr(dx[sl], dpre[sl].float() @ w1[e].float()) < 1e-2
 
 
-def test_wgrad(dev):
+def test_wgrad(dev, pair):
     g = torch.Generator().manual_seed(4)
-    E, M, N = len(COUNTS), 256, 512
+    E, M, N = len(COUNTS), (256 if pair else 128), 512  # M % 256 == 0 -> pair engine
     offs, be, nmb, rows, max_rows = _layout(COUNTS, dev)
     oh = offs.tolist()
     a = _rows(COUNTS, oh, M, dev, g)
