@@ -357,7 +357,7 @@ def run_gpu(args, c) -> None:
         if n == 1 and not args.no_cpu_baseline:
             thr = cpu_threads()
             out["cpu_baseline"] = cpu_baseline(c, args.cpu_sample_tokens, thr)
-        print(json.dumps(out), flush=True)
+        emit(out)
     if n > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -402,7 +402,7 @@ def run_reference(args, c) -> None:
         "e2e": {"value": round(value, 2), "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(out), flush=True)
+    emit(out)
 
 
 def main():
@@ -418,10 +418,25 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     c = CONFIGS[args.config]
+    # stdout carries exactly one JSON line: everything else (NCCL's version banner, library
+    # chatter) is routed to stderr at the fd level; the JSON goes to the saved stdout fd.
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     if args.impl == "reference":
         run_reference(args, c)
     else:
         run_gpu(args, c)
+
+
+_JSON_OUT = None
+
+
+def emit(out: dict) -> None:
+    stream = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    stream.write(json.dumps(out) + "\n")
+    stream.flush()
 
 
 if __name__ == "__main__":

@@ -78,6 +78,14 @@ def load():
         raise MoEKernelError(
             f"{LIB_PATH} is missing: build it with `python -m paper_2603_07685_b200.build` "
             "(or __graft_entry__.build()); there is no CPU fallback")
+    csrc = LIB_PATH.parent / "csrc"
+    if csrc.is_dir():
+        newest = max((p.stat().st_mtime for p in csrc.iterdir()), default=0.0)
+        if newest > LIB_PATH.stat().st_mtime:
+            import sys
+
+            print(f"WARNING: {LIB_PATH.name} is older than csrc/; rebuild it "
+                  "(python -m paper_2603_07685_b200.build)", file=sys.stderr)
     lib = ctypes.CDLL(str(LIB_PATH))
     for name, argtypes in SIGNATURES.items():
         fn = getattr(lib, name)

@@ -132,8 +132,7 @@ def gemm_f32(a, b, block_expert, num_m_blocks, out=None, max_rows=None):
     if out is None:
         out = torch.empty((rows, N), dtype=torch.float32, device=a.device)
     _lib.call("moe_gg_gemm_f32", a.data_ptr(), b.data_ptr(), a_rows, rows, K, N, e,
-              block_expert.data_ptr(), num_m_blocks.data_ptr(), out.data_ptr(), int(pair),
-              _stream())
+              block_expert.data_ptr(), num_m_blocks.data_ptr(), out.data_ptr(), _stream())
     return out
 
 

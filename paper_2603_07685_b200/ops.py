@@ -7,6 +7,7 @@ function; the kernels cite them line by line.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import torch
@@ -186,7 +187,11 @@ def plan_max_rows(T: int, K: int, E: int, capacity: int = -1, pad: bool = False,
 
 def pick_align(T: int, K: int, E: int) -> int:
     """256-row expert blocks (CTA-pair GEMM engine) when experts are large enough that the
-    extra padding is negligible; 128 otherwise (e.g. DeepSeek-shape at EP=1, ~128 rows)."""
+    extra padding is negligible; 128 otherwise (e.g. DeepSeek-shape at EP=1, ~128 rows).
+    MOE_B200_ALIGN=128|256 overrides (A/B measurements)."""
+    forced = os.environ.get("MOE_B200_ALIGN")
+    if forced:
+        return int(forced)
     return 2 * ALIGN if T * K >= 8 * 2 * ALIGN * E else ALIGN
 
 
