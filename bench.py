@@ -178,8 +178,14 @@ def run_gpu(args, c) -> None:
     dy = torch.randn((T, h), device=dev, generator=g).to(bf)
     gw = torch.Generator(device=dev).manual_seed(99)  # weights identical on every rank
     w_r = (torch.randn((h, E), device=dev, generator=gw) * h ** -0.5).to(bf).requires_grad_()
-    if c.get("skew"):
-        pass
+    skew = args.skew if args.skew is not None else c.get("skew", 0.0)
+    if skew:
+        # config 5 skewed routing: logits += alpha * b_e, b_e = -log(1+e),
+        # exactly, through one constant-1 input feature whose router weights are alpha*b
+        x[:, 0] = 1.0
+        with torch.no_grad():
+            b = -torch.log1p(torch.arange(E, device=dev, dtype=torch.float32)) * skew
+            w_r[0, :] = b.to(bf)
     e_loc = E // n
     w1 = (torch.randn((e_loc, 2 * m, h), device=dev, generator=g) * h ** -0.5).to(bf)
     w2 = (torch.randn((e_loc, h, m), device=dev, generator=g) * m ** -0.5).to(bf)
@@ -263,31 +269,70 @@ def run_gpu(args, c) -> None:
     value = tokens / (ms_step / 1e3)
 
     # ---- e2e: host buffers through the public API ----------------------------------
+    # Each step's x and dY come from pinned host memory (H2D on a copy stream, double
+    # buffered so step i+1's copy overlaps step i's compute, like a data-loader prefetch);
+    # the step's aux loss is read back to the host. All copies are inside the timed region.
     x_host = x.cpu().pin_memory()
     dy_host = dy.cpu().pin_memory()
-    loss_host = torch.empty((), dtype=torch.float32).pin_memory()
-    xd = torch.empty_like(x)
-    dyd = torch.empty_like(dy)
+    loss_host = torch.empty((args.steps,), dtype=torch.float32).pin_memory()
+    bufs = [(torch.empty_like(x), torch.empty_like(dy)) for _ in range(2)]
+    copy_stream = torch.cuda.Stream(device=dev)
+    landed = [torch.cuda.Event() for _ in range(2)]
+    released = [torch.cuda.Event() for _ in range(2)]
+    main = torch.cuda.current_stream()
 
-    def e2e_step():
-        xd.copy_(x_host, non_blocking=True)
-        dyd.copy_(dy_host, non_blocking=True)
-        y, aux = step(xd, dyd)
-        loss_host.copy_(aux.detach(), non_blocking=True)
+    def h2d(slot):
+        with torch.cuda.stream(copy_stream):
+            copy_stream.wait_event(released[slot])
+            bufs[slot][0].copy_(x_host, non_blocking=True)
+            bufs[slot][1].copy_(dy_host, non_blocking=True)
+            landed[slot].record(copy_stream)
 
-    e2e_step()
+    def e2e_run(steps):
+        for s in range(2):
+            released[s].record(main)
+        h2d(0)
+        for i in range(steps):
+            slot = i % 2
+            if i + 1 < steps:
+                h2d(1 - slot)
+            main.wait_event(landed[slot])
+            _, aux = step(*bufs[slot])
+            released[slot].record(main)
+            loss_host[i].copy_(aux.detach(), non_blocking=True)
+
+    e2e_run(2)
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(args.steps):
-        e2e_step()
+    e2e_run(args.steps)
     e1.record()
     barrier()
     e2e_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
     if n > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
+
+    # ---- routing statistics of this workload (global counts; config 5 drop fraction) ----
+    from paper_2603_07685_b200 import ops
+
+    with torch.no_grad():
+        rr = ops.router_forward(x, w_r.detach(), K, c["score"])
+        cnt = rr.counts.to(torch.int64)
+        if n > 1:
+            allc = torch.empty((n, E), dtype=torch.int64, device=dev)
+            dist.all_gather_into_tensor(allc, cnt)
+            cnt = allc.sum(0)
+    cnt = cnt.cpu().double()
+    cap_g = cfg.capacity(n * T)
+    routing_stats = {
+        "skew_alpha": skew,
+        "max_over_mean_expert_load": round(float(cnt.max() / cnt.mean()), 4),
+        "capacity_per_expert": cap_g if cap_g >= 0 else None,
+        "drop_fraction": (round(float(1 - cnt.clamp(max=cap_g).sum() / cnt.sum()), 5)
+                          if cap_g >= 0 else 0.0),
+    }
 
     if rank == 0:
         peaks = {}
@@ -318,7 +363,8 @@ def run_gpu(args, c) -> None:
                 "workload": f"{c['name']}: E={E}, top-{K}, h={h}, ffn={m}, {T} tokens/GPU, "
                             f"{c['score']} router, aux coeff {AUX_COEFF}"
                             + (f", shared expert {c['shared']}" if c.get("shared") else "")
-                            + (f", capacity factor {c['cf']} pad" if c.get("cf") else ", dropless"),
+                            + (f", capacity factor {c['cf']} pad" if c.get("cf") else ", dropless")
+                            + (f", router skew alpha {skew} (b_e = -log(1+e))" if skew else ""),
                 "global_batch": tokens,
                 "tokens_per_gpu": T,
                 "parallelism": f"ep{n}",
@@ -353,6 +399,7 @@ def run_gpu(args, c) -> None:
             "kernel_ms_per_step": {k_: round(sum(v) / args.steps, 4) for k_, v in
                                    sorted(per_kernel.items(), key=lambda kv: -sum(kv[1]))},
             "clocks": clk,
+            "routing": routing_stats,
         }
         if n == 1 and not args.no_cpu_baseline:
             thr = cpu_threads()
@@ -414,6 +461,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-tokens", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--skew", type=float, default=None,
+                    help="router logit skew alpha (config 5 sweep: 0, 0.5, 1, 2)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
