@@ -206,7 +206,8 @@ def run_gpu(args, c) -> None:
         ep = EPGroup(dist.group.WORLD)
 
         def layer(xx):
-            return moe_forward_ep(xx, w_r, w1, w2, cfg, ep, None, w1s, w2s)
+            return moe_forward_ep(xx, w_r, w1, w2, cfg, ep, None, w1s, w2s,
+                                  transport=args.ep_transport)
     else:
         def layer(xx):
             return moe_forward(xx, w_r, w1, w2, cfg, None, w1s, w2s)
@@ -368,6 +369,7 @@ def run_gpu(args, c) -> None:
                 "global_batch": tokens,
                 "tokens_per_gpu": T,
                 "parallelism": f"ep{n}",
+                "ep_transport": args.ep_transport if n > 1 else None,
                 "l2": "inputs larger than L2 (x alone is "
                       f"{T * h * 2 / 1e6:.0f} MB; expert weights {E * 3 * h * m * 2 / 1e9:.2f} GB)",
             },
@@ -461,6 +463,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-tokens", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ep-transport", default="p2p", choices=["p2p", "nccl"],
+                    help="EP exchange: fused NVLink peer-memory kernels (p2p) or NCCL a2a")
     ap.add_argument("--skew", type=float, default=None,
                     help="router logit skew alpha (config 5 sweep: 0, 0.5, 1, 2)")
     args = ap.parse_args()

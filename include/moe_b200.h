@@ -90,6 +90,28 @@ int moe_combine_bwd(const void* dy, const void* o_rows, int T, int K, int h,
 int moe_dprob_from_partials(const int* inv_map, long long n, const float* partial, int ldp,
                             float* dprob, void* stream);
 
+/* ------------------------------------------------------------------ EP over NVLink peer memory
+ * The EP all-to-all (bytes modelled by perf.a2a_send_volume perf.py:62-70) fused into the
+ * permute / combine kernels: `peers` are device arrays [EP] of the symmetric (peer-mapped)
+ * row buffers of every rank; a selection's row on its expert's rank is base[e] + inv_c[t,k]
+ * (inv_c from a compact moe_permute_plan). Push kernels end with a system-scope fence; the
+ * caller orders them against the consumers with a stream-ordered collective. */
+int moe_ep_dispatch_push(const void* x, int T, int K, int h, const int* topk_idx,
+                         const int* inv_c, const int* base, int el,
+                         const unsigned long long* peers, const float* prob,
+                         const unsigned long long* prob_peers, void* stream);
+int moe_ep_combine_pull(const unsigned long long* peers, int T, int K, int h,
+                        const int* topk_idx, const int* inv_c, const int* base, int el,
+                        const float* weights, const void* resid, const void* extra,
+                        const void* extra2, void* out, void* stream);
+int moe_ep_combine_bwd_push(const void* dy, const unsigned long long* o_peers,
+                            const unsigned long long* d_peers, int T, int K, int h,
+                            const int* topk_idx, const int* inv_c, const int* base, int el,
+                            const float* prob, float* dprob, void* stream);
+int moe_ep_dprob_pull(const unsigned long long* part_peers, int T, int K, const int* topk_idx,
+                      const int* inv_c, const int* base, int el, int ldp, float* dprob,
+                      void* stream);
+
 /* ------------------------------------------------------------------ grouped GEMM (tcgen05)
  * replaces expert_activation()/expert_forward() routing.py:59-68 per expert block and the
  * corresponding backward GEMMs. flags bit 0 (grouped-M calls): the plan's

@@ -1,0 +1,310 @@
+// Expert-parallel exchange fused into the permute / combine kernels over NVLink peer memory.
+//
+// The all-to-all of the reference's EP model (pkg/src/moelab/perf.py:62-70 counts its bytes;
+// PAPER.md:204-211 describes the dispatcher) is not a separate collective here: every rank
+// holds symmetric (peer-mapped) row buffers, and
+//   * dispatch  = the permute gather, but each token row is stored straight into the
+//                 destination rank's 128/256-row padded expert plan (NVLink P2P stores);
+//   * combine   = the unpermute/combine gather-reduce, but expert-output rows are loaded
+//                 straight from the expert rank's buffer (NVLink P2P loads);
+//   * backward  = the combine backward pushes p*dY to the expert rank and pulls the expert
+//                 output row for dprob in the same pass; the dX combine pulls dXp rows.
+// Destination rows: row = base[e] + inv_c[t,k], where inv_c is the row of the selection in
+// the source rank's compact expert-major plan (moe_permute_plan, align 1) and base[e] is the
+// host-computed offset of this source's block inside expert e's padded block on its rank
+// (padded offset + rows of lower source ranks - compact offset), so the rows of expert e
+// on its home rank are ordered (source rank, token) = global token order, exactly the
+// oracle's permute order on the global batch (routing.py:155-163).
+//
+// Kernels end with __threadfence_system(); cross-rank completion is established by a
+// stream-ordered NCCL collective between the push and the consumer (no spin-waits).
+#include "common.cuh"
+
+namespace moe {
+namespace ep {
+
+__device__ __forceinline__ int4 ld_v4(const void* p) {
+  int4 r;
+  asm volatile("ld.global.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void acc8(float (&a)[8], int4 v, float w, bool weighted) {
+  const uint32_t* u = reinterpret_cast<const uint32_t*>(&v);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 f = unpack_bf16x2(u[j]);
+    const float x0 = weighted ? __fmul_rn(f.x, w) : f.x;
+    const float x1 = weighted ? __fmul_rn(f.y, w) : f.y;
+    a[2 * j] = __fadd_rn(a[2 * j], x0);
+    a[2 * j + 1] = __fadd_rn(a[2 * j + 1], x1);
+  }
+}
+__device__ __forceinline__ int4 pack8(const float (&a)[8]) {
+  int4 o;
+  o.x = pack_bf16x2(a[0], a[1]);
+  o.y = pack_bf16x2(a[2], a[3]);
+  o.z = pack_bf16x2(a[4], a[5]);
+  o.w = pack_bf16x2(a[6], a[7]);
+  return o;
+}
+
+// Dispatch: x[t] -> peers[rank(e)][base[e] + inv_c[t,k]] for every kept selection.
+template <int VPL>
+__global__ void dispatch_push_kernel(const int4* __restrict__ x, int T, int K, int hv,
+                                     const int* __restrict__ topk_idx,
+                                     const int* __restrict__ inv_c,
+                                     const int* __restrict__ base, int el,
+                                     const unsigned long long* __restrict__ peers,
+                                     const float* __restrict__ prob,
+                                     const unsigned long long* __restrict__ prob_peers) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = lane_id();
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp; t < T; t += nwarps) {
+    const int4* src = x + (long long)t * hv;
+    for (int c0 = 0; c0 < hv; c0 += 32 * VPL) {
+      int4 v[VPL];
+      bool loaded = false;
+      for (int k = 0; k < K; ++k) {
+        const int d = __ldg(inv_c + (long long)t * K + k);
+        if (d < 0) continue;
+        const int e = __ldg(topk_idx + (long long)t * K + k);
+        const int r = e / el;
+        const long long row = (long long)__ldg(base + e) + d;
+        if (!loaded) {
+#pragma unroll
+          for (int u = 0; u < VPL; ++u) {
+            const int c = c0 + u * 32 + lane;
+            if (c < hv) v[u] = ld_nc_v4(src + c);
+          }
+          loaded = true;
+        }
+        int4* dst = reinterpret_cast<int4*>(peers[r]) + row * hv;
+#pragma unroll
+        for (int u = 0; u < VPL; ++u) {
+          const int c = c0 + u * 32 + lane;
+          if (c < hv) dst[c] = v[u];
+        }
+        if (c0 == 0 && lane == 0 && prob_peers)
+          reinterpret_cast<float*>(prob_peers[r])[row] = prob[(long long)t * K + k];
+      }
+    }
+  }
+  __threadfence_system();
+}
+
+// Combine (pull): y[t] = sum_k w_k * peers[rank(e)][row]  (+resid if no kept) (+extra, extra2)
+template <int VPL>
+__global__ void combine_pull_kernel(const unsigned long long* __restrict__ peers, int T, int K,
+                                    int hv, const int* __restrict__ topk_idx,
+                                    const int* __restrict__ inv_c,
+                                    const int* __restrict__ base, int el,
+                                    const float* __restrict__ weights,
+                                    const int4* __restrict__ resid,
+                                    const int4* __restrict__ extra,
+                                    const int4* __restrict__ extra2, int4* __restrict__ out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = lane_id();
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp; t < T; t += nwarps) {
+    bool any = false;
+    for (int c0 = 0; c0 < hv; c0 += 32 * VPL) {
+      float a[VPL][8];
+#pragma unroll
+      for (int u = 0; u < VPL; ++u)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[u][j] = 0.f;
+      for (int k = 0; k < K; ++k) {
+        const int d = __ldg(inv_c + (long long)t * K + k);
+        if (d < 0) continue;
+        any = true;
+        const int e = __ldg(topk_idx + (long long)t * K + k);
+        const long long row = (long long)__ldg(base + e) + d;
+        const int4* rrow = reinterpret_cast<const int4*>(peers[e / el]) + row * hv;
+        const float w = weights ? __ldg(weights + (long long)t * K + k) : 1.0f;
+        int4 v[VPL];
+#pragma unroll
+        for (int u = 0; u < VPL; ++u) {
+          const int c = c0 + u * 32 + lane;
+          if (c < hv) v[u] = ld_v4(rrow + c);
+        }
+#pragma unroll
+        for (int u = 0; u < VPL; ++u) {
+          const int c = c0 + u * 32 + lane;
+          if (c < hv) acc8(a[u], v[u], w, weights != nullptr);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < VPL; ++u) {
+        const int c = c0 + u * 32 + lane;
+        if (c >= hv) continue;
+        if (extra) acc8(a[u], ld_nc_v4(extra + (long long)t * hv + c), 1.f, false);
+        if (extra2) acc8(a[u], ld_nc_v4(extra2 + (long long)t * hv + c), 1.f, false);
+        if (!any && resid) acc8(a[u], ld_nc_v4(resid + (long long)t * hv + c), 1.f, false);
+        st_na_v4(out + (long long)t * hv + c, pack8(a[u]));
+      }
+    }
+  }
+}
+
+// Combine backward (push): per kept selection, dO row = p * dY[t] is stored into the expert
+// rank's buffer and dprob = <dY[t], O row> is computed from the expert output pulled over
+// NVLink (o_peers NULL: mem-efficient combine, unscaled dY pushed, no dprob here).
+__global__ void combine_bwd_push_kernel(const int4* __restrict__ dy,
+                                        const unsigned long long* __restrict__ o_peers,
+                                        const unsigned long long* __restrict__ d_peers, int T,
+                                        int K, int hv, const int* __restrict__ topk_idx,
+                                        const int* __restrict__ inv_c,
+                                        const int* __restrict__ base, int el,
+                                        const float* __restrict__ prob,
+                                        float* __restrict__ dprob) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = lane_id();
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp; t < T; t += nwarps) {
+    for (int k = 0; k < K; ++k) {
+      const long long i = (long long)t * K + k;
+      const int d = __ldg(inv_c + i);
+      if (d < 0) {
+        if (lane == 0 && dprob) dprob[i] = 0.f;
+        continue;
+      }
+      const int e = __ldg(topk_idx + i);
+      const int r = e / el;
+      const long long row = (long long)__ldg(base + e) + d;
+      const float p = prob ? __ldg(prob + i) : 1.0f;
+      const int4* yr = dy + (long long)t * hv;
+      const int4* orow = o_peers ? reinterpret_cast<const int4*>(o_peers[r]) + row * hv : nullptr;
+      int4* drow = reinterpret_cast<int4*>(d_peers[r]) + row * hv;
+      float dot = 0.f;
+      for (int c = lane; c < hv; c += 32) {
+        const int4 v = ld_nc_v4(yr + c);
+        const uint32_t* u = reinterpret_cast<const uint32_t*>(&v);
+        if (orow) {
+          const int4 ov = ld_v4(orow + c);
+          const uint32_t* uo = reinterpret_cast<const uint32_t*>(&ov);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 a = unpack_bf16x2(u[j]);
+            const float2 b = unpack_bf16x2(uo[j]);
+            dot += a.x * b.x + a.y * b.y;
+          }
+        }
+        int4 w;
+        if (prob) {
+          uint32_t* uw = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 a = unpack_bf16x2(u[j]);
+            uw[j] = pack_bf16x2(a.x * p, a.y * p);
+          }
+        } else {
+          w = v;
+        }
+        drow[c] = w;
+      }
+      if (dprob && orow) {
+        dot = warp_sum(dot);
+        if (lane == 0) dprob[i] = dot;
+      }
+    }
+  }
+  __threadfence_system();
+}
+
+// dprob (mem-efficient combine): sum of the expert rank's fc2-dgrad row partials, pulled.
+__global__ void dprob_pull_kernel(const unsigned long long* __restrict__ part_peers, long long n,
+                                  int K, const int* __restrict__ topk_idx,
+                                  const int* __restrict__ inv_c, const int* __restrict__ base,
+                                  int el, int ldp, float* __restrict__ dprob) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int d = inv_c[i];
+  float s = 0.f;
+  if (d >= 0) {
+    const int e = topk_idx[i];
+    const long long row = (long long)base[e] + d;
+    const float* pr = reinterpret_cast<const float*>(part_peers[e / el]) + row * ldp;
+    for (int j = 0; j < ldp; ++j) s += pr[j];
+  }
+  dprob[i] = s;
+}
+
+static int sms() {
+  static int n = 0;
+  if (!n) {
+    int d = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+  }
+  return n;
+}
+static int warp_grid(long long items) {
+  const long long blocks = ceil_div_ll(items > 0 ? items : 1, 8);
+  const long long cap = (long long)sms() * 8;
+  return (int)(blocks < cap ? blocks : cap);
+}
+
+}  // namespace ep
+}  // namespace moe
+
+using namespace moe;
+using namespace moe::ep;
+
+extern "C" {
+
+int moe_ep_dispatch_push(const void* x, int T, int K, int h, const int* topk_idx,
+                         const int* inv_c, const int* base, int el,
+                         const unsigned long long* peers, const float* prob,
+                         const unsigned long long* prob_peers, void* stream) {
+  if (h % 8 || el < 1) return kErrInvalidArg;
+  if (T == 0) return kOk;
+  dispatch_push_kernel<4><<<warp_grid(T), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const int4*>(x), T, K, h / 8, topk_idx, inv_c, base, el, peers, prob,
+      prob_peers);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+int moe_ep_combine_pull(const unsigned long long* peers, int T, int K, int h,
+                        const int* topk_idx, const int* inv_c, const int* base, int el,
+                        const float* weights, const void* resid, const void* extra,
+                        const void* extra2, void* out, void* stream) {
+  if (h % 8 || el < 1) return kErrInvalidArg;
+  if (T == 0) return kOk;
+  combine_pull_kernel<4><<<warp_grid(T), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      peers, T, K, h / 8, topk_idx, inv_c, base, el, weights, static_cast<const int4*>(resid),
+      static_cast<const int4*>(extra), static_cast<const int4*>(extra2),
+      static_cast<int4*>(out));
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+int moe_ep_combine_bwd_push(const void* dy, const unsigned long long* o_peers,
+                            const unsigned long long* d_peers, int T, int K, int h,
+                            const int* topk_idx, const int* inv_c, const int* base, int el,
+                            const float* prob, float* dprob, void* stream) {
+  if (h % 8 || el < 1) return kErrInvalidArg;
+  if (T == 0) return kOk;
+  combine_bwd_push_kernel<<<warp_grid(T), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const int4*>(dy), o_peers, d_peers, T, K, h / 8, topk_idx, inv_c, base, el,
+      prob, dprob);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+int moe_ep_dprob_pull(const unsigned long long* part_peers, int T, int K, const int* topk_idx,
+                      const int* inv_c, const int* base, int el, int ldp, float* dprob,
+                      void* stream) {
+  const long long n = (long long)T * K;
+  if (n == 0) return kOk;
+  dprob_pull_kernel<<<(int)ceil_div_ll(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      part_peers, n, K, topk_idx, inv_c, base, el, ldp, dprob);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+}  // extern "C"

@@ -281,15 +281,235 @@ class _MoEEPFunction(torch.autograd.Function):
         return (dx, dw_r.to(torch.bfloat16), dw1, dw2, None, dw1s, dw2s, None, None)
 
 
+# ----------------------------------------------------------------------------------------
+# NVLink peer-memory transport: the exchange is fused into the permute / combine kernels
+# (csrc/ep.cu). Token rows are pushed straight into the expert rank's padded plan and the
+# expert outputs / dX rows are pulled back inside the combine; no send buffer, no NCCL
+# all-to-all, no regroup copies. Stream-ordered NCCL barriers order pushes vs. consumers.
+
+
+class SymmPool:
+    """Symmetric (peer-mapped) buffers of one EP group. Every rank requests the same sizes
+    in the same order (sizes come from the all-gathered counts), so growth is collective."""
+
+    def __init__(self, ep: EPGroup, dev):
+        import torch.distributed._symmetric_memory as symm
+
+        self._symm = symm
+        self.ep = ep
+        self.dev = dev
+        self.bufs = {}
+        self.bar = torch.zeros((1,), dtype=torch.float32, device=dev)
+
+    def get(self, name: str, numel: int, dtype):
+        cur = self.bufs.get(name)
+        if cur is None or cur[0].numel() < numel or cur[0].dtype != dtype:
+            cap = int(numel * 1.25) + 4096
+            t = self._symm.empty(cap, dtype=dtype, device=self.dev)
+            h = self._symm.rendezvous(t, self.ep.group)
+            ptrs = [int(p) for p in h.buffer_ptrs]
+            off = int(getattr(h, "offset", 0))
+            if ptrs[self.ep.rank] != t.data_ptr():
+                ptrs = [p + off for p in ptrs]
+            assert ptrs[self.ep.rank] == t.data_ptr(), "symmetric-memory peer pointers"
+            peers = torch.tensor(ptrs, dtype=torch.int64, device=self.dev)
+            # start from zeros (no NaN garbage in rows that are never pushed) before any
+            # peer can write into it
+            t.zero_()
+            self.barrier()
+            cur = (t, peers, h)
+            self.bufs[name] = cur
+        return cur[0], cur[1]
+
+    def barrier(self):
+        """Stream-ordered cross-rank barrier (an NCCL all-reduce of one float)."""
+        dist.all_reduce(self.bar, group=self.ep.group)
+
+
+_POOLS: dict = {}
+
+
+def _pool(ep: EPGroup, dev) -> SymmPool:
+    key = (id(ep.group), dev.index)
+    if key not in _POOLS:
+        _POOLS[key] = SymmPool(ep, dev)
+    return _POOLS[key]
+
+
+def p2p_tables(counts_all: np.ndarray, rank: int, capacity: int, pad: bool, align: int):
+    """Host tables of the fused transport, identical math on every rank.
+
+    Returns (base[E] for this source rank, rows_pad of every rank, this rank's EPHostPlan).
+    base[e] = padded offset of expert e on its rank + rows of lower source ranks for e
+              - this rank's compact offset of e, so dest row = base[e] + inv_c[t, k].
+    """
+    counts_all = np.asarray(counts_all, dtype=np.int64)
+    n, E = counts_all.shape
+    el = E // n
+    plans = [ep_host_plan(counts_all, r, capacity, pad, align) for r in range(n)]
+    kept = plans[0].kept                                     # [n, E], same on every rank
+    prefix = _excl_cumsum(kept, axis=0)[rank]                # rows of lower ranks, per e
+    off_c = _excl_cumsum(kept[rank])                         # compact offsets on this rank
+    off_pad_e = np.concatenate([plans[e // el].off_pad[e % el: e % el + 1] for e in range(E)])
+    base = (off_pad_e + prefix - off_c).astype(np.int64)
+    return base, [p.rows_pad for p in plans], plans[rank]
+
+
+class _MoEEPP2PFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w_r, w1, w2, sel_bias, w1s, w2s, cfg: MoEConfig, ep: EPGroup):
+        t, h = x.shape
+        E, K = cfg.num_experts, cfg.top_k
+        n = ep.n
+        dev = x.device
+        pool = _pool(ep, dev)
+        stream = torch.cuda.current_stream().cuda_stream
+        w_r_t, w_r_pad = ops.stage_router_weight(w_r)
+        r = ops.router_forward(x, w_r, K, cfg.score, sel_bias, 0.0, w_r_t=w_r_t)
+        stats = torch.cat([r.counts.float(), r.mean_scores])
+        gathered = torch.empty((n, 2 * E), dtype=torch.float32, device=dev)
+        dist.all_gather_into_tensor(gathered, stats, group=ep.group)  # also the reuse barrier
+        g = gathered.cpu().numpy()  # the one host sync of the EP forward
+        counts_all = np.rint(g[:, :E]).astype(np.int64)
+        cap = cfg.capacity(n * t)
+        align = ops.pick_align(n * t, K, E)
+        pair = align == 2 * ops.ALIGN
+        base, rows_all, hp = p2p_tables(counts_all, ep.rank, cap, cfg.pad_to_capacity, align)
+        aux_v, aux_g = global_aux(counts_all, g[:, E:], t, K, cfg.aux_loss_coeff)
+        rows_alloc = max(max(rows_all), 2 * ops.ALIGN)
+        el = hp.el
+        # one pinned H2D copy of every small table
+        cap_local = hp.cap_local if hp.cap_local is not None else np.full(E, -1)
+        meta = np.array([hp.rows_pad // ops.ALIGN, hp.rows_pad, 0], dtype=np.int64)
+        parts = [base, cap_local, hp.table.astype(np.int64), hp.block_expert, meta]
+        lens = [len(p) for p in parts]
+        tab = torch.from_numpy(np.concatenate(parts).astype(np.int32)).pin_memory().to(
+            dev, non_blocking=True)
+        base_d, cap_d, table_d, be_d, meta_d = torch.split(tab, lens)
+        smallf = torch.from_numpy(np.concatenate([[aux_v], aux_g]).astype(np.float32))
+        smallf = smallf.pin_memory().to(dev, non_blocking=True)
+        aux = smallf[0].clone()
+        r.aux_grad = smallf[1:]
+        nmb = meta_d[0:1]
+        off_pad_d = table_d[2 * n * el: 2 * n * el + el + 1]
+
+        splan = ops.build_plan(r.topk_idx, r.topk_prob, E, -1, False,
+                               cap_e=cap_d if hp.cap_local is not None else None, compact=True)
+        xp, xp_peers = pool.get("xp", rows_alloc * h, torch.bfloat16)
+        xp = xp[: rows_alloc * h].view(rows_alloc, h)
+        prob_peers = None
+        row_prob = None
+        if cfg.mem_efficient:
+            pr, prob_peers = pool.get("prob", rows_alloc, torch.float32)
+            row_prob = pr[:rows_alloc]
+        map_pad = torch.empty((rows_alloc,), dtype=torch.int32, device=dev)
+        if hp.rows_pad:
+            _lib.call("moe_ep_regroup_map", table_d.data_ptr(), n, el, hp.rows_pad,
+                      map_pad.data_ptr(), None, stream)
+        # zero this rank's padding / phantom rows (disjoint from the rows peers push)
+        _lib.call("moe_zero_pad_rows", meta_d.data_ptr(), map_pad.data_ptr(), h, xp.data_ptr(),
+                  stream)
+        # (row_prob of padding rows: zero at allocation, else a stale finite prob of a row
+        # whose activation is exactly zero; never cleared here, peers may already be pushing)
+        _lib.call("moe_ep_dispatch_push", x.data_ptr(), t, K, h, r.topk_idx.data_ptr(),
+                  splan.inv_map.data_ptr(), base_d.data_ptr(), el, xp_peers.data_ptr(),
+                  r.topk_prob.data_ptr() if cfg.mem_efficient else None,
+                  prob_peers.data_ptr() if prob_peers is not None else None, stream)
+        pool.barrier()
+        preact, act = gemm.fc1_fwd(xp, w1, be_d, nmb, row_prob, pair=pair)
+        o, o_peers = pool.get("o", rows_alloc * h, torch.bfloat16)
+        o = o[: rows_alloc * h].view(rows_alloc, h)
+        gemm.fc2_fwd(act, w2, be_d, nmb, out=o, pair=pair)
+        shared = shared_expert_forward(x, w1s, w2s) if w1s is not None else None
+        pool.barrier()
+        y = torch.empty_like(x)
+        _lib.call("moe_ep_combine_pull", o_peers.data_ptr(), t, K, h, r.topk_idx.data_ptr(),
+                  splan.inv_map.data_ptr(), base_d.data_ptr(), el,
+                  None if cfg.mem_efficient else r.topk_prob.data_ptr(),
+                  x.data_ptr() if cap >= 0 else None,
+                  shared[-1].data_ptr() if shared is not None else None, None, y.data_ptr(),
+                  stream)
+        ctx.cfg, ctx.ep, ctx.r, ctx.splan, ctx.cap, ctx.pair = cfg, ep, r, splan, cap, pair
+        ctx.tabs = (base_d, be_d, nmb, meta_d, off_pad_d, map_pad, rows_alloc, el)
+        ctx.row_prob = row_prob
+        ctx.shared = shared[:-1] if shared is not None else None
+        ctx.save_for_backward(x, w_r_pad, w1, w2, preact, act, w1s, w2s)
+        return y, aux
+
+    @staticmethod
+    def backward(ctx, dy, daux):
+        cfg, ep, r, splan = ctx.cfg, ctx.ep, ctx.r, ctx.splan
+        base_d, be_d, nmb, meta_d, off_pad_d, map_pad, rows_alloc, el = ctx.tabs
+        x, w_r_pad, w1, w2, preact, act, w1s, w2s = ctx.saved_tensors
+        t, h = x.shape
+        K = cfg.top_k
+        dev = x.device
+        pool = _pool(ep, dev)
+        stream = torch.cuda.current_stream().cuda_stream
+        dy = dy.contiguous()
+        xp, _ = pool.get("xp", rows_alloc * h, torch.bfloat16)
+        xp = xp[: rows_alloc * h].view(rows_alloc, h)
+        _, o_peers = pool.get("o", rows_alloc * h, torch.bfloat16)
+        d_o, d_peers = pool.get("do", rows_alloc * h, torch.bfloat16)
+        d_o = d_o[: rows_alloc * h].view(rows_alloc, h)
+        _lib.call("moe_zero_pad_rows", meta_d.data_ptr(), map_pad.data_ptr(), h, d_o.data_ptr(),
+                  stream)
+        dprob = torch.empty((t, K), dtype=torch.float32, device=dev)
+        _lib.call("moe_ep_combine_bwd_push", dy.data_ptr(),
+                  None if cfg.mem_efficient else o_peers.data_ptr(), d_peers.data_ptr(), t, K,
+                  h, r.topk_idx.data_ptr(), splan.inv_map.data_ptr(), base_d.data_ptr(), el,
+                  None if cfg.mem_efficient else r.topk_prob.data_ptr(),
+                  None if cfg.mem_efficient else dprob.data_ptr(), stream)
+        pool.barrier()
+        part_peers = None
+        if cfg.mem_efficient:
+            ldp = w2.shape[2] // 256
+            part, part_peers = pool.get("part", rows_alloc * ldp, torch.float32)
+            part = part[: rows_alloc * ldp].view(rows_alloc, ldp)
+            d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, be_d, nmb, row_prob=ctx.row_prob,
+                                      pair=ctx.pair, part=part)
+        else:
+            d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, be_d, nmb, pair=ctx.pair)
+        dw2 = gemm.wgrad(d_o, act, off_pad_d, el)
+        dxp, dxp_peers = pool.get("dxp", rows_alloc * h, torch.bfloat16)
+        dxp = dxp[: rows_alloc * h].view(rows_alloc, h)
+        gemm.fc1_dgrad(d_pre, w1, be_d, nmb, out=dxp, pair=ctx.pair)
+        dw1 = gemm.wgrad(d_pre, xp, off_pad_d, el)
+        pool.barrier()
+        if cfg.mem_efficient:
+            _lib.call("moe_ep_dprob_pull", part_peers.data_ptr(), t, K, r.topk_idx.data_ptr(),
+                      splan.inv_map.data_ptr(), base_d.data_ptr(), el, w2.shape[2] // 256,
+                      dprob.data_ptr(), stream)
+        aux_scale = None if daux is None else daux.float()
+        dw_r, dx_router = ops.router_backward(x, w_r_pad, r, dprob, cfg.score,
+                                              aux_scale=aux_scale)
+        dx_shared = dw1s = dw2s = None
+        if ctx.shared is not None:
+            dx_shared, dw1s, dw2s = shared_expert_backward(x, dy, w1s, w2s, ctx.shared)
+        dx = torch.empty_like(x)
+        _lib.call("moe_ep_combine_pull", dxp_peers.data_ptr(), t, K, h, r.topk_idx.data_ptr(),
+                  splan.inv_map.data_ptr(), base_d.data_ptr(), el, None,
+                  dy.data_ptr() if ctx.cap >= 0 else None, dx_router.data_ptr(),
+                  dx_shared.data_ptr() if dx_shared is not None else None, dx.data_ptr(),
+                  stream)
+        # no rank may overwrite the symmetric buffers before every rank has pulled
+        pool.barrier()
+        return (dx, dw_r.to(torch.bfloat16), dw1, dw2, None, dw1s, dw2s, None, None)
+
+
 def moe_forward_ep(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
-                   selection_bias=None, w1_shared=None, w2_shared=None):
+                   selection_bias=None, w1_shared=None, w2_shared=None, transport: str = "p2p"):
     """EP MoE layer: w1_local [E/EP, 2m, h], w2_local [E/EP, h, m] are this rank's experts
     (global experts [rank*E/EP, (rank+1)*E/EP)). Returns (y [T,h], global aux).
+
+    transport "p2p" (default): the exchange is fused into the permute / combine kernels over
+    NVLink peer memory (csrc/ep.cu). "nccl": permute -> NCCL all_to_all_single -> regroup
+    (the baseline dispatcher, kept for A/B measurement).
 
     The router weight gradient returned is this rank's partial sum over its own tokens;
     W_r is replicated, so its all-reduce belongs to the data-parallel gradient sync.
     """
     if cfg.num_experts % ep.n:
         raise ValueError(f"num_experts {cfg.num_experts} not divisible by EP {ep.n}")
-    return _MoEEPFunction.apply(x, w_r, w1_local, w2_local, selection_bias, w1_shared,
-                                w2_shared, cfg, ep)
+    fn = {"p2p": _MoEEPP2PFunction, "nccl": _MoEEPFunction}[transport]
+    return fn.apply(x, w_r, w1_local, w2_local, selection_bias, w1_shared, w2_shared, cfg, ep)

@@ -83,14 +83,14 @@ def fc2_fwd(act, w2, block_expert, num_m_blocks, out=None, max_rows=None, pair=F
 
 
 def fc2_dgrad(dout, w2, preact, block_expert, num_m_blocks, row_prob=None, want_dprob=False,
-              d_preact=None, max_rows=None, pair=False):
+              d_preact=None, max_rows=None, pair=False, part=None):
+    """part: optional preallocated [rows, m/256] fp32 dprob partials (implies want_dprob)."""
     a_rows, h = dout.shape
     rows = a_rows if max_rows is None else max_rows
     e, _, m = w2.shape
     if d_preact is None:
         d_preact = torch.empty((rows, 2 * m), dtype=torch.bfloat16, device=dout.device)
-    part = None
-    if want_dprob:
+    if want_dprob and part is None:
         part = torch.empty((rows, m // 256), dtype=torch.float32, device=dout.device)
     _lib.call("moe_gg_fc2_dgrad", dout.data_ptr(), w2.data_ptr(), preact.data_ptr(), a_rows, rows,
               h, m, e, block_expert.data_ptr(), num_m_blocks.data_ptr(), _ptr(row_prob),

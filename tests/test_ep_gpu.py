@@ -33,7 +33,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, case, q):
+def _worker(rank, world, port, case, q, transport):
     try:
         import torch.distributed as dist
 
@@ -73,7 +73,11 @@ def _worker(rank, world, port, case, q):
         w1d = gemm.interleave_gate_up(gate[mine].to(dev), up[mine].to(dev)).requires_grad_(True)
         w2d = w2[mine].to(dev).contiguous().requires_grad_(True)
         ep = EPGroup()
-        y, aux = moe_forward_ep(x, w_rd, w1d, w2d, cfg, ep)
+        y, aux = moe_forward_ep(x, w_rd, w1d, w2d, cfg, ep, transport=transport)
+        # a second step exercises buffer reuse across steps (symmetric pools, barriers)
+        for p_ in (x, w_rd, w1d, w2d):
+            p_.grad = None
+        y, aux = moe_forward_ep(x, w_rd, w1d, w2d, cfg, ep, transport=transport)
         torch.autograd.backward([y, aux], [dy_g[sl].to(dev), torch.ones_like(aux)])
         dwr = w_rd.grad.float().clone()
         dist.all_reduce(dwr)
@@ -121,8 +125,9 @@ def _worker(rank, world, port, case, q):
         q.put((rank, traceback.format_exc() + repr(exc)))
 
 
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
 @pytest.mark.parametrize("name", list(CASES))
-def test_ep_layer_matches_global_oracle(name):
+def test_ep_layer_matches_global_oracle(name, transport):
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
     world = min(torch.cuda.device_count(), 8)
@@ -133,7 +138,7 @@ def test_ep_layer_matches_global_oracle(name):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES[name], q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES[name], q, transport))
              for r in range(world)]
     for p in procs:
         p.start()
