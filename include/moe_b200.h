@@ -100,11 +100,13 @@ int moe_ep_dispatch_push(const void* x, int T, int K, int h, const int* topk_idx
                          const int* inv_c, const int* base, int el,
                          const unsigned long long* peers, const float* prob,
                          const unsigned long long* prob_peers, void* stream);
+/* rows_copy (nullable): local compact copy of the pulled rows, indexed by inv_c */
 int moe_ep_combine_pull(const unsigned long long* peers, int T, int K, int h,
                         const int* topk_idx, const int* inv_c, const int* base, int el,
                         const float* weights, const void* resid, const void* extra,
-                        const void* extra2, void* out, void* stream);
-int moe_ep_combine_bwd_push(const void* dy, const unsigned long long* o_peers,
+                        const void* extra2, void* out, void* rows_copy, void* stream);
+/* o_local: the forward's rows_copy (dprob = <dY, O>); NULL for the mem-efficient combine */
+int moe_ep_combine_bwd_push(const void* dy, const void* o_local,
                             const unsigned long long* d_peers, int T, int K, int h,
                             const int* topk_idx, const int* inv_c, const int* base, int el,
                             const float* prob, float* dprob, void* stream);

@@ -49,7 +49,7 @@ SIGNATURES: dict[str, list] = {
     "moe_dprob_from_partials": [P, L, P, I, P, P],
     # EP over NVLink peer memory (csrc/ep.cu)
     "moe_ep_dispatch_push": [P, I, I, I, P, P, P, I, P, P, P, P],
-    "moe_ep_combine_pull": [P, I, I, I, P, P, P, I, P, P, P, P, P, P],
+    "moe_ep_combine_pull": [P, I, I, I, P, P, P, I, P, P, P, P, P, P, P],
     "moe_ep_combine_bwd_push": [P, P, P, I, I, I, P, P, P, I, P, P, P],
     "moe_ep_dprob_pull": [P, I, I, P, P, P, I, I, P, P],
     # grouped GEMM (csrc/grouped_gemm.cu)

@@ -4,11 +4,12 @@
 // PAPER.md:204-211 describes the dispatcher) is not a separate collective here: every rank
 // holds symmetric (peer-mapped) row buffers, and
 //   * dispatch  = the permute gather, but each token row is stored straight into the
-//                 destination rank's 128/256-row padded expert plan (NVLink P2P stores);
+//                 destination rank's padded expert plan (NVLink P2P stores);
 //   * combine   = the unpermute/combine gather-reduce, but expert-output rows are loaded
-//                 straight from the expert rank's buffer (NVLink P2P loads);
-//   * backward  = the combine backward pushes p*dY to the expert rank and pulls the expert
-//                 output row for dprob in the same pass; the dX combine pulls dXp rows.
+//                 straight from the expert rank's buffer (NVLink P2P loads, K rows in
+//                 flight per lane); the pulled rows are also kept in a local compact copy;
+//   * backward  = the combine backward computes dprob against that local copy and pushes
+//                 p*dY to the expert rank in the same pass; the dX combine pulls dXp rows.
 // Destination rows: row = base[e] + inv_c[t,k], where inv_c is the row of the selection in
 // the source rank's compact expert-major plan (moe_permute_plan, align 1) and base[e] is the
 // host-computed offset of this source's block inside expert e's padded block on its rank
@@ -16,7 +17,7 @@
 // on its home rank are ordered (source rank, token) = global token order, exactly the
 // oracle's permute order on the global batch (routing.py:155-163).
 //
-// Kernels end with __threadfence_system(); cross-rank completion is established by a
+// Push kernels end with __threadfence_system(); cross-rank completion is established by a
 // stream-ordered NCCL collective between the push and the consumer (no spin-waits).
 #include "common.cuh"
 
@@ -96,8 +97,10 @@ __global__ void dispatch_push_kernel(const int4* __restrict__ x, int T, int K, i
   __threadfence_system();
 }
 
-// Combine (pull): y[t] = sum_k w_k * peers[rank(e)][row]  (+resid if no kept) (+extra, extra2)
-template <int VPL>
+// Combine (pull): y[t] = sum_k w_k * peers[rank(e)][base[e] + inv_c]  (+resid if no kept)
+// (+extra, extra2); with rows_copy, each pulled row is also stored at rows_copy[inv_c].
+// K <= KMAX: the K rows of a chunk are all loaded before any is accumulated (MLP).
+template <int VPL, int KMAX>
 __global__ void combine_pull_kernel(const unsigned long long* __restrict__ peers, int T, int K,
                                     int hv, const int* __restrict__ topk_idx,
                                     const int* __restrict__ inv_c,
@@ -105,38 +108,57 @@ __global__ void combine_pull_kernel(const unsigned long long* __restrict__ peers
                                     const float* __restrict__ weights,
                                     const int4* __restrict__ resid,
                                     const int4* __restrict__ extra,
-                                    const int4* __restrict__ extra2, int4* __restrict__ out) {
+                                    const int4* __restrict__ extra2, int4* __restrict__ out,
+                                    int4* __restrict__ rows_copy) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = lane_id();
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int t = warp; t < T; t += nwarps) {
+    const int4* rows[KMAX];
+    int4* copy[KMAX];
+    float w[KMAX];
     bool any = false;
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      rows[k] = nullptr;
+      copy[k] = nullptr;
+      w[k] = 0.f;
+      if (k < K) {
+        const int d = __ldg(inv_c + (long long)t * K + k);
+        if (d >= 0) {
+          const int e = __ldg(topk_idx + (long long)t * K + k);
+          rows[k] = reinterpret_cast<const int4*>(peers[e / el]) +
+                    ((long long)__ldg(base + e) + d) * hv;
+          if (rows_copy) copy[k] = rows_copy + (long long)d * hv;
+          w[k] = weights ? __ldg(weights + (long long)t * K + k) : 1.0f;
+          any = true;
+        }
+      }
+    }
     for (int c0 = 0; c0 < hv; c0 += 32 * VPL) {
+      int4 v[KMAX][VPL];
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+#pragma unroll
+        for (int u = 0; u < VPL; ++u) {
+          const int c = c0 + u * 32 + lane;
+          if (rows[k] && c < hv) v[k][u] = ld_v4(rows[k] + c);
+        }
       float a[VPL][8];
 #pragma unroll
       for (int u = 0; u < VPL; ++u)
 #pragma unroll
         for (int j = 0; j < 8; ++j) a[u][j] = 0.f;
-      for (int k = 0; k < K; ++k) {
-        const int d = __ldg(inv_c + (long long)t * K + k);
-        if (d < 0) continue;
-        any = true;
-        const int e = __ldg(topk_idx + (long long)t * K + k);
-        const long long row = (long long)__ldg(base + e) + d;
-        const int4* rrow = reinterpret_cast<const int4*>(peers[e / el]) + row * hv;
-        const float w = weights ? __ldg(weights + (long long)t * K + k) : 1.0f;
-        int4 v[VPL];
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
 #pragma unroll
         for (int u = 0; u < VPL; ++u) {
           const int c = c0 + u * 32 + lane;
-          if (c < hv) v[u] = ld_v4(rrow + c);
+          if (rows[k] && c < hv) {
+            acc8(a[u], v[k][u], w[k], weights != nullptr);
+            if (copy[k]) st_na_v4(copy[k] + c, v[k][u]);
+          }
         }
-#pragma unroll
-        for (int u = 0; u < VPL; ++u) {
-          const int c = c0 + u * 32 + lane;
-          if (c < hv) acc8(a[u], v[u], w, weights != nullptr);
-        }
-      }
 #pragma unroll
       for (int u = 0; u < VPL; ++u) {
         const int c = c0 + u * 32 + lane;
@@ -150,11 +172,13 @@ __global__ void combine_pull_kernel(const unsigned long long* __restrict__ peers
   }
 }
 
-// Combine backward (push): per kept selection, dO row = p * dY[t] is stored into the expert
-// rank's buffer and dprob = <dY[t], O row> is computed from the expert output pulled over
-// NVLink (o_peers NULL: mem-efficient combine, unscaled dY pushed, no dprob here).
+// Combine backward (push): per kept selection, p * dY[t] is stored into the expert rank's
+// row and dprob = <dY[t], O row> is computed against the LOCAL compact copy of the expert
+// output (o_local[inv_c], written by the forward pull). o_local NULL: mem-efficient
+// combine (unscaled dY pushed, dprob comes from the expert rank's partials).
+template <int VPL, int KMAX>
 __global__ void combine_bwd_push_kernel(const int4* __restrict__ dy,
-                                        const unsigned long long* __restrict__ o_peers,
+                                        const int4* __restrict__ o_local,
                                         const unsigned long long* __restrict__ d_peers, int T,
                                         int K, int hv, const int* __restrict__ topk_idx,
                                         const int* __restrict__ inv_c,
@@ -165,50 +189,70 @@ __global__ void combine_bwd_push_kernel(const int4* __restrict__ dy,
   const int lane = lane_id();
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int t = warp; t < T; t += nwarps) {
-    for (int k = 0; k < K; ++k) {
-      const long long i = (long long)t * K + k;
-      const int d = __ldg(inv_c + i);
-      if (d < 0) {
-        if (lane == 0 && dprob) dprob[i] = 0.f;
-        continue;
+    const int4* orow[KMAX];
+    int4* drow[KMAX];
+    float p[KMAX], dot[KMAX];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      orow[k] = nullptr;
+      drow[k] = nullptr;
+      p[k] = 1.f;
+      dot[k] = 0.f;
+      if (k < K) {
+        const long long i = (long long)t * K + k;
+        const int d = __ldg(inv_c + i);
+        if (d >= 0) {
+          const int e = __ldg(topk_idx + i);
+          const long long row = (long long)__ldg(base + e) + d;
+          if (o_local) orow[k] = o_local + (long long)d * hv;
+          drow[k] = reinterpret_cast<int4*>(d_peers[e / el]) + row * hv;
+          if (prob) p[k] = __ldg(prob + i);
+        }
       }
-      const int e = __ldg(topk_idx + i);
-      const int r = e / el;
-      const long long row = (long long)__ldg(base + e) + d;
-      const float p = prob ? __ldg(prob + i) : 1.0f;
-      const int4* yr = dy + (long long)t * hv;
-      const int4* orow = o_peers ? reinterpret_cast<const int4*>(o_peers[r]) + row * hv : nullptr;
-      int4* drow = reinterpret_cast<int4*>(d_peers[r]) + row * hv;
-      float dot = 0.f;
-      for (int c = lane; c < hv; c += 32) {
-        const int4 v = ld_nc_v4(yr + c);
-        const uint32_t* u = reinterpret_cast<const uint32_t*>(&v);
-        if (orow) {
-          const int4 ov = ld_v4(orow + c);
-          const uint32_t* uo = reinterpret_cast<const uint32_t*>(&ov);
+    }
+    for (int c0 = 0; c0 < hv; c0 += 32 * VPL) {
+      int4 y[VPL], ov[KMAX][VPL];
+#pragma unroll
+      for (int u = 0; u < VPL; ++u) {
+        const int c = c0 + u * 32 + lane;
+        if (c < hv) y[u] = ld_nc_v4(dy + (long long)t * hv + c);
+      }
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+#pragma unroll
+        for (int u = 0; u < VPL; ++u) {
+          const int c = c0 + u * 32 + lane;
+          if (orow[k] && c < hv) ov[k][u] = ld_nc_v4(orow[k] + c);
+        }
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        if (!drow[k]) continue;
+#pragma unroll
+        for (int u = 0; u < VPL; ++u) {
+          const int c = c0 + u * 32 + lane;
+          if (c >= hv) continue;
+          const uint32_t* uy = reinterpret_cast<const uint32_t*>(&y[u]);
+          int4 wv;
+          uint32_t* uw = reinterpret_cast<uint32_t*>(&wv);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const float2 a = unpack_bf16x2(u[j]);
-            const float2 b = unpack_bf16x2(uo[j]);
-            dot += a.x * b.x + a.y * b.y;
+            const float2 a = unpack_bf16x2(uy[j]);
+            if (orow[k]) {
+              const float2 b = unpack_bf16x2(reinterpret_cast<const uint32_t*>(&ov[k][u])[j]);
+              dot[k] += a.x * b.x + a.y * b.y;
+            }
+            uw[j] = prob ? pack_bf16x2(a.x * p[k], a.y * p[k]) : uy[j];
           }
+          drow[k][c] = wv;
         }
-        int4 w;
-        if (prob) {
-          uint32_t* uw = reinterpret_cast<uint32_t*>(&w);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float2 a = unpack_bf16x2(u[j]);
-            uw[j] = pack_bf16x2(a.x * p, a.y * p);
-          }
-        } else {
-          w = v;
-        }
-        drow[c] = w;
       }
-      if (dprob && orow) {
-        dot = warp_sum(dot);
-        if (lane == 0) dprob[i] = dot;
+    }
+    if (dprob) {
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        if (k >= K) break;
+        const float s = warp_sum(dot[k]);
+        if (lane == 0) dprob[(long long)t * K + k] = (drow[k] && o_local) ? s : 0.f;
       }
     }
   }
@@ -272,26 +316,59 @@ int moe_ep_dispatch_push(const void* x, int T, int K, int h, const int* topk_idx
 int moe_ep_combine_pull(const unsigned long long* peers, int T, int K, int h,
                         const int* topk_idx, const int* inv_c, const int* base, int el,
                         const float* weights, const void* resid, const void* extra,
-                        const void* extra2, void* out, void* stream) {
-  if (h % 8 || el < 1) return kErrInvalidArg;
+                        const void* extra2, void* out, void* rows_copy, void* stream) {
+  if (h % 8 || el < 1 || K > 32) return kErrInvalidArg;
   if (T == 0) return kOk;
-  combine_pull_kernel<4><<<warp_grid(T), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      peers, T, K, h / 8, topk_idx, inv_c, base, el, weights, static_cast<const int4*>(resid),
-      static_cast<const int4*>(extra), static_cast<const int4*>(extra2),
-      static_cast<int4*>(out));
+  auto st = static_cast<cudaStream_t>(stream);
+  const auto* r = static_cast<const int4*>(resid);
+  const auto* x1 = static_cast<const int4*>(extra);
+  const auto* x2 = static_cast<const int4*>(extra2);
+  auto* o = static_cast<int4*>(out);
+  auto* cp = static_cast<int4*>(rows_copy);
+  const int hv = h / 8;
+#define PULL(V, KM)                                                                      \
+  combine_pull_kernel<V, KM><<<warp_grid(T), 256, 0, st>>>(peers, T, K, hv, topk_idx, inv_c, \
+                                                          base, el, weights, r, x1, x2, o, cp)
+  if (K <= 2)
+    PULL(4, 2);
+  else if (K <= 4)
+    PULL(4, 4);
+  else if (K <= 8)
+    PULL(2, 8);
+  else if (K <= 16)
+    PULL(1, 16);
+  else
+    PULL(1, 32);
+#undef PULL
   MOE_LAUNCH_CHECK();
   return kOk;
 }
 
-int moe_ep_combine_bwd_push(const void* dy, const unsigned long long* o_peers,
+int moe_ep_combine_bwd_push(const void* dy, const void* o_local,
                             const unsigned long long* d_peers, int T, int K, int h,
                             const int* topk_idx, const int* inv_c, const int* base, int el,
                             const float* prob, float* dprob, void* stream) {
-  if (h % 8 || el < 1) return kErrInvalidArg;
+  if (h % 8 || el < 1 || K > 32) return kErrInvalidArg;
   if (T == 0) return kOk;
-  combine_bwd_push_kernel<<<warp_grid(T), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const int4*>(dy), o_peers, d_peers, T, K, h / 8, topk_idx, inv_c, base, el,
-      prob, dprob);
+  auto st = static_cast<cudaStream_t>(stream);
+  const auto* y = static_cast<const int4*>(dy);
+  const auto* ol = static_cast<const int4*>(o_local);
+  const int hv = h / 8;
+#define PUSH(V, KM)                                                                        \
+  combine_bwd_push_kernel<V, KM><<<warp_grid(T), 256, 0, st>>>(y, ol, d_peers, T, K, hv,     \
+                                                              topk_idx, inv_c, base, el, prob, \
+                                                              dprob)
+  if (K <= 2)
+    PUSH(4, 2);
+  else if (K <= 4)
+    PUSH(4, 4);
+  else if (K <= 8)
+    PUSH(2, 8);
+  else if (K <= 16)
+    PUSH(1, 16);
+  else
+    PUSH(1, 32);
+#undef PUSH
   MOE_LAUNCH_CHECK();
   return kOk;
 }

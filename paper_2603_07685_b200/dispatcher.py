@@ -423,13 +423,19 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         shared = shared_expert_forward(x, w1s, w2s) if w1s is not None else None
         pool.barrier()
         y = torch.empty_like(x)
+        # local compact copy of the pulled expert outputs: the backward's dprob = <dY, O>
+        # then reads local memory instead of pulling O over NVLink a second time
+        o_local = None
+        if not cfg.mem_efficient:
+            o_local = torch.empty((max(sum(hp.send_splits), 1), h), dtype=x.dtype, device=dev)
         _lib.call("moe_ep_combine_pull", o_peers.data_ptr(), t, K, h, r.topk_idx.data_ptr(),
                   splan.inv_map.data_ptr(), base_d.data_ptr(), el,
                   None if cfg.mem_efficient else r.topk_prob.data_ptr(),
                   x.data_ptr() if cap >= 0 else None,
                   shared[-1].data_ptr() if shared is not None else None, None, y.data_ptr(),
-                  stream)
+                  o_local.data_ptr() if o_local is not None else None, stream)
         ctx.cfg, ctx.ep, ctx.r, ctx.splan, ctx.cap, ctx.pair = cfg, ep, r, splan, cap, pair
+        ctx.o_local = o_local
         ctx.tabs = (base_d, be_d, nmb, meta_d, off_pad_d, map_pad, rows_alloc, el)
         ctx.row_prob = row_prob
         ctx.shared = shared[:-1] if shared is not None else None
@@ -449,14 +455,13 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         dy = dy.contiguous()
         xp, _ = pool.get("xp", rows_alloc * h, torch.bfloat16)
         xp = xp[: rows_alloc * h].view(rows_alloc, h)
-        _, o_peers = pool.get("o", rows_alloc * h, torch.bfloat16)
         d_o, d_peers = pool.get("do", rows_alloc * h, torch.bfloat16)
         d_o = d_o[: rows_alloc * h].view(rows_alloc, h)
         _lib.call("moe_zero_pad_rows", meta_d.data_ptr(), map_pad.data_ptr(), h, d_o.data_ptr(),
                   stream)
         dprob = torch.empty((t, K), dtype=torch.float32, device=dev)
         _lib.call("moe_ep_combine_bwd_push", dy.data_ptr(),
-                  None if cfg.mem_efficient else o_peers.data_ptr(), d_peers.data_ptr(), t, K,
+                  None if cfg.mem_efficient else ctx.o_local.data_ptr(), d_peers.data_ptr(), t, K,
                   h, r.topk_idx.data_ptr(), splan.inv_map.data_ptr(), base_d.data_ptr(), el,
                   None if cfg.mem_efficient else r.topk_prob.data_ptr(),
                   None if cfg.mem_efficient else dprob.data_ptr(), stream)
@@ -490,7 +495,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         _lib.call("moe_ep_combine_pull", dxp_peers.data_ptr(), t, K, h, r.topk_idx.data_ptr(),
                   splan.inv_map.data_ptr(), base_d.data_ptr(), el, None,
                   dy.data_ptr() if ctx.cap >= 0 else None, dx_router.data_ptr(),
-                  dx_shared.data_ptr() if dx_shared is not None else None, dx.data_ptr(),
+                  dx_shared.data_ptr() if dx_shared is not None else None, dx.data_ptr(), None,
                   stream)
         # no rank may overwrite the symmetric buffers before every rank has pulled
         pool.barrier()

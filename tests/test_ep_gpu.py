@@ -22,6 +22,7 @@ CASES = {
     "sigmoid_many": dict(E=16, K=4, h=256, m=256, T=192, score="sigmoid", cf=None, pad=False),
     "mem_efficient": dict(E=8, K=2, h=256, m=256, T=128, score="softmax", cf=None, pad=False,
                           mem=True),
+    "top8": dict(E=16, K=8, h=256, m=256, T=160, score="softmax", cf=None, pad=False),
 }
 
 
