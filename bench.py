@@ -327,6 +327,29 @@ def run_gpu(args, c) -> None:
             cnt = allc.sum(0)
     cnt = cnt.cpu().double()
     cap_g = cfg.capacity(n * T)
+    # ---- NVLink traffic of the EP exchange (exact, from this step's device counts) -------
+    nvlink_stats = None
+    if n > 1:
+        from oracle.routing_ref import a2a_send_volume  # the reference byte model (perf.py:62)
+
+        from paper_2603_07685_b200.dispatcher import last_exchange
+
+        ex_names = ("moe_ep_dispatch_push", "moe_ep_combine_pull", "moe_ep_combine_bwd_push",
+                    "moe_gather_rows")
+        ex_ms = sum(sum(v) for k_, v in per_kernel.items() if k_ in ex_names) / args.steps
+        # per step: 4 one-way transfers of this rank's remote rows (x, O, dO, dX); with
+        # balanced routing each direction of the NVLink port carries ~4 x sent bytes
+        out_bytes = 2 * last_exchange["bytes_sent_remote"] + 2 * last_exchange["bytes_recv_remote"]
+        nvlink_stats = {
+            "transport": args.ep_transport,
+            "bytes_out_per_step_per_gpu": out_bytes,
+            "model_bytes_per_step_per_gpu": 4 * a2a_send_volume(T, K, h, n, 2),
+            "exchange_kernel_ms_per_step": round(ex_ms, 4),
+            "achieved_GBps_per_direction": (round(out_bytes / (ex_ms / 1e3) / 1e9, 1)
+                                            if ex_ms and args.ep_transport == "p2p" else None),
+            "peak_GBps_per_direction": 770.0,
+            "peak_source": "B200_PROFILING.md measured peer copy (nominal 900)",
+        }
     routing_stats = {
         "skew_alpha": skew,
         "max_over_mean_expert_load": round(float(cnt.max() / cnt.mean()), 4),
@@ -402,6 +425,7 @@ def run_gpu(args, c) -> None:
                                    sorted(per_kernel.items(), key=lambda kv: -sum(kv[1]))},
             "clocks": clk,
             "routing": routing_stats,
+            "nvlink": nvlink_stats,
         }
         if n == 1 and not args.no_cpu_baseline:
             thr = cpu_threads()

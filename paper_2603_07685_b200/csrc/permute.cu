@@ -357,10 +357,80 @@ __global__ void combine_kernel(const int4* __restrict__ rows, int T, int K, int 
   }
 }
 
-// Combine backward (standard combine): for each kept selection of token t
+// Combine backward, K <= KMAX (token-major): each dY chunk is read ONCE per token and the K
+// expert-output rows of the chunk are loaded together; per selection
 //   dO[dest] = p * dY[t]          (bf16, input of the fc2 dgrad / wgrad)
 //   dprob[t,k] = <dY[t], O[dest]> (fp32; 0 for dropped selections)
 // With O == NULL (mem-efficient combine) it only scatters dY unscaled.
+template <int VPL, int KMAX>
+__global__ void combine_bwd_mlp_kernel(const int4* __restrict__ dy,
+                                       const int4* __restrict__ o_rows, int T, int K, int hv,
+                                       const int* __restrict__ inv_map,
+                                       const float* __restrict__ prob,
+                                       int4* __restrict__ d_rows, float* __restrict__ dprob) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = lane_id();
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp; t < T; t += nwarps) {
+    int dst[KMAX];
+    float p[KMAX], dot[KMAX];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      dst[k] = k < K ? __ldg(inv_map + (long long)t * K + k) : -1;
+      p[k] = (prob && dst[k] >= 0) ? __ldg(prob + (long long)t * K + k) : 1.f;
+      dot[k] = 0.f;
+    }
+    for (int c0 = 0; c0 < hv; c0 += 32 * VPL) {
+      int4 y[VPL], ov[KMAX][VPL];
+#pragma unroll
+      for (int u = 0; u < VPL; ++u) {
+        const int c = c0 + u * 32 + lane;
+        if (c < hv) y[u] = ld_nc_v4(dy + (long long)t * hv + c);
+      }
+      if (o_rows) {
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+#pragma unroll
+          for (int u = 0; u < VPL; ++u) {
+            const int c = c0 + u * 32 + lane;
+            if (dst[k] >= 0 && c < hv) ov[k][u] = ld_nc_v4(o_rows + (long long)dst[k] * hv + c);
+          }
+      }
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        if (dst[k] < 0) continue;
+#pragma unroll
+        for (int u = 0; u < VPL; ++u) {
+          const int c = c0 + u * 32 + lane;
+          if (c >= hv) continue;
+          const uint32_t* uy = reinterpret_cast<const uint32_t*>(&y[u]);
+          int4 wv;
+          uint32_t* uw = reinterpret_cast<uint32_t*>(&wv);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 a = unpack_bf16x2(uy[j]);
+            if (o_rows) {
+              const float2 b = unpack_bf16x2(reinterpret_cast<const uint32_t*>(&ov[k][u])[j]);
+              dot[k] += a.x * b.x + a.y * b.y;
+            }
+            uw[j] = prob ? pack_bf16x2(a.x * p[k], a.y * p[k]) : uy[j];
+          }
+          st_na_v4(d_rows + (long long)dst[k] * hv + c, wv);
+        }
+      }
+    }
+    if (dprob) {
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        if (k >= K) break;
+        const float s = warp_sum(dot[k]);
+        if (lane == 0) dprob[(long long)t * K + k] = (dst[k] >= 0 && o_rows) ? s : 0.f;
+      }
+    }
+  }
+}
+
+// Combine backward, any K (selection-major fallback).
 __global__ void combine_bwd_kernel(const int4* __restrict__ dy, const int4* __restrict__ o_rows,
                                    int T, int K, int hv, const int* __restrict__ inv_map,
                                    const float* __restrict__ prob, int4* __restrict__ d_rows,
@@ -631,9 +701,22 @@ int moe_combine_bwd(const void* dy, const void* o_rows, int T, int K, int h, con
                     const float* prob, void* d_rows, float* dprob, void* stream) {
   if (h % 8) return kErrInvalidArg;
   if (T == 0) return kOk;
-  combine_bwd_kernel<<<warp_grid(T), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const int4*>(dy), static_cast<const int4*>(o_rows), T, K, h / 8, inv_map, prob,
-      static_cast<int4*>(d_rows), dprob);
+  auto st = static_cast<cudaStream_t>(stream);
+  const auto* y = static_cast<const int4*>(dy);
+  const auto* o = static_cast<const int4*>(o_rows);
+  auto* d = static_cast<int4*>(d_rows);
+  const int hv = h / 8;
+  if (K <= 2)
+    combine_bwd_mlp_kernel<4, 2><<<warp_grid(T), 256, 0, st>>>(y, o, T, K, hv, inv_map, prob, d,
+                                                              dprob);
+  else if (K <= 4)
+    combine_bwd_mlp_kernel<4, 4><<<warp_grid(T), 256, 0, st>>>(y, o, T, K, hv, inv_map, prob, d,
+                                                              dprob);
+  else if (K <= 8)
+    combine_bwd_mlp_kernel<2, 8><<<warp_grid(T), 256, 0, st>>>(y, o, T, K, hv, inv_map, prob, d,
+                                                              dprob);
+  else
+    combine_bwd_kernel<<<warp_grid(T), 256, 0, st>>>(y, o, T, K, hv, inv_map, prob, d, dprob);
   MOE_LAUNCH_CHECK();
   return kOk;
 }

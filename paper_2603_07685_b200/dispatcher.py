@@ -201,6 +201,7 @@ class _MoEEPFunction(torch.autograd.Function):
         cap = cfg.capacity(n * t)  # global capacity on the global batch
         align = ops.pick_align(n * t, K, E)
         hp = ep_host_plan(counts_all, ep.rank, cap, cfg.pad_to_capacity, align)
+        _record_exchange(hp, h)
         pair = align == 2 * ops.ALIGN
         aux_v, aux_g = global_aux(counts_all, g[:, E:], t, K, cfg.aux_loss_coeff)
         small = torch.from_numpy(np.concatenate([[aux_v], aux_g]).astype(np.float32))
@@ -328,6 +329,23 @@ class SymmPool:
 
 _POOLS: dict = {}
 
+# Exact rows / bytes of the last forward's exchange on this rank (measurement only):
+# rows this rank sends to other ranks and receives from them; each of the four exchanges
+# of a fwd+bwd step (x dispatch, output combine, dO dispatch, dX combine) moves one
+# direction's bytes of this amount over NVLink.
+last_exchange: dict = {}
+
+
+def _record_exchange(hp: EPHostPlan, h: int, width: int = 2):
+    me = hp.rank
+    el = hp.el
+    sent_remote = sum(s for d, s in enumerate(hp.send_splits) if d != me)
+    recv_remote = sum(s for d, s in enumerate(hp.recv_splits) if d != me)
+    last_exchange.update(rows_sent_remote=int(sent_remote), rows_recv_remote=int(recv_remote),
+                         bytes_sent_remote=int(sent_remote) * h * width,
+                         bytes_recv_remote=int(recv_remote) * h * width,
+                         local_experts=el)
+
 
 def _pool(ep: EPGroup, dev) -> SymmPool:
     key = (id(ep.group), dev.index)
@@ -375,6 +393,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         align = ops.pick_align(n * t, K, E)
         pair = align == 2 * ops.ALIGN
         base, rows_all, hp = p2p_tables(counts_all, ep.rank, cap, cfg.pad_to_capacity, align)
+        _record_exchange(hp, h)
         aux_v, aux_g = global_aux(counts_all, g[:, E:], t, K, cfg.aux_loss_coeff)
         rows_alloc = max(max(rows_all), 2 * ops.ALIGN)
         el = hp.el
