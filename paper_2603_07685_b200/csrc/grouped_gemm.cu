@@ -37,7 +37,13 @@ constexpr int BN = 256;  // output columns per tile
 constexpr int BK = 64;   // 64 bf16 = 128 B = one SWIZZLE_128B row
 constexpr int UMMA_K = 16;
 constexpr int TMEM_COLS = 512;  // 2 accumulator stages x 256 fp32 columns
-constexpr int NUM_THREADS = 192;
+// Epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter, each owning half the
+// tile's columns). Measured on B200: 8 warps did not speed up the dSwiGLU epilogue and cost
+// ~13% on fc1+SwiGLU (the extra warps share the MMA issuer's SMSP), so 4 it is.
+constexpr int EPI_WARPS = 4;
+constexpr int EPI_HALVES = EPI_WARPS / 4;
+constexpr int EPI_COLS = BN / EPI_HALVES;  // 128 columns per epilogue warp
+constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr int BAND_M = 16;  // raster: 16 M units share each swept n-block (L2 reuse)
 
 template <int CG>
@@ -191,7 +197,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 4 * CG);
+      mbar_init(&tempty_bar[s], EPI_WARPS * CG);
     }
     fence_mbar_init();
     fence_async_shared();
@@ -322,8 +328,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else {
-    // ===================== epilogue (warps 2..5, one TMEM lane quarter each) ==========
+    // ===================== epilogue (warps 2..9: lane quarter x column half) ===========
     const int q = warp & 3;
+    const int half = (warp - 2) / 4;
+    const int cb = half * EPI_COLS;  // this warp's first tile column
     const int row_local = q * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     int acc = 0;
@@ -336,18 +344,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // Expert with no rows: its weight gradient is exactly zero.
         if constexpr (EPI == EPI_BF16) {
           __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) +
-                             tl.expert * p.out_expert_stride + row * p.ldo + tl.n0;
+                             tl.expert * p.out_expert_stride + row * p.ldo + tl.n0 + cb;
           const int4 z = make_int4(0, 0, 0, 0);
 #pragma unroll 4
-          for (int c = 0; c < BN / 8; ++c) reinterpret_cast<int4*>(o)[c] = z;
+          for (int c = 0; c < EPI_COLS / 8; ++c) reinterpret_cast<int4*>(o)[c] = z;
         } else if constexpr (EPI == EPI_F32) {
           float* o = reinterpret_cast<float*>(p.out) + tl.expert * p.out_expert_stride +
-                     row * p.ldo + tl.n0;
+                     row * p.ldo + tl.n0 + cb;
           const int4 z = make_int4(0, 0, 0, 0);
 #pragma unroll 4
-          for (int c = 0; c < BN / 4; ++c) reinterpret_cast<int4*>(o)[c] = z;
+          for (int c = 0; c < EPI_COLS / 4; ++c) reinterpret_cast<int4*>(o)[c] = z;
         }
         continue;
+      }
+      // dSwiGLU: the first chunk's pre-activation (DRAM/L2 latency) is fetched while the
+      // tile's MMAs are still running; later chunks are prefetched one chunk ahead.
+      int4 pre_g[4], pre_u[4];
+      if constexpr (EPI == EPI_DSWIGLU) {
+        const __nv_bfloat16* pr = p.aux + row * p.ld_aux;
+        const int jc = tl.n0 + cb;
+        const long long pos0 = (long long)(jc >> 7) * 256 + (jc & 127);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          pre_g[v] = reinterpret_cast<const int4*>(pr + pos0)[v];
+          pre_u[v] = reinterpret_cast<const int4*>(pr + pos0 + 128)[v];
+        }
       }
       mbar_wait(&tfull_bar[acc], acc_ph);
       tc_fence_after();
@@ -356,13 +377,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if constexpr (EPI == EPI_BF16 || EPI == EPI_F32) {
         const long long ebase = GROUPED_K ? tl.expert * p.out_expert_stride : 0;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = 0; c < EPI_COLS / 32; ++c) {
+          const int col = cb + c * 32;
           uint32_t r[32];
-          tmem_ld_32x32b_x32(t_base + c * 32, r);
+          tmem_ld_32x32b_x32(t_base + col, r);
           tmem_ld_wait();
           if constexpr (EPI == EPI_BF16) {
             __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + ebase + row * p.ldo +
-                               tl.n0 + c * 32;
+                               tl.n0 + col;
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
               int4 w;
@@ -373,7 +395,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               reinterpret_cast<int4*>(o)[v] = w;
             }
           } else {
-            float* o = reinterpret_cast<float*>(p.out) + ebase + row * p.ldo + tl.n0 + c * 32;
+            float* o = reinterpret_cast<float*>(p.out) + ebase + row * p.ldo + tl.n0 + col;
 #pragma unroll
             for (int v = 0; v < 8; ++v)
               reinterpret_cast<int4*>(o)[v] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2],
@@ -381,16 +403,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       } else if constexpr (EPI == EPI_SWIGLU) {
-        // Tile columns [0,128) = gate rows, [128,256) = up rows of the interleaved W1.
+        // Tile columns [0,128) = gate rows, [128,256) = up rows of the interleaved W1; this
+        // warp takes gate columns [half*64, +64) and the matching up columns.
         const float scale = p.row_scale ? __ldg(p.row_scale + row) : 1.0f;
-        __nv_bfloat16* pre = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo + tl.n0;
+        __nv_bfloat16* pre =
+            reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo + tl.n0 + (cb >> 1);
         __nv_bfloat16* act =
-            reinterpret_cast<__nv_bfloat16*>(p.out2) + row * p.ldo2 + (tl.n0 >> 1);
+            reinterpret_cast<__nv_bfloat16*>(p.out2) + row * p.ldo2 + (tl.n0 >> 1) + (cb >> 1);
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < EPI_COLS / 64; ++c) {
           uint32_t g[32], u[32];
-          tmem_ld_32x32b_x32(t_base + c * 32, g);
-          tmem_ld_32x32b_x32(t_base + 128 + c * 32, u);
+          tmem_ld_32x32b_x32(t_base + (cb >> 1) + c * 32, g);
+          tmem_ld_32x32b_x32(t_base + 128 + (cb >> 1) + c * 32, u);
           tmem_ld_wait();
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
@@ -420,16 +444,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const __nv_bfloat16* pre_row = p.aux + row * p.ld_aux;
         __nv_bfloat16* dpre_row = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = 0; c < EPI_COLS / 32; ++c) {
           uint32_t r[32];
-          tmem_ld_32x32b_x32(t_base + c * 32, r);
-          const int j0 = tl.n0 + c * 32;
+          tmem_ld_32x32b_x32(t_base + cb + c * 32, r);
+          const int j0 = tl.n0 + cb + c * 32;
           const long long pos = (long long)(j0 >> 7) * 256 + (j0 & 127);
           int4 gv[4], uv[4];
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
-            gv[v] = reinterpret_cast<const int4*>(pre_row + pos)[v];
-            uv[v] = reinterpret_cast<const int4*>(pre_row + pos + 128)[v];
+            gv[v] = pre_g[v];
+            uv[v] = pre_u[v];
+          }
+          if (c + 1 < EPI_COLS / 32) {  // prefetch the next chunk's pre-activation
+            const int j1 = j0 + 32;
+            const long long pos1 = (long long)(j1 >> 7) * 256 + (j1 & 127);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              pre_g[v] = reinterpret_cast<const int4*>(pre_row + pos1)[v];
+              pre_u[v] = reinterpret_cast<const int4*>(pre_row + pos1 + 128)[v];
+            }
           }
           tmem_ld_wait();
 #pragma unroll
@@ -459,7 +492,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             reinterpret_cast<int4*>(dpre_row + pos + 128)[v] = wu;
           }
         }
-        if (p.row_partial) p.row_partial[row * p.ld_partial + tl.n0 / BN] = dp_acc;
+        if (p.row_partial)
+          p.row_partial[row * p.ld_partial + (tl.n0 / BN) * EPI_HALVES + half] = dp_acc;
       }
       tc_fence_before();
       __syncwarp();
@@ -666,7 +700,7 @@ int moe_gg_fc2_dgrad(const void* dout, const void* w2, const void* preact, int a
   p.ld_aux = 2 * m;
   p.row_scale = row_prob;
   p.row_partial = dprob_partial;
-  p.ld_partial = m / BN;
+  p.ld_partial = (m / BN) * EPI_HALVES;  // one partial per (n-tile, epilogue half)
   return run<false, true, false, EPI_DSWIGLU>(dout, h, a_rows, w2, m, (uint64_t)num_experts * h,
                                               p, p.max_m_blocks, pair,
                                               static_cast<cudaStream_t>(stream));

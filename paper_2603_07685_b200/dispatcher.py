@@ -487,7 +487,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         pool.barrier()
         part_peers = None
         if cfg.mem_efficient:
-            ldp = w2.shape[2] // 256
+            ldp = gemm.dprob_partials(w2.shape[2])
             part, part_peers = pool.get("part", rows_alloc * ldp, torch.float32)
             part = part[: rows_alloc * ldp].view(rows_alloc, ldp)
             d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, be_d, nmb, row_prob=ctx.row_prob,
@@ -502,7 +502,8 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         pool.barrier()
         if cfg.mem_efficient:
             _lib.call("moe_ep_dprob_pull", part_peers.data_ptr(), t, K, r.topk_idx.data_ptr(),
-                      splan.inv_map.data_ptr(), base_d.data_ptr(), el, w2.shape[2] // 256,
+                      splan.inv_map.data_ptr(), base_d.data_ptr(), el,
+                      gemm.dprob_partials(w2.shape[2]),
                       dprob.data_ptr(), stream)
         aux_scale = None if daux is None else daux.float()
         dw_r, dx_router = ops.router_backward(x, w_r_pad, r, dprob, cfg.score,

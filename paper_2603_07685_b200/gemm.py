@@ -13,6 +13,12 @@ from . import _lib
 
 BLOCK_M = 128
 GATE_UP_BLOCK = 128  # gate/up rows interleave granularity inside the stacked W1
+EPI_HALVES = 1       # epilogue warps per TMEM lane quarter (csrc/grouped_gemm.cu EPI_WARPS/4)
+
+
+def dprob_partials(m: int) -> int:
+    """Per-row dprob partials the fc2-dgrad epilogue writes: one per (256-col tile, half)."""
+    return (m // 256) * EPI_HALVES
 
 
 def _ptr(t):
@@ -91,7 +97,7 @@ def fc2_dgrad(dout, w2, preact, block_expert, num_m_blocks, row_prob=None, want_
     if d_preact is None:
         d_preact = torch.empty((rows, 2 * m), dtype=torch.bfloat16, device=dout.device)
     if want_dprob and part is None:
-        part = torch.empty((rows, m // 256), dtype=torch.float32, device=dout.device)
+        part = torch.empty((rows, dprob_partials(m)), dtype=torch.float32, device=dout.device)
     _lib.call("moe_gg_fc2_dgrad", dout.data_ptr(), w2.data_ptr(), preact.data_ptr(), a_rows, rows,
               h, m, e, block_expert.data_ptr(), num_m_blocks.data_ptr(), _ptr(row_prob),
               d_preact.data_ptr(), _ptr(part), int(pair), _stream())
