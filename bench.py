@@ -335,7 +335,7 @@ def run_gpu(args, c) -> None:
         from paper_2603_07685_b200.dispatcher import last_exchange
 
         ex_names = ("moe_ep_dispatch_push", "moe_ep_combine_pull", "moe_ep_combine_bwd_push",
-                    "moe_gather_rows")
+                    "moe_gather_rows", "moe_ep_dispatch_dedup", "moe_ep_expand_grad")
         ex_ms = sum(sum(v) for k_, v in per_kernel.items() if k_ in ex_names) / args.steps
         # per step: 4 one-way transfers of this rank's remote rows (x, O, dO, dX); with
         # balanced routing each direction of the NVLink port carries ~4 x sent bytes
@@ -347,6 +347,8 @@ def run_gpu(args, c) -> None:
             "exchange_kernel_ms_per_step": round(ex_ms, 4),
             "achieved_GBps_per_direction": (round(out_bytes / (ex_ms / 1e3) / 1e9, 1)
                                             if ex_ms and args.ep_transport == "p2p" else None),
+            "note": ("p2p_dedup sends one row per (token, rank): fewer bytes than counted here"
+                     if args.ep_transport == "p2p_dedup" else None),
             "peak_GBps_per_direction": 770.0,
             "peak_source": "B200_PROFILING.md measured peer copy (nominal 900)",
         }
@@ -487,7 +489,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-tokens", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ep-transport", default="p2p", choices=["p2p", "nccl"],
+    ap.add_argument("--ep-transport", default="p2p", choices=["p2p", "p2p_dedup", "nccl"],
                     help="EP exchange: fused NVLink peer-memory kernels (p2p) or NCCL a2a")
     ap.add_argument("--skew", type=float, default=None,
                     help="router logit skew alpha (config 5 sweep: 0, 0.5, 1, 2)")

@@ -113,6 +113,23 @@ int moe_ep_combine_bwd_push(const void* dy, const void* o_local,
 int moe_ep_dprob_pull(const unsigned long long* part_peers, int T, int K, const int* topk_idx,
                       const int* inv_c, const int* base, int el, int ldp, float* dprob,
                       void* stream);
+/* Token de-duplication (HybridEP-style; leg byte model perf.py:81-160):
+ * one row per (token, destination rank) crosses NVLink; the destination expands it to its
+ * expert rows and pre-reduces the token's expert outputs. */
+int moe_ep_token_ranks(const int* topk_idx, const int* inv_c, int T, int K, int el,
+                       int* rank_idx, int* sel_j, int* sel_pos, void* stream);
+int moe_ep_dispatch_dedup(const void* x, int T, int K, int h, const int* topk_idx,
+                          const int* inv_c, const int* base, int el, const int* rank_idx,
+                          const int* inv_rank, const int* tbase, const int* sel_j,
+                          const int* sel_pos, const float* prob,
+                          const unsigned long long* tok_peers,
+                          const unsigned long long* map_peers,
+                          const unsigned long long* srows_peers,
+                          const unsigned long long* sprob_peers,
+                          const unsigned long long* rprob_peers, void* stream);
+int moe_ep_fill_pad_map(const int* map_pad, int rows, int* map, void* stream);
+int moe_ep_expand_grad(const void* tok, const int* map, int rows, int h, const float* rowprob,
+                       const void* o, void* d_o, float* dprob_rows, void* stream);
 
 /* ------------------------------------------------------------------ grouped GEMM (tcgen05)
  * replaces expert_activation()/expert_forward() routing.py:59-68 per expert block and the

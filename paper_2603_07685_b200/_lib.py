@@ -52,6 +52,10 @@ SIGNATURES: dict[str, list] = {
     "moe_ep_combine_pull": [P, I, I, I, P, P, P, I, P, P, P, P, P, P, P],
     "moe_ep_combine_bwd_push": [P, P, P, I, I, I, P, P, P, I, P, P, P],
     "moe_ep_dprob_pull": [P, I, I, P, P, P, I, I, P, P],
+    "moe_ep_token_ranks": [P, P, I, I, I, P, P, P, P],
+    "moe_ep_dispatch_dedup": [P, I, I, I, P, P, P, I, P, P, P, P, P, P, P, P, P, P, P, P],
+    "moe_ep_fill_pad_map": [P, I, P, P],
+    "moe_ep_expand_grad": [P, P, I, I, P, P, P, P, P],
     # grouped GEMM (csrc/grouped_gemm.cu)
     "moe_gg_fc1_fwd": [P, P, I, I, I, I, I, P, P, P, P, P, I, P],
     "moe_gg_fc2_fwd": [P, P, I, I, I, I, I, P, P, P, I, P],

@@ -277,6 +277,171 @@ __global__ void dprob_pull_kernel(const unsigned long long* __restrict__ part_pe
   dprob[i] = s;
 }
 
+// ---------------------------------------------------------------- token de-duplication
+// (HybridEP-style; byte model perf.py:81-160): a token is sent ONCE to
+// every destination rank that hosts at least one of its kept experts; the destination
+// expands it to its expert rows locally and pre-reduces the token's expert outputs before
+// the source pulls one row per (token, rank).
+
+// Per token: distinct destination ranks of its kept selections (ascending, -1 padded), and
+// per selection the index of its rank in that list and its position among the token's
+// selections on that rank. Selections are ascending by expert, so ranks are non-decreasing.
+__global__ void token_ranks_kernel(const int* __restrict__ topk_idx,
+                                   const int* __restrict__ inv_c, int T, int K, int el,
+                                   int* __restrict__ rank_idx, int* __restrict__ sel_j,
+                                   int* __restrict__ sel_pos) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  int j = -1, pos = 0, last = -1;
+  for (int k = 0; k < K; ++k) {
+    const long long i = (long long)t * K + k;
+    if (inv_c[i] < 0) {
+      sel_j[i] = -1;
+      sel_pos[i] = -1;
+      continue;
+    }
+    const int r = topk_idx[i] / el;
+    if (r != last) {
+      ++j;
+      pos = 0;
+      last = r;
+      rank_idx[(long long)t * K + j] = r;
+    } else {
+      ++pos;
+    }
+    sel_j[i] = j;
+    sel_pos[i] = pos;
+  }
+  for (int jj = j + 1; jj < K; ++jj) rank_idx[(long long)t * K + jj] = -1;
+}
+
+// Dedup dispatch: x[t] -> tok_peers[d][tbase[d] + inv_rank[t,j]] once per distinct rank d,
+// plus, per kept selection on d: expand map (expert row -> token row), the token row's
+// slot table (row, prob) used by the destination's partial combine, and the row's prob.
+template <int VPL>
+__global__ void dispatch_dedup_kernel(const int4* __restrict__ x, int T, int K, int hv,
+                                      const int* __restrict__ topk_idx,
+                                      const int* __restrict__ inv_c,
+                                      const int* __restrict__ base, int el,
+                                      const int* __restrict__ rank_idx,
+                                      const int* __restrict__ inv_rank,
+                                      const int* __restrict__ tbase,
+                                      const int* __restrict__ sel_j,
+                                      const int* __restrict__ sel_pos,
+                                      const float* __restrict__ prob,
+                                      const unsigned long long* __restrict__ tok_peers,
+                                      const unsigned long long* __restrict__ map_peers,
+                                      const unsigned long long* __restrict__ srows_peers,
+                                      const unsigned long long* __restrict__ sprob_peers,
+                                      const unsigned long long* __restrict__ rprob_peers) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = lane_id();
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp; t < T; t += nwarps) {
+    const long long tk = (long long)t * K;
+    // metadata: lane k handles selection k, lane j handles the -1 fill of rank slot j
+    for (int k = lane; k < K; k += 32) {
+      const int j = __ldg(sel_j + tk + k);
+      if (j < 0) continue;
+      const int e = __ldg(topk_idx + tk + k);
+      const int d = e / el;
+      const long long r = (long long)__ldg(base + e) + __ldg(inv_c + tk + k);
+      const long long trow = (long long)__ldg(tbase + d) + __ldg(inv_rank + tk + j);
+      const float p = prob ? __ldg(prob + tk + k) : 1.0f;
+      reinterpret_cast<int*>(map_peers[d])[r] = (int)trow;
+      reinterpret_cast<int*>(srows_peers[d])[trow * K + __ldg(sel_pos + tk + k)] = (int)r;
+      reinterpret_cast<float*>(sprob_peers[d])[trow * K + __ldg(sel_pos + tk + k)] = p;
+      reinterpret_cast<float*>(rprob_peers[d])[r] = p;
+    }
+    for (int j = lane; j < K; j += 32) {
+      const int d = __ldg(rank_idx + tk + j);
+      if (d < 0) continue;
+      int cnt = 0;
+      for (int k = 0; k < K; ++k) cnt += (__ldg(sel_j + tk + k) == j);
+      const long long trow = (long long)__ldg(tbase + d) + __ldg(inv_rank + tk + j);
+      for (int pos = cnt; pos < K; ++pos)
+        reinterpret_cast<int*>(srows_peers[d])[trow * K + pos] = -1;
+    }
+    // the row itself, once per destination rank
+    const int4* src = x + (long long)t * hv;
+    for (int c0 = 0; c0 < hv; c0 += 32 * VPL) {
+      int4 v[VPL];
+#pragma unroll
+      for (int u = 0; u < VPL; ++u) {
+        const int c = c0 + u * 32 + lane;
+        if (c < hv) v[u] = ld_nc_v4(src + c);
+      }
+      for (int j = 0; j < K; ++j) {
+        const int d = __ldg(rank_idx + tk + j);
+        if (d < 0) break;
+        const long long trow = (long long)__ldg(tbase + d) + __ldg(inv_rank + tk + j);
+        int4* dst = reinterpret_cast<int4*>(tok_peers[d]) + trow * hv;
+#pragma unroll
+        for (int u = 0; u < VPL; ++u) {
+          const int c = c0 + u * 32 + lane;
+          if (c < hv) dst[c] = v[u];
+        }
+      }
+    }
+  }
+  __threadfence_system();
+}
+
+// map[r] = -1 for the padding / phantom rows of the local plan (map_pad < 0); real rows
+// are written by the sources' dedup dispatch (disjoint entries, no race).
+__global__ void fill_pad_map_kernel(const int* __restrict__ map_pad, int rows,
+                                    int* __restrict__ map) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
+    if (map_pad[r] < 0) map[r] = -1;
+}
+
+// Expert-side backward expansion: d_o[r] = p_r * tok[map[r]] (p_r = 1 without rowprob),
+// dprob_rows[r] = <tok[map[r]], o[r]> (standard combine); zero rows where map[r] < 0.
+__global__ void expand_grad_kernel(const int4* __restrict__ tok, const int* __restrict__ map,
+                                   int rows, int hv, const float* __restrict__ rowprob,
+                                   const int4* __restrict__ o, int4* __restrict__ d_o,
+                                   float* __restrict__ dprob_rows) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = lane_id();
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int4 z = make_int4(0, 0, 0, 0);
+  for (int r = warp; r < rows; r += nwarps) {
+    const int s = __ldg(map + r);
+    int4* dr = d_o + (long long)r * hv;
+    if (s < 0) {
+      for (int c = lane; c < hv; c += 32) st_na_v4(dr + c, z);
+      if (lane == 0 && dprob_rows) dprob_rows[r] = 0.f;
+      continue;
+    }
+    const float p = rowprob ? __ldg(rowprob + r) : 1.0f;
+    const int4* tr = tok + (long long)s * hv;
+    const int4* orow = o ? o + (long long)r * hv : nullptr;
+    float dot = 0.f;
+    for (int c = lane; c < hv; c += 32) {
+      const int4 v = ld_nc_v4(tr + c);
+      const uint32_t* u = reinterpret_cast<const uint32_t*>(&v);
+      int4 w;
+      uint32_t* uw = reinterpret_cast<uint32_t*>(&w);
+      int4 ov;
+      if (orow) ov = ld_nc_v4(orow + c);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 a = unpack_bf16x2(u[j]);
+        if (orow) {
+          const float2 b = unpack_bf16x2(reinterpret_cast<const uint32_t*>(&ov)[j]);
+          dot += a.x * b.x + a.y * b.y;
+        }
+        uw[j] = rowprob ? pack_bf16x2(a.x * p, a.y * p) : u[j];
+      }
+      st_na_v4(dr + c, w);
+    }
+    if (dprob_rows) {
+      dot = warp_sum(dot);
+      if (lane == 0) dprob_rows[r] = orow ? dot : 0.f;
+    }
+  }
+}
+
 static int sms() {
   static int n = 0;
   if (!n) {
@@ -369,6 +534,55 @@ int moe_ep_combine_bwd_push(const void* dy, const void* o_local,
   else
     PUSH(1, 32);
 #undef PUSH
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+int moe_ep_token_ranks(const int* topk_idx, const int* inv_c, int T, int K, int el,
+                       int* rank_idx, int* sel_j, int* sel_pos, void* stream) {
+  if (el < 1 || K < 1) return kErrInvalidArg;
+  if (T == 0) return kOk;
+  token_ranks_kernel<<<ceil_div_i(T, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      topk_idx, inv_c, T, K, el, rank_idx, sel_j, sel_pos);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+int moe_ep_dispatch_dedup(const void* x, int T, int K, int h, const int* topk_idx,
+                          const int* inv_c, const int* base, int el, const int* rank_idx,
+                          const int* inv_rank, const int* tbase, const int* sel_j,
+                          const int* sel_pos, const float* prob,
+                          const unsigned long long* tok_peers,
+                          const unsigned long long* map_peers,
+                          const unsigned long long* srows_peers,
+                          const unsigned long long* sprob_peers,
+                          const unsigned long long* rprob_peers, void* stream) {
+  if (h % 8 || el < 1) return kErrInvalidArg;
+  if (T == 0) return kOk;
+  dispatch_dedup_kernel<4><<<warp_grid(T), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const int4*>(x), T, K, h / 8, topk_idx, inv_c, base, el, rank_idx, inv_rank,
+      tbase, sel_j, sel_pos, prob, tok_peers, map_peers, srows_peers, sprob_peers,
+      rprob_peers);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+int moe_ep_fill_pad_map(const int* map_pad, int rows, int* map, void* stream) {
+  if (rows <= 0) return kOk;
+  const int blocks = ceil_div_i(rows, 256) < sms() * 4 ? ceil_div_i(rows, 256) : sms() * 4;
+  fill_pad_map_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(map_pad, rows,
+                                                                             map);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+int moe_ep_expand_grad(const void* tok, const int* map, int rows, int h, const float* rowprob,
+                       const void* o, void* d_o, float* dprob_rows, void* stream) {
+  if (h % 8) return kErrInvalidArg;
+  if (rows <= 0) return kOk;
+  expand_grad_kernel<<<warp_grid(rows), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const int4*>(tok), map, rows, h / 8, rowprob, static_cast<const int4*>(o),
+      static_cast<int4*>(d_o), dprob_rows);
   MOE_LAUNCH_CHECK();
   return kOk;
 }

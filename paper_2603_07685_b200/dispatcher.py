@@ -522,19 +522,220 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         return (dx, dw_r.to(torch.bfloat16), dw1, dw2, None, dw1s, dw2s, None, None)
 
 
+def _excl(a):
+    a = np.asarray(a, dtype=np.int64)
+    return np.cumsum(a) - a
+
+
+class _MoEEPDedupFunction(torch.autograd.Function):
+    """p2p transport with token de-duplication: one row per (token, destination rank) over
+    NVLink each way; destinations expand rows locally and pre-reduce per-token outputs."""
+
+    @staticmethod
+    def forward(ctx, x, w_r, w1, w2, sel_bias, w1s, w2s, cfg: MoEConfig, ep: EPGroup):
+        t, h = x.shape
+        E, K = cfg.num_experts, cfg.top_k
+        n = ep.n
+        me = ep.rank
+        dev = x.device
+        pool = _pool(ep, dev)
+        stream = torch.cuda.current_stream().cuda_stream
+        i32 = dict(dtype=torch.int32, device=dev)
+        w_r_t, w_r_pad = ops.stage_router_weight(w_r)
+        r = ops.router_forward(x, w_r, K, cfg.score, sel_bias, 0.0, w_r_t=w_r_t)
+        cap = cfg.capacity(n * t)
+        el = E // n
+
+        def token_ranks(splan_):
+            rank_idx = torch.empty((t, K), **i32)
+            sel_j = torch.empty((t, K), **i32)
+            sel_pos = torch.empty((t, K), **i32)
+            _lib.call("moe_ep_token_ranks", r.topk_idx.data_ptr(), splan_.inv_map.data_ptr(), t, K,
+                      el, rank_idx.data_ptr(), sel_j.data_ptr(), sel_pos.data_ptr(), stream)
+            rplan_ = ops.build_plan(rank_idx, None, n, -1, False, compact=True)
+            return rank_idx, sel_j, sel_pos, rplan_
+
+        if cap < 0:
+            splan = ops.build_plan(r.topk_idx, r.topk_prob, E, -1, False, compact=True)
+            rank_idx, sel_j, sel_pos, rplan = token_ranks(splan)
+            stats = torch.cat([r.counts.float(), r.mean_scores, rplan.counts.float()])
+            gathered = torch.empty((n, 2 * E + n), dtype=torch.float32, device=dev)
+            dist.all_gather_into_tensor(gathered, stats, group=ep.group)
+            g = gathered.cpu().numpy()  # the one host sync of the forward
+            counts_all = np.rint(g[:, :E]).astype(np.int64)
+            ntok = np.rint(g[:, 2 * E:]).astype(np.int64)
+        else:
+            stats = torch.cat([r.counts.float(), r.mean_scores])
+            gathered = torch.empty((n, 2 * E), dtype=torch.float32, device=dev)
+            dist.all_gather_into_tensor(gathered, stats, group=ep.group)
+            g = gathered.cpu().numpy()
+            counts_all = np.rint(g[:, :E]).astype(np.int64)
+        align = ops.pick_align(n * t, K, E)
+        pair = align == 2 * ops.ALIGN
+        base, rows_all, hp = p2p_tables(counts_all, me, cap, cfg.pad_to_capacity, align)
+        _record_exchange(hp, h)
+        if cap >= 0:  # capacity: the local plan needs the global prefix first
+            cap_e = torch.from_numpy(hp.cap_local.astype(np.int32)).pin_memory().to(
+                dev, non_blocking=True)
+            splan = ops.build_plan(r.topk_idx, r.topk_prob, E, -1, False, cap_e=cap_e,
+                                   compact=True)
+            rank_idx, sel_j, sel_pos, rplan = token_ranks(splan)
+            tc = rplan.counts.float()
+            gat2 = torch.empty((n, n), dtype=torch.float32, device=dev)
+            dist.all_gather_into_tensor(gat2, tc, group=ep.group)
+            ntok = np.rint(gat2.cpu().numpy()).astype(np.int64)
+        aux_v, aux_g = global_aux(counts_all, g[:, E:2 * E], t, K, cfg.aux_loss_coeff)
+        # token-slot tables: this rank as source (tbase) and as destination (tok rows)
+        # ntok[s, d] = tokens source s sends to destination d (one row each)
+        recv_tok_off = np.stack([_excl(ntok[:, d]) for d in range(n)], axis=1)  # [s, d]
+        tbase = recv_tok_off[me] - _excl(ntok[me])
+        tok_recv = int(ntok[:, me].sum())
+        tok_cap = max(int(ntok.sum(axis=0).max()), 1)
+        rows_alloc = max(max(rows_all), 2 * ops.ALIGN)
+        meta = np.array([hp.rows_pad // ops.ALIGN, hp.rows_pad, 0], dtype=np.int64)
+        parts = [base, hp.table.astype(np.int64), hp.block_expert, meta, tbase]
+        lens = [len(p_) for p_ in parts]
+        tab = torch.from_numpy(np.concatenate(parts).astype(np.int32)).pin_memory().to(
+            dev, non_blocking=True)
+        base_d, table_d, be_d, meta_d, tbase_d = torch.split(tab, lens)
+        smallf = torch.from_numpy(np.concatenate([[aux_v], aux_g]).astype(np.float32))
+        smallf = smallf.pin_memory().to(dev, non_blocking=True)
+        aux = smallf[0].clone()
+        r.aux_grad = smallf[1:]
+        nmb = meta_d[0:1]
+        off_pad_d = table_d[2 * n * el: 2 * n * el + el + 1]
+
+        tok, tok_peers = pool.get("dd_tok", tok_cap * h, torch.bfloat16)
+        mp, map_peers = pool.get("dd_map", rows_alloc, torch.int32)
+        srows, srows_peers = pool.get("dd_srows", tok_cap * K, torch.int32)
+        sprob, sprob_peers = pool.get("dd_sprob", tok_cap * K, torch.float32)
+        rprob, rprob_peers = pool.get("dd_rprob", rows_alloc, torch.float32)
+        partial, partial_peers = pool.get("dd_partial", tok_cap * h, torch.bfloat16)
+        tok = tok[: tok_cap * h].view(tok_cap, h)
+        partial = partial[: tok_cap * h].view(tok_cap, h)
+        map_pad = torch.empty((rows_alloc,), **i32)
+        if hp.rows_pad:
+            _lib.call("moe_ep_regroup_map", table_d.data_ptr(), n, el, hp.rows_pad,
+                      map_pad.data_ptr(), None, stream)
+        _lib.call("moe_ep_fill_pad_map", map_pad.data_ptr(), hp.rows_pad, mp.data_ptr(), stream)
+        _lib.call("moe_ep_dispatch_dedup", x.data_ptr(), t, K, h, r.topk_idx.data_ptr(),
+                  splan.inv_map.data_ptr(), base_d.data_ptr(), el, rank_idx.data_ptr(),
+                  rplan.inv_map.data_ptr(), tbase_d.data_ptr(), sel_j.data_ptr(),
+                  sel_pos.data_ptr(), r.topk_prob.data_ptr(), tok_peers.data_ptr(),
+                  map_peers.data_ptr(), srows_peers.data_ptr(), sprob_peers.data_ptr(),
+                  rprob_peers.data_ptr(), stream)
+        pool.barrier()
+        xp = torch.empty((rows_alloc, h), dtype=x.dtype, device=dev)
+        if hp.rows_pad:
+            ops.gather_rows(tok, mp[:rows_alloc], n=hp.rows_pad, out=xp)
+        row_prob = rprob[:rows_alloc] if cfg.mem_efficient else None
+        preact, act = gemm.fc1_fwd(xp, w1, be_d, nmb, row_prob, pair=pair)
+        o = gemm.fc2_fwd(act, w2, be_d, nmb, pair=pair)
+        if tok_recv:
+            _lib.call("moe_combine", o.data_ptr(), tok_recv, K, h, srows.data_ptr(),
+                      None if cfg.mem_efficient else sprob.data_ptr(), None, None, None,
+                      partial.data_ptr(), stream)
+        shared = shared_expert_forward(x, w1s, w2s) if w1s is not None else None
+        pool.barrier()
+        y = torch.empty_like(x)
+        _lib.call("moe_ep_combine_pull", partial_peers.data_ptr(), t, K, h,
+                  rank_idx.data_ptr(), rplan.inv_map.data_ptr(), tbase_d.data_ptr(), 1, None,
+                  x.data_ptr() if cap >= 0 else None,
+                  shared[-1].data_ptr() if shared is not None else None, None, y.data_ptr(),
+                  None, stream)
+        ctx.cfg, ctx.ep, ctx.r, ctx.cap, ctx.pair = cfg, ep, r, cap, pair
+        ctx.st = (splan, rplan, rank_idx, base_d, tbase_d, be_d, nmb, off_pad_d, rows_alloc,
+                  hp.rows_pad, tok_cap, tok_recv, el)
+        ctx.shared = shared[:-1] if shared is not None else None
+        ctx.save_for_backward(x, w_r_pad, w1, w2, xp, preact, act, o, w1s, w2s)
+        return y, aux
+
+    @staticmethod
+    def backward(ctx, dy, daux):
+        cfg, ep, r = ctx.cfg, ctx.ep, ctx.r
+        (splan, rplan, rank_idx, base_d, tbase_d, be_d, nmb, off_pad_d, rows_alloc, rows_pad,
+         tok_cap, tok_recv, el) = ctx.st
+        x, w_r_pad, w1, w2, xp, preact, act, o, w1s, w2s = ctx.saved_tensors
+        t, h = x.shape
+        K = cfg.top_k
+        dev = x.device
+        pool = _pool(ep, dev)
+        stream = torch.cuda.current_stream().cuda_stream
+        dy = dy.contiguous()
+        tok, tok_peers = pool.get("dd_tok", tok_cap * h, torch.bfloat16)
+        tok = tok[: tok_cap * h].view(tok_cap, h)
+        mp, _ = pool.get("dd_map", rows_alloc, torch.int32)
+        srows, _ = pool.get("dd_srows", tok_cap * K, torch.int32)
+        rprob, _ = pool.get("dd_rprob", rows_alloc, torch.float32)
+        partial, partial_peers = pool.get("dd_partial", tok_cap * h, torch.bfloat16)
+        partial = partial[: tok_cap * h].view(tok_cap, h)
+        dprows, dprows_peers = pool.get("dd_dprob_rows", rows_alloc, torch.float32)
+        # dY once per (token, rank)
+        _lib.call("moe_ep_dispatch_push", dy.data_ptr(), t, K, h, rank_idx.data_ptr(),
+                  rplan.inv_map.data_ptr(), tbase_d.data_ptr(), 1, tok_peers.data_ptr(), None,
+                  None, stream)
+        pool.barrier()
+        d_o = torch.empty((rows_alloc, h), dtype=dy.dtype, device=dev)
+        _lib.call("moe_ep_expand_grad", tok.data_ptr(), mp.data_ptr(), rows_pad, h,
+                  None if cfg.mem_efficient else rprob.data_ptr(),
+                  None if cfg.mem_efficient else o.data_ptr(), d_o.data_ptr(),
+                  None if cfg.mem_efficient else dprows.data_ptr(), stream)
+        part_peers = None
+        if cfg.mem_efficient:
+            ldp = gemm.dprob_partials(w2.shape[2])
+            part, part_peers = pool.get("part", rows_alloc * ldp, torch.float32)
+            part = part[: rows_alloc * ldp].view(rows_alloc, ldp)
+            d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, be_d, nmb, row_prob=rprob[:rows_alloc],
+                                      pair=ctx.pair, part=part)
+        else:
+            d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, be_d, nmb, pair=ctx.pair)
+        dw2 = gemm.wgrad(d_o, act, off_pad_d, el)
+        dxp = gemm.fc1_dgrad(d_pre, w1, be_d, nmb, pair=ctx.pair)
+        dw1 = gemm.wgrad(d_pre, xp, off_pad_d, el)
+        if tok_recv:
+            _lib.call("moe_combine", dxp.data_ptr(), tok_recv, K, h, srows.data_ptr(), None,
+                      None, None, None, partial.data_ptr(), stream)
+        pool.barrier()
+        dprob = torch.empty((t, K), dtype=torch.float32, device=dev)
+        if cfg.mem_efficient:
+            _lib.call("moe_ep_dprob_pull", part_peers.data_ptr(), t, K, r.topk_idx.data_ptr(),
+                      splan.inv_map.data_ptr(), base_d.data_ptr(), el,
+                      gemm.dprob_partials(w2.shape[2]), dprob.data_ptr(), stream)
+        else:
+            _lib.call("moe_ep_dprob_pull", dprows_peers.data_ptr(), t, K, r.topk_idx.data_ptr(),
+                      splan.inv_map.data_ptr(), base_d.data_ptr(), el, 1, dprob.data_ptr(),
+                      stream)
+        aux_scale = None if daux is None else daux.float()
+        dw_r, dx_router = ops.router_backward(x, w_r_pad, r, dprob, cfg.score,
+                                              aux_scale=aux_scale)
+        dx_shared = dw1s = dw2s = None
+        if ctx.shared is not None:
+            dx_shared, dw1s, dw2s = shared_expert_backward(x, dy, w1s, w2s, ctx.shared)
+        dx = torch.empty_like(x)
+        _lib.call("moe_ep_combine_pull", partial_peers.data_ptr(), t, K, h, rank_idx.data_ptr(),
+                  rplan.inv_map.data_ptr(), tbase_d.data_ptr(), 1, None,
+                  dy.data_ptr() if ctx.cap >= 0 else None, dx_router.data_ptr(),
+                  dx_shared.data_ptr() if dx_shared is not None else None, dx.data_ptr(), None,
+                  stream)
+        pool.barrier()
+        return (dx, dw_r.to(torch.bfloat16), dw1, dw2, None, dw1s, dw2s, None, None)
+
+
 def moe_forward_ep(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
                    selection_bias=None, w1_shared=None, w2_shared=None, transport: str = "p2p"):
     """EP MoE layer: w1_local [E/EP, 2m, h], w2_local [E/EP, h, m] are this rank's experts
     (global experts [rank*E/EP, (rank+1)*E/EP)). Returns (y [T,h], global aux).
 
     transport "p2p" (default): the exchange is fused into the permute / combine kernels over
-    NVLink peer memory (csrc/ep.cu). "nccl": permute -> NCCL all_to_all_single -> regroup
-    (the baseline dispatcher, kept for A/B measurement).
+    NVLink peer memory (csrc/ep.cu). "p2p_dedup": the same with token de-duplication (one
+    row per (token, destination rank) each way; HybridEP-style). "nccl": permute -> NCCL
+    all_to_all_single -> regroup (the baseline dispatcher, kept for A/B measurement).
 
     The router weight gradient returned is this rank's partial sum over its own tokens;
     W_r is replicated, so its all-reduce belongs to the data-parallel gradient sync.
     """
     if cfg.num_experts % ep.n:
         raise ValueError(f"num_experts {cfg.num_experts} not divisible by EP {ep.n}")
-    fn = {"p2p": _MoEEPP2PFunction, "nccl": _MoEEPFunction}[transport]
+    fn = {"p2p": _MoEEPP2PFunction, "p2p_dedup": _MoEEPDedupFunction,
+          "nccl": _MoEEPFunction}[transport]
     return fn.apply(x, w_r, w1_local, w2_local, selection_bias, w1_shared, w2_shared, cfg, ep)

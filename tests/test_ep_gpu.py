@@ -126,7 +126,7 @@ def _worker(rank, world, port, case, q, transport):
         q.put((rank, traceback.format_exc() + repr(exc)))
 
 
-@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+@pytest.mark.parametrize("transport", ["p2p", "p2p_dedup", "nccl"])
 @pytest.mark.parametrize("name", list(CASES))
 def test_ep_layer_matches_global_oracle(name, transport):
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
