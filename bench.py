@@ -346,7 +346,8 @@ def run_gpu(args, c) -> None:
             "model_bytes_per_step_per_gpu": 4 * a2a_send_volume(T, K, h, n, 2),
             "exchange_kernel_ms_per_step": round(ex_ms, 4),
             "achieved_GBps_per_direction": (round(out_bytes / (ex_ms / 1e3) / 1e9, 1)
-                                            if ex_ms and args.ep_transport == "p2p" else None),
+                                            if ex_ms and args.ep_transport in ("p2p", "auto")
+                                            and K < 4 else None),
             "note": ("p2p_dedup sends one row per (token, rank): fewer bytes than counted here"
                      if args.ep_transport == "p2p_dedup" else None),
             "peak_GBps_per_direction": 770.0,
@@ -489,7 +490,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-tokens", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ep-transport", default="p2p", choices=["p2p", "p2p_dedup", "nccl"],
+    ap.add_argument("--ep-transport", default="auto",
+                    choices=["auto", "p2p", "p2p_dedup", "nccl"],
                     help="EP exchange: fused NVLink peer-memory kernels (p2p) or NCCL a2a")
     ap.add_argument("--skew", type=float, default=None,
                     help="router logit skew alpha (config 5 sweep: 0, 0.5, 1, 2)")
