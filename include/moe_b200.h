@@ -128,6 +128,11 @@ int moe_ep_dispatch_dedup(const void* x, int T, int K, int h, const int* topk_id
                           const unsigned long long* sprob_peers,
                           const unsigned long long* rprob_peers, void* stream);
 int moe_ep_fill_pad_map(const int* map_pad, int rows, int* map, void* stream);
+/* ECHO hot-expert cloning (planners.py:243-389): rewrite each selection to the virtual
+ * expert (expert segment on its serving rank) that owns its global position. */
+int moe_ep_echo_rewrite(const int* topk_idx, const int* inv_c, int T, int K, int ns,
+                        const int* gbase, const int* seg_start, const int* seg_v, int* topk_v,
+                        void* stream);
 int moe_ep_expand_grad(const void* tok, const int* map, int rows, int h, const float* rowprob,
                        const void* o, void* d_o, float* dprob_rows, void* stream);
 

@@ -55,6 +55,7 @@ SIGNATURES: dict[str, list] = {
     "moe_ep_token_ranks": [P, P, I, I, I, P, P, P, P],
     "moe_ep_dispatch_dedup": [P, I, I, I, P, P, P, I, P, P, P, P, P, P, P, P, P, P, P, P],
     "moe_ep_fill_pad_map": [P, I, P, P],
+    "moe_ep_echo_rewrite": [P, P, I, I, I, P, P, P, P, P],
     "moe_ep_expand_grad": [P, P, I, I, P, P, P, P, P],
     # grouped GEMM (csrc/grouped_gemm.cu)
     "moe_gg_fc1_fwd": [P, P, I, I, I, I, I, P, P, P, P, P, I, P],

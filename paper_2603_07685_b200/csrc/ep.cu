@@ -442,6 +442,31 @@ __global__ void expand_grad_kernel(const int4* __restrict__ tok, const int* __re
   }
 }
 
+// ECHO (hot-expert cloning, reference planners.py:243-389): selection (t,k) of expert e at
+// global position p = gbase[e] + inv_c[t,k] is served by the segment j with
+// seg_start[e,j] <= p < seg_start[e,j+1]; its virtual expert is seg_v[e,j].
+__global__ void echo_rewrite_kernel(const int* __restrict__ topk_idx,
+                                    const int* __restrict__ inv_c, long long n, int ns,
+                                    const int* __restrict__ gbase,
+                                    const int* __restrict__ seg_start,
+                                    const int* __restrict__ seg_v, int* __restrict__ topk_v) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int d = inv_c[i];
+  if (d < 0) {
+    topk_v[i] = -1;
+    return;
+  }
+  const int e = topk_idx[i];
+  const int p = gbase[e] + d;
+  int v = seg_v[e * ns];
+  for (int j = 1; j < ns; ++j) {
+    const int s = seg_start[e * ns + j];
+    if (s <= p && seg_v[e * ns + j] >= 0) v = seg_v[e * ns + j];
+  }
+  topk_v[i] = v;
+}
+
 static int sms() {
   static int n = 0;
   if (!n) {
@@ -563,6 +588,18 @@ int moe_ep_dispatch_dedup(const void* x, int T, int K, int h, const int* topk_id
       static_cast<const int4*>(x), T, K, h / 8, topk_idx, inv_c, base, el, rank_idx, inv_rank,
       tbase, sel_j, sel_pos, prob, tok_peers, map_peers, srows_peers, sprob_peers,
       rprob_peers);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+int moe_ep_echo_rewrite(const int* topk_idx, const int* inv_c, int T, int K, int ns,
+                        const int* gbase, const int* seg_start, const int* seg_v, int* topk_v,
+                        void* stream) {
+  const long long n = (long long)T * K;
+  if (ns < 1) return kErrInvalidArg;
+  if (n == 0) return kOk;
+  echo_rewrite_kernel<<<(int)ceil_div_ll(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      topk_idx, inv_c, n, ns, gbase, seg_start, seg_v, topk_v);
   MOE_LAUNCH_CHECK();
   return kOk;
 }

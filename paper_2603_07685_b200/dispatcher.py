@@ -31,6 +31,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib, gemm, ops
+from . import echo as echo_mod
 from .layer import MoEConfig, shared_expert_backward, shared_expert_forward
 
 
@@ -322,12 +323,20 @@ class SymmPool:
             self.bufs[name] = cur
         return cur[0], cur[1]
 
+    def remote(self, name: str, peer: int, numel: int, dtype):
+        """Tensor view of `peer`'s copy of buffer `name` (NVLink peer memory)."""
+        t, _, h = self.bufs[name]
+        return h.get_remote_tensor(peer, (t.numel(),), dtype)[:numel]
+
     def barrier(self):
         """Stream-ordered cross-rank barrier (an NCCL all-reduce of one float)."""
         dist.all_reduce(self.bar, group=self.ep.group)
 
 
 _POOLS: dict = {}
+
+# Last ECHO plan (measurement only): clones, pre/post max rank load.
+last_echo: dict = {}
 
 # Exact rows / bytes of the last forward's exchange on this rank (measurement only):
 # rows this rank sends to other ranks and receives from them; each of the four exchanges
@@ -373,9 +382,84 @@ def p2p_tables(counts_all: np.ndarray, rank: int, capacity: int, pad: bool, alig
     return base, [p.rows_pad for p in plans], plans[rank]
 
 
+def _echo_route(r, counts_all, E, K, n, me, slots, dev, stream):
+    """ECHO plan + virtual-expert rewrite of this rank's selections (see echo.py)."""
+    el = E // n
+    plan = echo_mod.echo_plan(counts_all.sum(axis=0), el, slots)
+    layout = echo_mod.echo_layout(counts_all, plan, el, slots)
+    t = r.topk_idx.shape[0]
+    splan0 = ops.build_plan(r.topk_idx, r.topk_prob, E, -1, False, compact=True)
+    prefix_me = (np.cumsum(counts_all, axis=0) - counts_all)[me]
+    gbase = prefix_me - (np.cumsum(counts_all[me]) - counts_all[me])
+    ns = layout.seg_start.shape[1]
+    tab = np.concatenate([gbase, layout.seg_start.ravel(), layout.seg_v.ravel()])
+    tab = torch.from_numpy(tab.astype(np.int32)).pin_memory().to(dev, non_blocking=True)
+    gbase_d, start_d, v_d = torch.split(tab, [E, E * ns, E * ns])
+    topk_v = torch.empty_like(r.topk_idx)
+    _lib.call("moe_ep_echo_rewrite", r.topk_idx.data_ptr(), splan0.inv_map.data_ptr(), t, K, ns,
+              gbase_d.data_ptr(), start_d.data_ptr(), v_d.data_ptr(), topk_v.data_ptr(), stream)
+    last_echo.clear()
+    last_echo.update(clones=[(c.expert, c.rank, c.tokens) for c in plan.clones],
+                     pre_max_load=plan.pre_max_load, post_max_load=plan.post_max_load,
+                     target_load=plan.target_load)
+    return topk_v, n * layout.el_v, layout.counts_v, layout
+
+
+def _echo_weights(pool, ep, w1, w2, layout):
+    """Stacked weights of this rank's virtual experts: own experts, then its clone slots
+    filled with the home experts' weights pulled over NVLink."""
+    el = w1.shape[0]
+    me = ep.rank
+    out = []
+    for w, name in ((w1, "echo_w1"), (w2, "echo_w2")):
+        exp, _ = pool.get(name, w.numel(), w.dtype)
+        exp[: w.numel()].copy_(w.reshape(-1))
+        pool.barrier()
+        ext = torch.empty((el + layout.slots,) + tuple(w.shape[1:]), dtype=w.dtype,
+                          device=w.device)
+        ext[:el].copy_(w)
+        per = w[0].numel()
+        for g in range(layout.slots):
+            e = int(layout.slot_expert[me, g])
+            if e < 0:
+                ext[el + g].zero_()
+                continue
+            home, j = e // el, e % el
+            src = pool.remote(name, home, w.numel(), w.dtype)[j * per:(j + 1) * per]
+            ext[el + g].copy_(src.view(w.shape[1:]))
+        out.append(ext)
+    return out[0], out[1]
+
+
+def _echo_reduce(pool, ep, dw_ext, layout, el, name):
+    """echo_grad_reduce (planners.py:379-387): home gradient + clone gradients, plan order."""
+    me = ep.rank
+    slots = layout.slots
+    per = dw_ext[0].numel()
+    exp, _ = pool.get(name, max(slots, 1) * per, dw_ext.dtype)
+    if slots:
+        exp[: slots * per].copy_(dw_ext[el:].reshape(-1))
+    pool.barrier()
+    own = dw_ext[:el].float()
+    slot_of = {}
+    for r in range(layout.slot_expert.shape[0]):
+        for g in range(slots):
+            if layout.slot_expert[r, g] >= 0:
+                slot_of[(int(layout.slot_expert[r, g]), r)] = g
+    for c in layout.plan.clones:
+        if c.expert // el != me:
+            continue
+        g = slot_of[(c.expert, c.rank)]
+        src = pool.remote(name, c.rank, slots * per, dw_ext.dtype)[g * per:(g + 1) * per]
+        own[c.expert % el] += src.view(dw_ext.shape[1:]).float()
+    pool.barrier()
+    return own.to(dw_ext.dtype)
+
+
 class _MoEEPP2PFunction(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, w_r, w1, w2, sel_bias, w1s, w2s, cfg: MoEConfig, ep: EPGroup):
+    def forward(ctx, x, w_r, w1, w2, sel_bias, w1s, w2s, cfg: MoEConfig, ep: EPGroup,
+                echo_slots: int = 0):
         t, h = x.shape
         E, K = cfg.num_experts, cfg.top_k
         n = ep.n
@@ -390,15 +474,23 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         g = gathered.cpu().numpy()  # the one host sync of the EP forward
         counts_all = np.rint(g[:, :E]).astype(np.int64)
         cap = cfg.capacity(n * t)
-        align = ops.pick_align(n * t, K, E)
+        # ECHO: route to virtual experts (expert segments on their serving ranks)
+        topk_use, E_use, counts_use, layout = r.topk_idx, E, counts_all, None
+        if echo_slots:
+            if cap >= 0:
+                raise ValueError("ECHO cloning applies to dropless routing (no capacity)")
+            topk_use, E_use, counts_use, layout = _echo_route(r, counts_all, E, K, n, ep.rank,
+                                                              echo_slots, dev, stream)
+        align = ops.pick_align(n * t, K, E_use)
         pair = align == 2 * ops.ALIGN
-        base, rows_all, hp = p2p_tables(counts_all, ep.rank, cap, cfg.pad_to_capacity, align)
+        base, rows_all, hp = p2p_tables(counts_use, ep.rank, cap, cfg.pad_to_capacity, align)
         _record_exchange(hp, h)
         aux_v, aux_g = global_aux(counts_all, g[:, E:], t, K, cfg.aux_loss_coeff)
         rows_alloc = max(max(rows_all), 2 * ops.ALIGN)
         el = hp.el
         # one pinned H2D copy of every small table
-        cap_local = hp.cap_local if hp.cap_local is not None else np.full(E, -1)
+        ctx_topk = topk_use
+        cap_local = hp.cap_local if hp.cap_local is not None else np.full(E_use, -1)
         meta = np.array([hp.rows_pad // ops.ALIGN, hp.rows_pad, 0], dtype=np.int64)
         parts = [base, cap_local, hp.table.astype(np.int64), hp.block_expert, meta]
         lens = [len(p) for p in parts]
@@ -412,8 +504,10 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         nmb = meta_d[0:1]
         off_pad_d = table_d[2 * n * el: 2 * n * el + el + 1]
 
-        splan = ops.build_plan(r.topk_idx, r.topk_prob, E, -1, False,
+        splan = ops.build_plan(topk_use, r.topk_prob, E_use, -1, False,
                                cap_e=cap_d if hp.cap_local is not None else None, compact=True)
+        if layout is not None:
+            w1, w2 = _echo_weights(pool, ep, w1, w2, layout)
         xp, xp_peers = pool.get("xp", rows_alloc * h, torch.bfloat16)
         xp = xp[: rows_alloc * h].view(rows_alloc, h)
         prob_peers = None
@@ -430,7 +524,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
                   stream)
         # (row_prob of padding rows: zero at allocation, else a stale finite prob of a row
         # whose activation is exactly zero; never cleared here, peers may already be pushing)
-        _lib.call("moe_ep_dispatch_push", x.data_ptr(), t, K, h, r.topk_idx.data_ptr(),
+        _lib.call("moe_ep_dispatch_push", x.data_ptr(), t, K, h, ctx_topk.data_ptr(),
                   splan.inv_map.data_ptr(), base_d.data_ptr(), el, xp_peers.data_ptr(),
                   r.topk_prob.data_ptr() if cfg.mem_efficient else None,
                   prob_peers.data_ptr() if prob_peers is not None else None, stream)
@@ -447,13 +541,14 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         o_local = None
         if not cfg.mem_efficient:
             o_local = torch.empty((max(sum(hp.send_splits), 1), h), dtype=x.dtype, device=dev)
-        _lib.call("moe_ep_combine_pull", o_peers.data_ptr(), t, K, h, r.topk_idx.data_ptr(),
+        _lib.call("moe_ep_combine_pull", o_peers.data_ptr(), t, K, h, ctx_topk.data_ptr(),
                   splan.inv_map.data_ptr(), base_d.data_ptr(), el,
                   None if cfg.mem_efficient else r.topk_prob.data_ptr(),
                   x.data_ptr() if cap >= 0 else None,
                   shared[-1].data_ptr() if shared is not None else None, None, y.data_ptr(),
                   o_local.data_ptr() if o_local is not None else None, stream)
         ctx.cfg, ctx.ep, ctx.r, ctx.splan, ctx.cap, ctx.pair = cfg, ep, r, splan, cap, pair
+        ctx.topk_use, ctx.layout, ctx.el_own = topk_use, layout, E // n
         ctx.o_local = o_local
         ctx.tabs = (base_d, be_d, nmb, meta_d, off_pad_d, map_pad, rows_alloc, el)
         ctx.row_prob = row_prob
@@ -465,6 +560,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
     def backward(ctx, dy, daux):
         cfg, ep, r, splan = ctx.cfg, ctx.ep, ctx.r, ctx.splan
         base_d, be_d, nmb, meta_d, off_pad_d, map_pad, rows_alloc, el = ctx.tabs
+        ctx_topk = ctx.topk_use
         x, w_r_pad, w1, w2, preact, act, w1s, w2s = ctx.saved_tensors
         t, h = x.shape
         K = cfg.top_k
@@ -481,7 +577,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         dprob = torch.empty((t, K), dtype=torch.float32, device=dev)
         _lib.call("moe_ep_combine_bwd_push", dy.data_ptr(),
                   None if cfg.mem_efficient else ctx.o_local.data_ptr(), d_peers.data_ptr(), t, K,
-                  h, r.topk_idx.data_ptr(), splan.inv_map.data_ptr(), base_d.data_ptr(), el,
+                  h, ctx_topk.data_ptr(), splan.inv_map.data_ptr(), base_d.data_ptr(), el,
                   None if cfg.mem_efficient else r.topk_prob.data_ptr(),
                   None if cfg.mem_efficient else dprob.data_ptr(), stream)
         pool.barrier()
@@ -501,7 +597,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         dw1 = gemm.wgrad(d_pre, xp, off_pad_d, el)
         pool.barrier()
         if cfg.mem_efficient:
-            _lib.call("moe_ep_dprob_pull", part_peers.data_ptr(), t, K, r.topk_idx.data_ptr(),
+            _lib.call("moe_ep_dprob_pull", part_peers.data_ptr(), t, K, ctx_topk.data_ptr(),
                       splan.inv_map.data_ptr(), base_d.data_ptr(), el,
                       gemm.dprob_partials(w2.shape[2]),
                       dprob.data_ptr(), stream)
@@ -512,14 +608,17 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         if ctx.shared is not None:
             dx_shared, dw1s, dw2s = shared_expert_backward(x, dy, w1s, w2s, ctx.shared)
         dx = torch.empty_like(x)
-        _lib.call("moe_ep_combine_pull", dxp_peers.data_ptr(), t, K, h, r.topk_idx.data_ptr(),
+        _lib.call("moe_ep_combine_pull", dxp_peers.data_ptr(), t, K, h, ctx_topk.data_ptr(),
                   splan.inv_map.data_ptr(), base_d.data_ptr(), el, None,
                   dy.data_ptr() if ctx.cap >= 0 else None, dx_router.data_ptr(),
                   dx_shared.data_ptr() if dx_shared is not None else None, dx.data_ptr(), None,
                   stream)
         # no rank may overwrite the symmetric buffers before every rank has pulled
         pool.barrier()
-        return (dx, dw_r.to(torch.bfloat16), dw1, dw2, None, dw1s, dw2s, None, None)
+        if ctx.layout is not None:  # clone weight gradients back into the home experts
+            dw1 = _echo_reduce(pool, ep, dw1, ctx.layout, ctx.el_own, "echo_dw1")
+            dw2 = _echo_reduce(pool, ep, dw2, ctx.layout, ctx.el_own, "echo_dw2")
+        return (dx, dw_r.to(torch.bfloat16), dw1, dw2, None, dw1s, dw2s, None, None, None)
 
 
 def _excl(a):
@@ -722,7 +821,8 @@ class _MoEEPDedupFunction(torch.autograd.Function):
 
 
 def moe_forward_ep(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
-                   selection_bias=None, w1_shared=None, w2_shared=None, transport: str = "auto"):
+                   selection_bias=None, w1_shared=None, w2_shared=None, transport: str = "auto",
+                   echo_slots: int = 0):
     """EP MoE layer: w1_local [E/EP, 2m, h], w2_local [E/EP, h, m] are this rank's experts
     (global experts [rank*E/EP, (rank+1)*E/EP)). Returns (y [T,h], global aux).
 
@@ -740,6 +840,10 @@ def moe_forward_ep(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
         # measured on B200 (EP=4): dedup wins for top-8 (Qwen3 +5%, DeepSeek +1%); for
         # top-2 most tokens already hit distinct ranks and the local expand costs more
         transport = "p2p_dedup" if cfg.top_k >= 4 else "p2p"
+    if echo_slots:
+        # ECHO hot-expert cloning runs on the p2p transport (virtual experts)
+        return _MoEEPP2PFunction.apply(x, w_r, w1_local, w2_local, selection_bias, w1_shared,
+                                       w2_shared, cfg, ep, int(echo_slots))
     fn = {"p2p": _MoEEPP2PFunction, "p2p_dedup": _MoEEPDedupFunction,
           "nccl": _MoEEPFunction}[transport]
     return fn.apply(x, w_r, w1_local, w2_local, selection_bias, w1_shared, w2_shared, cfg, ep)

@@ -24,6 +24,14 @@ CASES = {
                           mem=True),
     "top8": dict(E=16, K=8, h=256, m=256, T=160, score="softmax", cf=None, pad=False),
 }
+# ECHO hot-expert cloning (dropless, a strongly preferred expert): the cloned computation
+# must equal the un-cloned global oracle exactly as any other EP run.
+ECHO_CASES = {
+    "echo_hot_expert": dict(E=8, K=2, h=256, m=256, T=256, score="softmax", cf=None, pad=False,
+                            hot=0.4, echo=2),
+    "echo_hot_top4": dict(E=16, K=4, h=256, m=256, T=192, score="sigmoid", cf=None, pad=False,
+                          hot=0.4, echo=1),
+}
 
 
 def _port():
@@ -60,6 +68,10 @@ def _worker(rank, world, port, case, q, transport):
             # push routing towards low expert ids (capacity drops on the global batch)
             x_g = (x_g.float() + torch.linspace(1.0, 0.0, h)[None, :] * 0.5).to(bf)
             w_r[:, 0] += 0.05
+        if case.get("hot"):
+            # one hot expert: a constant feature whose router weight favours expert 0
+            x_g[:, 0] = 1.0
+            w_r[0, 0] += case["hot"] * h ** 0.5
         w_r = w_r.to(bf)
         up = (torch.randn((E, m, h), generator=g) * h ** -0.5).to(bf)
         gate = (torch.randn((E, m, h), generator=g) * h ** -0.5).to(bf)
@@ -74,11 +86,16 @@ def _worker(rank, world, port, case, q, transport):
         w1d = gemm.interleave_gate_up(gate[mine].to(dev), up[mine].to(dev)).requires_grad_(True)
         w2d = w2[mine].to(dev).contiguous().requires_grad_(True)
         ep = EPGroup()
-        y, aux = moe_forward_ep(x, w_rd, w1d, w2d, cfg, ep, transport=transport)
+        echo = case.get("echo", 0)
+        y, aux = moe_forward_ep(x, w_rd, w1d, w2d, cfg, ep, transport=transport, echo_slots=echo)
         # a second step exercises buffer reuse across steps (symmetric pools, barriers)
         for p_ in (x, w_rd, w1d, w2d):
             p_.grad = None
-        y, aux = moe_forward_ep(x, w_rd, w1d, w2d, cfg, ep, transport=transport)
+        y, aux = moe_forward_ep(x, w_rd, w1d, w2d, cfg, ep, transport=transport, echo_slots=echo)
+        if echo:
+            from paper_2603_07685_b200.dispatcher import last_echo
+            if not last_echo.get("clones"):
+                raise AssertionError(f"ECHO made no clones: {last_echo}")
         torch.autograd.backward([y, aux], [dy_g[sl].to(dev), torch.ones_like(aux)])
         dwr = w_rd.grad.float().clone()
         dist.all_reduce(dwr)
@@ -129,17 +146,26 @@ def _worker(rank, world, port, case, q, transport):
 @pytest.mark.parametrize("transport", ["p2p", "p2p_dedup", "nccl"])
 @pytest.mark.parametrize("name", list(CASES))
 def test_ep_layer_matches_global_oracle(name, transport):
+    _run(CASES[name], transport)
+
+
+@pytest.mark.parametrize("name", list(ECHO_CASES))
+def test_ep_echo_matches_global_oracle(name):
+    _run(ECHO_CASES[name], "p2p")
+
+
+def _run(case, transport):
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
     world = min(torch.cuda.device_count(), 8)
-    while CASES[name]["E"] % world:
+    while case["E"] % world:
         world -= 1
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES[name], q, transport))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q, transport))
              for r in range(world)]
     for p in procs:
         p.start()
