@@ -40,6 +40,8 @@ CONFIGS = {
     "capacity": dict(E=8, K=2, h=4096, m=14336, T=16384, score="softmax", cf=1.0, pad=True,
                      name="Mixtral-shape, capacity factor 1.0 drop-and-pad"),
     "tiny": dict(E=8, K=2, h=256, m=512, T=4096, score="softmax", name="tiny MoE layer"),
+    "skewed": dict(E=8, K=2, h=4096, m=14336, T=16384, score="softmax", skew=1.0,
+                   name="Mixtral-shape, dropless, skewed router (ECHO target)"),
 }
 AUX_COEFF = 1e-2
 METRIC = "MoE layer fwd+bwd tokens/s & grouped-GEMM TFLOPS at 1/2/4/8 B200 (EP)"
@@ -207,7 +209,7 @@ def run_gpu(args, c) -> None:
 
         def layer(xx):
             return moe_forward_ep(xx, w_r, w1, w2, cfg, ep, None, w1s, w2s,
-                                  transport=args.ep_transport)
+                                  transport=args.ep_transport, echo_slots=args.echo_slots)
     else:
         def layer(xx):
             return moe_forward(xx, w_r, w1, w2, cfg, None, w1s, w2s)
@@ -428,6 +430,9 @@ def run_gpu(args, c) -> None:
                                    sorted(per_kernel.items(), key=lambda kv: -sum(kv[1]))},
             "clocks": clk,
             "routing": routing_stats,
+            "echo": (dict(slots=args.echo_slots, **__import__(
+                "paper_2603_07685_b200.dispatcher", fromlist=["x"]).last_echo)
+                if args.echo_slots and n > 1 else None),
             "nvlink": nvlink_stats,
         }
         if n == 1 and not args.no_cpu_baseline:
@@ -493,6 +498,8 @@ def main():
     ap.add_argument("--ep-transport", default="auto",
                     choices=["auto", "p2p", "p2p_dedup", "nccl"],
                     help="EP exchange: fused NVLink peer-memory kernels (p2p) or NCCL a2a")
+    ap.add_argument("--echo-slots", type=int, default=0,
+                    help="ECHO hot-expert clone slots per rank (EP, dropless)")
     ap.add_argument("--skew", type=float, default=None,
                     help="router logit skew alpha (config 5 sweep: 0, 0.5, 1, 2)")
     args = ap.parse_args()
