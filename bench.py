@@ -133,14 +133,15 @@ def cpu_baseline(c, sample_tokens: int, threads: int, reps: int = 1) -> dict:
     w2 = (rng.standard_normal((h, m), dtype=f32) * m ** -0.5).astype(f32)
     params = R.ExpertParams(w1=[up] * e, w2=[w2] * e, gate=[gate] * e)
     dy = rng.standard_normal((sample_tokens, h), dtype=f32)
-    best = None
-    for _ in range(reps):
+    def one_step() -> float:
         t0 = time.perf_counter()
         B.moe_forward_backward(x, w_r, params, dy, score=c["score"], top_k=k, coeff=AUX_COEFF)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
+        return time.perf_counter() - t0
+
+    times = [one_step() for _ in range(reps)]
+    best = min(times)
     return {"value": sample_tokens / best, "unit": "tokens/s", "cores": threads,
-            "kind": "port", "seconds": best,
+            "kind": "port", "seconds": best, "times": times, "step": one_step,
             "sample": (f"{sample_tokens} tokens of the {c['name']} (E={e},K={k},h={h},m={m}), "
                        f"fwd+bwd, oracle/backward_ref.py numpy fp32, best of {reps}")}
 
@@ -437,7 +438,8 @@ def run_gpu(args, c) -> None:
         }
         if n == 1 and not args.no_cpu_baseline:
             thr = cpu_threads()
-            out["cpu_baseline"] = cpu_baseline(c, args.cpu_sample_tokens, thr)
+            cb = cpu_baseline(c, args.cpu_sample_tokens, thr)
+            out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         emit(out)
     if n > 1:
         dist.barrier()
@@ -452,13 +454,11 @@ def run_reference(args, c) -> None:
     if rank != 0:
         return
     thr = cpu_threads()
-    times = []
-    base = None
-    for i in range(args.warmup + args.steps):
-        b = cpu_baseline(c, args.cpu_sample_tokens, thr)
-        if i >= args.warmup:
-            times.append(b["seconds"])
-            base = b
+    # inputs and weights are built once; warm-up steps run untimed, then K timed steps
+    base = cpu_baseline(c, args.cpu_sample_tokens, thr, reps=1)
+    for _ in range(max(args.warmup - 1, 0)):
+        base["step"]()
+    times = [base["step"]() for _ in range(args.steps)]
     sec = statistics.mean(times)
     value = args.cpu_sample_tokens / sec
     out = {
