@@ -59,21 +59,32 @@ def gemm_flops_per_token(c) -> float:
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md).
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Each sample carries nvidia-smi's own timestamp; only samples inside the timed window
+    [window(start), window(end)] count (the pipe may deliver lines late, and samples from
+    idle set-up phases must not enter the median)."""
+
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self):
+    def __init__(self, gpu_index: int = 0):
         self.proc = None
-        self.lines: list[str] = []
+        self.lines: list[tuple[float, str]] = []
+        self.gpu = gpu_index
+        self.t0 = self.t1 = None
 
     def start(self):
+        import shutil
+
+        cmd = ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+               "-i", str(self.gpu), "-lms", "50"]
+        if shutil.which("stdbuf"):
+            cmd = ["stdbuf", "-oL"] + cmd
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                         text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except (OSError, FileNotFoundError):
@@ -81,11 +92,29 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def window(self, start: bool):
+        if start:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+
+    @staticmethod
+    def _stamp(s: str):
+        import datetime
+
+        for fmt in ("%Y/%m/%d %H:%M:%S.%f", "%Y/%m/%d %H:%M:%S"):
+            try:
+                return datetime.datetime.strptime(s, fmt).timestamp()
+            except ValueError:
+                pass
+        return None
 
     def stop(self) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)  # let the samples of the window's tail arrive
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -94,16 +123,21 @@ class ClockSampler:
         self.t.join(timeout=2)
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for arrived, ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 9:
+            if len(parts) < 10:
+                continue
+            ts = self._stamp(parts[0])
+            if ts is None:
+                ts = arrived
+            if self.t0 is not None and not (self.t0 <= ts <= (self.t1 or ts)):
                 continue
             try:
-                sm.append(float(parts[1]))
-                smax.append(float(parts[2]))
+                sm.append(float(parts[2]))
+                smax.append(float(parts[3]))
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[5:9]):
+            for nm, v in zip(names, parts[6:10]):
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None,
@@ -230,7 +264,7 @@ def run_gpu(args, c) -> None:
 
     # nvidia-smi start-up contends with the driver: start sampling before the warm-up and
     # wait for its first sample so the timed region only sees the steady 100 ms polling.
-    clocks = ClockSampler()
+    clocks = ClockSampler(dev.index if dev.index is not None else 0)
     if rank == 0:
         clocks.start()
         t_wait = time.time()
@@ -249,11 +283,13 @@ def run_gpu(args, c) -> None:
     barrier()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    clocks.window(True)
     t_start.record()
     for _ in range(args.steps):
         step(x, dy)
     t_end.record()
     barrier()
+    clocks.window(False)
     _lib.stats.timing = False
     launches = _lib.stats.launches
     ms_total = t_start.elapsed_time(t_end)
@@ -343,16 +379,22 @@ def run_gpu(args, c) -> None:
         # per step: 4 one-way transfers of this rank's remote rows (x, O, dO, dX); with
         # balanced routing each direction of the NVLink port carries ~4 x sent bytes
         out_bytes = 2 * last_exchange["bytes_sent_remote"] + 2 * last_exchange["bytes_recv_remote"]
+        tr = args.ep_transport
+        if tr == "auto":
+            tr = "p2p_dedup" if K >= 4 else "p2p"
+        # p2p: the two return transfers (O, dX) run inside the fc2 / fc1-dgrad epilogues,
+        # so only the two pushes (x, dO) are standalone exchange kernels
+        standalone_bytes = (2 * last_exchange["bytes_sent_remote"] if tr == "p2p" else out_bytes)
         nvlink_stats = {
-            "transport": args.ep_transport,
+            "transport": tr,
             "bytes_out_per_step_per_gpu": out_bytes,
             "model_bytes_per_step_per_gpu": 4 * a2a_send_volume(T, K, h, n, 2),
             "exchange_kernel_ms_per_step": round(ex_ms, 4),
-            "achieved_GBps_per_direction": (round(out_bytes / (ex_ms / 1e3) / 1e9, 1)
-                                            if ex_ms and args.ep_transport in ("p2p", "auto")
-                                            and K < 4 else None),
+            "returns_fused_in_gemm_epilogue": tr == "p2p",
+            "achieved_GBps_per_direction": (round(standalone_bytes / (ex_ms / 1e3) / 1e9, 1)
+                                            if ex_ms and tr in ("p2p", "p2p_pull") else None),
             "note": ("p2p_dedup sends one row per (token, rank): fewer bytes than counted here"
-                     if args.ep_transport == "p2p_dedup" else None),
+                     if tr == "p2p_dedup" else None),
             "peak_GBps_per_direction": 770.0,
             "peak_source": "B200_PROFILING.md measured peer copy (nominal 900)",
         }
@@ -489,14 +531,14 @@ def run_reference(args, c) -> None:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-tokens", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ep-transport", default="auto",
-                    choices=["auto", "p2p", "p2p_dedup", "nccl"],
+                    choices=["auto", "p2p", "p2p_pull", "p2p_dedup", "nccl"],
                     help="EP exchange: fused NVLink peer-memory kernels (p2p) or NCCL a2a")
     ap.add_argument("--echo-slots", type=int, default=0,
                     help="ECHO hot-expert clone slots per rank (EP, dropless)")

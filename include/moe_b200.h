@@ -68,6 +68,13 @@ int moe_permute_plan(const int* topk_idx, const float* topk_prob, int T, int K, 
  * the global batch) via the per-expert cap_e of moe_permute_plan. */
 int moe_ep_regroup_map(const int* table, int n, int el, int rows_pad, int* map_pad,
                        int* map_recv, void* stream);
+/* Per padded row of the expert rank's plan: the address of that row in its source rank's
+ * compact buffer (peers[s] + (dst_off[s*el+e] + q) * row_bytes; 0 for padding / phantom
+ * rows). Feeds the *_scatter GEMMs, which return expert outputs / dX rows over NVLink from
+ * their epilogue (the return all-to-all of perf.a2a_send_volume perf.py:62-70). */
+int moe_ep_row_dst(const int* table, int n, int el, int rows_pad, const int* dst_off,
+                   const unsigned long long* peers, long long row_bytes,
+                   unsigned long long* row_dst, void* stream);
 int moe_permute_compact_map(const int* meta, const int* off_c, const int* off_pad, int E,
                             const int* row_src, long long* row_id_map, int* compact_to_pad,
                             int max_compact, void* stream);
@@ -147,6 +154,17 @@ int moe_gg_fc1_fwd(const void* xp, const void* w1, int a_rows, int max_rows, int
 int moe_gg_fc2_fwd(const void* act, const void* w2, int a_rows, int max_rows, int m, int h,
                    int num_experts, const int* block_expert, const int* num_m_blocks,
                    void* out, int flags, void* stream);
+/* fc2 forward / fc1 dgrad storing output row r at address row_dst[r] (0 = not stored): the
+ * EP return transfer (combine / dX) fused into the GEMM epilogue, rows written straight into
+ * peer GPUs' memory over NVLink. */
+int moe_gg_fc2_fwd_scatter(const void* act, const void* w2, int a_rows, int max_rows, int m,
+                           int h, int num_experts, const int* block_expert,
+                           const int* num_m_blocks, const unsigned long long* row_dst, int flags,
+                           void* stream);
+int moe_gg_fc1_dgrad_scatter(const void* d_preact, const void* w1, int a_rows, int max_rows,
+                             int m, int h, int num_experts, const int* block_expert,
+                             const int* num_m_blocks, const unsigned long long* row_dst,
+                             int flags, void* stream);
 int moe_gg_fc2_dgrad(const void* dout, const void* w2, const void* preact, int a_rows,
                      int max_rows, int h, int m, int num_experts, const int* block_expert,
                      const int* num_m_blocks, const float* row_prob, void* d_preact,

@@ -40,6 +40,7 @@ SIGNATURES: dict[str, list] = {
     "moe_permute_plan": [P, P, I, I, I, I, P, I, P, I, I, P, P, P, P, P, P, P, P, P, P, P, P,
                          P],
     "moe_ep_regroup_map": [P, I, I, I, P, P, P],
+    "moe_ep_row_dst": [P, I, I, I, P, P, L, P, P],
     "moe_permute_compact_map": [P, P, P, I, P, P, P, I, P],
     "moe_permute_gather": [P, I, I, I, P, P, P, P, P],
     "moe_zero_pad_rows": [P, P, I, P, P],
@@ -60,6 +61,8 @@ SIGNATURES: dict[str, list] = {
     # grouped GEMM (csrc/grouped_gemm.cu)
     "moe_gg_fc1_fwd": [P, P, I, I, I, I, I, P, P, P, P, P, I, P],
     "moe_gg_fc2_fwd": [P, P, I, I, I, I, I, P, P, P, I, P],
+    "moe_gg_fc2_fwd_scatter": [P, P, I, I, I, I, I, P, P, P, I, P],
+    "moe_gg_fc1_dgrad_scatter": [P, P, I, I, I, I, I, P, P, P, I, P],
     "moe_gg_fc2_dgrad": [P, P, P, I, I, I, I, I, P, P, P, P, P, I, P],
     "moe_gg_fc1_dgrad": [P, P, I, I, I, I, I, P, P, P, I, P],
     "moe_gg_wgrad": [P, P, I, I, I, I, P, P, P],

@@ -80,6 +80,10 @@ struct Params {
   const float* row_scale;
   float* row_partial;
   int ld_partial;
+  // EPI_BF16 grouped-M scatter: absolute destination address of each output row (0 = drop
+  // the row). Rows may live in peer GPUs' memory (NVLink): the EP combine / dX exchange is
+  // fused into the producing GEMM's epilogue.
+  const unsigned long long* row_dst;
 };
 
 struct Tile {
@@ -383,8 +387,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tmem_ld_32x32b_x32(t_base + col, r);
           tmem_ld_wait();
           if constexpr (EPI == EPI_BF16) {
-            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + ebase + row * p.ldo +
-                               tl.n0 + col;
+            __nv_bfloat16* o;
+            if (!GROUPED_K && p.row_dst) {
+              const unsigned long long dst = __ldg(p.row_dst + row);
+              if (dst == 0ull) continue;
+              o = reinterpret_cast<__nv_bfloat16*>(dst) + tl.n0 + col;
+            } else {
+              o = reinterpret_cast<__nv_bfloat16*>(p.out) + ebase + row * p.ldo + tl.n0 + col;
+            }
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
               int4 w;
@@ -510,6 +520,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
 
+  // scattered rows may be in peer memory: make them visible system-wide before the
+  // stream-ordered collective that publishes them
+  if (EPI == EPI_BF16 && !GROUPED_K && p.row_dst && warp >= 2) __threadfence_system();
   tc_fence_before();
   if constexpr (CG == 2) {
     cluster_sync_all();
@@ -655,14 +668,15 @@ int moe_gg_fc1_fwd(const void* xp, const void* w1, int a_rows, int max_rows, int
                                               static_cast<cudaStream_t>(stream));
 }
 
-// fc2 forward: out[rows, h] = act[rows, m] * w2_e^T, w2[E, h, m].
-int moe_gg_fc2_fwd(const void* act, const void* w2, int a_rows, int max_rows, int m, int h,
-                   int num_experts, const int* block_expert, const int* num_m_blocks, void* out,
-                   int flags, void* stream) {
+static int fc2_fwd_impl(const void* act, const void* w2, int a_rows, int max_rows, int m,
+                        int h, int num_experts, const int* block_expert,
+                        const int* num_m_blocks, void* out, const unsigned long long* row_dst,
+                        int flags, void* stream) {
   const int pair = flags & kFlagPair;
   if (m % BK || h % BN || max_rows % (BM * (pair ? 2 : 1)) || a_rows > max_rows)
     return kErrInvalidArg;
   Params p{};
+  p.row_dst = row_dst;
   p.num_m_blocks = num_m_blocks;
   p.block_expert = block_expert;
   p.max_m_blocks = max_rows / BM;
@@ -674,6 +688,26 @@ int moe_gg_fc2_fwd(const void* act, const void* w2, int a_rows, int max_rows, in
   return run<false, false, false, EPI_BF16>(act, m, a_rows, w2, m, (uint64_t)num_experts * h, p,
                                             p.max_m_blocks, pair,
                                             static_cast<cudaStream_t>(stream));
+}
+
+// fc2 forward: out[rows, h] = act[rows, m] * w2_e^T, w2[E, h, m].
+int moe_gg_fc2_fwd(const void* act, const void* w2, int a_rows, int max_rows, int m, int h,
+                   int num_experts, const int* block_expert, const int* num_m_blocks, void* out,
+                   int flags, void* stream) {
+  return fc2_fwd_impl(act, w2, a_rows, max_rows, m, h, num_experts, block_expert, num_m_blocks,
+                      out, nullptr, flags, stream);
+}
+
+// fc2 forward whose output row r is stored at address row_dst[r] (0 = not stored): the EP
+// combine's return transfer fused into the GEMM epilogue (rows land in the source rank's
+// compact buffer over NVLink).
+int moe_gg_fc2_fwd_scatter(const void* act, const void* w2, int a_rows, int max_rows, int m,
+                           int h, int num_experts, const int* block_expert,
+                           const int* num_m_blocks, const unsigned long long* row_dst, int flags,
+                           void* stream) {
+  if (!row_dst) return kErrInvalidArg;
+  return fc2_fwd_impl(act, w2, a_rows, max_rows, m, h, num_experts, block_expert, num_m_blocks,
+                      nullptr, row_dst, flags, stream);
 }
 
 // fc2 data-gradient fused with the SwiGLU backward.
@@ -706,14 +740,15 @@ int moe_gg_fc2_dgrad(const void* dout, const void* w2, const void* preact, int a
                                               static_cast<cudaStream_t>(stream));
 }
 
-// fc1 data-gradient: dxp[rows, h] = d_preact[rows, 2m] * w1_e  (w1[E, 2m, h] read MN-major).
-int moe_gg_fc1_dgrad(const void* d_preact, const void* w1, int a_rows, int max_rows, int m,
-                     int h, int num_experts, const int* block_expert, const int* num_m_blocks,
-                     void* dxp, int flags, void* stream) {
+static int fc1_dgrad_impl(const void* d_preact, const void* w1, int a_rows, int max_rows,
+                          int m, int h, int num_experts, const int* block_expert,
+                          const int* num_m_blocks, void* dxp,
+                          const unsigned long long* row_dst, int flags, void* stream) {
   const int pair = flags & kFlagPair;
   if ((2 * m) % BK || h % BN || max_rows % (BM * (pair ? 2 : 1)) || a_rows > max_rows)
     return kErrInvalidArg;
   Params p{};
+  p.row_dst = row_dst;
   p.num_m_blocks = num_m_blocks;
   p.block_expert = block_expert;
   p.max_m_blocks = max_rows / BM;
@@ -725,6 +760,25 @@ int moe_gg_fc1_dgrad(const void* d_preact, const void* w1, int a_rows, int max_r
   return run<false, true, false, EPI_BF16>(d_preact, 2 * m, a_rows, w1, h,
                                            (uint64_t)num_experts * 2 * m, p, p.max_m_blocks,
                                            pair, static_cast<cudaStream_t>(stream));
+}
+
+// fc1 data-gradient: dxp[rows, h] = d_preact[rows, 2m] * w1_e  (w1[E, 2m, h] read MN-major).
+int moe_gg_fc1_dgrad(const void* d_preact, const void* w1, int a_rows, int max_rows, int m,
+                     int h, int num_experts, const int* block_expert, const int* num_m_blocks,
+                     void* dxp, int flags, void* stream) {
+  return fc1_dgrad_impl(d_preact, w1, a_rows, max_rows, m, h, num_experts, block_expert,
+                        num_m_blocks, dxp, nullptr, flags, stream);
+}
+
+// fc1 data-gradient with the dX return transfer fused into the epilogue (see
+// moe_gg_fc2_fwd_scatter).
+int moe_gg_fc1_dgrad_scatter(const void* d_preact, const void* w1, int a_rows, int max_rows,
+                             int m, int h, int num_experts, const int* block_expert,
+                             const int* num_m_blocks, const unsigned long long* row_dst,
+                             int flags, void* stream) {
+  if (!row_dst) return kErrInvalidArg;
+  return fc1_dgrad_impl(d_preact, w1, a_rows, max_rows, m, h, num_experts, block_expert,
+                        num_m_blocks, nullptr, row_dst, flags, stream);
 }
 
 // Weight gradient with the reduction over each expert's token rows:

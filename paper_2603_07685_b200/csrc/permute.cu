@@ -634,6 +634,54 @@ int moe_ep_regroup_map(const int* table, int n, int el, int rows_pad, int* map_p
   return kOk;
 }
 
+// Destination address of every padded row of the expert rank's plan in its SOURCE rank's
+// compact buffer: row (local expert e, source s, q-th of s's rows for e) ->
+// peers[s] + (dst_off[s * el + e] + q) * row_bytes; padding / phantom rows -> 0.
+__global__ void row_dst_kernel(const int* __restrict__ tab, int n, int el, int rows_pad,
+                               const int* __restrict__ dst_off,
+                               const unsigned long long* __restrict__ peers,
+                               long long row_bytes, unsigned long long* __restrict__ row_dst) {
+  const int* kept = tab;
+  const int* off_pad = tab + 2 * n * el;
+  const int* real = off_pad + el + 1;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows_pad;
+       r += gridDim.x * blockDim.x) {
+    int lo = 0, hi = el - 1;  // last e with off_pad[e] <= r
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (off_pad[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    const int e = lo;
+    const int j = r - off_pad[e];
+    unsigned long long dst = 0ull;
+    if (j < real[e]) {
+      int acc = 0;
+      for (int s = 0; s < n; ++s) {
+        const int k = kept[s * el + e];
+        if (j < acc + k) {
+          dst = peers[s] + static_cast<unsigned long long>(dst_off[s * el + e] + (j - acc)) *
+                               static_cast<unsigned long long>(row_bytes);
+          break;
+        }
+        acc += k;
+      }
+    }
+    row_dst[r] = dst;
+  }
+}
+
+int moe_ep_row_dst(const int* table, int n, int el, int rows_pad, const int* dst_off,
+                   const unsigned long long* peers, long long row_bytes,
+                   unsigned long long* row_dst, void* stream) {
+  if (n < 1 || el < 1 || row_bytes <= 0 || (row_bytes & 15)) return kErrInvalidArg;
+  if (rows_pad <= 0) return kOk;
+  const int g = ceil_div_i(rows_pad, 256);
+  row_dst_kernel<<<g < sms() * 8 ? g : sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      table, n, el, rows_pad, dst_off, peers, row_bytes, row_dst);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
 // Oracle-layout (compact) row_id_map (int64, -1 phantom) and compact->padded row index.
 int moe_permute_compact_map(const int* meta, const int* off_c, const int* off_pad, int E,
                             const int* row_src, long long* row_id_map, int* compact_to_pad,

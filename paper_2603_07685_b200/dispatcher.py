@@ -356,8 +356,11 @@ def _record_exchange(hp: EPHostPlan, h: int, width: int = 2):
                          local_experts=el)
 
 
-def _pool(ep: EPGroup, dev) -> SymmPool:
-    key = (id(ep.group), dev.index)
+def _pool(ep: EPGroup, dev, tag: str = "") -> SymmPool:
+    """Symmetric buffers per (EP group, device, tag). Layers that are alive at the same time
+    (several MoE layers before their backward) must use distinct tags: a layer's received
+    rows stay in its pool until its backward has run."""
+    key = (id(ep.group), dev.index, tag)
     if key not in _POOLS:
         _POOLS[key] = SymmPool(ep, dev)
     return _POOLS[key]
@@ -459,12 +462,12 @@ def _echo_reduce(pool, ep, dw_ext, layout, el, name):
 class _MoEEPP2PFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w_r, w1, w2, sel_bias, w1s, w2s, cfg: MoEConfig, ep: EPGroup,
-                echo_slots: int = 0):
+                echo_slots: int = 0, scatter: bool = True, tag: str = ""):
         t, h = x.shape
         E, K = cfg.num_experts, cfg.top_k
         n = ep.n
         dev = x.device
-        pool = _pool(ep, dev)
+        pool = _pool(ep, dev, tag)
         stream = torch.cuda.current_stream().cuda_stream
         w_r_t, w_r_pad = ops.stage_router_weight(w_r)
         r = ops.router_forward(x, w_r, K, cfg.score, sel_bias, 0.0, w_r_t=w_r_t)
@@ -492,11 +495,14 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         ctx_topk = topk_use
         cap_local = hp.cap_local if hp.cap_local is not None else np.full(E_use, -1)
         meta = np.array([hp.rows_pad // ops.ALIGN, hp.rows_pad, 0], dtype=np.int64)
-        parts = [base, cap_local, hp.table.astype(np.int64), hp.block_expert, meta]
+        # dst_off[s, j]: source s's compact offset of this rank's j-th (virtual) expert, where
+        # the scatter epilogues return that expert's rows
+        dst_off = _excl_cumsum(hp.kept, axis=1)[:, ep.rank * el:(ep.rank + 1) * el].ravel()
+        parts = [base, cap_local, hp.table.astype(np.int64), hp.block_expert, meta, dst_off]
         lens = [len(p) for p in parts]
         tab = torch.from_numpy(np.concatenate(parts).astype(np.int32)).pin_memory().to(
             dev, non_blocking=True)
-        base_d, cap_d, table_d, be_d, meta_d = torch.split(tab, lens)
+        base_d, cap_d, table_d, be_d, meta_d, dst_off_d = torch.split(tab, lens)
         smallf = torch.from_numpy(np.concatenate([[aux_v], aux_g]).astype(np.float32))
         smallf = smallf.pin_memory().to(dev, non_blocking=True)
         aux = smallf[0].clone()
@@ -530,23 +536,48 @@ class _MoEEPP2PFunction(torch.autograd.Function):
                   prob_peers.data_ptr() if prob_peers is not None else None, stream)
         pool.barrier()
         preact, act = gemm.fc1_fwd(xp, w1, be_d, nmb, row_prob, pair=pair)
-        o, o_peers = pool.get("o", rows_alloc * h, torch.bfloat16)
-        o = o[: rows_alloc * h].view(rows_alloc, h)
-        gemm.fc2_fwd(act, w2, be_d, nmb, out=o, pair=pair)
-        shared = shared_expert_forward(x, w1s, w2s) if w1s is not None else None
-        pool.barrier()
         y = torch.empty_like(x)
-        # local compact copy of the pulled expert outputs: the backward's dprob = <dY, O>
-        # then reads local memory instead of pulling O over NVLink a second time
-        o_local = None
-        if not cfg.mem_efficient:
-            o_local = torch.empty((max(sum(hp.send_splits), 1), h), dtype=x.dtype, device=dev)
-        _lib.call("moe_ep_combine_pull", o_peers.data_ptr(), t, K, h, ctx_topk.data_ptr(),
-                  splan.inv_map.data_ptr(), base_d.data_ptr(), el,
-                  None if cfg.mem_efficient else r.topk_prob.data_ptr(),
-                  x.data_ptr() if cap >= 0 else None,
-                  shared[-1].data_ptr() if shared is not None else None, None, y.data_ptr(),
-                  o_local.data_ptr() if o_local is not None else None, stream)
+        row_dst_dx = None
+        if scatter:
+            # expert outputs go straight from fc2's epilogue into each source rank's compact
+            # buffer over NVLink; the combine is then purely local
+            rows_c = max(t * K, 1)
+            orecv, orecv_peers = pool.get("orecv", rows_c * h, torch.bfloat16)
+            o_local = orecv[: rows_c * h].view(rows_c, h)
+            _, dxrecv_peers = pool.get("dxrecv", rows_c * h, torch.bfloat16)
+            row_dst = torch.empty((2, rows_alloc), dtype=torch.int64, device=dev)
+            for i, pp in enumerate((orecv_peers, dxrecv_peers)):
+                _lib.call("moe_ep_row_dst", table_d.data_ptr(), n, el, hp.rows_pad,
+                          dst_off_d.data_ptr(), pp.data_ptr(), h * 2, row_dst[i].data_ptr(),
+                          stream)
+            row_dst_dx = row_dst[1]
+            gemm.fc2_fwd_scatter(act, w2, be_d, nmb, row_dst[0], pair=pair)
+            shared = shared_expert_forward(x, w1s, w2s) if w1s is not None else None
+            pool.barrier()
+            _lib.call("moe_combine", o_local.data_ptr(), t, K, h, splan.inv_map.data_ptr(),
+                      None if cfg.mem_efficient else r.topk_prob.data_ptr(),
+                      x.data_ptr() if cap >= 0 else None,
+                      shared[-1].data_ptr() if shared is not None else None, None,
+                      y.data_ptr(), stream)
+        else:
+            o, o_peers = pool.get("o", rows_alloc * h, torch.bfloat16)
+            o = o[: rows_alloc * h].view(rows_alloc, h)
+            gemm.fc2_fwd(act, w2, be_d, nmb, out=o, pair=pair)
+            shared = shared_expert_forward(x, w1s, w2s) if w1s is not None else None
+            pool.barrier()
+            # local compact copy of the pulled expert outputs: the backward's dprob = <dY, O>
+            # then reads local memory instead of pulling O over NVLink a second time
+            o_local = None
+            if not cfg.mem_efficient:
+                o_local = torch.empty((max(sum(hp.send_splits), 1), h), dtype=x.dtype,
+                                      device=dev)
+            _lib.call("moe_ep_combine_pull", o_peers.data_ptr(), t, K, h, ctx_topk.data_ptr(),
+                      splan.inv_map.data_ptr(), base_d.data_ptr(), el,
+                      None if cfg.mem_efficient else r.topk_prob.data_ptr(),
+                      x.data_ptr() if cap >= 0 else None,
+                      shared[-1].data_ptr() if shared is not None else None, None, y.data_ptr(),
+                      o_local.data_ptr() if o_local is not None else None, stream)
+        ctx.scatter, ctx.tag, ctx.row_dst_dx = scatter, tag, row_dst_dx
         ctx.cfg, ctx.ep, ctx.r, ctx.splan, ctx.cap, ctx.pair = cfg, ep, r, splan, cap, pair
         ctx.topk_use, ctx.layout, ctx.el_own = topk_use, layout, E // n
         ctx.o_local = o_local
@@ -565,7 +596,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         t, h = x.shape
         K = cfg.top_k
         dev = x.device
-        pool = _pool(ep, dev)
+        pool = _pool(ep, dev, ctx.tag)
         stream = torch.cuda.current_stream().cuda_stream
         dy = dy.contiguous()
         xp, _ = pool.get("xp", rows_alloc * h, torch.bfloat16)
@@ -591,10 +622,15 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         else:
             d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, be_d, nmb, pair=ctx.pair)
         dw2 = gemm.wgrad(d_o, act, off_pad_d, el)
-        dxp, dxp_peers = pool.get("dxp", rows_alloc * h, torch.bfloat16)
-        dxp = dxp[: rows_alloc * h].view(rows_alloc, h)
-        gemm.fc1_dgrad(d_pre, w1, be_d, nmb, out=dxp, pair=ctx.pair)
+        if ctx.scatter:  # dX rows return from fc1_dgrad's epilogue into the source ranks
+            gemm.fc1_dgrad_scatter(d_pre, w1, be_d, nmb, ctx.row_dst_dx, pair=ctx.pair)
+        else:
+            dxp, dxp_peers = pool.get("dxp", rows_alloc * h, torch.bfloat16)
+            dxp = dxp[: rows_alloc * h].view(rows_alloc, h)
+            gemm.fc1_dgrad(d_pre, w1, be_d, nmb, out=dxp, pair=ctx.pair)
         dw1 = gemm.wgrad(d_pre, xp, off_pad_d, el)
+        # also orders every rank's reads of its symmetric buffers (xp, d_o) before any
+        # peer's next write into them
         pool.barrier()
         if cfg.mem_efficient:
             _lib.call("moe_ep_dprob_pull", part_peers.data_ptr(), t, K, ctx_topk.data_ptr(),
@@ -608,17 +644,26 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         if ctx.shared is not None:
             dx_shared, dw1s, dw2s = shared_expert_backward(x, dy, w1s, w2s, ctx.shared)
         dx = torch.empty_like(x)
-        _lib.call("moe_ep_combine_pull", dxp_peers.data_ptr(), t, K, h, ctx_topk.data_ptr(),
-                  splan.inv_map.data_ptr(), base_d.data_ptr(), el, None,
-                  dy.data_ptr() if ctx.cap >= 0 else None, dx_router.data_ptr(),
-                  dx_shared.data_ptr() if dx_shared is not None else None, dx.data_ptr(), None,
-                  stream)
-        # no rank may overwrite the symmetric buffers before every rank has pulled
-        pool.barrier()
+        if ctx.scatter:
+            rows_c = max(t * K, 1)
+            dxrecv, _ = pool.get("dxrecv", rows_c * h, torch.bfloat16)
+            _lib.call("moe_combine", dxrecv.data_ptr(), t, K, h, splan.inv_map.data_ptr(), None,
+                      dy.data_ptr() if ctx.cap >= 0 else None, dx_router.data_ptr(),
+                      dx_shared.data_ptr() if dx_shared is not None else None, dx.data_ptr(),
+                      stream)
+        else:
+            _lib.call("moe_ep_combine_pull", dxp_peers.data_ptr(), t, K, h, ctx_topk.data_ptr(),
+                      splan.inv_map.data_ptr(), base_d.data_ptr(), el, None,
+                      dy.data_ptr() if ctx.cap >= 0 else None, dx_router.data_ptr(),
+                      dx_shared.data_ptr() if dx_shared is not None else None, dx.data_ptr(),
+                      None, stream)
+            # no rank may overwrite the symmetric buffers before every rank has pulled
+            pool.barrier()
         if ctx.layout is not None:  # clone weight gradients back into the home experts
             dw1 = _echo_reduce(pool, ep, dw1, ctx.layout, ctx.el_own, "echo_dw1")
             dw2 = _echo_reduce(pool, ep, dw2, ctx.layout, ctx.el_own, "echo_dw2")
-        return (dx, dw_r.to(torch.bfloat16), dw1, dw2, None, dw1s, dw2s, None, None, None)
+        return (dx, dw_r.to(torch.bfloat16), dw1, dw2, None, dw1s, dw2s, None, None, None, None,
+                None)
 
 
 def _excl(a):
@@ -631,13 +676,14 @@ class _MoEEPDedupFunction(torch.autograd.Function):
     NVLink each way; destinations expand rows locally and pre-reduce per-token outputs."""
 
     @staticmethod
-    def forward(ctx, x, w_r, w1, w2, sel_bias, w1s, w2s, cfg: MoEConfig, ep: EPGroup):
+    def forward(ctx, x, w_r, w1, w2, sel_bias, w1s, w2s, cfg: MoEConfig, ep: EPGroup,
+                tag: str = ""):
         t, h = x.shape
         E, K = cfg.num_experts, cfg.top_k
         n = ep.n
         me = ep.rank
         dev = x.device
-        pool = _pool(ep, dev)
+        pool = _pool(ep, dev, tag)
         stream = torch.cuda.current_stream().cuda_stream
         i32 = dict(dtype=torch.int32, device=dev)
         w_r_t, w_r_pad = ops.stage_router_weight(w_r)
@@ -742,7 +788,7 @@ class _MoEEPDedupFunction(torch.autograd.Function):
                   x.data_ptr() if cap >= 0 else None,
                   shared[-1].data_ptr() if shared is not None else None, None, y.data_ptr(),
                   None, stream)
-        ctx.cfg, ctx.ep, ctx.r, ctx.cap, ctx.pair = cfg, ep, r, cap, pair
+        ctx.cfg, ctx.ep, ctx.r, ctx.cap, ctx.pair, ctx.tag = cfg, ep, r, cap, pair, tag
         ctx.st = (splan, rplan, rank_idx, base_d, tbase_d, be_d, nmb, off_pad_d, rows_alloc,
                   hp.rows_pad, tok_cap, tok_recv, el)
         ctx.shared = shared[:-1] if shared is not None else None
@@ -758,7 +804,7 @@ class _MoEEPDedupFunction(torch.autograd.Function):
         t, h = x.shape
         K = cfg.top_k
         dev = x.device
-        pool = _pool(ep, dev)
+        pool = _pool(ep, dev, ctx.tag)
         stream = torch.cuda.current_stream().cuda_stream
         dy = dy.contiguous()
         tok, tok_peers = pool.get("dd_tok", tok_cap * h, torch.bfloat16)
@@ -817,19 +863,27 @@ class _MoEEPDedupFunction(torch.autograd.Function):
                   dx_shared.data_ptr() if dx_shared is not None else None, dx.data_ptr(), None,
                   stream)
         pool.barrier()
-        return (dx, dw_r.to(torch.bfloat16), dw1, dw2, None, dw1s, dw2s, None, None)
+        return (dx, dw_r.to(torch.bfloat16), dw1, dw2, None, dw1s, dw2s, None, None, None)
 
 
 def moe_forward_ep(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
                    selection_bias=None, w1_shared=None, w2_shared=None, transport: str = "auto",
-                   echo_slots: int = 0):
+                   echo_slots: int = 0, tag: str = ""):
     """EP MoE layer: w1_local [E/EP, 2m, h], w2_local [E/EP, h, m] are this rank's experts
     (global experts [rank*E/EP, (rank+1)*E/EP)). Returns (y [T,h], global aux).
 
-    transport "auto" (default): "p2p_dedup" for top_k >= 4, else "p2p". "p2p": the exchange is fused into the permute / combine kernels over
-    NVLink peer memory (csrc/ep.cu). "p2p_dedup": the same with token de-duplication (one
-    row per (token, destination rank) each way; HybridEP-style). "nccl": permute -> NCCL
-    all_to_all_single -> regroup (the baseline dispatcher, kept for A/B measurement).
+    transport:
+      "auto" (default): "p2p_dedup" for top_k >= 4, else "p2p".
+      "p2p": tokens are pushed over NVLink peer memory straight into the expert rank's
+        padded plan (csrc/ep.cu); expert outputs and dX rows return from the fc2 / fc1-dgrad
+        GEMM epilogues, which store each row into its source rank's buffer over NVLink, so
+        both combines are local.
+      "p2p_pull": the previous p2p variant, where the combines pull the rows back over
+        NVLink (kept for A/B measurement).
+      "p2p_dedup": token de-duplication (one row per (token, destination rank) each way;
+        HybridEP-style).
+      "nccl": permute -> NCCL all_to_all_single -> regroup (the baseline dispatcher).
+    tag: buffer namespace; give every MoE layer that is alive at the same time its own.
 
     The router weight gradient returned is this rank's partial sum over its own tokens;
     W_r is replicated, so its all-reduce belongs to the data-parallel gradient sync.
@@ -840,10 +894,12 @@ def moe_forward_ep(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
         # measured on B200 (EP=4): dedup wins for top-8 (Qwen3 +5%, DeepSeek +1%); for
         # top-2 most tokens already hit distinct ranks and the local expand costs more
         transport = "p2p_dedup" if cfg.top_k >= 4 else "p2p"
-    if echo_slots:
+    args = (x, w_r, w1_local, w2_local, selection_bias, w1_shared, w2_shared, cfg, ep)
+    if echo_slots or transport in ("p2p", "p2p_pull"):
         # ECHO hot-expert cloning runs on the p2p transport (virtual experts)
-        return _MoEEPP2PFunction.apply(x, w_r, w1_local, w2_local, selection_bias, w1_shared,
-                                       w2_shared, cfg, ep, int(echo_slots))
-    fn = {"p2p": _MoEEPP2PFunction, "p2p_dedup": _MoEEPDedupFunction,
-          "nccl": _MoEEPFunction}[transport]
-    return fn.apply(x, w_r, w1_local, w2_local, selection_bias, w1_shared, w2_shared, cfg, ep)
+        return _MoEEPP2PFunction.apply(*args, int(echo_slots), transport != "p2p_pull", tag)
+    if transport == "p2p_dedup":
+        return _MoEEPDedupFunction.apply(*args, tag)
+    if transport == "nccl":
+        return _MoEEPFunction.apply(*args)
+    raise ValueError(f"unknown transport {transport!r}")

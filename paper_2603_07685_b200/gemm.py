@@ -88,6 +88,26 @@ def fc2_fwd(act, w2, block_expert, num_m_blocks, out=None, max_rows=None, pair=F
     return out
 
 
+def fc2_fwd_scatter(act, w2, block_expert, num_m_blocks, row_dst, max_rows=None, pair=False):
+    """fc2 forward storing row r at address row_dst[r] (int64 device tensor; 0 = skip)."""
+    a_rows, m = act.shape
+    rows = a_rows if max_rows is None else max_rows
+    e, h, _ = w2.shape
+    _lib.call("moe_gg_fc2_fwd_scatter", act.data_ptr(), w2.data_ptr(), a_rows, rows, m, h, e,
+              block_expert.data_ptr(), num_m_blocks.data_ptr(), row_dst.data_ptr(), int(pair),
+              _stream())
+
+
+def fc1_dgrad_scatter(d_preact, w1, block_expert, num_m_blocks, row_dst, max_rows=None,
+                      pair=False):
+    a_rows, m2 = d_preact.shape
+    rows = a_rows if max_rows is None else max_rows
+    e, _, h = w1.shape
+    _lib.call("moe_gg_fc1_dgrad_scatter", d_preact.data_ptr(), w1.data_ptr(), a_rows, rows,
+              m2 // 2, h, e, block_expert.data_ptr(), num_m_blocks.data_ptr(),
+              row_dst.data_ptr(), int(pair), _stream())
+
+
 def fc2_dgrad(dout, w2, preact, block_expert, num_m_blocks, row_prob=None, want_dprob=False,
               d_preact=None, max_rows=None, pair=False, part=None):
     """part: optional preallocated [rows, m/256] fp32 dprob partials (implies want_dprob)."""

@@ -143,7 +143,7 @@ def _worker(rank, world, port, case, q, transport):
         q.put((rank, traceback.format_exc() + repr(exc)))
 
 
-@pytest.mark.parametrize("transport", ["p2p", "p2p_dedup", "nccl"])
+@pytest.mark.parametrize("transport", ["p2p", "p2p_pull", "p2p_dedup", "nccl"])
 @pytest.mark.parametrize("name", list(CASES))
 def test_ep_layer_matches_global_oracle(name, transport):
     _run(CASES[name], transport)
