@@ -374,7 +374,8 @@ def run_gpu(args, c) -> None:
         from paper_2603_07685_b200.dispatcher import last_exchange
 
         ex_names = ("moe_ep_dispatch_push", "moe_ep_combine_pull", "moe_ep_combine_bwd_push",
-                    "moe_gather_rows", "moe_ep_dispatch_dedup", "moe_ep_expand_grad")
+                    "moe_gather_rows", "moe_ep_dispatch_dedup", "moe_ep_expand_grad",
+                    "moe_ep_dispatch_push_dest", "moe_ep_combine_bwd_push_dest")
         ex_ms = sum(sum(v) for k_, v in per_kernel.items() if k_ in ex_names) / args.steps
         # per step: 4 one-way transfers of this rank's remote rows (x, O, dO, dX); with
         # balanced routing each direction of the NVLink port carries ~4 x sent bytes
@@ -384,15 +385,18 @@ def run_gpu(args, c) -> None:
             tr = "p2p_dedup" if K >= 4 else "p2p"
         # p2p: the two return transfers (O, dX) run inside the fc2 / fc1-dgrad epilogues,
         # so only the two pushes (x, dO) are standalone exchange kernels
-        standalone_bytes = (2 * last_exchange["bytes_sent_remote"] if tr == "p2p" else out_bytes)
+        standalone_bytes = (2 * last_exchange["bytes_sent_remote"] if tr in ("p2p", "p2p_sync")
+                            else out_bytes)
         nvlink_stats = {
             "transport": tr,
             "bytes_out_per_step_per_gpu": out_bytes,
             "model_bytes_per_step_per_gpu": 4 * a2a_send_volume(T, K, h, n, 2),
             "exchange_kernel_ms_per_step": round(ex_ms, 4),
-            "returns_fused_in_gemm_epilogue": tr == "p2p",
+            "returns_fused_in_gemm_epilogue": tr in ("p2p", "p2p_sync"),
+            "dispatch_overlapped_with_gemm": tr == "p2p",
             "achieved_GBps_per_direction": (round(standalone_bytes / (ex_ms / 1e3) / 1e9, 1)
-                                            if ex_ms and tr in ("p2p", "p2p_pull") else None),
+                                            if ex_ms and tr in ("p2p", "p2p_sync", "p2p_pull")
+                                            else None),
             "note": ("p2p_dedup sends one row per (token, rank): fewer bytes than counted here"
                      if tr == "p2p_dedup" else None),
             "peak_GBps_per_direction": 770.0,
@@ -538,7 +542,7 @@ def main():
     ap.add_argument("--cpu-sample-tokens", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ep-transport", default="auto",
-                    choices=["auto", "p2p", "p2p_pull", "p2p_dedup", "nccl"],
+                    choices=["auto", "p2p", "p2p_sync", "p2p_pull", "p2p_dedup", "nccl"],
                     help="EP exchange: fused NVLink peer-memory kernels (p2p) or NCCL a2a")
     ap.add_argument("--echo-slots", type=int, default=0,
                     help="ECHO hot-expert clone slots per rank (EP, dropless)")

@@ -107,6 +107,21 @@ int moe_ep_dispatch_push(const void* x, int T, int K, int h, const int* topk_idx
                          const int* inv_c, const int* base, int el,
                          const unsigned long long* peers, const float* prob,
                          const unsigned long long* prob_peers, void* stream);
+/* Overlapped dispatch: push only the selections whose expert lives on rank `dest`, then
+ * moe_ep_signal publishes flag_peers[dest][slot] = epoch (release, system scope). The
+ * consumer GEMM (moe_gg_fc1_fwd_ep / moe_gg_fc2_dgrad_ep) waits per 128-row block for the
+ * source ranks moe_ep_block_need lists, so the exchange overlaps the grouped GEMM. */
+int moe_ep_dispatch_push_dest(const void* x, int T, int K, int h, const int* topk_idx,
+                              const int* inv_c, const int* base, int el,
+                              const unsigned long long* peers, const float* prob,
+                              const unsigned long long* prob_peers, int dest, void* stream);
+int moe_ep_signal(const unsigned long long* flag_peers, int dest, int slot, unsigned int epoch,
+                  void* stream);
+/* Load / configure the kernels above before the first overlapped step (CUDA lazy loading
+ * of a kernel launched beside a GEMM that waits for it would deadlock). */
+int moe_ep_prepare(void);
+int moe_ep_block_need(const int* table, int n, int el, int me, int nblocks, int cg,
+                      unsigned int* need, int* order, void* stream);
 /* rows_copy (nullable): local compact copy of the pulled rows, indexed by inv_c */
 int moe_ep_combine_pull(const unsigned long long* peers, int T, int K, int h,
                         const int* topk_idx, const int* inv_c, const int* base, int el,
@@ -117,6 +132,10 @@ int moe_ep_combine_bwd_push(const void* dy, const void* o_local,
                             const unsigned long long* d_peers, int T, int K, int h,
                             const int* topk_idx, const int* inv_c, const int* base, int el,
                             const float* prob, float* dprob, void* stream);
+int moe_ep_combine_bwd_push_dest(const void* dy, const void* o_local,
+                                 const unsigned long long* d_peers, int T, int K, int h,
+                                 const int* topk_idx, const int* inv_c, const int* base, int el,
+                                 const float* prob, float* dprob, int dest, void* stream);
 int moe_ep_dprob_pull(const unsigned long long* part_peers, int T, int K, const int* topk_idx,
                       const int* inv_c, const int* base, int el, int ldp, float* dprob,
                       void* stream);
@@ -165,6 +184,22 @@ int moe_gg_fc1_dgrad_scatter(const void* d_preact, const void* w1, int a_rows, i
                              int m, int h, int num_experts, const int* block_expert,
                              const int* num_m_blocks, const unsigned long long* row_dst,
                              int flags, void* stream);
+/* fc1 forward / fc2 dgrad overlapped with the EP dispatch of their A operand: a tile's rows
+ * are read once src_flag[s] >= epoch for every source s in block_need[block]; tiles run in
+ * unit_order. status: int[8]; on a wait timeout (2 s) it receives [1, block, missing
+ * source mask, epoch, flags[0..3]] and the remaining waits fail fast. */
+int moe_gg_fc1_fwd_ep(const void* xp, const void* w1, int a_rows, int max_rows, int h, int m,
+                      int num_experts, const int* block_expert, const int* num_m_blocks,
+                      const float* row_prob, void* preact, void* act, int flags,
+                      const unsigned int* src_flag, unsigned int epoch,
+                      const unsigned int* block_need, const int* unit_order, int* status,
+                      void* stream);
+int moe_gg_fc2_dgrad_ep(const void* dout, const void* w2, const void* preact, int a_rows,
+                        int max_rows, int h, int m, int num_experts, const int* block_expert,
+                        const int* num_m_blocks, const float* row_prob, void* d_preact,
+                        float* dprob_partial, int flags, const unsigned int* src_flag,
+                        unsigned int epoch, const unsigned int* block_need,
+                        const int* unit_order, int* status, void* stream);
 int moe_gg_fc2_dgrad(const void* dout, const void* w2, const void* preact, int a_rows,
                      int max_rows, int h, int m, int num_experts, const int* block_expert,
                      const int* num_m_blocks, const float* row_prob, void* d_preact,

@@ -7,7 +7,7 @@ stream as the raw ``cudaStream_t`` of torch's current stream.
 from __future__ import annotations
 
 import ctypes
-from ctypes import c_float, c_int, c_int64, c_void_p
+from ctypes import c_float, c_int, c_int64, c_uint, c_void_p
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libmoe_b200.so"
@@ -27,6 +27,7 @@ P = c_void_p
 I = c_int
 L = c_int64
 F = c_float
+U = c_uint
 
 # name -> argtypes (all return int status)
 SIGNATURES: dict[str, list] = {
@@ -52,6 +53,11 @@ SIGNATURES: dict[str, list] = {
     "moe_ep_dispatch_push": [P, I, I, I, P, P, P, I, P, P, P, P],
     "moe_ep_combine_pull": [P, I, I, I, P, P, P, I, P, P, P, P, P, P, P],
     "moe_ep_combine_bwd_push": [P, P, P, I, I, I, P, P, P, I, P, P, P],
+    "moe_ep_combine_bwd_push_dest": [P, P, P, I, I, I, P, P, P, I, P, P, I, P],
+    "moe_ep_dispatch_push_dest": [P, I, I, I, P, P, P, I, P, P, P, I, P],
+    "moe_ep_signal": [P, I, I, U, P],
+    "moe_ep_prepare": [],
+    "moe_ep_block_need": [P, I, I, I, I, I, P, P, P],
     "moe_ep_dprob_pull": [P, I, I, P, P, P, I, I, P, P],
     "moe_ep_token_ranks": [P, P, I, I, I, P, P, P, P],
     "moe_ep_dispatch_dedup": [P, I, I, I, P, P, P, I, P, P, P, P, P, P, P, P, P, P, P, P],
@@ -63,6 +69,8 @@ SIGNATURES: dict[str, list] = {
     "moe_gg_fc2_fwd": [P, P, I, I, I, I, I, P, P, P, I, P],
     "moe_gg_fc2_fwd_scatter": [P, P, I, I, I, I, I, P, P, P, I, P],
     "moe_gg_fc1_dgrad_scatter": [P, P, I, I, I, I, I, P, P, P, I, P],
+    "moe_gg_fc1_fwd_ep": [P, P, I, I, I, I, I, P, P, P, P, P, I, P, U, P, P, P, P],
+    "moe_gg_fc2_dgrad_ep": [P, P, P, I, I, I, I, I, P, P, P, P, P, I, P, U, P, P, P, P],
     "moe_gg_fc2_dgrad": [P, P, P, I, I, I, I, I, P, P, P, P, P, I, P],
     "moe_gg_fc1_dgrad": [P, P, I, I, I, I, I, P, P, P, I, P],
     "moe_gg_wgrad": [P, P, I, I, I, I, P, P, P],
@@ -127,7 +135,7 @@ def check(status: int, what: str) -> None:
 
 # kernels of ours launched by one call of each entry point (cudaMemsetAsync not counted)
 KERNELS_PER_CALL = {name: 1 for name in SIGNATURES}
-KERNELS_PER_CALL.update({"moe_permute_plan": 5, "moe_permute_gather": 2})
+KERNELS_PER_CALL.update({"moe_permute_plan": 5, "moe_permute_gather": 2, "moe_ep_prepare": 0})
 
 
 class _Stats:

@@ -60,7 +60,8 @@ __global__ void dispatch_push_kernel(const int4* __restrict__ x, int T, int K, i
                                      const int* __restrict__ base, int el,
                                      const unsigned long long* __restrict__ peers,
                                      const float* __restrict__ prob,
-                                     const unsigned long long* __restrict__ prob_peers) {
+                                     const unsigned long long* __restrict__ prob_peers,
+                                     int dest) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = lane_id();
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -74,6 +75,7 @@ __global__ void dispatch_push_kernel(const int4* __restrict__ x, int T, int K, i
         if (d < 0) continue;
         const int e = __ldg(topk_idx + (long long)t * K + k);
         const int r = e / el;
+        if (dest >= 0 && r != dest) continue;
         const long long row = (long long)__ldg(base + e) + d;
         if (!loaded) {
 #pragma unroll
@@ -184,7 +186,7 @@ __global__ void combine_bwd_push_kernel(const int4* __restrict__ dy,
                                         const int* __restrict__ inv_c,
                                         const int* __restrict__ base, int el,
                                         const float* __restrict__ prob,
-                                        float* __restrict__ dprob) {
+                                        float* __restrict__ dprob, int dest) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = lane_id();
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -192,6 +194,7 @@ __global__ void combine_bwd_push_kernel(const int4* __restrict__ dy,
     const int4* orow[KMAX];
     int4* drow[KMAX];
     float p[KMAX], dot[KMAX];
+    bool any = false;
 #pragma unroll
     for (int k = 0; k < KMAX; ++k) {
       orow[k] = nullptr;
@@ -201,8 +204,9 @@ __global__ void combine_bwd_push_kernel(const int4* __restrict__ dy,
       if (k < K) {
         const long long i = (long long)t * K + k;
         const int d = __ldg(inv_c + i);
-        if (d >= 0) {
-          const int e = __ldg(topk_idx + i);
+        const int e = d >= 0 ? __ldg(topk_idx + i) : -1;
+        if (d >= 0 && (dest < 0 || e / el == dest)) {
+          any = true;
           const long long row = (long long)__ldg(base + e) + d;
           if (o_local) orow[k] = o_local + (long long)d * hv;
           drow[k] = reinterpret_cast<int4*>(d_peers[e / el]) + row * hv;
@@ -210,6 +214,7 @@ __global__ void combine_bwd_push_kernel(const int4* __restrict__ dy,
         }
       }
     }
+    if (dest >= 0 && !any) continue;  // no selection of this token goes to `dest`
     for (int c0 = 0; c0 < hv; c0 += 32 * VPL) {
       int4 y[VPL], ov[KMAX][VPL];
 #pragma unroll
@@ -252,7 +257,74 @@ __global__ void combine_bwd_push_kernel(const int4* __restrict__ dy,
       for (int k = 0; k < KMAX; ++k) {
         if (k >= K) break;
         const float s = warp_sum(dot[k]);
-        if (lane == 0) dprob[(long long)t * K + k] = (drow[k] && o_local) ? s : 0.f;
+        // per-destination passes write only their own selections (caller zero-fills)
+        if (lane == 0 && (dest < 0 || drow[k]))
+          dprob[(long long)t * K + k] = (drow[k] && o_local) ? s : 0.f;
+      }
+    }
+  }
+  __threadfence_system();
+}
+
+// Per-destination combine backward for the overlapped dispatch: the same math as
+// combine_bwd_push_kernel, one selection at a time (dY re-read from L2 per selection), so it
+// needs few registers. It runs beside a persistent GEMM whose 6 warps take up to 184
+// registers each: warps are spread round-robin over the 4 SM sub-partitions (16K registers
+// each), which leaves about 4.6K registers per sub-partition, i.e. <= 144 per thread here.
+template <int VPL>
+__global__ void __launch_bounds__(128) combine_bwd_push_sel_kernel(
+    const int4* __restrict__ dy, const int4* __restrict__ o_local,
+    const unsigned long long* __restrict__ d_peers, int T, int K, int hv,
+    const int* __restrict__ topk_idx, const int* __restrict__ inv_c,
+    const int* __restrict__ base, int el, const float* __restrict__ prob,
+    float* __restrict__ dprob, int dest) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = lane_id();
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp; t < T; t += nwarps) {
+    for (int k = 0; k < K; ++k) {
+      const long long i = (long long)t * K + k;
+      const int d = __ldg(inv_c + i);
+      if (d < 0) continue;
+      const int e = __ldg(topk_idx + i);
+      if (e / el != dest) continue;
+      const long long row = (long long)__ldg(base + e) + d;
+      int4* drow = reinterpret_cast<int4*>(d_peers[dest]) + row * hv;
+      const int4* orow = o_local ? o_local + (long long)d * hv : nullptr;
+      const float p = prob ? __ldg(prob + i) : 1.f;
+      float dot = 0.f;
+      for (int c0 = 0; c0 < hv; c0 += 32 * VPL) {
+        int4 y[VPL], ov[VPL];
+#pragma unroll
+        for (int u = 0; u < VPL; ++u) {
+          const int c = c0 + u * 32 + lane;
+          if (c < hv) {
+            y[u] = __ldg(dy + (long long)t * hv + c);
+            if (orow) ov[u] = ld_nc_v4(orow + c);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < VPL; ++u) {
+          const int c = c0 + u * 32 + lane;
+          if (c >= hv) continue;
+          const uint32_t* uy = reinterpret_cast<const uint32_t*>(&y[u]);
+          int4 wv;
+          uint32_t* uw = reinterpret_cast<uint32_t*>(&wv);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 a = unpack_bf16x2(uy[j]);
+            if (orow) {
+              const float2 b = unpack_bf16x2(reinterpret_cast<const uint32_t*>(&ov[u])[j]);
+              dot += a.x * b.x + a.y * b.y;
+            }
+            uw[j] = prob ? pack_bf16x2(a.x * p, a.y * p) : uy[j];
+          }
+          drow[c] = wv;
+        }
+      }
+      if (dprob) {
+        const float s = warp_sum(dot);
+        if (lane == 0) dprob[i] = o_local ? s : 0.f;
       }
     }
   }
@@ -476,6 +548,15 @@ static int sms() {
   }
   return n;
 }
+// Kernels that must run beside a persistent grouped GEMM (the overlapped dispatch) use the
+// GEMM's L1/shared split: an SM only hosts CTAs of kernels whose carve-out matches its
+// current configuration, so with the default (L1-preferring) carve-out a push CTA would wait
+// for the GEMM to drain, and the GEMM waits for the push.
+template <typename K>
+static void prefer_max_shared(K kern) {
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       static_cast<int>(cudaSharedmemCarveoutMaxShared));
+}
 static int warp_grid(long long items) {
   const long long blocks = ceil_div_ll(items > 0 ? items : 1, 8);
   const long long cap = (long long)sms() * 8;
@@ -498,7 +579,135 @@ int moe_ep_dispatch_push(const void* x, int T, int K, int h, const int* topk_idx
   if (T == 0) return kOk;
   dispatch_push_kernel<4><<<warp_grid(T), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const int4*>(x), T, K, h / 8, topk_idx, inv_c, base, el, peers, prob,
-      prob_peers);
+      prob_peers, -1);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+// Dispatch restricted to the selections whose expert lives on rank `dest`.
+int moe_ep_dispatch_push_dest(const void* x, int T, int K, int h, const int* topk_idx,
+                              const int* inv_c, const int* base, int el,
+                              const unsigned long long* peers, const float* prob,
+                              const unsigned long long* prob_peers, int dest, void* stream) {
+  if (h % 8 || el < 1 || dest < 0) return kErrInvalidArg;
+  if (T == 0) return kOk;
+  dispatch_push_kernel<4><<<warp_grid(T), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const int4*>(x), T, K, h / 8, topk_idx, inv_c, base, el, peers, prob,
+      prob_peers, dest);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+__global__ void signal_kernel(const unsigned long long* __restrict__ flag_peers, int dest,
+                              int slot, uint32_t epoch) {
+  __threadfence_system();
+  st_release_sys_u32(reinterpret_cast<uint32_t*>(flag_peers[dest]) + slot, epoch);
+}
+
+// Publish "this rank's rows for `dest` are complete": flag_peers[dest][slot] = epoch
+// (release, system scope), ordered after the preceding pushes on `stream`.
+int moe_ep_signal(const unsigned long long* flag_peers, int dest, int slot, unsigned int epoch,
+                  void* stream) {
+  if (dest < 0 || slot < 0) return kErrInvalidArg;
+  signal_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(flag_peers, dest, slot, epoch);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+// Per 128-row block of this rank's padded plan: bitmask of the source ranks whose rows it
+// holds (table of moe_ep_regroup_map), and the schedule of GEMM units (unit = `cg` blocks)
+// sorted by the arrival position of their latest source: source s pushes to ranks
+// s, s+1, ... in turn, so rank `me` receives from me, me-1, me-2, ... in that order.
+__global__ void block_need_kernel(const int* __restrict__ tab, int n, int el, int me,
+                                  int nblocks, int cg, uint32_t* __restrict__ need,
+                                  int* __restrict__ order) {
+  const int* kept = tab;
+  const int* off_pad = tab + 2 * n * el;
+  const int* real = off_pad + el + 1;
+  __shared__ int cnt[33];
+  __shared__ int base_s[33];
+  const int nunits = nblocks / cg;
+  if (threadIdx.x <= 32) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  // pass 1: masks and per-priority unit counts
+  for (int u = threadIdx.x; u < nunits; u += blockDim.x) {
+    int pri = 0;
+    for (int b = u * cg; b < (u + 1) * cg; ++b) {
+      const int r0 = b * 128, r1 = r0 + 128;
+      uint32_t m = 0;
+      for (int e = 0; e < el; ++e) {
+        const int lo = off_pad[e], hi = off_pad[e] + real[e];
+        if (hi <= r0 || lo >= r1) continue;
+        int acc = lo;
+        for (int s = 0; s < n; ++s) {
+          const int k = kept[s * el + e];
+          if (k > 0 && acc < r1 && acc + k > r0) {
+            m |= 1u << s;
+            const int pr = (me - s + n) % n;
+            pri = pr > pri ? pr : pri;
+          }
+          acc += k;
+        }
+      }
+      need[b] = m;
+    }
+    atomicAdd(&cnt[pri], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int a = 0;
+    for (int i = 0; i < n; ++i) {
+      base_s[i] = a;
+      a += cnt[i];
+    }
+  }
+  __syncthreads();
+  // pass 2: stable placement by priority (one warp per priority level keeps unit order)
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int pl = w; pl < n; pl += blockDim.x >> 5) {
+    int pos = base_s[pl];
+    for (int u0 = 0; u0 < nunits; u0 += 32) {
+      const int u = u0 + lane;
+      bool hit = false;
+      if (u < nunits) {
+        int pri = 0;
+        for (int b = u * cg; b < (u + 1) * cg; ++b) {
+          const uint32_t m = need[b];
+          for (int s = 0; s < n; ++s)
+            if (m >> s & 1u) {
+              const int pr = (me - s + n) % n;
+              pri = pr > pri ? pr : pri;
+            }
+        }
+        hit = pri == pl;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, hit);
+      if (hit) order[pos + __popc(bal & ((1u << lane) - 1u))] = u;
+      pos += __popc(bal);
+    }
+  }
+}
+
+// Load and configure every kernel the overlapped dispatch launches beside a running GEMM.
+// Must be called before the first overlapped step: with CUDA lazy loading, the first launch
+// of a kernel may wait for the device's running kernels, i.e. for a GEMM that waits for it.
+int moe_ep_prepare() {
+  prefer_max_shared(dispatch_push_kernel<4>);
+  prefer_max_shared(combine_bwd_push_sel_kernel<2>);
+  prefer_max_shared(signal_kernel);
+  cudaFuncAttributes a;
+  MOE_CUDA_CHECK(cudaFuncGetAttributes(&a, dispatch_push_kernel<4>));
+  MOE_CUDA_CHECK(cudaFuncGetAttributes(&a, combine_bwd_push_sel_kernel<2>));
+  MOE_CUDA_CHECK(cudaFuncGetAttributes(&a, signal_kernel));
+  return kOk;
+}
+
+int moe_ep_block_need(const int* table, int n, int el, int me, int nblocks, int cg,
+                      unsigned int* need, int* order, void* stream) {
+  if (n < 1 || n > 32 || el < 1 || (cg != 1 && cg != 2) || nblocks % cg) return kErrInvalidArg;
+  if (nblocks <= 0) return kOk;
+  block_need_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(table, n, el, me, nblocks,
+                                                                      cg, need, order);
   MOE_LAUNCH_CHECK();
   return kOk;
 }
@@ -534,20 +743,29 @@ int moe_ep_combine_pull(const unsigned long long* peers, int T, int K, int h,
   return kOk;
 }
 
-int moe_ep_combine_bwd_push(const void* dy, const void* o_local,
-                            const unsigned long long* d_peers, int T, int K, int h,
-                            const int* topk_idx, const int* inv_c, const int* base, int el,
-                            const float* prob, float* dprob, void* stream) {
+static int combine_bwd_push_impl(const void* dy, const void* o_local,
+                                 const unsigned long long* d_peers, int T, int K, int h,
+                                 const int* topk_idx, const int* inv_c, const int* base, int el,
+                                 const float* prob, float* dprob, int dest, void* stream) {
   if (h % 8 || el < 1 || K > 32) return kErrInvalidArg;
   if (T == 0) return kOk;
   auto st = static_cast<cudaStream_t>(stream);
   const auto* y = static_cast<const int4*>(dy);
   const auto* ol = static_cast<const int4*>(o_local);
   const int hv = h / 8;
+  if (dest >= 0) {
+    // runs concurrently with the persistent GEMM that waits for it (moe_gg_fc2_dgrad_ep)
+    const long long nb = ceil_div_ll(T, 4), cap = (long long)sms() * 16;
+    combine_bwd_push_sel_kernel<2><<<(int)(nb < cap ? nb : cap), 128, 0, st>>>(
+        y, ol, d_peers, T, K, hv, topk_idx, inv_c, base, el, prob, dprob, dest);
+    MOE_LAUNCH_CHECK();
+    return kOk;
+  }
+  const int grid = warp_grid(T), threads = 256;
 #define PUSH(V, KM)                                                                        \
-  combine_bwd_push_kernel<V, KM><<<warp_grid(T), 256, 0, st>>>(y, ol, d_peers, T, K, hv,     \
-                                                              topk_idx, inv_c, base, el, prob, \
-                                                              dprob)
+  combine_bwd_push_kernel<V, KM><<<grid, threads, 0, st>>>(y, ol, d_peers, T, K, hv,         \
+                                                          topk_idx, inv_c, base, el, prob,     \
+                                                          dprob, dest)
   if (K <= 2)
     PUSH(4, 2);
   else if (K <= 4)
@@ -561,6 +779,25 @@ int moe_ep_combine_bwd_push(const void* dy, const void* o_local,
 #undef PUSH
   MOE_LAUNCH_CHECK();
   return kOk;
+}
+
+int moe_ep_combine_bwd_push(const void* dy, const void* o_local,
+                            const unsigned long long* d_peers, int T, int K, int h,
+                            const int* topk_idx, const int* inv_c, const int* base, int el,
+                            const float* prob, float* dprob, void* stream) {
+  return combine_bwd_push_impl(dy, o_local, d_peers, T, K, h, topk_idx, inv_c, base, el, prob,
+                               dprob, -1, stream);
+}
+
+// Combine backward restricted to the selections whose expert lives on rank `dest`; dprob is
+// written for those selections only.
+int moe_ep_combine_bwd_push_dest(const void* dy, const void* o_local,
+                                 const unsigned long long* d_peers, int T, int K, int h,
+                                 const int* topk_idx, const int* inv_c, const int* base, int el,
+                                 const float* prob, float* dprob, int dest, void* stream) {
+  if (dest < 0) return kErrInvalidArg;
+  return combine_bwd_push_impl(dy, o_local, d_peers, T, K, h, topk_idx, inv_c, base, el, prob,
+                               dprob, dest, stream);
 }
 
 int moe_ep_token_ranks(const int* topk_idx, const int* inv_c, int T, int K, int el,

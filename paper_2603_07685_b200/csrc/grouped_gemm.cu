@@ -55,6 +55,16 @@ struct Cfg {
   static constexpr int STAGES = CG == 1 ? 4 : 6;
   static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
 };
+// Row-scatter epilogue (EPI_BF16, grouped-M, row_dst set): each epilogue warp stages its 32
+// rows x 128 columns (half a tile row) in shared memory and writes every row with one
+// 256-byte TMA bulk store to its destination (often a peer GPU over NVLink) instead of 16-B
+// per-thread stores, which NVLink serves poorly.
+constexpr int SCATTER_COLS = 128;
+constexpr int SCATTER_STAGE = 32 * SCATTER_COLS * 2;  // per epilogue warp
+template <int EPI, bool GROUPED_K, int CG>
+constexpr int smem_bytes() {
+  return Cfg<CG>::SMEM + ((EPI == 0 && !GROUPED_K) ? EPI_WARPS * SCATTER_STAGE : 0);
+}
 
 enum Epi : int { EPI_BF16 = 0, EPI_SWIGLU = 1, EPI_DSWIGLU = 2, EPI_F32 = 3 };
 
@@ -84,7 +94,44 @@ struct Params {
   // the row). Rows may live in peer GPUs' memory (NVLink): the EP combine / dX exchange is
   // fused into the producing GEMM's epilogue.
   const unsigned long long* row_dst;
+  // EP dispatch overlap (grouped-M): source rank s's rows of the A operand are pushed over
+  // NVLink while this GEMM runs; s then stores `epoch` into src_flag[s]. A tile's A rows are
+  // loaded only once every source in block_need[128-row block] has signalled; units run in
+  // unit_order (rows of early-arriving sources first). wait_status <- 1 on a 10 s timeout.
+  const uint32_t* src_flag;
+  uint32_t epoch;
+  const uint32_t* block_need;
+  const int* unit_order;
+  int* wait_status;
 };
+
+// Spin (bounded) until every source rank in `need` has published this epoch's rows. On a
+// timeout (2 s) the kernel records [1, block, missing sources, epoch, flags[0..3]] in
+// wait_status[0..7] and stops waiting (later waits of any CTA fail fast).
+__device__ __forceinline__ void wait_sources(const Params& p, uint32_t need, int blk) {
+  if (!need) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (need) {
+    const int s = __ffs(need) - 1;
+    if (static_cast<int>(ld_acquire_sys_u32(p.src_flag + s) - p.epoch) >= 0) {
+      need &= need - 1;
+      continue;
+    }
+    if (p.wait_status && *reinterpret_cast<volatile int*>(p.wait_status)) break;
+    if (globaltimer_ns() - t0 > 2000000000ull) {
+      if (p.wait_status && atomicCAS(p.wait_status, 0, 1) == 0) {
+        p.wait_status[1] = blk;
+        p.wait_status[2] = static_cast<int>(need);
+        p.wait_status[3] = static_cast<int>(p.epoch);
+        for (int i = 0; i < 4; ++i)
+          p.wait_status[4 + i] = static_cast<int>(ld_acquire_sys_u32(p.src_flag + i));
+      }
+      break;
+    }
+    __nanosleep(128);
+  }
+  fence_proxy_async_global();
+}
 
 struct Tile {
   int expert, m0, n0, k_begin, num_kb;
@@ -101,7 +148,8 @@ __device__ __forceinline__ void decode_tile(const Params& p, int t, int num_unit
     const int u0 = band * BAND_M;
     const int rows = min(BAND_M, num_units - u0);
     const int nb = rem / rows;
-    const int u = u0 + (rem - nb * rows);
+    int u = u0 + (rem - nb * rows);
+    if (p.unit_order) u = __ldg(p.unit_order + u);
     tl.expert = __ldg(p.block_expert + u * CG);
     tl.m0 = u * (BM * CG) + rank * BM;
     tl.n0 = nb * BN;
@@ -245,6 +293,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int t = first; t < num_tiles; t += stride) {
         Tile tl;
         decode_tile<GROUPED_K, CG>(p, t, num_units, rank, tl);
+        if constexpr (!GROUPED_K) {
+          if (p.src_flag) wait_sources(p, __ldg(p.block_need + tl.m0 / BM), tl.m0 / BM);
+        }
         for (int kb = 0; kb < tl.num_kb; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
           if (leader) mbar_arrive_expect_tx(&full_bar[s], C::STAGE * CG);
@@ -335,6 +386,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ===================== epilogue (warps 2..9: lane quarter x column half) ===========
     const int q = warp & 3;
     const int half = (warp - 2) / 4;
+    uint8_t* stage = smem + C::STAGES * C::STAGE + 256 + (warp - 2) * SCATTER_STAGE;
     const int cb = half * EPI_COLS;  // this warp's first tile column
     const int row_local = q * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
@@ -387,14 +439,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tmem_ld_32x32b_x32(t_base + col, r);
           tmem_ld_wait();
           if constexpr (EPI == EPI_BF16) {
-            __nv_bfloat16* o;
             if (!GROUPED_K && p.row_dst) {
-              const unsigned long long dst = __ldg(p.row_dst + row);
-              if (dst == 0ull) continue;
-              o = reinterpret_cast<__nv_bfloat16*>(dst) + tl.n0 + col;
-            } else {
-              o = reinterpret_cast<__nv_bfloat16*>(p.out) + ebase + row * p.ldo + tl.n0 + col;
+              // stage this lane's row chunk; one bulk store per (row, 128 columns)
+              const int hc = col % SCATTER_COLS;
+              uint8_t* srow = stage + lane * (SCATTER_COLS * 2);
+              if (hc == 0) bulk_wait_read_all();  // slot free again (previous half read)
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                int4 w;
+                w.x = pack_bf16x2(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1]));
+                w.y = pack_bf16x2(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3]));
+                w.z = pack_bf16x2(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5]));
+                w.w = pack_bf16x2(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
+                reinterpret_cast<int4*>(srow + hc * 2)[v] = w;
+              }
+              if (hc + 32 == SCATTER_COLS) {
+                const unsigned long long dst = __ldg(p.row_dst + row);
+                fence_async_shared();
+                if (dst) {
+                  bulk_store_s2g(reinterpret_cast<__nv_bfloat16*>(dst) + tl.n0 + col + 32 -
+                                     SCATTER_COLS,
+                                 srow, SCATTER_COLS * 2);
+                  bulk_commit();
+                }
+              }
+              continue;
             }
+            __nv_bfloat16* o =
+                reinterpret_cast<__nv_bfloat16*>(p.out) + ebase + row * p.ldo + tl.n0 + col;
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
               int4 w;
@@ -520,9 +592,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
 
-  // scattered rows may be in peer memory: make them visible system-wide before the
-  // stream-ordered collective that publishes them
-  if (EPI == EPI_BF16 && !GROUPED_K && p.row_dst && warp >= 2) __threadfence_system();
+  // scattered rows may be in peer memory: complete the bulk stores and make them visible
+  // system-wide before the stream-ordered collective that publishes them
+  if (EPI == EPI_BF16 && !GROUPED_K && p.row_dst && warp >= 2) {
+    bulk_wait_all();
+    __threadfence_system();
+  }
   tc_fence_before();
   if constexpr (CG == 2) {
     cluster_sync_all();
@@ -591,7 +666,7 @@ static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params&
   static bool attr_set = false;
   if (!attr_set) {
     MOE_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        Cfg<CG>::SMEM));
+                                        smem_bytes<EPI, GROUPED_K, CG>()));
     attr_set = true;
   }
   if (max_tiles <= 0) return kOk;
@@ -600,7 +675,7 @@ static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params&
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(NUM_THREADS);
-  cfg.dynamicSmemBytes = Cfg<CG>::SMEM;
+  cfg.dynamicSmemBytes = smem_bytes<EPI, GROUPED_K, CG>();
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -645,13 +720,31 @@ extern "C" {
 // act[rows, m] = silu(gate) * up (* row_prob[row] when row_prob != NULL).
 // a_rows: physical rows of xp (TMA bound; rows beyond read as zero), max_rows: rows of the
 // output buffers (multiple of 128; of 256 with the pair flag).
-int moe_gg_fc1_fwd(const void* xp, const void* w1, int a_rows, int max_rows, int h, int m,
-                   int num_experts, const int* block_expert, const int* num_m_blocks,
-                   const float* row_prob, void* preact, void* act, int flags, void* stream) {
+struct SourceWait {
+  const uint32_t* src_flag;
+  uint32_t epoch;
+  const uint32_t* block_need;
+  const int* unit_order;
+  int* status;
+};
+static void set_wait(Params& p, const SourceWait* w) {
+  if (!w) return;
+  p.src_flag = w->src_flag;
+  p.epoch = w->epoch;
+  p.block_need = w->block_need;
+  p.unit_order = w->unit_order;
+  p.wait_status = w->status;
+}
+
+static int fc1_fwd_impl(const void* xp, const void* w1, int a_rows, int max_rows, int h, int m,
+                        int num_experts, const int* block_expert, const int* num_m_blocks,
+                        const float* row_prob, void* preact, void* act, int flags,
+                        const SourceWait* w, void* stream) {
   const int pair = flags & kFlagPair;
   if (h % BK || (2 * m) % BN || max_rows % (BM * (pair ? 2 : 1)) || a_rows > max_rows)
     return kErrInvalidArg;
   Params p{};
+  set_wait(p, w);
   p.num_m_blocks = num_m_blocks;
   p.block_expert = block_expert;
   p.max_m_blocks = max_rows / BM;
@@ -666,6 +759,28 @@ int moe_gg_fc1_fwd(const void* xp, const void* w1, int a_rows, int max_rows, int
   return run<false, false, false, EPI_SWIGLU>(xp, h, a_rows, w1, h, (uint64_t)num_experts * 2 * m,
                                               p, p.max_m_blocks, pair,
                                               static_cast<cudaStream_t>(stream));
+}
+
+int moe_gg_fc1_fwd(const void* xp, const void* w1, int a_rows, int max_rows, int h, int m,
+                   int num_experts, const int* block_expert, const int* num_m_blocks,
+                   const float* row_prob, void* preact, void* act, int flags, void* stream) {
+  return fc1_fwd_impl(xp, w1, a_rows, max_rows, h, m, num_experts, block_expert, num_m_blocks,
+                      row_prob, preact, act, flags, nullptr, stream);
+}
+
+// fc1 forward overlapped with the EP dispatch: tiles wait for their rows' source ranks
+// (src_flag[s] >= epoch, written by moe_ep_signal after each source's push) and run in
+// unit_order. block_need[128-row block] = bitmask of source ranks.
+int moe_gg_fc1_fwd_ep(const void* xp, const void* w1, int a_rows, int max_rows, int h, int m,
+                      int num_experts, const int* block_expert, const int* num_m_blocks,
+                      const float* row_prob, void* preact, void* act, int flags,
+                      const unsigned int* src_flag, unsigned int epoch,
+                      const unsigned int* block_need, const int* unit_order, int* status,
+                      void* stream) {
+  if (!src_flag || !block_need) return kErrInvalidArg;
+  const SourceWait w{src_flag, epoch, block_need, unit_order, status};
+  return fc1_fwd_impl(xp, w1, a_rows, max_rows, h, m, num_experts, block_expert, num_m_blocks,
+                      row_prob, preact, act, flags, &w, stream);
 }
 
 static int fc2_fwd_impl(const void* act, const void* w2, int a_rows, int max_rows, int m,
@@ -714,14 +829,16 @@ int moe_gg_fc2_fwd_scatter(const void* act, const void* w2, int a_rows, int max_
 //   G[rows, m] = dout[rows, h] * w2_e  (w2[E, h, m] read MN-major)
 //   da = G * row_prob (mem-efficient) or G (standard); dprob_partial[row, m/256] = <G, act>
 //   d_preact (interleaved like preact) = [da * u * s(g)(1+g(1-s(g))), da * silu(g)]
-int moe_gg_fc2_dgrad(const void* dout, const void* w2, const void* preact, int a_rows,
-                     int max_rows, int h, int m, int num_experts, const int* block_expert,
-                     const int* num_m_blocks, const float* row_prob, void* d_preact,
-                     float* dprob_partial, int flags, void* stream) {
+static int fc2_dgrad_impl(const void* dout, const void* w2, const void* preact, int a_rows,
+                          int max_rows, int h, int m, int num_experts, const int* block_expert,
+                          const int* num_m_blocks, const float* row_prob, void* d_preact,
+                          float* dprob_partial, int flags, const SourceWait* w,
+                          void* stream) {
   const int pair = flags & kFlagPair;
   if (h % BK || m % BN || max_rows % (BM * (pair ? 2 : 1)) || a_rows > max_rows)
     return kErrInvalidArg;
   Params p{};
+  set_wait(p, w);
   p.num_m_blocks = num_m_blocks;
   p.block_expert = block_expert;
   p.max_m_blocks = max_rows / BM;
@@ -738,6 +855,27 @@ int moe_gg_fc2_dgrad(const void* dout, const void* w2, const void* preact, int a
   return run<false, true, false, EPI_DSWIGLU>(dout, h, a_rows, w2, m, (uint64_t)num_experts * h,
                                               p, p.max_m_blocks, pair,
                                               static_cast<cudaStream_t>(stream));
+}
+
+int moe_gg_fc2_dgrad(const void* dout, const void* w2, const void* preact, int a_rows,
+                     int max_rows, int h, int m, int num_experts, const int* block_expert,
+                     const int* num_m_blocks, const float* row_prob, void* d_preact,
+                     float* dprob_partial, int flags, void* stream) {
+  return fc2_dgrad_impl(dout, w2, preact, a_rows, max_rows, h, m, num_experts, block_expert,
+                        num_m_blocks, row_prob, d_preact, dprob_partial, flags, nullptr, stream);
+}
+
+// fc2 data-gradient overlapped with the EP dO dispatch (see moe_gg_fc1_fwd_ep).
+int moe_gg_fc2_dgrad_ep(const void* dout, const void* w2, const void* preact, int a_rows,
+                        int max_rows, int h, int m, int num_experts, const int* block_expert,
+                        const int* num_m_blocks, const float* row_prob, void* d_preact,
+                        float* dprob_partial, int flags, const unsigned int* src_flag,
+                        unsigned int epoch, const unsigned int* block_need,
+                        const int* unit_order, int* status, void* stream) {
+  if (!src_flag || !block_need) return kErrInvalidArg;
+  const SourceWait w{src_flag, epoch, block_need, unit_order, status};
+  return fc2_dgrad_impl(dout, w2, preact, a_rows, max_rows, h, m, num_experts, block_expert,
+                        num_m_blocks, row_prob, d_preact, dprob_partial, flags, &w, stream);
 }
 
 static int fc1_dgrad_impl(const void* d_preact, const void* w1, int a_rows, int max_rows,

@@ -302,6 +302,16 @@ class SymmPool:
         self.dev = dev
         self.bufs = {}
         self.bar = torch.zeros((1,), dtype=torch.float32, device=dev)
+        # dispatch/GEMM overlap: per-dispatch epoch (same sequence on every rank), the side
+        # stream the pushes run on, and the GEMMs' wait-timeout flag
+        self.epoch = 0
+        self.comm = torch.cuda.Stream(device=dev)
+        _lib.call("moe_ep_prepare")  # load the side-stream kernels now (lazy loading)
+        self.status = torch.zeros((8,), dtype=torch.int32, device=dev)
+
+    def next_epoch(self) -> int:
+        self.epoch += 1
+        return self.epoch
 
     def get(self, name: str, numel: int, dtype):
         cur = self.bufs.get(name)
@@ -354,6 +364,36 @@ def _record_exchange(hp: EPHostPlan, h: int, width: int = 2):
                          bytes_sent_remote=int(sent_remote) * h * width,
                          bytes_recv_remote=int(recv_remote) * h * width,
                          local_experts=el)
+
+
+def check_ep_status():
+    """Raise if an overlapped EP GEMM timed out waiting for a source rank (synchronises)."""
+    for key, pool in _POOLS.items():
+        st = pool.status.tolist()
+        if st[0]:
+            raise _lib.MoEKernelError(
+                f"EP dispatch wait timed out (pool {key}): block {st[1]}, missing sources "
+                f"mask {st[2]:#x}, epoch {st[3]}, flags[0:4] {st[4:]}")
+
+
+def _overlapped_push(pool, ep, push_one, stream_main):
+    """Run push_one(dest, stream) for dest = me, me+1, ... on the pool's side stream, each
+    followed by a release-store of this dispatch's epoch into dest's flag slot `me`; the
+    consumer GEMM on the main stream waits per block on those flags."""
+    n, me = ep.n, ep.rank
+    epoch = pool.next_epoch()
+    flags, flag_peers = pool.get("flags", 32, torch.int32)
+    ev = torch.cuda.Event()
+    ev.record(stream_main)
+    comm = pool.comm
+    comm.wait_event(ev)
+    cs = comm.cuda_stream
+    with torch.cuda.stream(comm):  # (also where _lib's optional timing events go)
+        for i in range(n):
+            d = (me + i) % n
+            push_one(d, cs)
+            _lib.call("moe_ep_signal", flag_peers.data_ptr(), d, me, epoch, cs)
+    return flags, epoch
 
 
 def _pool(ep: EPGroup, dev, tag: str = "") -> SymmPool:
@@ -462,7 +502,8 @@ def _echo_reduce(pool, ep, dw_ext, layout, el, name):
 class _MoEEPP2PFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w_r, w1, w2, sel_bias, w1s, w2s, cfg: MoEConfig, ep: EPGroup,
-                echo_slots: int = 0, scatter: bool = True, tag: str = ""):
+                echo_slots: int = 0, scatter: bool = True, tag: str = "",
+                overlap: bool = True):
         t, h = x.shape
         E, K = cfg.num_experts, cfg.top_k
         n = ep.n
@@ -530,12 +571,35 @@ class _MoEEPP2PFunction(torch.autograd.Function):
                   stream)
         # (row_prob of padding rows: zero at allocation, else a stale finite prob of a row
         # whose activation is exactly zero; never cleared here, peers may already be pushing)
-        _lib.call("moe_ep_dispatch_push", x.data_ptr(), t, K, h, ctx_topk.data_ptr(),
-                  splan.inv_map.data_ptr(), base_d.data_ptr(), el, xp_peers.data_ptr(),
-                  r.topk_prob.data_ptr() if cfg.mem_efficient else None,
-                  prob_peers.data_ptr() if prob_peers is not None else None, stream)
-        pool.barrier()
-        preact, act = gemm.fc1_fwd(xp, w1, be_d, nmb, row_prob, pair=pair)
+        push_args = (x.data_ptr(), t, K, h, ctx_topk.data_ptr(), splan.inv_map.data_ptr(),
+                     base_d.data_ptr(), el, xp_peers.data_ptr(),
+                     r.topk_prob.data_ptr() if cfg.mem_efficient else None,
+                     prob_peers.data_ptr() if prob_peers is not None else None)
+        overlap = overlap and scatter
+        wait = None
+        if overlap:
+            # pushes run destination by destination on a side stream while fc1 consumes the
+            # rows block by block as their sources signal (no barrier)
+            cg = 2 if pair else 1
+            nblocks = hp.rows_pad // ops.ALIGN
+            need = torch.zeros((max(rows_alloc // ops.ALIGN, 1),), dtype=torch.int32, device=dev)
+            order = torch.empty((max(nblocks // cg, 1),), dtype=torch.int32, device=dev)
+            if nblocks:
+                _lib.call("moe_ep_block_need", table_d.data_ptr(), n, el, ep.rank, nblocks, cg,
+                          need.data_ptr(), order.data_ptr(), stream)
+            main = torch.cuda.current_stream()
+            flags, epoch = _overlapped_push(
+                pool, ep, lambda d, cs: _lib.call("moe_ep_dispatch_push_dest", *push_args, d, cs),
+                main)
+            wait = (flags, epoch, need, order, pool.status)
+            preact, act = gemm.fc1_fwd(xp, w1, be_d, nmb, row_prob, pair=pair, wait=wait)
+            main.wait_stream(pool.comm)
+            ctx.need_order = (need, order)
+        else:
+            _lib.call("moe_ep_dispatch_push", *push_args, stream)
+            pool.barrier()
+            preact, act = gemm.fc1_fwd(xp, w1, be_d, nmb, row_prob, pair=pair)
+        ctx.overlap = overlap
         y = torch.empty_like(x)
         row_dst_dx = None
         if scatter:
@@ -605,22 +669,37 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         d_o = d_o[: rows_alloc * h].view(rows_alloc, h)
         _lib.call("moe_zero_pad_rows", meta_d.data_ptr(), map_pad.data_ptr(), h, d_o.data_ptr(),
                   stream)
-        dprob = torch.empty((t, K), dtype=torch.float32, device=dev)
-        _lib.call("moe_ep_combine_bwd_push", dy.data_ptr(),
-                  None if cfg.mem_efficient else ctx.o_local.data_ptr(), d_peers.data_ptr(), t, K,
-                  h, ctx_topk.data_ptr(), splan.inv_map.data_ptr(), base_d.data_ptr(), el,
-                  None if cfg.mem_efficient else r.topk_prob.data_ptr(),
-                  None if cfg.mem_efficient else dprob.data_ptr(), stream)
-        pool.barrier()
-        part_peers = None
+        push_args = (dy.data_ptr(), None if cfg.mem_efficient else ctx.o_local.data_ptr(),
+                     d_peers.data_ptr(), t, K, h, ctx_topk.data_ptr(), splan.inv_map.data_ptr(),
+                     base_d.data_ptr(), el,
+                     None if cfg.mem_efficient else r.topk_prob.data_ptr())
+        part_peers = part = None
         if cfg.mem_efficient:
             ldp = gemm.dprob_partials(w2.shape[2])
             part, part_peers = pool.get("part", rows_alloc * ldp, torch.float32)
             part = part[: rows_alloc * ldp].view(rows_alloc, ldp)
-            d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, be_d, nmb, row_prob=ctx.row_prob,
-                                      pair=ctx.pair, part=part)
+        wait = None
+        main = torch.cuda.current_stream()
+        if ctx.overlap:
+            # per-destination passes write dprob only for their own selections
+            dprob = torch.zeros((t, K), dtype=torch.float32, device=dev)
+            dp_ptr = None if cfg.mem_efficient else dprob.data_ptr()
+            flags, epoch = _overlapped_push(
+                pool, ep, lambda d, cs: _lib.call("moe_ep_combine_bwd_push_dest", *push_args,
+                                                  dp_ptr, d, cs), main)
+            wait = (flags, epoch, *ctx.need_order, pool.status)
         else:
-            d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, be_d, nmb, pair=ctx.pair)
+            dprob = torch.empty((t, K), dtype=torch.float32, device=dev)
+            _lib.call("moe_ep_combine_bwd_push", *push_args,
+                      None if cfg.mem_efficient else dprob.data_ptr(), stream)
+            pool.barrier()
+        if cfg.mem_efficient:
+            d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, be_d, nmb, row_prob=ctx.row_prob,
+                                      pair=ctx.pair, part=part, wait=wait)
+        else:
+            d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, be_d, nmb, pair=ctx.pair, wait=wait)
+        if ctx.overlap:
+            main.wait_stream(pool.comm)
         dw2 = gemm.wgrad(d_o, act, off_pad_d, el)
         if ctx.scatter:  # dX rows return from fc1_dgrad's epilogue into the source ranks
             gemm.fc1_dgrad_scatter(d_pre, w1, be_d, nmb, ctx.row_dst_dx, pair=ctx.pair)
@@ -663,7 +742,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
             dw1 = _echo_reduce(pool, ep, dw1, ctx.layout, ctx.el_own, "echo_dw1")
             dw2 = _echo_reduce(pool, ep, dw2, ctx.layout, ctx.el_own, "echo_dw2")
         return (dx, dw_r.to(torch.bfloat16), dw1, dw2, None, dw1s, dw2s, None, None, None, None,
-                None)
+                None, None)
 
 
 def _excl(a):
@@ -878,6 +957,10 @@ def moe_forward_ep(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
         padded plan (csrc/ep.cu); expert outputs and dX rows return from the fc2 / fc1-dgrad
         GEMM epilogues, which store each row into its source rank's buffer over NVLink, so
         both combines are local.
+        The pushes run destination by destination on a side stream and the consuming
+        GEMMs (fc1 fwd, fc2 dgrad) start as soon as each 128-row block's source ranks have
+        signalled (per-block flags, no barrier), so both dispatches overlap the GEMMs.
+      "p2p_sync": "p2p" without the dispatch overlap (push, barrier, GEMM).
       "p2p_pull": the previous p2p variant, where the combines pull the rows back over
         NVLink (kept for A/B measurement).
       "p2p_dedup": token de-duplication (one row per (token, destination rank) each way;
@@ -895,9 +978,10 @@ def moe_forward_ep(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
         # top-2 most tokens already hit distinct ranks and the local expand costs more
         transport = "p2p_dedup" if cfg.top_k >= 4 else "p2p"
     args = (x, w_r, w1_local, w2_local, selection_bias, w1_shared, w2_shared, cfg, ep)
-    if echo_slots or transport in ("p2p", "p2p_pull"):
+    if echo_slots or transport in ("p2p", "p2p_sync", "p2p_pull"):
         # ECHO hot-expert cloning runs on the p2p transport (virtual experts)
-        return _MoEEPP2PFunction.apply(*args, int(echo_slots), transport != "p2p_pull", tag)
+        return _MoEEPP2PFunction.apply(*args, int(echo_slots), transport != "p2p_pull", tag,
+                                       transport == "p2p" or bool(echo_slots))
     if transport == "p2p_dedup":
         return _MoEEPDedupFunction.apply(*args, tag)
     if transport == "nccl":

@@ -60,8 +60,16 @@ def deinterleave_cols(preact: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]
     return v[:, :, 0].reshape(r, m), v[:, :, 1].reshape(r, m)
 
 
+def _wait_args(wait):
+    """wait = (src_flag [n] int32, epoch, block_need [blocks] int32, unit_order [units] int32,
+    status [1] int32): the EP dispatch-overlap arguments of the *_ep GEMMs."""
+    flag, epoch, need, order, status = wait
+    return (flag.data_ptr(), int(epoch) & 0xFFFFFFFF, need.data_ptr(), _ptr(order),
+            _ptr(status))
+
+
 def fc1_fwd(xp, w1, block_expert, num_m_blocks, row_prob=None, preact=None, act=None,
-            max_rows=None, pair=False):
+            max_rows=None, pair=False, wait=None):
     a_rows, h = xp.shape
     rows = a_rows if max_rows is None else max_rows
     e, m2, _ = w1.shape
@@ -70,9 +78,13 @@ def fc1_fwd(xp, w1, block_expert, num_m_blocks, row_prob=None, preact=None, act=
         preact = torch.empty((rows, m2), dtype=torch.bfloat16, device=xp.device)
     if act is None:
         act = torch.empty((rows, m), dtype=torch.bfloat16, device=xp.device)
-    _lib.call("moe_gg_fc1_fwd", xp.data_ptr(), w1.data_ptr(), a_rows, rows, h, m, e,
-              block_expert.data_ptr(), num_m_blocks.data_ptr(), _ptr(row_prob),
-              preact.data_ptr(), act.data_ptr(), int(pair), _stream())
+    args = (xp.data_ptr(), w1.data_ptr(), a_rows, rows, h, m, e, block_expert.data_ptr(),
+            num_m_blocks.data_ptr(), _ptr(row_prob), preact.data_ptr(), act.data_ptr(),
+            int(pair))
+    if wait is None:
+        _lib.call("moe_gg_fc1_fwd", *args, _stream())
+    else:
+        _lib.call("moe_gg_fc1_fwd_ep", *args, *_wait_args(wait), _stream())
     return preact, act
 
 
@@ -109,7 +121,7 @@ def fc1_dgrad_scatter(d_preact, w1, block_expert, num_m_blocks, row_dst, max_row
 
 
 def fc2_dgrad(dout, w2, preact, block_expert, num_m_blocks, row_prob=None, want_dprob=False,
-              d_preact=None, max_rows=None, pair=False, part=None):
+              d_preact=None, max_rows=None, pair=False, part=None, wait=None):
     """part: optional preallocated [rows, m/256] fp32 dprob partials (implies want_dprob)."""
     a_rows, h = dout.shape
     rows = a_rows if max_rows is None else max_rows
@@ -118,9 +130,13 @@ def fc2_dgrad(dout, w2, preact, block_expert, num_m_blocks, row_prob=None, want_
         d_preact = torch.empty((rows, 2 * m), dtype=torch.bfloat16, device=dout.device)
     if want_dprob and part is None:
         part = torch.empty((rows, dprob_partials(m)), dtype=torch.float32, device=dout.device)
-    _lib.call("moe_gg_fc2_dgrad", dout.data_ptr(), w2.data_ptr(), preact.data_ptr(), a_rows, rows,
-              h, m, e, block_expert.data_ptr(), num_m_blocks.data_ptr(), _ptr(row_prob),
-              d_preact.data_ptr(), _ptr(part), int(pair), _stream())
+    args = (dout.data_ptr(), w2.data_ptr(), preact.data_ptr(), a_rows, rows, h, m, e,
+            block_expert.data_ptr(), num_m_blocks.data_ptr(), _ptr(row_prob),
+            d_preact.data_ptr(), _ptr(part), int(pair))
+    if wait is None:
+        _lib.call("moe_gg_fc2_dgrad", *args, _stream())
+    else:
+        _lib.call("moe_gg_fc2_dgrad_ep", *args, *_wait_args(wait), _stream())
     return d_preact, part
 
 

@@ -97,6 +97,8 @@ def _worker(rank, world, port, case, q, transport):
             if not last_echo.get("clones"):
                 raise AssertionError(f"ECHO made no clones: {last_echo}")
         torch.autograd.backward([y, aux], [dy_g[sl].to(dev), torch.ones_like(aux)])
+        from paper_2603_07685_b200.dispatcher import check_ep_status
+        check_ep_status()  # no overlapped GEMM timed out waiting for a source rank
         dwr = w_rd.grad.float().clone()
         dist.all_reduce(dwr)
         # global decision from the GPUs' own logits
@@ -143,7 +145,7 @@ def _worker(rank, world, port, case, q, transport):
         q.put((rank, traceback.format_exc() + repr(exc)))
 
 
-@pytest.mark.parametrize("transport", ["p2p", "p2p_pull", "p2p_dedup", "nccl"])
+@pytest.mark.parametrize("transport", ["p2p", "p2p_sync", "p2p_pull", "p2p_dedup", "nccl"])
 @pytest.mark.parametrize("name", list(CASES))
 def test_ep_layer_matches_global_oracle(name, transport):
     _run(CASES[name], transport)
