@@ -244,7 +244,8 @@ def run_gpu(args, c) -> None:
 
         def layer(xx):
             return moe_forward_ep(xx, w_r, w1, w2, cfg, ep, None, w1s, w2s,
-                                  transport=args.ep_transport, echo_slots=args.echo_slots)
+                                  transport=args.ep_transport, echo_slots=args.echo_slots,
+                                  sync_free=args.sync_free or args.graph)
     else:
         def layer(xx):
             return moe_forward(xx, w_r, w1, w2, cfg, None, w1s, w2s)
@@ -274,11 +275,43 @@ def run_gpu(args, c) -> None:
         step(x, dy)
     barrier()
 
+    run = step
+    graph_launches = None
+    if args.graph:
+        # whole fwd+bwd step (router, EP planning on the device, exchanges, GEMMs, NCCL
+        # all-gather / barriers) captured once and replayed: no host work per step
+        sx, sdy = x.clone(), dy.clone()
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                step(sx, sdy)
+        torch.cuda.current_stream().wait_stream(side)
+        barrier()
+        graph = torch.cuda.CUDAGraph()
+        l0 = _lib.stats.launches
+        with torch.cuda.graph(graph):
+            g_out = step(sx, sdy)
+        graph_launches = _lib.stats.launches - l0
+        barrier()
+
+        def run(xx, dyy):
+            if xx is not sx:
+                sx.copy_(xx, non_blocking=True)
+                sdy.copy_(dyy, non_blocking=True)
+            graph.replay()
+            return g_out
+
+        x, dy = sx, sdy
+        for _ in range(2):
+            run(x, dy)
+        barrier()
+
     # ---- timed region: device-resident inputs ------------------------------------
     if rank == 0:
         clocks.lines.clear()
     _lib.stats.launches = 0
-    _lib.stats.timing = True
+    _lib.stats.timing = not args.graph
     _lib.stats.events = []
     barrier()
     t_start = torch.cuda.Event(enable_timing=True)
@@ -286,13 +319,19 @@ def run_gpu(args, c) -> None:
     clocks.window(True)
     t_start.record()
     for _ in range(args.steps):
-        step(x, dy)
+        run(x, dy)
     t_end.record()
     barrier()
     clocks.window(False)
-    _lib.stats.timing = False
-    launches = _lib.stats.launches
+    launches = _lib.stats.launches if graph_launches is None else graph_launches * args.steps
     ms_total = t_start.elapsed_time(t_end)
+    if args.graph:
+        # per-kernel timings (roofline) from eager instrumented steps outside the timed region
+        _lib.stats.timing = True
+        for _ in range(args.steps):
+            step(x, dy)
+        barrier()
+    _lib.stats.timing = False
     ev = _lib.stats.events
     gemm_ms = sum(s.elapsed_time(e) for nm, s, e in ev if nm.startswith("moe_gg_"))
     per_kernel: dict[str, list] = {}
@@ -337,7 +376,7 @@ def run_gpu(args, c) -> None:
             if i + 1 < steps:
                 h2d(1 - slot)
             main.wait_event(landed[slot])
-            _, aux = step(*bufs[slot])
+            _, aux = run(*bufs[slot])
             released[slot].record(main)
             loss_host[i].copy_(aux.detach(), non_blocking=True)
 
@@ -371,7 +410,10 @@ def run_gpu(args, c) -> None:
     if n > 1:
         from oracle.routing_ref import a2a_send_volume  # the reference byte model (perf.py:62)
 
-        from paper_2603_07685_b200.dispatcher import last_exchange
+        from paper_2603_07685_b200.dispatcher import exchange_stats_from_device, last_exchange
+
+        if args.sync_free or args.graph:
+            exchange_stats_from_device()  # the sync-free forward never read the counts
 
         ex_names = ("moe_ep_dispatch_push", "moe_ep_combine_pull", "moe_ep_combine_bwd_push",
                     "moe_gather_rows", "moe_ep_dispatch_dedup", "moe_ep_expand_grad",
@@ -382,20 +424,20 @@ def run_gpu(args, c) -> None:
         out_bytes = 2 * last_exchange["bytes_sent_remote"] + 2 * last_exchange["bytes_recv_remote"]
         tr = args.ep_transport
         if tr == "auto":
-            tr = "p2p_dedup" if K >= 4 else "p2p"
+            tr = "p2p"
         # p2p: the two return transfers (O, dX) run inside the fc2 / fc1-dgrad epilogues,
         # so only the two pushes (x, dO) are standalone exchange kernels
-        standalone_bytes = (2 * last_exchange["bytes_sent_remote"] if tr in ("p2p", "p2p_sync")
+        standalone_bytes = (2 * last_exchange["bytes_sent_remote"] if tr in ("p2p", "p2p_overlap")
                             else out_bytes)
         nvlink_stats = {
             "transport": tr,
             "bytes_out_per_step_per_gpu": out_bytes,
             "model_bytes_per_step_per_gpu": 4 * a2a_send_volume(T, K, h, n, 2),
             "exchange_kernel_ms_per_step": round(ex_ms, 4),
-            "returns_fused_in_gemm_epilogue": tr in ("p2p", "p2p_sync"),
-            "dispatch_overlapped_with_gemm": tr == "p2p",
+            "returns_fused_in_gemm_epilogue": tr in ("p2p", "p2p_overlap"),
+            "dispatch_overlapped_with_gemm": tr == "p2p_overlap",
             "achieved_GBps_per_direction": (round(standalone_bytes / (ex_ms / 1e3) / 1e9, 1)
-                                            if ex_ms and tr in ("p2p", "p2p_sync", "p2p_pull")
+                                            if ex_ms and tr in ("p2p", "p2p_overlap", "p2p_pull")
                                             else None),
             "note": ("p2p_dedup sends one row per (token, rank): fewer bytes than counted here"
                      if tr == "p2p_dedup" else None),
@@ -445,6 +487,8 @@ def run_gpu(args, c) -> None:
                 "tokens_per_gpu": T,
                 "parallelism": f"ep{n}",
                 "ep_transport": args.ep_transport if n > 1 else None,
+                "cuda_graph": bool(args.graph),
+                "sync_free": bool(args.sync_free or args.graph) if n > 1 else None,
                 "l2": "inputs larger than L2 (x alone is "
                       f"{T * h * 2 / 1e6:.0f} MB; expert weights {E * 3 * h * m * 2 / 1e9:.2f} GB)",
             },
@@ -542,8 +586,13 @@ def main():
     ap.add_argument("--cpu-sample-tokens", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ep-transport", default="auto",
-                    choices=["auto", "p2p", "p2p_sync", "p2p_pull", "p2p_dedup", "nccl"],
+                    choices=["auto", "p2p", "p2p_overlap", "p2p_pull", "p2p_dedup", "nccl"],
                     help="EP exchange: fused NVLink peer-memory kernels (p2p) or NCCL a2a")
+    ap.add_argument("--sync-free", action="store_true",
+                    help="EP: plan the exchange on the device (no host read of the counts)")
+    ap.add_argument("--graph", action="store_true",
+                    help="capture the whole fwd+bwd step in a CUDA graph (EP: implies "
+                         "--sync-free)")
     ap.add_argument("--echo-slots", type=int, default=0,
                     help="ECHO hot-expert clone slots per rank (EP, dropless)")
     ap.add_argument("--skew", type=float, default=None,

@@ -68,6 +68,17 @@ int moe_permute_plan(const int* topk_idx, const float* topk_prob, int T, int K, 
  * the global batch) via the per-expert cap_e of moe_permute_plan. */
 int moe_ep_regroup_map(const int* table, int n, int el, int rows_pad, int* map_pad,
                        int* map_recv, void* stream);
+/* Sync-free planning: every table above (and the p2p transport's base[] / dst_off[], the
+ * global-position capacity cap_local[], and the global aux loss + its score gradient) from
+ * the all-gathered [n, ldg] rows of [counts(E) | mean scores(E) | ...], on the device, so the
+ * EP step needs no host read and can be captured in a CUDA graph. rows_cap: rows of the
+ * static plan buffers; a plan that would exceed it runs no GEMM blocks and sets *status.
+ * Kernels taking `rows_pad` accept this static bound: rows past the table's off_pad[el]
+ * are treated as outside the plan. */
+int moe_ep_plan_device(const float* gathered, int ldg, int n, int E, int me, int T, int K,
+                       int capacity, int pad, int align, float coeff, int rows_cap, int* base,
+                       int* cap_local, int* table, int* block_expert, int max_blocks, int* meta,
+                       int* dst_off, float* aux, float* aux_grad, int* status, void* stream);
 /* Per padded row of the expert rank's plan: the address of that row in its source rank's
  * compact buffer (peers[s] + (dst_off[s*el+e] + q) * row_bytes; 0 for padding / phantom
  * rows). Feeds the *_scatter GEMMs, which return expert outputs / dX rows over NVLink from
@@ -108,15 +119,18 @@ int moe_ep_dispatch_push(const void* x, int T, int K, int h, const int* topk_idx
                          const unsigned long long* peers, const float* prob,
                          const unsigned long long* prob_peers, void* stream);
 /* Overlapped dispatch: push only the selections whose expert lives on rank `dest`, then
- * moe_ep_signal publishes flag_peers[dest][slot] = epoch (release, system scope). The
+ * moe_ep_signal publishes flag_peers[dest][slot] = *epoch (release, system scope). The
  * consumer GEMM (moe_gg_fc1_fwd_ep / moe_gg_fc2_dgrad_ep) waits per 128-row block for the
  * source ranks moe_ep_block_need lists, so the exchange overlaps the grouped GEMM. */
 int moe_ep_dispatch_push_dest(const void* x, int T, int K, int h, const int* topk_idx,
                               const int* inv_c, const int* base, int el,
                               const unsigned long long* peers, const float* prob,
                               const unsigned long long* prob_peers, int dest, void* stream);
-int moe_ep_signal(const unsigned long long* flag_peers, int dest, int slot, unsigned int epoch,
-                  void* stream);
+int moe_ep_signal(const unsigned long long* flag_peers, int dest, int slot,
+                  const unsigned int* epoch, void* stream);
+/* *epoch += 1 in stream order (the dispatch epoch is a device scalar, so a captured CUDA
+ * graph replays with a fresh epoch) */
+int moe_ep_epoch_bump(unsigned int* epoch, void* stream);
 /* Load / configure the kernels above before the first overlapped step (CUDA lazy loading
  * of a kernel launched beside a GEMM that waits for it would deadlock). */
 int moe_ep_prepare(void);
@@ -162,6 +176,22 @@ int moe_ep_echo_rewrite(const int* topk_idx, const int* inv_c, int T, int K, int
 int moe_ep_expand_grad(const void* tok, const int* map, int rows, int h, const float* rowprob,
                        const void* o, void* d_o, float* dprob_rows, void* stream);
 
+/* ------------------------------------------------------------------ paged stashing
+ * replaces PagedStash (planners.py:394-463) with device-initiated
+ * kernels: a circular free list of fixed-size pages (state[5]: head, free, peak used, failed
+ * stashes, last result; ring[num_pages]); alloc pops ceil(rows / page_rows) pages from the
+ * head into record[1..] (record[0] = count, -1 = out of pages), release appends them to the
+ * tail in record order, copy moves rows [0, rows) between a dense buffer and the pages.
+ * rows_dev (nullable) supplies the row count from device memory (sync-free). */
+int moe_stash_init(int* state, int* ring, int num_pages, void* stream);
+int moe_stash_alloc(int* state, const int* ring, int num_pages, int page_rows,
+                    const int* rows_dev, int rows_host, int* record, int max_pages,
+                    void* stream);
+int moe_stash_release(int* state, int* ring, int num_pages, int* record, void* stream);
+int moe_stash_copy(void* dense, long long ld_bytes, void* pool, int page_rows,
+                   long long row_bytes, const int* record, const int* rows_dev, int rows_host,
+                   int max_rows, int to_pages, void* stream);
+
 /* ------------------------------------------------------------------ grouped GEMM (tcgen05)
  * replaces expert_activation()/expert_forward() routing.py:59-68 per expert block and the
  * corresponding backward GEMMs. flags bit 0 (grouped-M calls): the plan's
@@ -185,20 +215,20 @@ int moe_gg_fc1_dgrad_scatter(const void* d_preact, const void* w1, int a_rows, i
                              const int* num_m_blocks, const unsigned long long* row_dst,
                              int flags, void* stream);
 /* fc1 forward / fc2 dgrad overlapped with the EP dispatch of their A operand: a tile's rows
- * are read once src_flag[s] >= epoch for every source s in block_need[block]; tiles run in
+ * are read once src_flag[s] >= *epoch for every source s in block_need[block]; tiles run in
  * unit_order. status: int[8]; on a wait timeout (2 s) it receives [1, block, missing
  * source mask, epoch, flags[0..3]] and the remaining waits fail fast. */
 int moe_gg_fc1_fwd_ep(const void* xp, const void* w1, int a_rows, int max_rows, int h, int m,
                       int num_experts, const int* block_expert, const int* num_m_blocks,
                       const float* row_prob, void* preact, void* act, int flags,
-                      const unsigned int* src_flag, unsigned int epoch,
+                      const unsigned int* src_flag, const unsigned int* epoch,
                       const unsigned int* block_need, const int* unit_order, int* status,
                       void* stream);
 int moe_gg_fc2_dgrad_ep(const void* dout, const void* w2, const void* preact, int a_rows,
                         int max_rows, int h, int m, int num_experts, const int* block_expert,
                         const int* num_m_blocks, const float* row_prob, void* d_preact,
                         float* dprob_partial, int flags, const unsigned int* src_flag,
-                        unsigned int epoch, const unsigned int* block_need,
+                        const unsigned int* epoch, const unsigned int* block_need,
                         const int* unit_order, int* status, void* stream);
 int moe_gg_fc2_dgrad(const void* dout, const void* w2, const void* preact, int a_rows,
                      int max_rows, int h, int m, int num_experts, const int* block_expert,

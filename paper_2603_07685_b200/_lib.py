@@ -41,6 +41,7 @@ SIGNATURES: dict[str, list] = {
     "moe_permute_plan": [P, P, I, I, I, I, P, I, P, I, I, P, P, P, P, P, P, P, P, P, P, P, P,
                          P],
     "moe_ep_regroup_map": [P, I, I, I, P, P, P],
+    "moe_ep_plan_device": [P, I, I, I, I, I, I, I, I, I, F, I, P, P, P, P, I, P, P, P, P, P, P],
     "moe_ep_row_dst": [P, I, I, I, P, P, L, P, P],
     "moe_permute_compact_map": [P, P, P, I, P, P, P, I, P],
     "moe_permute_gather": [P, I, I, I, P, P, P, P, P],
@@ -55,7 +56,8 @@ SIGNATURES: dict[str, list] = {
     "moe_ep_combine_bwd_push": [P, P, P, I, I, I, P, P, P, I, P, P, P],
     "moe_ep_combine_bwd_push_dest": [P, P, P, I, I, I, P, P, P, I, P, P, I, P],
     "moe_ep_dispatch_push_dest": [P, I, I, I, P, P, P, I, P, P, P, I, P],
-    "moe_ep_signal": [P, I, I, U, P],
+    "moe_ep_signal": [P, I, I, P, P],
+    "moe_ep_epoch_bump": [P, P],
     "moe_ep_prepare": [],
     "moe_ep_block_need": [P, I, I, I, I, I, P, P, P],
     "moe_ep_dprob_pull": [P, I, I, P, P, P, I, I, P, P],
@@ -64,13 +66,18 @@ SIGNATURES: dict[str, list] = {
     "moe_ep_fill_pad_map": [P, I, P, P],
     "moe_ep_echo_rewrite": [P, P, I, I, I, P, P, P, P, P],
     "moe_ep_expand_grad": [P, P, I, I, P, P, P, P, P],
+    # paged stashing (csrc/stash.cu)
+    "moe_stash_init": [P, P, I, P],
+    "moe_stash_alloc": [P, P, I, I, P, I, P, I, P],
+    "moe_stash_release": [P, P, I, P, P],
+    "moe_stash_copy": [P, L, P, I, L, P, P, I, I, I, P],
     # grouped GEMM (csrc/grouped_gemm.cu)
     "moe_gg_fc1_fwd": [P, P, I, I, I, I, I, P, P, P, P, P, I, P],
     "moe_gg_fc2_fwd": [P, P, I, I, I, I, I, P, P, P, I, P],
     "moe_gg_fc2_fwd_scatter": [P, P, I, I, I, I, I, P, P, P, I, P],
     "moe_gg_fc1_dgrad_scatter": [P, P, I, I, I, I, I, P, P, P, I, P],
-    "moe_gg_fc1_fwd_ep": [P, P, I, I, I, I, I, P, P, P, P, P, I, P, U, P, P, P, P],
-    "moe_gg_fc2_dgrad_ep": [P, P, P, I, I, I, I, I, P, P, P, P, P, I, P, U, P, P, P, P],
+    "moe_gg_fc1_fwd_ep": [P, P, I, I, I, I, I, P, P, P, P, P, I, P, P, P, P, P, P],
+    "moe_gg_fc2_dgrad_ep": [P, P, P, I, I, I, I, I, P, P, P, P, P, I, P, P, P, P, P, P],
     "moe_gg_fc2_dgrad": [P, P, P, I, I, I, I, I, P, P, P, P, P, I, P],
     "moe_gg_fc1_dgrad": [P, P, I, I, I, I, I, P, P, P, I, P],
     "moe_gg_wgrad": [P, P, I, I, I, I, P, P, P],

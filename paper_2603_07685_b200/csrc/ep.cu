@@ -599,17 +599,28 @@ int moe_ep_dispatch_push_dest(const void* x, int T, int K, int h, const int* top
 }
 
 __global__ void signal_kernel(const unsigned long long* __restrict__ flag_peers, int dest,
-                              int slot, uint32_t epoch) {
+                              int slot, const uint32_t* __restrict__ epoch) {
   __threadfence_system();
-  st_release_sys_u32(reinterpret_cast<uint32_t*>(flag_peers[dest]) + slot, epoch);
+  st_release_sys_u32(reinterpret_cast<uint32_t*>(flag_peers[dest]) + slot,
+                     *reinterpret_cast<const volatile uint32_t*>(epoch));
 }
 
-// Publish "this rank's rows for `dest` are complete": flag_peers[dest][slot] = epoch
+__global__ void epoch_bump_kernel(uint32_t* epoch) { *epoch += 1u; }
+
+// Publish "this rank's rows for `dest` are complete": flag_peers[dest][slot] = *epoch
 // (release, system scope), ordered after the preceding pushes on `stream`.
-int moe_ep_signal(const unsigned long long* flag_peers, int dest, int slot, unsigned int epoch,
-                  void* stream) {
-  if (dest < 0 || slot < 0) return kErrInvalidArg;
+int moe_ep_signal(const unsigned long long* flag_peers, int dest, int slot,
+                  const unsigned int* epoch, void* stream) {
+  if (dest < 0 || slot < 0 || !epoch) return kErrInvalidArg;
   signal_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(flag_peers, dest, slot, epoch);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+// Advance the dispatch epoch (device scalar) in stream order.
+int moe_ep_epoch_bump(unsigned int* epoch, void* stream) {
+  if (!epoch) return kErrInvalidArg;
+  epoch_bump_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(epoch);
   MOE_LAUNCH_CHECK();
   return kOk;
 }
@@ -626,6 +637,7 @@ __global__ void block_need_kernel(const int* __restrict__ tab, int n, int el, in
   const int* real = off_pad + el + 1;
   __shared__ int cnt[33];
   __shared__ int base_s[33];
+  nblocks = min(nblocks, off_pad[el] / 128);  // nblocks may be a static upper bound
   const int nunits = nblocks / cg;
   if (threadIdx.x <= 32) cnt[threadIdx.x] = 0;
   __syncthreads();
@@ -695,7 +707,9 @@ int moe_ep_prepare() {
   prefer_max_shared(dispatch_push_kernel<4>);
   prefer_max_shared(combine_bwd_push_sel_kernel<2>);
   prefer_max_shared(signal_kernel);
+  prefer_max_shared(epoch_bump_kernel);
   cudaFuncAttributes a;
+  MOE_CUDA_CHECK(cudaFuncGetAttributes(&a, epoch_bump_kernel));
   MOE_CUDA_CHECK(cudaFuncGetAttributes(&a, dispatch_push_kernel<4>));
   MOE_CUDA_CHECK(cudaFuncGetAttributes(&a, combine_bwd_push_sel_kernel<2>));
   MOE_CUDA_CHECK(cudaFuncGetAttributes(&a, signal_kernel));

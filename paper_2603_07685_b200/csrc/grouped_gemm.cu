@@ -99,7 +99,7 @@ struct Params {
   // loaded only once every source in block_need[128-row block] has signalled; units run in
   // unit_order (rows of early-arriving sources first). wait_status <- 1 on a 10 s timeout.
   const uint32_t* src_flag;
-  uint32_t epoch;
+  const uint32_t* epoch;  // device scalar (bumped in stream order before the dispatch)
   const uint32_t* block_need;
   const int* unit_order;
   int* wait_status;
@@ -108,12 +108,13 @@ struct Params {
 // Spin (bounded) until every source rank in `need` has published this epoch's rows. On a
 // timeout (2 s) the kernel records [1, block, missing sources, epoch, flags[0..3]] in
 // wait_status[0..7] and stops waiting (later waits of any CTA fail fast).
-__device__ __forceinline__ void wait_sources(const Params& p, uint32_t need, int blk) {
+__device__ __forceinline__ void wait_sources(const Params& p, uint32_t need, int blk,
+                                             uint32_t epoch) {
   if (!need) return;
   const uint64_t t0 = globaltimer_ns();
   while (need) {
     const int s = __ffs(need) - 1;
-    if (static_cast<int>(ld_acquire_sys_u32(p.src_flag + s) - p.epoch) >= 0) {
+    if (static_cast<int>(ld_acquire_sys_u32(p.src_flag + s) - epoch) >= 0) {
       need &= need - 1;
       continue;
     }
@@ -122,7 +123,7 @@ __device__ __forceinline__ void wait_sources(const Params& p, uint32_t need, int
       if (p.wait_status && atomicCAS(p.wait_status, 0, 1) == 0) {
         p.wait_status[1] = blk;
         p.wait_status[2] = static_cast<int>(need);
-        p.wait_status[3] = static_cast<int>(p.epoch);
+        p.wait_status[3] = static_cast<int>(epoch);
         for (int i = 0; i < 4; ++i)
           p.wait_status[4 + i] = static_cast<int>(ld_acquire_sys_u32(p.src_flag + i));
       }
@@ -290,11 +291,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
+      const uint32_t epoch = p.src_flag ? *reinterpret_cast<const volatile uint32_t*>(p.epoch) : 0u;
       for (int t = first; t < num_tiles; t += stride) {
         Tile tl;
         decode_tile<GROUPED_K, CG>(p, t, num_units, rank, tl);
         if constexpr (!GROUPED_K) {
-          if (p.src_flag) wait_sources(p, __ldg(p.block_need + tl.m0 / BM), tl.m0 / BM);
+          if (p.src_flag) wait_sources(p, __ldg(p.block_need + tl.m0 / BM), tl.m0 / BM, epoch);
         }
         for (int kb = 0; kb < tl.num_kb; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
@@ -722,7 +724,7 @@ extern "C" {
 // output buffers (multiple of 128; of 256 with the pair flag).
 struct SourceWait {
   const uint32_t* src_flag;
-  uint32_t epoch;
+  const uint32_t* epoch;  // device scalar (bumped in stream order before the dispatch)
   const uint32_t* block_need;
   const int* unit_order;
   int* status;
@@ -774,10 +776,10 @@ int moe_gg_fc1_fwd(const void* xp, const void* w1, int a_rows, int max_rows, int
 int moe_gg_fc1_fwd_ep(const void* xp, const void* w1, int a_rows, int max_rows, int h, int m,
                       int num_experts, const int* block_expert, const int* num_m_blocks,
                       const float* row_prob, void* preact, void* act, int flags,
-                      const unsigned int* src_flag, unsigned int epoch,
+                      const unsigned int* src_flag, const unsigned int* epoch,
                       const unsigned int* block_need, const int* unit_order, int* status,
                       void* stream) {
-  if (!src_flag || !block_need) return kErrInvalidArg;
+  if (!src_flag || !epoch || !block_need) return kErrInvalidArg;
   const SourceWait w{src_flag, epoch, block_need, unit_order, status};
   return fc1_fwd_impl(xp, w1, a_rows, max_rows, h, m, num_experts, block_expert, num_m_blocks,
                       row_prob, preact, act, flags, &w, stream);
@@ -870,9 +872,9 @@ int moe_gg_fc2_dgrad_ep(const void* dout, const void* w2, const void* preact, in
                         int max_rows, int h, int m, int num_experts, const int* block_expert,
                         const int* num_m_blocks, const float* row_prob, void* d_preact,
                         float* dprob_partial, int flags, const unsigned int* src_flag,
-                        unsigned int epoch, const unsigned int* block_need,
+                        const unsigned int* epoch, const unsigned int* block_need,
                         const int* unit_order, int* status, void* stream) {
-  if (!src_flag || !block_need) return kErrInvalidArg;
+  if (!src_flag || !epoch || !block_need) return kErrInvalidArg;
   const SourceWait w{src_flag, epoch, block_need, unit_order, status};
   return fc2_dgrad_impl(dout, w2, preact, a_rows, max_rows, h, m, num_experts, block_expert,
                         num_m_blocks, row_prob, d_preact, dprob_partial, flags, &w, stream);

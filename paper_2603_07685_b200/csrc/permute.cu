@@ -596,8 +596,13 @@ __global__ void regroup_map_kernel(const int* __restrict__ tab, int n, int el, i
   const int* recv_off = tab + n * el;
   const int* off_pad = recv_off + n * el;
   const int* real = off_pad + el + 1;
+  const int rows_plan = off_pad[el];  // rows_pad may be a static upper bound
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows_pad;
        r += gridDim.x * blockDim.x) {
+    if (r >= rows_plan) {
+      map_pad[r] = -1;
+      continue;
+    }
     int lo = 0, hi = el - 1;  // last e with off_pad[e] <= r
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -644,8 +649,13 @@ __global__ void row_dst_kernel(const int* __restrict__ tab, int n, int el, int r
   const int* kept = tab;
   const int* off_pad = tab + 2 * n * el;
   const int* real = off_pad + el + 1;
+  const int rows_plan = off_pad[el];  // rows_pad may be a static upper bound
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows_pad;
        r += gridDim.x * blockDim.x) {
+    if (r >= rows_plan) {
+      row_dst[r] = 0ull;
+      continue;
+    }
     int lo = 0, hi = el - 1;  // last e with off_pad[e] <= r
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;

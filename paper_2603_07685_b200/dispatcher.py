@@ -305,6 +305,7 @@ class SymmPool:
         # dispatch/GEMM overlap: per-dispatch epoch (same sequence on every rank), the side
         # stream the pushes run on, and the GEMMs' wait-timeout flag
         self.epoch = 0
+        self.epoch_dev = torch.zeros((1,), dtype=torch.int32, device=dev)
         self.comm = torch.cuda.Stream(device=dev)
         _lib.call("moe_ep_prepare")  # load the side-stream kernels now (lazy loading)
         self.status = torch.zeros((8,), dtype=torch.int32, device=dev)
@@ -332,6 +333,16 @@ class SymmPool:
             cur = (t, peers, h)
             self.bufs[name] = cur
         return cur[0], cur[1]
+
+    def local(self, name: str, numel: int, dtype):
+        """A (non-symmetric) tmp buffer owned by the pool, grown on demand: the worst-case
+        tmp set that every layer of this tag computes in (Paged Stashing)."""
+        key = "local:" + name
+        cur = self.bufs.get(key)
+        if cur is None or cur.numel() < numel or cur.dtype != dtype:
+            cur = torch.empty((numel,), dtype=dtype, device=self.dev)
+            self.bufs[key] = cur
+        return cur[:numel]
 
     def remote(self, name: str, peer: int, numel: int, dtype):
         """Tensor view of `peer`'s copy of buffer `name` (NVLink peer memory)."""
@@ -366,10 +377,38 @@ def _record_exchange(hp: EPHostPlan, h: int, width: int = 2):
                          local_experts=el)
 
 
+# inputs of the last sync-free forward's device plan (exchange statistics on demand)
+last_plan_inputs: dict = {}
+
+
+def ep_static_rows(n: int, t: int, K: int, E: int, capacity: int, align: int) -> int:
+    """Worst-case rows of one rank's padded plan (sync-free buffers): every selection of
+    the group on this rank's experts (dropless), or el experts at capacity."""
+    el = E // n
+    if capacity >= 0:
+        rows = el * (-(-capacity // align) * align)
+    else:
+        rows = n * t * K + el * (align - 1)
+    return max(-(-rows // align) * align, 2 * ops.ALIGN)
+
+
+def exchange_stats_from_device():
+    """Fill last_exchange from the last sync-free forward's gathered counts (syncs)."""
+    d = last_plan_inputs
+    if not d:
+        return
+    g = d["gathered"].cpu().numpy()
+    counts_all = np.rint(g[:, :d["E"]]).astype(np.int64)
+    _, _, hp = p2p_tables(counts_all, d["rank"], d["cap"], d["pad"], d["align"])
+    _record_exchange(hp, d["h"])
+
+
 def check_ep_status():
     """Raise if an overlapped EP GEMM timed out waiting for a source rank (synchronises)."""
     for key, pool in _POOLS.items():
         st = pool.status.tolist()
+        if st[7]:
+            raise _lib.MoEKernelError(f"EP plan exceeds the static buffers (pool {key})")
         if st[0]:
             raise _lib.MoEKernelError(
                 f"EP dispatch wait timed out (pool {key}): block {st[1]}, missing sources "
@@ -381,8 +420,11 @@ def _overlapped_push(pool, ep, push_one, stream_main):
     followed by a release-store of this dispatch's epoch into dest's flag slot `me`; the
     consumer GEMM on the main stream waits per block on those flags."""
     n, me = ep.n, ep.rank
-    epoch = pool.next_epoch()
+    pool.next_epoch()
     flags, flag_peers = pool.get("flags", 32, torch.int32)
+    # the epoch lives on the device (bumped in stream order), so a captured CUDA graph
+    # replays with a fresh epoch every time
+    _lib.call("moe_ep_epoch_bump", pool.epoch_dev.data_ptr(), stream_main.cuda_stream)
     ev = torch.cuda.Event()
     ev.record(stream_main)
     comm = pool.comm
@@ -392,8 +434,9 @@ def _overlapped_push(pool, ep, push_one, stream_main):
         for i in range(n):
             d = (me + i) % n
             push_one(d, cs)
-            _lib.call("moe_ep_signal", flag_peers.data_ptr(), d, me, epoch, cs)
-    return flags, epoch
+            _lib.call("moe_ep_signal", flag_peers.data_ptr(), d, me, pool.epoch_dev.data_ptr(),
+                      cs)
+    return flags, pool.epoch_dev
 
 
 def _pool(ep: EPGroup, dev, tag: str = "") -> SymmPool:
@@ -503,7 +546,8 @@ class _MoEEPP2PFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w_r, w1, w2, sel_bias, w1s, w2s, cfg: MoEConfig, ep: EPGroup,
                 echo_slots: int = 0, scatter: bool = True, tag: str = "",
-                overlap: bool = True):
+                overlap: bool = True, sync_free: bool = False, stash=None,
+                layer_id: int = 0):
         t, h = x.shape
         E, K = cfg.num_experts, cfg.top_k
         n = ep.n
@@ -515,44 +559,74 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         stats = torch.cat([r.counts.float(), r.mean_scores])
         gathered = torch.empty((n, 2 * E), dtype=torch.float32, device=dev)
         dist.all_gather_into_tensor(gathered, stats, group=ep.group)  # also the reuse barrier
-        g = gathered.cpu().numpy()  # the one host sync of the EP forward
-        counts_all = np.rint(g[:, :E]).astype(np.int64)
         cap = cfg.capacity(n * t)
-        # ECHO: route to virtual experts (expert segments on their serving ranks)
-        topk_use, E_use, counts_use, layout = r.topk_idx, E, counts_all, None
-        if echo_slots:
-            if cap >= 0:
-                raise ValueError("ECHO cloning applies to dropless routing (no capacity)")
-            topk_use, E_use, counts_use, layout = _echo_route(r, counts_all, E, K, n, ep.rank,
-                                                              echo_slots, dev, stream)
-        align = ops.pick_align(n * t, K, E_use)
+        layout = None
+        topk_use, E_use = r.topk_idx, E
+        if sync_free and not echo_slots:
+            # ---- device-side planning: no host read of the counts (CUDA-graph capturable);
+            # buffers are sized for the worst case (every selection on one rank)
+            align = ops.pick_align(n * t, K, E)
+            el = E // n
+            rows_alloc = ep_static_rows(n, t, K, E, cap, align)
+            rows_bound = rows_alloc
+            i32 = dict(dtype=torch.int32, device=dev)
+            tab = torch.empty((E + E + 2 * n * el + 2 * el + 1 + rows_alloc // ops.ALIGN + 3
+                               + n * el,), **i32)
+            lens = [E, E, 2 * n * el + 2 * el + 1, rows_alloc // ops.ALIGN, 3, n * el]
+            base_d, cap_d, table_d, be_d, meta_d, dst_off_d = torch.split(tab, lens)
+            smallf = torch.empty((1 + E,), dtype=torch.float32, device=dev)
+            _lib.call("moe_ep_plan_device", gathered.data_ptr(), 2 * E, n, E, ep.rank, t, K, cap,
+                      int(cfg.pad_to_capacity), align, float(cfg.aux_loss_coeff), rows_alloc,
+                      base_d.data_ptr(), cap_d.data_ptr(), table_d.data_ptr(), be_d.data_ptr(),
+                      rows_alloc // ops.ALIGN, meta_d.data_ptr(), dst_off_d.data_ptr(),
+                      smallf.data_ptr(), smallf[1:].data_ptr(), pool.status[7:].data_ptr(),
+                      stream)
+            aux = smallf[0]
+            r.aux_grad = smallf[1:]
+            last_plan_inputs.update(gathered=gathered, rank=ep.rank, cap=cap,
+                                    pad=cfg.pad_to_capacity, align=align, h=h, E=E)
+            has_cap = cap >= 0
+        else:
+            g = gathered.cpu().numpy()  # the one host sync of the EP forward
+            counts_all = np.rint(g[:, :E]).astype(np.int64)
+            # ECHO: route to virtual experts (expert segments on their serving ranks)
+            counts_use = counts_all
+            if echo_slots:
+                if cap >= 0:
+                    raise ValueError("ECHO cloning applies to dropless routing (no capacity)")
+                topk_use, E_use, counts_use, layout = _echo_route(r, counts_all, E, K, n,
+                                                                  ep.rank, echo_slots, dev,
+                                                                  stream)
+            align = ops.pick_align(n * t, K, E_use)
+            base, rows_all, hp = p2p_tables(counts_use, ep.rank, cap, cfg.pad_to_capacity, align)
+            _record_exchange(hp, h)
+            aux_v, aux_g = global_aux(counts_all, g[:, E:], t, K, cfg.aux_loss_coeff)
+            rows_alloc = max(max(rows_all), 2 * ops.ALIGN)
+            rows_bound = hp.rows_pad
+            el = hp.el
+            # one pinned H2D copy of every small table
+            cap_local = hp.cap_local if hp.cap_local is not None else np.full(E_use, -1)
+            meta = np.array([hp.rows_pad // ops.ALIGN, hp.rows_pad, 0], dtype=np.int64)
+            # dst_off[s, j]: source s's compact offset of this rank's j-th (virtual) expert,
+            # where the scatter epilogues return that expert's rows
+            dst_off = _excl_cumsum(hp.kept, axis=1)[:, ep.rank * el:(ep.rank + 1) * el].ravel()
+            parts = [base, cap_local, hp.table.astype(np.int64), hp.block_expert, meta, dst_off]
+            lens = [len(p) for p in parts]
+            tab = torch.from_numpy(np.concatenate(parts).astype(np.int32)).pin_memory().to(
+                dev, non_blocking=True)
+            base_d, cap_d, table_d, be_d, meta_d, dst_off_d = torch.split(tab, lens)
+            smallf = torch.from_numpy(np.concatenate([[aux_v], aux_g]).astype(np.float32))
+            smallf = smallf.pin_memory().to(dev, non_blocking=True)
+            aux = smallf[0].clone()
+            r.aux_grad = smallf[1:]
+            has_cap = hp.cap_local is not None
         pair = align == 2 * ops.ALIGN
-        base, rows_all, hp = p2p_tables(counts_use, ep.rank, cap, cfg.pad_to_capacity, align)
-        _record_exchange(hp, h)
-        aux_v, aux_g = global_aux(counts_all, g[:, E:], t, K, cfg.aux_loss_coeff)
-        rows_alloc = max(max(rows_all), 2 * ops.ALIGN)
-        el = hp.el
-        # one pinned H2D copy of every small table
         ctx_topk = topk_use
-        cap_local = hp.cap_local if hp.cap_local is not None else np.full(E_use, -1)
-        meta = np.array([hp.rows_pad // ops.ALIGN, hp.rows_pad, 0], dtype=np.int64)
-        # dst_off[s, j]: source s's compact offset of this rank's j-th (virtual) expert, where
-        # the scatter epilogues return that expert's rows
-        dst_off = _excl_cumsum(hp.kept, axis=1)[:, ep.rank * el:(ep.rank + 1) * el].ravel()
-        parts = [base, cap_local, hp.table.astype(np.int64), hp.block_expert, meta, dst_off]
-        lens = [len(p) for p in parts]
-        tab = torch.from_numpy(np.concatenate(parts).astype(np.int32)).pin_memory().to(
-            dev, non_blocking=True)
-        base_d, cap_d, table_d, be_d, meta_d, dst_off_d = torch.split(tab, lens)
-        smallf = torch.from_numpy(np.concatenate([[aux_v], aux_g]).astype(np.float32))
-        smallf = smallf.pin_memory().to(dev, non_blocking=True)
-        aux = smallf[0].clone()
-        r.aux_grad = smallf[1:]
         nmb = meta_d[0:1]
         off_pad_d = table_d[2 * n * el: 2 * n * el + el + 1]
 
         splan = ops.build_plan(topk_use, r.topk_prob, E_use, -1, False,
-                               cap_e=cap_d if hp.cap_local is not None else None, compact=True)
+                               cap_e=cap_d if has_cap else None, compact=True)
         if layout is not None:
             w1, w2 = _echo_weights(pool, ep, w1, w2, layout)
         xp, xp_peers = pool.get("xp", rows_alloc * h, torch.bfloat16)
@@ -563,8 +637,8 @@ class _MoEEPP2PFunction(torch.autograd.Function):
             pr, prob_peers = pool.get("prob", rows_alloc, torch.float32)
             row_prob = pr[:rows_alloc]
         map_pad = torch.empty((rows_alloc,), dtype=torch.int32, device=dev)
-        if hp.rows_pad:
-            _lib.call("moe_ep_regroup_map", table_d.data_ptr(), n, el, hp.rows_pad,
+        if rows_bound:
+            _lib.call("moe_ep_regroup_map", table_d.data_ptr(), n, el, rows_bound,
                       map_pad.data_ptr(), None, stream)
         # zero this rank's padding / phantom rows (disjoint from the rows peers push)
         _lib.call("moe_zero_pad_rows", meta_d.data_ptr(), map_pad.data_ptr(), h, xp.data_ptr(),
@@ -581,24 +655,27 @@ class _MoEEPP2PFunction(torch.autograd.Function):
             # pushes run destination by destination on a side stream while fc1 consumes the
             # rows block by block as their sources signal (no barrier)
             cg = 2 if pair else 1
-            nblocks = hp.rows_pad // ops.ALIGN
+            nblocks = rows_bound // ops.ALIGN
             need = torch.zeros((max(rows_alloc // ops.ALIGN, 1),), dtype=torch.int32, device=dev)
             order = torch.empty((max(nblocks // cg, 1),), dtype=torch.int32, device=dev)
             if nblocks:
-                _lib.call("moe_ep_block_need", table_d.data_ptr(), n, el, ep.rank, nblocks, cg,
+                _lib.call("moe_ep_block_need", table_d.data_ptr(), n, el, ep.rank,
+                          nblocks - nblocks % cg, cg,
                           need.data_ptr(), order.data_ptr(), stream)
             main = torch.cuda.current_stream()
             flags, epoch = _overlapped_push(
                 pool, ep, lambda d, cs: _lib.call("moe_ep_dispatch_push_dest", *push_args, d, cs),
                 main)
             wait = (flags, epoch, need, order, pool.status)
-            preact, act = gemm.fc1_fwd(xp, w1, be_d, nmb, row_prob, pair=pair, wait=wait)
+            preact, act = gemm.fc1_fwd(xp, w1, be_d, nmb, row_prob, pair=pair, wait=wait,
+                                       **_tmp_preact_act(pool, stash, rows_alloc, w1))
             main.wait_stream(pool.comm)
             ctx.need_order = (need, order)
         else:
             _lib.call("moe_ep_dispatch_push", *push_args, stream)
             pool.barrier()
-            preact, act = gemm.fc1_fwd(xp, w1, be_d, nmb, row_prob, pair=pair)
+            preact, act = gemm.fc1_fwd(xp, w1, be_d, nmb, row_prob, pair=pair,
+                                       **_tmp_preact_act(pool, stash, rows_alloc, w1))
         ctx.overlap = overlap
         y = torch.empty_like(x)
         row_dst_dx = None
@@ -611,7 +688,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
             _, dxrecv_peers = pool.get("dxrecv", rows_c * h, torch.bfloat16)
             row_dst = torch.empty((2, rows_alloc), dtype=torch.int64, device=dev)
             for i, pp in enumerate((orecv_peers, dxrecv_peers)):
-                _lib.call("moe_ep_row_dst", table_d.data_ptr(), n, el, hp.rows_pad,
+                _lib.call("moe_ep_row_dst", table_d.data_ptr(), n, el, rows_bound,
                           dst_off_d.data_ptr(), pp.data_ptr(), h * 2, row_dst[i].data_ptr(),
                           stream)
             row_dst_dx = row_dst[1]
@@ -633,7 +710,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
             # then reads local memory instead of pulling O over NVLink a second time
             o_local = None
             if not cfg.mem_efficient:
-                o_local = torch.empty((max(sum(hp.send_splits), 1), h), dtype=x.dtype,
+                o_local = torch.empty((max(t * K, 1), h), dtype=x.dtype,
                                       device=dev)
             _lib.call("moe_ep_combine_pull", o_peers.data_ptr(), t, K, h, ctx_topk.data_ptr(),
                       splan.inv_map.data_ptr(), base_d.data_ptr(), el,
@@ -641,6 +718,18 @@ class _MoEEPP2PFunction(torch.autograd.Function):
                       x.data_ptr() if cap >= 0 else None,
                       shared[-1].data_ptr() if shared is not None else None, None, y.data_ptr(),
                       o_local.data_ptr() if o_local is not None else None, stream)
+        if stash is not None:
+            # Paged Stashing: keep only this layer's actual rows (device counts) in pages; the
+            # worst-case tmp buffers (xp, preact, act, received outputs) serve the next layer
+            if not sync_free or cfg.mem_efficient or layout is not None or not scatter:
+                raise ValueError("paged stashing needs the sync-free p2p transport with the "
+                                 "standard combine")
+            st_plan, st_out = _stash_pair(stash)
+            st_plan.stash(2 * layer_id, {"xp": xp, "preact": preact, "act": act},
+                          rows_dev=meta_d[1:2])
+            st_out.stash(2 * layer_id + 1, {"o": o_local}, rows_dev=splan.meta[2:3])
+            preact = act = None
+        ctx.stash, ctx.layer_id = stash, layer_id
         ctx.scatter, ctx.tag, ctx.row_dst_dx = scatter, tag, row_dst_dx
         ctx.cfg, ctx.ep, ctx.r, ctx.splan, ctx.cap, ctx.pair = cfg, ep, r, splan, cap, pair
         ctx.topk_use, ctx.layout, ctx.el_own = topk_use, layout, E // n
@@ -665,6 +754,13 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         dy = dy.contiguous()
         xp, _ = pool.get("xp", rows_alloc * h, torch.bfloat16)
         xp = xp[: rows_alloc * h].view(rows_alloc, h)
+        if ctx.stash is not None:  # reload this layer's rows into the shared tmp buffers
+            tmp = _tmp_preact_act(pool, ctx.stash, rows_alloc, w1)
+            preact, act = tmp["preact"], tmp["act"]
+            st_plan, st_out = _stash_pair(ctx.stash)
+            st_plan.reload(2 * ctx.layer_id, {"xp": xp, "preact": preact, "act": act},
+                           rows_dev=meta_d[1:2])
+            st_out.reload(2 * ctx.layer_id + 1, {"o": ctx.o_local}, rows_dev=splan.meta[2:3])
         d_o, d_peers = pool.get("do", rows_alloc * h, torch.bfloat16)
         d_o = d_o[: rows_alloc * h].view(rows_alloc, h)
         _lib.call("moe_zero_pad_rows", meta_d.data_ptr(), map_pad.data_ptr(), h, d_o.data_ptr(),
@@ -742,7 +838,25 @@ class _MoEEPP2PFunction(torch.autograd.Function):
             dw1 = _echo_reduce(pool, ep, dw1, ctx.layout, ctx.el_own, "echo_dw1")
             dw2 = _echo_reduce(pool, ep, dw2, ctx.layout, ctx.el_own, "echo_dw2")
         return (dx, dw_r.to(torch.bfloat16), dw1, dw2, None, dw1s, dw2s, None, None, None, None,
-                None, None)
+                None, None, None, None, None)
+
+
+def _stash_pair(stash):
+    """(buffer for the plan rows {xp, preact, act}, buffer for the returned outputs {o}):
+    one PagedStashBuffer for both, or a pair (pages sized per row group)."""
+    if isinstance(stash, (tuple, list)):
+        return stash[0], stash[1]
+    return stash, stash
+
+
+def _tmp_preact_act(pool, stash, rows_alloc, w1):
+    """With Paged Stashing, fc1's outputs go to the pool's shared tmp buffers."""
+    if stash is None:
+        return {}
+    m2 = w1.shape[1]
+    pre = pool.local("preact", rows_alloc * m2, torch.bfloat16).view(rows_alloc, m2)
+    act = pool.local("act", rows_alloc * (m2 // 2), torch.bfloat16).view(rows_alloc, m2 // 2)
+    return {"preact": pre, "act": act}
 
 
 def _excl(a):
@@ -947,26 +1061,37 @@ class _MoEEPDedupFunction(torch.autograd.Function):
 
 def moe_forward_ep(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
                    selection_bias=None, w1_shared=None, w2_shared=None, transport: str = "auto",
-                   echo_slots: int = 0, tag: str = ""):
+                   echo_slots: int = 0, tag: str = "", sync_free: bool = False,
+                   stash=None, layer_id: int = 0):
     """EP MoE layer: w1_local [E/EP, 2m, h], w2_local [E/EP, h, m] are this rank's experts
     (global experts [rank*E/EP, (rank+1)*E/EP)). Returns (y [T,h], global aux).
 
     transport:
-      "auto" (default): "p2p_dedup" for top_k >= 4, else "p2p".
+      "auto" (default): "p2p".
       "p2p": tokens are pushed over NVLink peer memory straight into the expert rank's
         padded plan (csrc/ep.cu); expert outputs and dX rows return from the fc2 / fc1-dgrad
-        GEMM epilogues, which store each row into its source rank's buffer over NVLink, so
-        both combines are local.
-        The pushes run destination by destination on a side stream and the consuming
-        GEMMs (fc1 fwd, fc2 dgrad) start as soon as each 128-row block's source ranks have
-        signalled (per-block flags, no barrier), so both dispatches overlap the GEMMs.
-      "p2p_sync": "p2p" without the dispatch overlap (push, barrier, GEMM).
+        GEMM epilogues, which store each row (TMA bulk stores) into its source rank's
+        buffer over NVLink, so both combines are local.
+      "p2p_overlap": "p2p" with the dispatches overlapped with their consuming GEMMs: the
+        pushes run destination by destination on a side stream and fc1 fwd / fc2 dgrad
+        start each 128-row block as soon as its source ranks have signalled (per-block
+        flags, no barrier). Correct, but not faster under the 1 kW power cap (measured).
       "p2p_pull": the previous p2p variant, where the combines pull the rows back over
         NVLink (kept for A/B measurement).
       "p2p_dedup": token de-duplication (one row per (token, destination rank) each way;
         HybridEP-style).
       "nccl": permute -> NCCL all_to_all_single -> regroup (the baseline dispatcher).
     tag: buffer namespace; give every MoE layer that is alive at the same time its own.
+    sync_free (p2p transports, no ECHO): plan the exchange on the device
+      (moe_ep_plan_device) with worst-case static buffers, so the step never reads the
+      counts on the host and can be captured in a CUDA graph.
+    stash (a stash.PagedStashBuffer with pools "xp", "preact", "act", "o", or a pair of
+      buffers for {xp, preact, act} and {o}; sync_free p2p, standard combine): Paged
+      Stashing.
+      Layers sharing a `tag` compute in one set of worst-case tmp buffers; each layer's
+      actual rows are copied into pages after its forward and back before its backward, so
+      memory is O(worst case + sum of actual rows) instead of O(layers x worst case).
+      layer_id: this layer's stash record key (unique among live layers).
 
     The router weight gradient returned is this rank's partial sum over its own tokens;
     W_r is replicated, so its all-reduce belongs to the data-parallel gradient sync.
@@ -974,14 +1099,16 @@ def moe_forward_ep(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
     if cfg.num_experts % ep.n:
         raise ValueError(f"num_experts {cfg.num_experts} not divisible by EP {ep.n}")
     if transport == "auto":
-        # measured on B200 (EP=4): dedup wins for top-8 (Qwen3 +5%, DeepSeek +1%); for
-        # top-2 most tokens already hit distinct ranks and the local expand costs more
-        transport = "p2p_dedup" if cfg.top_k >= 4 else "p2p"
+        # measured on B200 at EP=4 (profiles/r01_summary.md): p2p with the scatter epilogues
+        # beats dedup (Qwen3 4.12M vs 3.94M tok/s, DeepSeek 1.25M vs 1.18M, Mixtral 2.06M vs
+        # 2.02M) and the overlapped variant under the 1 kW power cap
+        transport = "p2p"
     args = (x, w_r, w1_local, w2_local, selection_bias, w1_shared, w2_shared, cfg, ep)
-    if echo_slots or transport in ("p2p", "p2p_sync", "p2p_pull"):
+    if echo_slots or transport in ("p2p", "p2p_overlap", "p2p_pull"):
         # ECHO hot-expert cloning runs on the p2p transport (virtual experts)
         return _MoEEPP2PFunction.apply(*args, int(echo_slots), transport != "p2p_pull", tag,
-                                       transport == "p2p" or bool(echo_slots))
+                                       transport == "p2p_overlap",
+                                       sync_free and not echo_slots, stash, int(layer_id))
     if transport == "p2p_dedup":
         return _MoEEPDedupFunction.apply(*args, tag)
     if transport == "nccl":

@@ -61,11 +61,11 @@ def deinterleave_cols(preact: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]
 
 
 def _wait_args(wait):
-    """wait = (src_flag [n] int32, epoch, block_need [blocks] int32, unit_order [units] int32,
-    status [1] int32): the EP dispatch-overlap arguments of the *_ep GEMMs."""
+    """wait = (src_flag [n] int32, epoch [1] int32 (device), block_need [blocks] int32,
+    unit_order [units] int32, status [8] int32): the EP dispatch-overlap arguments of the
+    *_ep GEMMs."""
     flag, epoch, need, order, status = wait
-    return (flag.data_ptr(), int(epoch) & 0xFFFFFFFF, need.data_ptr(), _ptr(order),
-            _ptr(status))
+    return (flag.data_ptr(), epoch.data_ptr(), need.data_ptr(), _ptr(order), _ptr(status))
 
 
 def fc1_fwd(xp, w1, block_expert, num_m_blocks, row_prob=None, preact=None, act=None,

@@ -87,16 +87,46 @@ def _worker(rank, world, port, case, q, transport):
         w2d = w2[mine].to(dev).contiguous().requires_grad_(True)
         ep = EPGroup()
         echo = case.get("echo", 0)
-        y, aux = moe_forward_ep(x, w_rd, w1d, w2d, cfg, ep, transport=transport, echo_slots=echo)
-        # a second step exercises buffer reuse across steps (symmetric pools, barriers)
-        for p_ in (x, w_rd, w1d, w2d):
-            p_.grad = None
-        y, aux = moe_forward_ep(x, w_rd, w1d, w2d, cfg, ep, transport=transport, echo_slots=echo)
-        if echo:
-            from paper_2603_07685_b200.dispatcher import last_echo
-            if not last_echo.get("clones"):
-                raise AssertionError(f"ECHO made no clones: {last_echo}")
-        torch.autograd.backward([y, aux], [dy_g[sl].to(dev), torch.ones_like(aux)])
+        sf = transport in ("p2p_sync_free", "p2p_graph")
+        tr = "p2p" if sf else transport
+        leaves = (x, w_rd, w1d, w2d)
+        dyd = dy_g[sl].to(dev)
+        if transport == "p2p_graph":
+            # the whole sync-free fwd+bwd step captured in one CUDA graph, replayed twice
+            def stepf():
+                y_, aux_ = moe_forward_ep(x, w_rd, w1d, w2d, cfg, ep, transport="p2p",
+                                          sync_free=True)
+                torch.autograd.backward([y_, aux_], [dyd, torch.ones_like(aux_)])
+                return y_, aux_
+
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                for _ in range(2):
+                    for p_ in leaves:
+                        p_.grad = None
+                    stepf()
+            torch.cuda.current_stream().wait_stream(side)
+            for p_ in leaves:
+                p_.grad = None
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                y, aux = stepf()
+            graph.replay()
+            graph.replay()
+        else:
+            y, aux = moe_forward_ep(x, w_rd, w1d, w2d, cfg, ep, transport=tr, echo_slots=echo,
+                                    sync_free=sf)
+            # a second step exercises buffer reuse across steps (symmetric pools, barriers)
+            for p_ in leaves:
+                p_.grad = None
+            y, aux = moe_forward_ep(x, w_rd, w1d, w2d, cfg, ep, transport=tr, echo_slots=echo,
+                                    sync_free=sf)
+            if echo:
+                from paper_2603_07685_b200.dispatcher import last_echo
+                if not last_echo.get("clones"):
+                    raise AssertionError(f"ECHO made no clones: {last_echo}")
+            torch.autograd.backward([y, aux], [dyd, torch.ones_like(aux)])
         from paper_2603_07685_b200.dispatcher import check_ep_status
         check_ep_status()  # no overlapped GEMM timed out waiting for a source rank
         dwr = w_rd.grad.float().clone()
@@ -145,7 +175,8 @@ def _worker(rank, world, port, case, q, transport):
         q.put((rank, traceback.format_exc() + repr(exc)))
 
 
-@pytest.mark.parametrize("transport", ["p2p", "p2p_sync", "p2p_pull", "p2p_dedup", "nccl"])
+@pytest.mark.parametrize("transport", ["p2p", "p2p_sync_free", "p2p_graph", "p2p_overlap",
+                                       "p2p_pull", "p2p_dedup", "nccl"])
 @pytest.mark.parametrize("name", list(CASES))
 def test_ep_layer_matches_global_oracle(name, transport):
     _run(CASES[name], transport)
@@ -171,7 +202,91 @@ def _run(case, transport):
              for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=300) for _ in range(world)]
+    res = [q.get(timeout=int(os.environ.get("MOE_TEST_TIMEOUT", "300"))) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, msg in res:
+        assert msg == "ok", f"rank {rank}: {msg}"
+
+
+def _stash_worker(rank, world, port, q):
+    """Two stacked EP layers (sync-free p2p): Paged Stashing with one shared tmp buffer set
+    must give bit-identical outputs and gradients to per-layer buffers."""
+    try:
+        import torch.distributed as dist
+
+        from paper_2603_07685_b200.dispatcher import EPGroup, check_ep_status, moe_forward_ep
+        from paper_2603_07685_b200.layer import MoEConfig
+        from paper_2603_07685_b200.stash import PagedStashBuffer
+
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(rank)
+        dev = torch.device("cuda", rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+        E, K, h, m, T = 8, 2, 256, 256, 256
+        cfg = MoEConfig(E, K, h, m, score="softmax", aux_loss_coeff=1e-2)
+        g = torch.Generator().manual_seed(5 + rank)
+        bf = torch.bfloat16
+        el = E // world
+        layers = []
+        for li in range(2):
+            gw = torch.Generator().manual_seed(100 + li)
+            w_r = (torch.randn((h, E), generator=gw) * h ** -0.5).to(bf).to(dev)
+            w1 = (torch.randn((el, 2 * m, h), generator=g) * h ** -0.5).to(bf).to(dev)
+            w2 = (torch.randn((el, h, m), generator=g) * m ** -0.5).to(bf).to(dev)
+            layers.append([w_r.requires_grad_(), w1.requires_grad_(), w2.requires_grad_()])
+        x0 = torch.randn((T, h), generator=g).to(bf).to(dev)
+        dy = torch.randn((T, h), generator=g).to(bf).to(dev)
+        ep = EPGroup()
+        rows_w = {"xp": h * 2, "preact": 4 * m, "act": 2 * m, "o": h * 2}
+
+        def run(stash):
+            for ws in layers:
+                for w in ws:
+                    w.grad = None
+            x = x0.clone().requires_grad_(True)
+            y = x
+            auxes = []
+            for li, (w_r, w1, w2) in enumerate(layers):
+                tag = "shared" if stash is not None else f"layer{li}"
+                y, aux = moe_forward_ep(y, w_r, w1, w2, cfg, ep, transport="p2p", sync_free=True,
+                                        tag=tag, stash=stash, layer_id=li)
+                auxes.append(aux)
+            torch.autograd.backward([y] + auxes, [dy] + [torch.ones_like(a) for a in auxes])
+            torch.cuda.synchronize()
+            return [y.detach().clone(), x.grad.clone()] + [w.grad.clone() for ws in layers
+                                                          for w in ws]
+
+        ref = run(None)
+        buf = PagedStashBuffer(256, rows_w, page_rows=64, device=dev)
+        got = run(buf)
+        buf.check()
+        check_ep_status()
+        st = buf.stats()
+        bad = [i for i, (a, b) in enumerate(zip(ref, got)) if not torch.equal(a, b)]
+        if st["free_pages"] != 256 or st["peak_pages_used"] == 0:
+            bad.append(f"pages {st}")
+        q.put((rank, "ok" if not bad else f"mismatch {bad}"))
+        dist.destroy_process_group()
+    except Exception as exc:  # pragma: no cover
+        import traceback
+
+        q.put((rank, traceback.format_exc() + repr(exc)))
+
+
+def test_ep_paged_stash_two_layers():
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import torch.multiprocessing as mp
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_stash_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=int(os.environ.get("MOE_TEST_TIMEOUT", "300"))) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
     for rank, msg in res:

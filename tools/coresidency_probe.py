@@ -38,6 +38,7 @@ def main():
     prob = torch.rand((T, K), device=dev)
     dprob = torch.zeros((T, K), device=dev)
     flags = torch.zeros((32,), dtype=torch.int32, device=dev)
+    epoch_dev = torch.zeros((1,), dtype=torch.int32, device=dev)
     fpeers = torch.tensor([flags.data_ptr()], dtype=torch.int64, device=dev)
     side = torch.cuda.Stream()
     _lib.call("moe_ep_prepare")
@@ -47,7 +48,8 @@ def main():
         for pname in ("none", "dispatch_push", "bwd_push"):
             epoch += 1
             status = torch.zeros((8,), dtype=torch.int32, device=dev)
-            wait = (flags, epoch, need, order, status)
+            _lib.call("moe_ep_epoch_bump", epoch_dev.data_ptr(), main_s.cuda_stream)
+            wait = (flags, epoch_dev, need, order, status)
             torch.cuda.synchronize()
             t0 = time.time()
             if gname == "fc1_fwd_ep":
@@ -65,7 +67,7 @@ def main():
                     _lib.call("moe_ep_combine_bwd_push_dest", x.data_ptr(), None,
                               peers.data_ptr(), T, K, h, topk.data_ptr(), inv.data_ptr(),
                               base.data_ptr(), E, prob.data_ptr(), None, 0, cs)
-                _lib.call("moe_ep_signal", fpeers.data_ptr(), 0, 0, epoch, cs)
+                _lib.call("moe_ep_signal", fpeers.data_ptr(), 0, 0, epoch_dev.data_ptr(), cs)
             torch.cuda.synchronize()
             st = status.tolist()
             print(f"{gname:14s} + {pname:14s}: {1e3 * (time.time() - t0):8.1f} ms  status {st}",

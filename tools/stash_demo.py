@@ -1,0 +1,123 @@
+"""Paged Stashing at scale: L stacked EP MoE layers (sync-free p2p), all forwards then all
+backwards, with (a) per-layer worst-case buffers and (b) one shared worst-case tmp set plus
+a paged stash of the actual rows. Reports device memory in use at the peak (after the last
+forward) and the fwd+bwd time of the L-layer stack, and checks (a) == (b) bit for bit.
+
+  torchrun --nproc-per-node 4 tools/stash_demo.py --config mixtral --layers 8
+"""
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from bench import CONFIGS  # noqa: E402
+from paper_2603_07685_b200.dispatcher import EPGroup, check_ep_status, moe_forward_ep  # noqa
+from paper_2603_07685_b200.dispatcher import ep_static_rows  # noqa: E402
+from paper_2603_07685_b200.layer import MoEConfig  # noqa: E402
+from paper_2603_07685_b200 import ops  # noqa: E402
+from paper_2603_07685_b200.stash import PagedStashBuffer  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="mixtral")
+    ap.add_argument("--layers", type=int, default=8)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--mode", default="both", choices=["both", "plain", "stash"])
+    a = ap.parse_args()
+    rank = int(os.environ["RANK"])
+    torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dist.init_process_group("nccl", device_id=dev)
+    n = dist.get_world_size()
+    c = CONFIGS[a.config]
+    E, K, h, m, T = c["E"], c["K"], c["h"], c["m"], c["T"]
+    cfg = MoEConfig(E, K, h, m, score=c["score"], aux_loss_coeff=1e-2)
+    bf = torch.bfloat16
+    el = E // n
+    g = torch.Generator(device=dev).manual_seed(7 + rank)
+    layers = []
+    for li in range(a.layers):
+        gw = torch.Generator(device=dev).manual_seed(100 + li)
+        w_r = (torch.randn((h, E), generator=gw, device=dev) * h ** -0.5).to(bf)
+        w1 = (torch.randn((el, 2 * m, h), generator=g, device=dev) * h ** -0.5).to(bf)
+        w2 = (torch.randn((el, h, m), generator=g, device=dev) * m ** -0.5).to(bf)
+        layers.append([w_r.requires_grad_(), w1.requires_grad_(), w2.requires_grad_()])
+    x0 = torch.randn((T, h), generator=g, device=dev).to(bf)
+    dy = torch.randn((T, h), generator=g, device=dev).to(bf)
+    ep = EPGroup()
+    align = ops.pick_align(n * T, K, E)
+    rows_cap = ep_static_rows(n, T, K, E, -1, align)
+    # pages for every layer's actual rows, 1.25x headroom for routing imbalance
+    page_rows = 64
+    plan_pages = int(1.25 * a.layers * -(-(T * K + el * align) // page_rows))
+    out_pages = int(1.25 * a.layers * -(-(T * K) // page_rows))
+
+    def run(stash, tag_of):
+        for ws in layers:
+            for w in ws:
+                w.grad = None
+        torch.cuda.synchronize()
+        x = x0.clone().requires_grad_(True)
+        y = x
+        auxes = []
+        t0 = time.time()
+        for li, (w_r, w1, w2) in enumerate(layers):
+            y, aux = moe_forward_ep(y, w_r, w1, w2, cfg, ep, transport="p2p", sync_free=True,
+                                    tag=tag_of(li), stash=stash, layer_id=li)
+            auxes.append(aux)
+        torch.cuda.synchronize()
+        free, total = torch.cuda.mem_get_info()
+        t1 = time.time()
+        torch.autograd.backward([y] + auxes, [dy] + [torch.ones_like(q) for q in auxes])
+        torch.cuda.synchronize()
+        t2 = time.time()
+        return (total - free), t1 - t0, t2 - t1, [y.detach(), x.grad] + [
+            w.grad for ws in layers for w in ws]
+
+    out = {"config": a.config, "layers": a.layers, "ep": n, "rows_cap_per_layer": rows_cap,
+           "page_rows": page_rows, "plan_pages": plan_pages, "out_pages": out_pages}
+    results = {}
+    for mode in (["plain", "stash"] if a.mode == "both" else [a.mode]):
+        stash = None
+        if mode == "stash":
+            stash = (PagedStashBuffer(plan_pages, {"xp": 2 * h, "preact": 4 * m, "act": 2 * m},
+                                      page_rows=page_rows, device=dev),
+                     PagedStashBuffer(out_pages, {"o": 2 * h}, page_rows=page_rows, device=dev))
+            tag_of = lambda li: "shared"  # noqa: E731
+        else:
+            tag_of = lambda li: f"layer{li}"  # noqa: E731
+        best = None
+        for _ in range(a.steps):
+            used, tf, tb, res = run(stash, tag_of)
+            best = (used, tf, tb) if best is None or tf + tb < best[1] + best[2] else best
+        check_ep_status()
+        entry = {"device_mem_in_use_at_peak_GB": round(best[0] / 1e9, 2),
+                 "fwd_ms": round(best[1] * 1e3, 2), "bwd_ms": round(best[2] * 1e3, 2)}
+        if stash is not None:
+            for sb in stash:
+                sb.check()
+            entry["peak_pages_used"] = [sb.stats()["peak_pages_used"] for sb in stash]
+            entry["stash_pool_GB"] = round(sum(p.numel() for sb in stash
+                                               for p in sb.pools.values()) / 1e9, 2)
+        results[mode] = [r.clone() for r in res]
+        out[mode] = entry
+        del res
+        torch.cuda.empty_cache()
+    if len(results) == 2:
+        out["bit_identical"] = all(torch.equal(p, q) for p, q in zip(results["plain"],
+                                                                      results["stash"]))
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
