@@ -207,6 +207,7 @@ def run_gpu(args, c) -> None:
     if E % n:
         raise SystemExit(f"E={E} not divisible by {n} ranks")
     cfg = MoEConfig(E, K, h, m, score=c["score"], aux_loss_coeff=AUX_COEFF,
+                    precision=args.precision,
                     capacity_factor=c.get("cf"), pad_to_capacity=c.get("pad", False),
                     shared_ffn_hidden=c.get("shared", 0))
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -475,7 +476,7 @@ def run_gpu(args, c) -> None:
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
-            "dtype": "bf16",
+            "dtype": "bf16" if args.precision == "bf16" else "mxfp8 fwd GEMMs, bf16 bwd",
             "data": "synthetic (seeded N(0,1) tokens, N(0,1/fan_in) random-init weights)",
             "config": {
                 "workload": f"{c['name']}: E={E}, top-{K}, h={h}, ffn={m}, {T} tokens/GPU, "
@@ -588,6 +589,9 @@ def main():
     ap.add_argument("--ep-transport", default="auto",
                     choices=["auto", "p2p", "p2p_overlap", "p2p_pull", "p2p_dedup", "nccl"],
                     help="EP exchange: fused NVLink peer-memory kernels (p2p) or NCCL a2a")
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "mxfp8"],
+                    help="forward expert GEMMs: bf16 (headline) or MXFP8 (block-scaled "
+                         "tcgen05; backward stays bf16)")
     ap.add_argument("--sync-free", action="store_true",
                     help="EP: plan the exchange on the device (no host read of the counts)")
     ap.add_argument("--graph", action="store_true",

@@ -246,6 +246,27 @@ int moe_gg_gemm_f32(const void* a, const void* b, int a_rows, int max_rows, int 
                     int num_experts, const int* block_expert, const int* num_m_blocks,
                     float* out, void* stream);
 
+/* ------------------------------------------------------------------ MXFP8
+ * replaces the reference's MXFP8 recipe (quant.py:62-64, :166-201; formats.py:16-139):
+ * 1x32 blocks along K, E8M0 scale 2^ceil(log2(amax/448)), E4M3 round-to-nearest-even codes.
+ * Scales are written in the tiled layout of the block-scaled GEMM (per 128-row tile and
+ * 128-wide K stage a 512-byte chunk; byte i*16 + c*4 + j = row c*32 + i, K-block j) and,
+ * optionally, plain [rows, K/32]. w1_m > 0: x is a stacked W1 [E, 2m, h] in the bf16
+ * engine's 128-row gate/up interleave and the output rows use the MXFP8 engine's 64-row
+ * interleave (row remap fused into the quantisation). */
+int moe_mxfp8_quantize(const void* x, long long ldx, int rows, int K, void* codes,
+                       long long ldc, void* sf_plain, void* sf_tiled, int w1_m, void* stream);
+/* block-scaled tcgen05 grouped GEMMs (kind::mxf8f6f4, UMMA 128x128x32): bf16 output, and
+ * fc1 + SwiGLU with the activation re-quantised to MXFP8 in the epilogue (fc2's A operand);
+ * w1q interleaves gate/up in 64-row blocks. */
+int moe_gg_mxfp8_gemm(const void* a, const void* sfa, int a_rows, int max_rows, int K, int N,
+                      const void* b, const void* sfb, int num_experts, const int* block_expert,
+                      const int* num_m_blocks, void* out, void* stream);
+int moe_gg_mxfp8_fc1(const void* xq, const void* sfx, int a_rows, int max_rows, int h, int m,
+                     const void* w1q, const void* sfw, int num_experts, const int* block_expert,
+                     const int* num_m_blocks, void* preact, void* act, void* act_q,
+                     void* act_sf, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,445 @@
+// Block-scaled MXFP8 grouped GEMM on the 5th-gen tensor cores (the
+// paper's Blackwell recipe, reference emulation quant.py:166-201).
+//
+//   D[rows, N] = sum_k  (A_codes * 2^(sfA - 127)) (B_codes * 2^(sfB - 127))^T,  fp32 in TMEM
+//
+// A: E4M3 codes [rows, K] (the padded expert-major plan), B: E4M3 codes [E * N, K] (K-major
+// expert weights), both with 1x32-block E8M0 scales in the tiled layout written by
+// moe_mxfp8_quantize / the fc1 epilogue. tcgen05.mma.kind::mxf8f6f4.block_scale, UMMA
+// 128 x 128 x 32, one CTA per SM (persistent), warp-specialised like the bf16 engine:
+//   warp 0: TMA (A, B tiles; scale chunks by 1-D bulk copies), warp 1: tcgen05.cp of the
+//   scale chunks smem -> TMEM, then 4 block-scaled MMAs per 128-wide K stage, warps 2-5:
+//   epilogue from a double-buffered TMEM accumulator.
+// TMEM: accumulators at columns [0, 256), scale factors at [256, 264) (SFA 4 columns, SFB 4
+// columns: row r's scale for the stage's K-block j is byte j of column r / 32, lane r % 32,
+// replicated over the 4 lane quarters by tcgen05.cp 32x128b.warpx4).
+//
+// Epilogues: EPI_BF16 (fc2: bf16 rows) and EPI_SWIGLU_Q (fc1: the MXFP8 W1 copy interleaves
+// gate/up in 64-row blocks, so every 128-wide tile holds matching gate and up columns; it
+// writes preact in the bf16 engine's 128-interleaved layout, act in bf16, AND act quantised
+// to MXFP8 -- each thread holds exactly one 32-element block of its row -- so fc2 reads
+// fp8 codes without a separate quantisation pass).
+#include <cudaTypedefs.h>
+#include <cuda_fp8.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace moe {
+namespace mx8 {
+
+constexpr int BM = 128, BN = 128, BK = 128;  // BK in fp8 elements (= bytes)
+constexpr int UMMA_K = 32;
+constexpr int STAGES = 6;
+constexpr int A_STAGE = BM * BK, B_STAGE = BN * BK, SF_CHUNK = 512;
+constexpr int STAGE = A_STAGE + B_STAGE + 2 * SF_CHUNK;
+constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+constexpr int TMEM_COLS = 512;
+constexpr int SF_COL = 256;
+constexpr int EPI_WARPS = 4;
+constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
+constexpr int BAND_M = 16;
+
+enum Epi : int { EPI_BF16 = 0, EPI_SWIGLU_Q = 1 };
+
+struct Params {
+  const int* num_m_blocks;
+  const int* block_expert;
+  int N, K;
+  const uint8_t* sfa;  // tiled, per (128-row tile, K stage) 512 B
+  const uint8_t* sfb;
+  void* out;           // EPI_BF16: bf16 [rows, ldo]; EPI_SWIGLU_Q: preact [rows, 2m]
+  long long ldo;
+  void* act;           // EPI_SWIGLU_Q: bf16 [rows, m] (nullable)
+  uint8_t* act_q;      // EPI_SWIGLU_Q: E4M3 codes [rows, m]
+  uint8_t* act_sf;     // EPI_SWIGLU_Q: tiled scales for K = m
+  int m;
+};
+
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// 32 rows x 16 B, no swizzle, rows contiguous (core matrices 8 x 16 B, SBO 128 B)
+__device__ __forceinline__ uint64_t sf_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((128u >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((128u >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  return d;  // layout type 0: SWIZZLE_NONE
+}
+__device__ __forceinline__ void tmem_cp_sf(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc)
+               : "memory");
+}
+// Block-scaled instruction descriptor: E4M3 x E4M3, E8M0 scales, K-major, M=128, N=128.
+__host__ __device__ constexpr uint32_t idesc_mx(int j) {
+  return (static_cast<uint32_t>(j) << 4)          // B scale-factor id (byte)
+         | (0u << 7) | (0u << 10)                 // A, B format: E4M3
+         | (static_cast<uint32_t>(BN >> 3) << 17)  // N / 8
+         | (1u << 23)                             // scale format: E8M0
+         | (static_cast<uint32_t>(BM >> 4) << 24)  // M / 16
+         | (static_cast<uint32_t>(j) << 29);      // A scale-factor id
+}
+__device__ __forceinline__ void umma_mx(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t sfa, uint32_t sfb,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%4], [%5], p;\n\t}"
+      ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(sfa), "r"(sfb), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+
+__device__ __forceinline__ int e8m0_exp(float amax) {
+  if (!(amax > 0.f)) return -127;
+  int q;
+  const float f = frexpf(amax, &q);
+  int e = q - 9 + (f > 0.875f ? 1 : 0);
+  return e < -127 ? -127 : (e > 127 ? 127 : e);
+}
+
+struct Tile {
+  int expert, m0, n0;
+};
+__device__ __forceinline__ void decode_tile(const Params& p, int t, int num_units, Tile& tl) {
+  const int nb_count = p.N / BN;
+  const int band = t / (BAND_M * nb_count);
+  const int rem = t - band * BAND_M * nb_count;
+  const int u0 = band * BAND_M;
+  const int rows = min(BAND_M, num_units - u0);
+  const int nb = rem / rows;
+  const int u = u0 + (rem - nb * rows);
+  tl.expert = __ldg(p.block_expert + u);
+  tl.m0 = u * BM;
+  tl.n0 = nb * BN;
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    mxfp8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                      const __grid_constant__ CUtensorMap tmap_b, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  auto sa = [&](int s) { return smem + s * STAGE; };
+  auto sb = [&](int s) { return smem + s * STAGE + A_STAGE; };
+  auto ssfa = [&](int s) { return smem + s * STAGE + A_STAGE + B_STAGE; };
+  auto ssfb = [&](int s) { return smem + s * STAGE + A_STAGE + B_STAGE + SF_CHUNK; };
+
+  const int warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], EPI_WARPS);
+    }
+    fence_mbar_init();
+    fence_async_shared();
+  }
+  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_units = *p.num_m_blocks;
+  const int num_tiles = num_units * (p.N / BN);
+  const int num_kb = p.K / BK;
+  const int kst = p.K / BK;  // K stages per 128-row scale tile
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        Tile tl;
+        decode_tile(p, t, num_units, tl);
+        const long long brow = (long long)tl.expert * p.N + tl.n0;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full_bar[s], STAGE);
+          tma_load_2d(sa(s), &tmap_a, &full_bar[s], kb * BK, tl.m0);
+          tma_load_2d(sb(s), &tmap_b, &full_bar[s], kb * BK, static_cast<int>(brow));
+          bulk_g2s(ssfa(s), p.sfa + ((long long)(tl.m0 / BM) * kst + kb) * SF_CHUNK, SF_CHUNK,
+                   &full_bar[s]);
+          bulk_g2s(ssfb(s), p.sfb + ((brow / BN) * kst + kb) * SF_CHUNK, SF_CHUNK,
+                   &full_bar[s]);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t acc_ph = 0;
+      const uint32_t t_sfa = tmem_base + SF_COL, t_sfb = tmem_base + SF_COL + 4;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          // scale chunks smem -> TMEM (ordered before the MMAs below: same tcgen05 pipe)
+          tmem_cp_sf(t_sfa, sf_desc(smem_u32(ssfa(s))));
+          tmem_cp_sf(t_sfb, sf_desc(smem_u32(ssfb(s))));
+          const uint32_t a_base = smem_u32(sa(s)), b_base = smem_u32(sb(s));
+#pragma unroll
+          for (int j = 0; j < BK / UMMA_K; ++j) {
+            umma_mx(d_tmem, make_sdesc_sw128(a_base + j * UMMA_K, 16, 1024),
+                    make_sdesc_sw128(b_base + j * UMMA_K, 16, 1024), idesc_mx(j), t_sfa, t_sfb,
+                    (kb | j) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[s]);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        umma_commit(&tfull_bar[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_ph ^= 1;
+        }
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int row_local = q * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      Tile tl;
+      decode_tile(p, t, num_units, tl);
+      const long long row = tl.m0 + row_local;
+      mbar_wait(&tfull_bar[acc], acc_ph);
+      tc_fence_after();
+      const uint32_t t_base = tmem_base + lane_off + acc * BN;
+      if constexpr (EPI == EPI_BF16) {
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo + tl.n0;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_base + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            int4 w;
+            w.x = pack_bf16x2(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1]));
+            w.y = pack_bf16x2(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3]));
+            w.z = pack_bf16x2(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5]));
+            w.w = pack_bf16x2(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
+            reinterpret_cast<int4*>(o + c * 32)[v] = w;
+          }
+        }
+      } else {
+        // tile columns [0, 64) = gate rows g0 + [0, 64), [64, 128) = the matching up rows
+        const int g0 = tl.n0 / 2;
+        __nv_bfloat16* pre = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo +
+                             (g0 >> 7) * 256 + (g0 & 127);
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          uint32_t g[32], u[32];
+          tmem_ld_32x32b_x32(t_base + c * 32, g);
+          tmem_ld_32x32b_x32(t_base + 64 + c * 32, u);
+          tmem_ld_wait();
+          uint32_t a2[16];
+          float amax = 0.f;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float g_0 = __uint_as_float(g[2 * i]), g_1 = __uint_as_float(g[2 * i + 1]);
+            const float u_0 = __uint_as_float(u[2 * i]), u_1 = __uint_as_float(u[2 * i + 1]);
+            a2[i] = pack_bf16x2(silu_f(g_0) * u_0, silu_f(g_1) * u_1);
+            const float2 ab = unpack_bf16x2(a2[i]);  // quantise the bf16 activation
+            amax = fmaxf(amax, fmaxf(fabsf(ab.x), fabsf(ab.y)));
+          }
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            int4 wg, wu;
+            uint32_t* pg = reinterpret_cast<uint32_t*>(&wg);
+            uint32_t* pu = reinterpret_cast<uint32_t*>(&wu);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int i = 8 * v + 2 * j;
+              pg[j] = pack_bf16x2(__uint_as_float(g[i]), __uint_as_float(g[i + 1]));
+              pu[j] = pack_bf16x2(__uint_as_float(u[i]), __uint_as_float(u[i + 1]));
+            }
+            reinterpret_cast<int4*>(pre + c * 32)[v] = wg;
+            reinterpret_cast<int4*>(pre + 128 + c * 32)[v] = wu;
+          }
+          const int col = g0 + c * 32;  // activation column = MX block col / 32
+          if (p.act) {
+            int4* ad = reinterpret_cast<int4*>(reinterpret_cast<__nv_bfloat16*>(p.act) +
+                                               row * p.m + col);
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+              ad[v] = make_int4(a2[4 * v], a2[4 * v + 1], a2[4 * v + 2], a2[4 * v + 3]);
+          }
+          const int e = e8m0_exp(amax);
+          const float inv = __int_as_float((127 - e) << 23);
+          uint32_t qv[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float2 x0 = unpack_bf16x2(a2[2 * k]), x1 = unpack_bf16x2(a2[2 * k + 1]);
+            const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
+                make_float2(x0.x * inv, x0.y * inv), __NV_SATFINITE, __NV_E4M3);
+            const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
+                make_float2(x1.x * inv, x1.y * inv), __NV_SATFINITE, __NV_E4M3);
+            qv[k] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+          }
+          int4* qd = reinterpret_cast<int4*>(p.act_q + row * p.m + col);
+          qd[0] = make_int4(qv[0], qv[1], qv[2], qv[3]);
+          qd[1] = make_int4(qv[4], qv[5], qv[6], qv[7]);
+          const int kb = col / 32, kblocks = p.m / 32;
+          const int rr = static_cast<int>(row & 127);
+          p.act_sf[((row >> 7) * (kblocks >> 2) + (kb >> 2)) * 512 + (rr & 31) * 16 +
+                   (rr >> 5) * 4 + (kb & 3)] = static_cast<uint8_t>(e + 127);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_ph ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+// 2-D u8 tensor [outer, inner], 128 x 128 boxes, 128B swizzle
+static int make_tmap_u8(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer) {
+  auto fn = encode_fn();
+  if (!fn) return kErrCuda;
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (inner & 15)) return kErrInvalidArg;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner};
+  cuuint32_t box[2] = {128, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? kOk : kErrCuda;
+}
+
+template <int EPI>
+static int launch(const void* a, int a_rows, const void* b, int num_experts, Params p,
+                  int max_m_blocks, cudaStream_t stream) {
+  CUtensorMap ta, tb;
+  int st;
+  if ((st = make_tmap_u8(&ta, a, p.K, a_rows))) return st;
+  if ((st = make_tmap_u8(&tb, b, p.K, (uint64_t)num_experts * p.N))) return st;
+  auto kern = mxfp8_gemm_kernel<EPI>;
+  static bool attr = false;
+  if (!attr) {
+    MOE_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int tiles = max_m_blocks * (p.N / BN);
+  if (tiles <= 0) return kOk;
+  kern<<<tiles < sms ? tiles : sms, NUM_THREADS, SMEM, stream>>>(ta, tb, p);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+}  // namespace mx8
+}  // namespace moe
+
+using namespace moe;
+using namespace moe::mx8;
+
+extern "C" {
+
+// out[rows, N] (bf16) = A x B_e^T with MXFP8 operands (fc2 forward: A = act codes [rows, m],
+// B = W2 codes [E, h, m]).
+int moe_gg_mxfp8_gemm(const void* a, const void* sfa, int a_rows, int max_rows, int K, int N,
+                      const void* b, const void* sfb, int num_experts, const int* block_expert,
+                      const int* num_m_blocks, void* out, void* stream) {
+  if (K % BK || N % BN || max_rows % BM || a_rows > max_rows) return kErrInvalidArg;
+  Params p{};
+  p.num_m_blocks = num_m_blocks;
+  p.block_expert = block_expert;
+  p.N = N;
+  p.K = K;
+  p.sfa = static_cast<const uint8_t*>(sfa);
+  p.sfb = static_cast<const uint8_t*>(sfb);
+  p.out = out;
+  p.ldo = N;
+  return launch<EPI_BF16>(a, a_rows, b, num_experts, p, max_rows / BM,
+                          static_cast<cudaStream_t>(stream));
+}
+
+// fc1 forward + SwiGLU with MXFP8 operands: B = W1 codes [E, 2m, h] interleaved gate/up in
+// 64-row blocks (moe_mxfp8_interleave_w1). Writes preact (bf16, the bf16 engine's
+// 128-interleaved layout), act (bf16, nullable) and act as MXFP8 (codes + tiled scales).
+int moe_gg_mxfp8_fc1(const void* xq, const void* sfx, int a_rows, int max_rows, int h, int m,
+                     const void* w1q, const void* sfw, int num_experts, const int* block_expert,
+                     const int* num_m_blocks, void* preact, void* act, void* act_q,
+                     void* act_sf, void* stream) {
+  if (h % BK || m % 128 || max_rows % BM || a_rows > max_rows || !act_q || !act_sf)
+    return kErrInvalidArg;
+  Params p{};
+  p.num_m_blocks = num_m_blocks;
+  p.block_expert = block_expert;
+  p.N = 2 * m;
+  p.K = h;
+  p.sfa = static_cast<const uint8_t*>(sfx);
+  p.sfb = static_cast<const uint8_t*>(sfw);
+  p.out = preact;
+  p.ldo = 2 * m;
+  p.act = act;
+  p.act_q = static_cast<uint8_t*>(act_q);
+  p.act_sf = static_cast<uint8_t*>(act_sf);
+  p.m = m;
+  return launch<EPI_SWIGLU_Q>(xq, a_rows, w1q, num_experts, p, max_rows / BM,
+                              static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

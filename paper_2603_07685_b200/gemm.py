@@ -188,3 +188,81 @@ def wgrad_f32(a, b, offsets, num_groups, max_rows=None, out=None):
     _lib.call("moe_gg_wgrad_f32", a.data_ptr(), b.data_ptr(), rows, M, N, num_groups,
               offsets.data_ptr(), out.data_ptr(), _stream())
     return out
+
+
+# ---------------------------------------------------------------- MXFP8 (csrc/mxfp8.cu,
+# csrc/grouped_gemm_mxfp8.cu): 1x32 E8M0-scaled E4M3 operands, block-scaled tcgen05 MMA.
+
+def mxfp8_quantize(x: torch.Tensor, rows_pad: int | None = None, plain: bool = False,
+                   w1_m: int = 0):
+    """x bf16 [rows, K] -> (codes uint8 [rows_pad, K], tiled scales uint8, plain scales
+    uint8 [rows, K/32] or None). Rows past `rows` in the tiled layout read scale 0.
+    w1_m: x is a stacked bf16-engine W1 (rows = E * 2m); emit the 64-row interleave."""
+    rows, k = x.shape
+    rp = rows_pad if rows_pad is not None else -(-rows // 128) * 128
+    if rp > rows:
+        codes = torch.zeros((rp, k), dtype=torch.uint8, device=x.device)
+        sf_t = torch.zeros((rp * k // 32,), dtype=torch.uint8, device=x.device)
+    else:
+        codes = torch.empty((rp, k), dtype=torch.uint8, device=x.device)
+        sf_t = torch.empty((rp * k // 32,), dtype=torch.uint8, device=x.device)
+    sf_p = torch.empty((rows, k // 32), dtype=torch.uint8, device=x.device) if plain else None
+    _lib.call("moe_mxfp8_quantize", x.data_ptr(), x.stride(0), rows, k, codes.data_ptr(), k,
+              _ptr(sf_p), sf_t.data_ptr(), int(w1_m), _stream())
+    return codes, sf_t, sf_p
+
+
+def mxfp8_quantize_w1(w1: torch.Tensor):
+    """bf16-engine W1 [E, 2m, h] (128-row gate/up interleave) -> MXFP8 codes/scales in the
+    MXFP8 engine's 64-row interleave (one fused pass)."""
+    e, m2, h = w1.shape
+    codes, sf, _ = mxfp8_quantize(w1.reshape(e * m2, h), w1_m=m2 // 2)
+    return codes, sf
+
+
+def interleave_gate_up_mx(gate: torch.Tensor, up: torch.Tensor) -> torch.Tensor:
+    """[E, m, h] gate / up -> [E, 2m, h] with 64-row gate/up blocks (the MXFP8 fc1 tile of
+    128 columns then holds matching gate and up rows)."""
+    e, m, h = gate.shape
+    g = gate.reshape(e, m // 64, 64, h)
+    u = up.reshape(e, m // 64, 64, h)
+    return torch.stack([g, u], dim=2).reshape(e, 2 * m, h).contiguous()
+
+
+def mxfp8_quantize_weight(w: torch.Tensor):
+    """Stacked K-major weights [E, N, K] -> (codes [E*N, K], tiled scales)."""
+    e, n, k = w.shape
+    codes, sf, _ = mxfp8_quantize(w.reshape(e * n, k))
+    return codes, sf
+
+
+def mxfp8_gemm(aq, sfa, bq, sfb, num_experts, block_expert, num_m_blocks, N,
+               out=None, max_rows=None):
+    """out[rows, N] bf16 = dequant(aq) @ dequant(bq_e)^T per 128-row block's expert."""
+    a_rows, k = aq.shape
+    rows = a_rows if max_rows is None else max_rows
+    if out is None:
+        out = torch.empty((rows, N), dtype=torch.bfloat16, device=aq.device)
+    _lib.call("moe_gg_mxfp8_gemm", aq.data_ptr(), sfa.data_ptr(), a_rows, rows, k, N,
+              bq.data_ptr(), sfb.data_ptr(), num_experts, block_expert.data_ptr(),
+              num_m_blocks.data_ptr(), out.data_ptr(), _stream())
+    return out
+
+
+def mxfp8_fc1(xq, sfx, w1q, sfw, num_experts, block_expert, num_m_blocks, m, max_rows=None,
+              want_act=True):
+    """fc1 + SwiGLU on MXFP8 operands (w1q from interleave_gate_up_mx). Returns (preact bf16
+    [rows, 2m] in the bf16 engine's layout, act bf16 [rows, m] or None, act codes [rows, m],
+    act tiled scales) -- the last two are fc2's MXFP8 A operand."""
+    a_rows, h = xq.shape
+    rows = a_rows if max_rows is None else max_rows
+    dev = xq.device
+    preact = torch.empty((rows, 2 * m), dtype=torch.bfloat16, device=dev)
+    act = torch.empty((rows, m), dtype=torch.bfloat16, device=dev) if want_act else None
+    act_q = torch.empty((rows, m), dtype=torch.uint8, device=dev)
+    act_sf = torch.zeros((rows * m // 32,), dtype=torch.uint8, device=dev)
+    _lib.call("moe_gg_mxfp8_fc1", xq.data_ptr(), sfx.data_ptr(), a_rows, rows, h, m,
+              w1q.data_ptr(), sfw.data_ptr(), num_experts, block_expert.data_ptr(),
+              num_m_blocks.data_ptr(), preact.data_ptr(), _ptr(act), act_q.data_ptr(),
+              act_sf.data_ptr(), _stream())
+    return preact, act, act_q, act_sf

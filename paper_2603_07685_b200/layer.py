@@ -34,6 +34,10 @@ class MoEConfig:
     pad_to_capacity: bool = False     # --moe-pad-expert-input-to-capacity
     mem_efficient: bool = False       # combine_mem_efficient (prob folded into act)
     shared_ffn_hidden: int = 0        # DeepSeek shared expert width (0 = none)
+    # forward expert GEMMs: "bf16", or "mxfp8" (the paper's Blackwell recipe, 1x32 E8M0
+    # blocks, quant.py:62-64; block-scaled tcgen05 MMA, activations re-quantised in fc1's
+    # epilogue). The backward GEMMs stay bf16.
+    precision: str = "bf16"
 
     def capacity(self, num_tokens: int) -> int:
         """expert_capacity() routing.py:250-251 (k = top_k since every token selects K)."""
@@ -55,9 +59,12 @@ class _MoEFunction(torch.autograd.Function):
                               align=ops.pick_align(t, cfg.top_k, e))
         xp = ops.permute_gather(x, plan)
         row_prob = plan.row_prob if cfg.mem_efficient else None
-        preact, act = gemm.fc1_fwd(xp, w1, plan.block_expert, plan.num_m_blocks, row_prob,
-                                   pair=plan.pair)
-        o = gemm.fc2_fwd(act, w2, plan.block_expert, plan.num_m_blocks, pair=plan.pair)
+        if cfg.precision == "mxfp8":
+            preact, act, o = _mxfp8_experts(xp, w1, w2, plan, e)
+        else:
+            preact, act = gemm.fc1_fwd(xp, w1, plan.block_expert, plan.num_m_blocks, row_prob,
+                                       pair=plan.pair)
+            o = gemm.fc2_fwd(act, w2, plan.block_expert, plan.num_m_blocks, pair=plan.pair)
         shared = shared_expert_forward(x, w1s, w2s) if w1s is not None else None
         y = ops.combine(o, plan, None if cfg.mem_efficient else r.topk_prob,
                         resid=x if cap >= 0 else None,
@@ -100,6 +107,21 @@ class _MoEFunction(torch.autograd.Function):
         return (dx, dw_r.to(torch.bfloat16), dw1, dw2, None, dw1s, dw2s, None)
 
 
+def _mxfp8_experts(xp, w1, w2, plan, e):
+    """MXFP8 forward experts: quantise the permuted rows and the (current) weights, fc1 +
+    SwiGLU with the activation re-quantised in its epilogue, fc2 -- all block-scaled tcgen05.
+    Returns the bf16 preact / act the bf16 backward needs and the expert outputs."""
+    m = w2.shape[2]
+    h = xp.shape[1]
+    xq, xsf, _ = gemm.mxfp8_quantize(xp)
+    w1q, w1sf = gemm.mxfp8_quantize_w1(w1)
+    w2q, w2sf = gemm.mxfp8_quantize_weight(w2)
+    preact, act, aq, asf = gemm.mxfp8_fc1(xq, xsf, w1q, w1sf, e, plan.block_expert,
+                                          plan.num_m_blocks, m)
+    o = gemm.mxfp8_gemm(aq, asf, w2q, w2sf, e, plan.block_expert, plan.num_m_blocks, h)
+    return preact, act, o
+
+
 def shared_expert_forward(x, w1s, w2s):
     """DeepSeek shared expert (latent_moe_forward's shared term, routing.py:276-278): a dense
     SwiGLU MLP on every token, run as a 1-group grouped GEMM. Returns saved state + output."""
@@ -127,6 +149,10 @@ def shared_expert_backward(x, dy, w1s, w2s, saved):
 def moe_forward(x, w_r, w1, w2, cfg: MoEConfig, selection_bias=None, w1_shared=None,
                 w2_shared=None):
     """Functional MoE layer: returns (y [T,h] bf16, aux [] fp32). Differentiable."""
+    if cfg.precision not in ("bf16", "mxfp8"):
+        raise ValueError(f"unknown precision {cfg.precision!r}")
+    if cfg.precision == "mxfp8" and cfg.mem_efficient:
+        raise ValueError("mxfp8 experts use the standard combine")
     return _MoEFunction.apply(x, w_r, w1, w2, selection_bias, w1_shared, w2_shared, cfg)
 
 

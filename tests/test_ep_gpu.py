@@ -42,6 +42,27 @@ def _port():
     return p
 
 
+def _exit_worker(q):
+    """Flush the result queue and leave without NCCL / symmetric-memory teardown: a
+    teardown that blocks would keep the GPUs busy for the next test."""
+    try:
+        torch.cuda.synchronize()
+    except Exception:  # pragma: no cover
+        pass
+    q.close()
+    q.join_thread()
+    os._exit(0)
+
+
+def _join_all(procs):
+    for p in procs:
+        p.join(timeout=30)
+    for p in procs:
+        if p.is_alive():
+            p.kill()
+            p.join(timeout=10)
+
+
 def _worker(rank, world, port, case, q, transport):
     try:
         import torch.distributed as dist
@@ -168,11 +189,11 @@ def _worker(rank, world, port, case, q, transport):
         if aux_err > 1e-4:
             bad["aux"] = aux_err
         q.put((rank, "ok" if not bad else f"errors {bad}"))
-        dist.destroy_process_group()
     except Exception as exc:  # pragma: no cover
         import traceback
 
         q.put((rank, traceback.format_exc() + repr(exc)))
+    _exit_worker(q)
 
 
 @pytest.mark.parametrize("transport", ["p2p", "p2p_sync_free", "p2p_graph", "p2p_overlap",
@@ -202,9 +223,11 @@ def _run(case, transport):
              for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=int(os.environ.get("MOE_TEST_TIMEOUT", "300"))) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=60)
+    try:
+        res = [q.get(timeout=int(os.environ.get("MOE_TEST_TIMEOUT", "300")))
+               for _ in range(world)]
+    finally:
+        _join_all(procs)
     for rank, msg in res:
         assert msg == "ok", f"rank {rank}: {msg}"
 
@@ -267,11 +290,11 @@ def _stash_worker(rank, world, port, q):
         if st["free_pages"] != 256 or st["peak_pages_used"] == 0:
             bad.append(f"pages {st}")
         q.put((rank, "ok" if not bad else f"mismatch {bad}"))
-        dist.destroy_process_group()
     except Exception as exc:  # pragma: no cover
         import traceback
 
         q.put((rank, traceback.format_exc() + repr(exc)))
+    _exit_worker(q)
 
 
 def test_ep_paged_stash_two_layers():
@@ -286,8 +309,10 @@ def test_ep_paged_stash_two_layers():
     procs = [ctx.Process(target=_stash_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=int(os.environ.get("MOE_TEST_TIMEOUT", "300"))) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=60)
+    try:
+        res = [q.get(timeout=int(os.environ.get("MOE_TEST_TIMEOUT", "300")))
+               for _ in range(world)]
+    finally:
+        _join_all(procs)
     for rank, msg in res:
         assert msg == "ok", f"rank {rank}: {msg}"

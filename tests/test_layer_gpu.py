@@ -59,7 +59,7 @@ def f64(t):
     return t.detach().double().cpu().numpy()
 
 
-def run_case(cfg: MoEConfig, T, seed, dev):
+def run_case(cfg: MoEConfig, T, seed, dev, y_tol=Y_TOL, g_tol=G_TOL):
     x, w_r, gate, up, w2, dy, shared = make(cfg, T, seed, dev)
     xd = x.to(dev).requires_grad_(True)
     w_rd = w_r.to(dev).requires_grad_(True)
@@ -111,20 +111,20 @@ def run_case(cfg: MoEConfig, T, seed, dev):
                                     top_k=1, coeff=0.0)
         dx_ref = dx_ref + rs["dx"]
         dgs, dus = gemm.split_gate_up(w1s.grad)
-        assert relfro(f64(dgs[0]), rs["dgate"][0]) < G_TOL
-        assert relfro(f64(dus[0]), rs["dw1"][0]) < G_TOL
-        assert relfro(f64(w2s.grad[0]), rs["dw2"][0]) < G_TOL
-    assert relfro(f64(y), y_ref) < Y_TOL
+        assert relfro(f64(dgs[0]), rs["dgate"][0]) < g_tol
+        assert relfro(f64(dus[0]), rs["dw1"][0]) < g_tol
+        assert relfro(f64(w2s.grad[0]), rs["dw2"][0]) < g_tol
+    assert relfro(f64(y), y_ref) < y_tol
     assert abs(float(aux) - ref["aux"]) <= 1e-4 * max(abs(ref["aux"]), 1e-6)
-    assert relfro(f64(xd.grad), dx_ref) < G_TOL
-    assert relfro(f64(w_rd.grad), ref["dw_r"]) < G_TOL
+    assert relfro(f64(xd.grad), dx_ref) < g_tol
+    assert relfro(f64(w_rd.grad), ref["dw_r"]) < g_tol
     dg, du = gemm.split_gate_up(w1d.grad)
     for e in range(cfg.num_experts):
         if dec.effective_counts()[e] == 0:
             continue
-        assert relfro(f64(dg[e]), ref["dgate"][e]) < G_TOL, e
-        assert relfro(f64(du[e]), ref["dw1"][e]) < G_TOL, e
-        assert relfro(f64(w2d.grad[e]), ref["dw2"][e]) < G_TOL, e
+        assert relfro(f64(dg[e]), ref["dgate"][e]) < g_tol, e
+        assert relfro(f64(du[e]), ref["dw1"][e]) < g_tol, e
+        assert relfro(f64(w2d.grad[e]), ref["dw2"][e]) < g_tol, e
 
 
 def test_softmax_standard_dropless(dev):
@@ -155,3 +155,13 @@ def test_shared_expert_sigmoid(dev):
 
 def test_experts_128_top8(dev):
     run_case(MoEConfig(128, 8, 256, 256, aux_loss_coeff=1e-2), 1024, 6, dev)
+
+
+def test_mxfp8_forward_experts(dev):
+    """MXFP8 forward expert GEMMs (block-scaled tcgen05, fused activation re-quantisation),
+    bf16 backward. Routing and maps stay bit-exact; values carry the MXFP8 quantisation error
+    (E4M3: 3 mantissa bits; measured y relFro 0.066 on this case: x, W1, act and W2 are each
+    quantised), so the tolerance is the recipe's (0.1 / 0.12), not bf16's.
+    GEMM-level parity against the dequantised oracle is tests/test_mxfp8.py."""
+    cfg = MoEConfig(8, 2, 256, 256, score="softmax", aux_loss_coeff=1e-2, precision="mxfp8")
+    run_case(cfg, 512, 21, dev, y_tol=0.1, g_tol=0.12)

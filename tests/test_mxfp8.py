@@ -1,0 +1,125 @@
+"""MXFP8: the oracle (oracle/mxfp8_ref.py) against codes and scales
+produced by the reference quantizer (tests/golden/mxfp8_golden.npz, quant.py:166-201); the
+device quantizer bit-exact against both; the block-scaled tcgen05 grouped GEMMs against the
+reference's dequantize-then-multiply GEMM (fp64) on the same codes."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import mxfp8_ref as M
+
+GOLD = np.load(Path(__file__).resolve().parent / "golden" / "mxfp8_golden.npz")
+
+
+def test_oracle_matches_reference_golden():
+    codes, scales = M.quantize_mxfp8(GOLD["x"].astype(np.float64))
+    assert np.array_equal(codes, GOLD["codes"])
+    assert np.array_equal(scales, GOLD["scales"])
+    assert np.array_equal(M.dequantize_mxfp8(codes, scales), GOLD["dequant"])
+
+
+def test_tiled_scale_layout():
+    s = np.arange(256 * 8, dtype=np.int64).reshape(256, 8).astype(np.uint8)
+    t = M.tile_scales(s, 256)
+    for row, kb in [(0, 0), (5, 3), (37, 1), (127, 7), (128, 0), (200, 6)]:
+        tile, rr = divmod(row, 128)
+        off = (tile * 2 + kb // 4) * 512 + (rr % 32) * 16 + (rr // 32) * 4 + kb % 4
+        assert t[off] == s[row, kb]
+
+
+def _bf16(a):
+    return torch.from_numpy(np.asarray(a, dtype=np.float32)).to(torch.bfloat16)
+
+
+@pytest.mark.gpu
+def test_device_quantizer_bit_exact():
+    from paper_2603_07685_b200 import gemm
+
+    dev = torch.device("cuda", 0)
+    x = torch.from_numpy(GOLD["x"]).to(torch.bfloat16).to(dev)
+    codes, sf_t, sf_p = gemm.mxfp8_quantize(x, plain=True)
+    r = x.shape[0]
+    assert np.array_equal(codes[:r].cpu().numpy(), GOLD["codes"])
+    assert np.array_equal(sf_p.cpu().numpy(), GOLD["scales"])
+    assert np.array_equal(sf_t.cpu().numpy(), M.tile_scales(GOLD["scales"], codes.shape[0]))
+
+
+def _plan(rows_per_expert, dev):
+    be = np.concatenate([np.full(r // 128, e) for e, r in enumerate(rows_per_expert)])
+    return (torch.tensor(be, dtype=torch.int32, device=dev),
+            torch.tensor([len(be)], dtype=torch.int32, device=dev), int(sum(rows_per_expert)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("E,K,N", [(2, 256, 256), (3, 512, 384)])
+def test_mxfp8_grouped_gemm_matches_dequant_gemm(E, K, N):
+    from paper_2603_07685_b200 import gemm
+
+    dev = torch.device("cuda", 0)
+    g = torch.Generator().manual_seed(E * 7 + K)
+    rows_e = [256, 128, 384][:E]
+    be, nmb, rows = _plan(rows_e, dev)
+    a = (torch.randn((rows, K), generator=g) * 3).to(torch.bfloat16)
+    a[100:128] = 0  # padding-like rows
+    w = (torch.randn((E, N, K), generator=g) * 0.05).to(torch.bfloat16)
+    aq, asf, asp = gemm.mxfp8_quantize(a.to(dev), plain=True)
+    wq, wsf, wsp = gemm.mxfp8_quantize(w.reshape(E * N, K).to(dev), plain=True)
+    out = gemm.mxfp8_gemm(aq, asf, wq, wsf, E, be, nmb, N).float().cpu().numpy()
+    ad = M.dequantize_mxfp8(aq.cpu().numpy()[:rows], asp.cpu().numpy())
+    wd = M.dequantize_mxfp8(wq.cpu().numpy(), wsp.cpu().numpy()).reshape(E, N, K)
+    ref = np.concatenate([ad[sum(rows_e[:e]):sum(rows_e[:e + 1])] @ wd[e].T
+                          for e in range(E)])
+    err = np.linalg.norm(out - ref) / np.linalg.norm(ref)
+    assert err < 4e-3, err
+
+
+@pytest.mark.gpu
+def test_mxfp8_fc1_swiglu_and_fused_act_quantisation():
+    from paper_2603_07685_b200 import gemm
+
+    dev = torch.device("cuda", 0)
+    g = torch.Generator().manual_seed(11)
+    E, h, m = 2, 256, 256
+    rows_e = [128, 256]
+    be, nmb, rows = _plan(rows_e, dev)
+    x = torch.randn((rows, h), generator=g).to(torch.bfloat16)
+    gate = (torch.randn((E, m, h), generator=g) * h ** -0.5).to(torch.bfloat16)
+    up = (torch.randn((E, m, h), generator=g) * h ** -0.5).to(torch.bfloat16)
+    xq, xsf, xsp = gemm.mxfp8_quantize(x.to(dev), plain=True)
+    w1 = gemm.interleave_gate_up_mx(gate.to(dev), up.to(dev))
+    wq, wsf, wsp = gemm.mxfp8_quantize(w1.reshape(E * 2 * m, h), plain=True)
+    preact, act, act_q, act_sf = gemm.mxfp8_fc1(xq, xsf, wq, wsf, E, be, nmb, m)
+    torch.cuda.synchronize()
+    xd = M.dequantize_mxfp8(xq.cpu().numpy()[:rows], xsp.cpu().numpy())
+    wd = M.dequantize_mxfp8(wq.cpu().numpy(), wsp.cpu().numpy()).reshape(E, 2 * m, h)
+    gd = wd.reshape(E, m // 64, 2, 64, h)[:, :, 0].reshape(E, m, h)
+    ud = wd.reshape(E, m // 64, 2, 64, h)[:, :, 1].reshape(E, m, h)
+    off = np.cumsum([0] + rows_e)
+    zg = np.concatenate([xd[off[e]:off[e + 1]] @ gd[e].T for e in range(E)])
+    zu = np.concatenate([xd[off[e]:off[e + 1]] @ ud[e].T for e in range(E)])
+    pg, pu = gemm.deinterleave_cols(preact)
+    rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)  # noqa: E731
+    assert rel(pg.float().cpu().numpy(), zg) < 4e-3
+    assert rel(pu.float().cpu().numpy(), zu) < 4e-3
+    a_ref = zg / (1 + np.exp(-zg)) * zu
+    assert rel(act.float().cpu().numpy(), a_ref) < 1e-2
+    # the fused quantisation equals quantize(act) of the kernel's own bf16 activation
+    codes, scales = M.quantize_mxfp8(act.float().cpu().numpy().astype(np.float64))
+    assert np.array_equal(act_q.cpu().numpy(), codes)
+    assert np.array_equal(act_sf.cpu().numpy(), M.tile_scales(scales, rows))
+
+
+@pytest.mark.gpu
+def test_w1_remap_quantisation_equals_interleave_then_quantise():
+    from paper_2603_07685_b200 import gemm
+
+    dev = torch.device("cuda", 0)
+    g = torch.Generator().manual_seed(2)
+    E, m, h = 2, 256, 256
+    gate = torch.randn((E, m, h), generator=g).to(torch.bfloat16).to(dev)
+    up = torch.randn((E, m, h), generator=g).to(torch.bfloat16).to(dev)
+    a = gemm.mxfp8_quantize_w1(gemm.interleave_gate_up(gate, up))
+    b = gemm.mxfp8_quantize_weight(gemm.interleave_gate_up_mx(gate, up))
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])

@@ -72,6 +72,10 @@ def main():
             y, aux = moe_forward_ep(y, w_r, w1, w2, cfg, ep, transport="p2p", sync_free=True,
                                     tag=tag_of(li), stash=stash, layer_id=li)
             auxes.append(aux)
+            if stash is not None and os.environ.get("STASH_DEBUG") and rank == 0:
+                print("layer", li, [sb.stats() for sb in stash],
+                      [sb.records[sb._slot[2 * li + k]][0].item() for k, sb in
+                       enumerate(stash)], file=sys.stderr, flush=True)
         torch.cuda.synchronize()
         free, total = torch.cuda.mem_get_info()
         t1 = time.time()
