@@ -31,10 +31,19 @@ namespace mx8 {
 
 constexpr int BM = 128, BN = 128, BK = 128;  // BK in fp8 elements (= bytes)
 constexpr int UMMA_K = 32;
-constexpr int STAGES = 6;
-constexpr int A_STAGE = BM * BK, B_STAGE = BN * BK, SF_CHUNK = 512;
-constexpr int STAGE = A_STAGE + B_STAGE + 2 * SF_CHUNK;
-constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+constexpr int A_STAGE = BM * BK, SF_CHUNK = 512;
+// CG = 1: UMMA 128 x 128 per CTA. CG = 2: CTA pair, UMMA 256 x 128 (cta_group::2): each CTA
+// stages its 128 rows of A and half (64 rows) of the B tile, and its own copy of both scale
+// chunks; per-SM shared-memory operand traffic drops from 8 KB to 6 KB per 1 MFLOP and the
+// ring holds 8 stages instead of 6 (more time to hide TMA latency at fp8 MMA rates).
+template <int CG>
+struct Cfg {
+  static constexpr int B_ROWS = BN / CG;
+  static constexpr int B_STAGE = B_ROWS * BK;
+  static constexpr int STAGE = A_STAGE + B_STAGE + 2 * SF_CHUNK;
+  static constexpr int STAGES = CG == 1 ? 6 : 8;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+};
 constexpr int TMEM_COLS = 512;
 constexpr int SF_COL = 256;
 constexpr int EPI_WARPS = 4;
@@ -57,13 +66,6 @@ struct Params {
   int m;
 };
 
-__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-      ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
 // 32 rows x 16 B, no swizzle, rows contiguous (core matrices 8 x 16 B, SBO 128 B)
 __device__ __forceinline__ uint64_t sf_desc(uint32_t saddr) {
   uint64_t d = 0;
@@ -78,13 +80,59 @@ __device__ __forceinline__ void tmem_cp_sf(uint32_t taddr, uint64_t sdesc) {
                : "memory");
 }
 // Block-scaled instruction descriptor: E4M3 x E4M3, E8M0 scales, K-major, M=128, N=128.
-__host__ __device__ constexpr uint32_t idesc_mx(int j) {
+__host__ __device__ constexpr uint32_t idesc_mx(int j, int M) {
   return (static_cast<uint32_t>(j) << 4)          // B scale-factor id (byte)
          | (0u << 7) | (0u << 10)                 // A, B format: E4M3
          | (static_cast<uint32_t>(BN >> 3) << 17)  // N / 8
          | (1u << 23)                             // scale format: E8M0
-         | (static_cast<uint32_t>(BM >> 4) << 24)  // M / 16
+         | (static_cast<uint32_t>(M >> 4) << 24)   // M / 16
          | (static_cast<uint32_t>(j) << 29);      // A scale-factor id
+}
+__device__ __forceinline__ void umma_mx_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t sfa, uint32_t sfb,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%4], [%5], p;\n\t}"
+      ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(sfa), "r"(sfb), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_cp_sf_pair(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const void* tmap,
+                                                 uint64_t* bar, int x, int y) {
+  const uint32_t bar_leader = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_leader), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], m;\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, 0;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
 }
 __device__ __forceinline__ void umma_mx(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                         uint32_t idesc, uint32_t sfa, uint32_t sfb,
@@ -110,7 +158,9 @@ __device__ __forceinline__ int e8m0_exp(float amax) {
 struct Tile {
   int expert, m0, n0;
 };
-__device__ __forceinline__ void decode_tile(const Params& p, int t, int num_units, Tile& tl) {
+template <int CG>
+__device__ __forceinline__ void decode_tile(const Params& p, int t, int num_units, int rank,
+                                            Tile& tl) {
   const int nb_count = p.N / BN;
   const int band = t / (BAND_M * nb_count);
   const int rem = t - band * BAND_M * nb_count;
@@ -118,72 +168,100 @@ __device__ __forceinline__ void decode_tile(const Params& p, int t, int num_unit
   const int rows = min(BAND_M, num_units - u0);
   const int nb = rem / rows;
   const int u = u0 + (rem - nb * rows);
-  tl.expert = __ldg(p.block_expert + u);
-  tl.m0 = u * BM;
+  tl.expert = __ldg(p.block_expert + u * CG);
+  tl.m0 = u * BM * CG + rank * BM;
   tl.n0 = nb * BN;
 }
 
-template <int EPI>
+template <int EPI, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     mxfp8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
-                      const __grid_constant__ CUtensorMap tmap_b, const Params p) {
+                      const __grid_constant__ CUtensorMap tmap_b,
+                      const __grid_constant__ CUtensorMap tmap_sfa,
+                      const __grid_constant__ CUtensorMap tmap_sfb, const Params p) {
+  using C = Cfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
-  uint64_t* empty_bar = full_bar + STAGES;
-  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty_bar = full_bar + C::STAGES;
+  uint64_t* tfull_bar = empty_bar + C::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-  auto sa = [&](int s) { return smem + s * STAGE; };
-  auto sb = [&](int s) { return smem + s * STAGE + A_STAGE; };
-  auto ssfa = [&](int s) { return smem + s * STAGE + A_STAGE + B_STAGE; };
-  auto ssfb = [&](int s) { return smem + s * STAGE + A_STAGE + B_STAGE + SF_CHUNK; };
+  auto sa = [&](int s) { return smem + s * C::STAGE; };
+  auto sb = [&](int s) { return smem + s * C::STAGE + A_STAGE; };
+  auto ssfa = [&](int s) { return smem + s * C::STAGE + A_STAGE + C::B_STAGE; };
+  auto ssfb = [&](int s) { return smem + s * C::STAGE + A_STAGE + C::B_STAGE + SF_CHUNK; };
 
   const int warp = warp_id(), lane = lane_id();
+  const int rank = CG == 2 ? static_cast<int>(cluster_rank()) : 0;
+  const bool leader = rank == 0;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
-    for (int s = 0; s < STAGES; ++s) {
+    tma_prefetch_desc(&tmap_sfa);
+    tma_prefetch_desc(&tmap_sfb);
+    for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], EPI_WARPS);
+      mbar_init(&tempty_bar[s], EPI_WARPS * CG);
     }
     fence_mbar_init();
     fence_async_shared();
   }
-  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (CG == 1) {
+      tmem_alloc<TMEM_COLS>(tmem_slot);
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) {
+    cluster_sync_all();
+  } else {
+    __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int num_units = *p.num_m_blocks;
+  const int num_units = *p.num_m_blocks / CG;
   const int num_tiles = num_units * (p.N / BN);
   const int num_kb = p.K / BK;
   const int kst = p.K / BK;  // K stages per 128-row scale tile
+  const int first = blockIdx.x / CG, stride = gridDim.x / CG;
 
   if (warp == 0) {
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = first; t < num_tiles; t += stride) {
         Tile tl;
-        decode_tile(p, t, num_units, tl);
-        const long long brow = (long long)tl.expert * p.N + tl.n0;
+        decode_tile<CG>(p, t, num_units, rank, tl);
+        const int brow = tl.expert * p.N + tl.n0;  // first B row of the (full) N tile
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full_bar[s], STAGE);
-          tma_load_2d(sa(s), &tmap_a, &full_bar[s], kb * BK, tl.m0);
-          tma_load_2d(sb(s), &tmap_b, &full_bar[s], kb * BK, static_cast<int>(brow));
-          bulk_g2s(ssfa(s), p.sfa + ((long long)(tl.m0 / BM) * kst + kb) * SF_CHUNK, SF_CHUNK,
-                   &full_bar[s]);
-          bulk_g2s(ssfb(s), p.sfb + ((brow / BN) * kst + kb) * SF_CHUNK, SF_CHUNK,
-                   &full_bar[s]);
-          if (++s == STAGES) {
+          if (leader) mbar_arrive_expect_tx(&full_bar[s], C::STAGE * CG);
+          auto load = [&](void* dst, const CUtensorMap* tm, int x, int y) {
+            if constexpr (CG == 1)
+              tma_load_2d(dst, tm, &full_bar[s], x, y);
+            else
+              tma_load_2d_pair(dst, tm, &full_bar[s], x, y);
+          };
+          load(sa(s), &tmap_a, kb * BK, tl.m0);
+          load(sb(s), &tmap_b, kb * BK, brow + rank * C::B_ROWS);
+          // scale chunks viewed as [chunks * 2, 256] bytes: box {256, 2} = one 512-B chunk;
+          // each CTA holds the chunk of its own 128 A rows and the full N tile's B chunk
+          load(ssfa(s), &tmap_sfa, 0, ((tl.m0 / BM) * kst + kb) * 2);
+          load(ssfb(s), &tmap_sfb, 0, ((brow / BN) * kst + kb) * 2);
+          if (++s == C::STAGES) {
             s = 0;
             ph ^= 1;
           }
@@ -191,36 +269,52 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && leader) {
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
       uint32_t acc_ph = 0;
       const uint32_t t_sfa = tmem_base + SF_COL, t_sfb = tmem_base + SF_COL + 4;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = first; t < num_tiles; t += stride) {
         mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full_bar[s], ph);
           tc_fence_after();
-          // scale chunks smem -> TMEM (ordered before the MMAs below: same tcgen05 pipe)
-          tmem_cp_sf(t_sfa, sf_desc(smem_u32(ssfa(s))));
-          tmem_cp_sf(t_sfb, sf_desc(smem_u32(ssfb(s))));
+          // scale chunks smem -> TMEM (ordered before the MMAs below: same tcgen05 pipe;
+          // with cta_group::2 each CTA's chunk goes to its own TMEM)
+          if constexpr (CG == 1) {
+            tmem_cp_sf(t_sfa, sf_desc(smem_u32(ssfa(s))));
+            tmem_cp_sf(t_sfb, sf_desc(smem_u32(ssfb(s))));
+          } else {
+            tmem_cp_sf_pair(t_sfa, sf_desc(smem_u32(ssfa(s))));
+            tmem_cp_sf_pair(t_sfb, sf_desc(smem_u32(ssfb(s))));
+          }
           const uint32_t a_base = smem_u32(sa(s)), b_base = smem_u32(sb(s));
 #pragma unroll
           for (int j = 0; j < BK / UMMA_K; ++j) {
-            umma_mx(d_tmem, make_sdesc_sw128(a_base + j * UMMA_K, 16, 1024),
-                    make_sdesc_sw128(b_base + j * UMMA_K, 16, 1024), idesc_mx(j), t_sfa, t_sfb,
-                    (kb | j) != 0 ? 1u : 0u);
+            const uint64_t ad = make_sdesc_sw128(a_base + j * UMMA_K, 16, 1024);
+            const uint64_t bd = make_sdesc_sw128(b_base + j * UMMA_K, 16, 1024);
+            if constexpr (CG == 1)
+              umma_mx(d_tmem, ad, bd, idesc_mx(j, BM), t_sfa, t_sfb, (kb | j) != 0 ? 1u : 0u);
+            else
+              umma_mx_pair(d_tmem, ad, bd, idesc_mx(j, 2 * BM), t_sfa, t_sfb,
+                           (kb | j) != 0 ? 1u : 0u);
           }
-          umma_commit(&empty_bar[s]);
-          if (++s == STAGES) {
+          if constexpr (CG == 1)
+            umma_commit(&empty_bar[s]);
+          else
+            umma_commit_pair(&empty_bar[s]);
+          if (++s == C::STAGES) {
             s = 0;
             ph ^= 1;
           }
         }
-        umma_commit(&tfull_bar[acc]);
+        if constexpr (CG == 1)
+          umma_commit(&tfull_bar[acc]);
+        else
+          umma_commit_pair(&tfull_bar[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_ph ^= 1;
@@ -233,9 +327,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     int acc = 0;
     uint32_t acc_ph = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int t = first; t < num_tiles; t += stride) {
       Tile tl;
-      decode_tile(p, t, num_units, tl);
+      decode_tile<CG>(p, t, num_units, rank, tl);
       const long long row = tl.m0 + row_local;
       mbar_wait(&tfull_bar[acc], acc_ph);
       tc_fence_after();
@@ -323,7 +417,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 1)
+          mbar_arrive(&tempty_bar[acc]);
+        else
+          mbar_arrive_leader(&tempty_bar[acc]);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_ph ^= 1;
@@ -331,10 +430,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) {
+    cluster_sync_all();
+  } else {
+    __syncthreads();
+  }
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<TMEM_COLS>(tmem_base);
+    if constexpr (CG == 1) {
+      tmem_dealloc<TMEM_COLS>(tmem_base);
+    } else {
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(TMEM_COLS)
+                   : "memory");
+    }
   }
 }
 
@@ -351,42 +460,73 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   });
   return fn;
 }
-// 2-D u8 tensor [outer, inner], 128 x 128 boxes, 128B swizzle
-static int make_tmap_u8(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer) {
+// 2-D u8 tensor [outer, inner] with box {box_inner, box_outer}
+static int make_tmap_u8(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
+                        uint32_t box_inner, uint32_t box_outer, bool swizzle) {
   auto fn = encode_fn();
   if (!fn) return kErrCuda;
   if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (inner & 15)) return kErrInvalidArg;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {inner};
-  cuuint32_t box[2] = {128, 128};
+  cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box,
-                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? kOk : kErrCuda;
 }
 
-template <int EPI>
-static int launch(const void* a, int a_rows, const void* b, int num_experts, Params p,
-                  int max_m_blocks, cudaStream_t stream) {
-  CUtensorMap ta, tb;
-  int st;
-  if ((st = make_tmap_u8(&ta, a, p.K, a_rows))) return st;
-  if ((st = make_tmap_u8(&tb, b, p.K, (uint64_t)num_experts * p.N))) return st;
-  auto kern = mxfp8_gemm_kernel<EPI>;
+template <int EPI, int CG>
+static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tsa,
+                     const CUtensorMap& tsb, const Params& p, int max_m_blocks,
+                     cudaStream_t stream) {
+  auto kern = mxfp8_gemm_kernel<EPI, CG>;
   static bool attr = false;
   if (!attr) {
-    MOE_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    MOE_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        Cfg<CG>::SMEM));
     attr = true;
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int tiles = max_m_blocks * (p.N / BN);
+  const int tiles = (max_m_blocks / CG) * (p.N / BN);
   if (tiles <= 0) return kOk;
-  kern<<<tiles < sms ? tiles : sms, NUM_THREADS, SMEM, stream>>>(ta, tb, p);
-  MOE_LAUNCH_CHECK();
+  int grid = tiles * CG < sms ? tiles * CG : sms;
+  grid -= grid % CG;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = Cfg<CG>::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CG;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  MOE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tsa, tsb, p));
   return kOk;
+}
+
+template <int EPI>
+static int launch(const void* a, int a_rows, int max_rows, const void* b, int num_experts,
+                  Params p, int pair, cudaStream_t stream) {
+  CUtensorMap ta, tb, tsa, tsb;
+  int st;
+  const int cg = pair ? 2 : 1;
+  const long long b_rows = (long long)num_experts * p.N;
+  if ((st = make_tmap_u8(&ta, a, p.K, a_rows, BK, BM, true))) return st;
+  if ((st = make_tmap_u8(&tb, b, p.K, b_rows, BK, BN / cg, true))) return st;
+  // scale chunks: [rows/128 * K/128 chunks] x 512 B viewed as [2 * chunks, 256]
+  const long long sfa_chunks = (long long)(max_rows / BM) * (p.K / BK);
+  const long long sfb_chunks = (b_rows / BN) * (p.K / BK);
+  if ((st = make_tmap_u8(&tsa, p.sfa, 256, 2 * sfa_chunks, 256, 2, false))) return st;
+  if ((st = make_tmap_u8(&tsb, p.sfb, 256, 2 * sfb_chunks, 256, 2, false))) return st;
+  if (pair) return launch_cg<EPI, 2>(ta, tb, tsa, tsb, p, max_rows / BM, stream);
+  return launch_cg<EPI, 1>(ta, tb, tsa, tsb, p, max_rows / BM, stream);
 }
 
 }  // namespace mx8
@@ -401,8 +541,10 @@ extern "C" {
 // B = W2 codes [E, h, m]).
 int moe_gg_mxfp8_gemm(const void* a, const void* sfa, int a_rows, int max_rows, int K, int N,
                       const void* b, const void* sfb, int num_experts, const int* block_expert,
-                      const int* num_m_blocks, void* out, void* stream) {
-  if (K % BK || N % BN || max_rows % BM || a_rows > max_rows) return kErrInvalidArg;
+                      const int* num_m_blocks, void* out, int flags, void* stream) {
+  const int pair = flags & 1;
+  if (K % BK || N % BN || max_rows % (BM * (pair ? 2 : 1)) || a_rows > max_rows)
+    return kErrInvalidArg;
   Params p{};
   p.num_m_blocks = num_m_blocks;
   p.block_expert = block_expert;
@@ -412,7 +554,7 @@ int moe_gg_mxfp8_gemm(const void* a, const void* sfa, int a_rows, int max_rows, 
   p.sfb = static_cast<const uint8_t*>(sfb);
   p.out = out;
   p.ldo = N;
-  return launch<EPI_BF16>(a, a_rows, b, num_experts, p, max_rows / BM,
+  return launch<EPI_BF16>(a, a_rows, max_rows, b, num_experts, p, pair,
                           static_cast<cudaStream_t>(stream));
 }
 
@@ -422,8 +564,10 @@ int moe_gg_mxfp8_gemm(const void* a, const void* sfa, int a_rows, int max_rows, 
 int moe_gg_mxfp8_fc1(const void* xq, const void* sfx, int a_rows, int max_rows, int h, int m,
                      const void* w1q, const void* sfw, int num_experts, const int* block_expert,
                      const int* num_m_blocks, void* preact, void* act, void* act_q,
-                     void* act_sf, void* stream) {
-  if (h % BK || m % 128 || max_rows % BM || a_rows > max_rows || !act_q || !act_sf)
+                     void* act_sf, int flags, void* stream) {
+  const int pair = flags & 1;
+  if (h % BK || m % 128 || max_rows % (BM * (pair ? 2 : 1)) || a_rows > max_rows || !act_q ||
+      !act_sf)
     return kErrInvalidArg;
   Params p{};
   p.num_m_blocks = num_m_blocks;
@@ -438,7 +582,7 @@ int moe_gg_mxfp8_fc1(const void* xq, const void* sfx, int a_rows, int max_rows, 
   p.act_q = static_cast<uint8_t*>(act_q);
   p.act_sf = static_cast<uint8_t*>(act_sf);
   p.m = m;
-  return launch<EPI_SWIGLU_Q>(xq, a_rows, w1q, num_experts, p, max_rows / BM,
+  return launch<EPI_SWIGLU_Q>(xq, a_rows, max_rows, w1q, num_experts, p, pair,
                               static_cast<cudaStream_t>(stream));
 }
 

@@ -237,7 +237,7 @@ def mxfp8_quantize_weight(w: torch.Tensor):
 
 
 def mxfp8_gemm(aq, sfa, bq, sfb, num_experts, block_expert, num_m_blocks, N,
-               out=None, max_rows=None):
+               out=None, max_rows=None, pair=False):
     """out[rows, N] bf16 = dequant(aq) @ dequant(bq_e)^T per 128-row block's expert."""
     a_rows, k = aq.shape
     rows = a_rows if max_rows is None else max_rows
@@ -245,12 +245,12 @@ def mxfp8_gemm(aq, sfa, bq, sfb, num_experts, block_expert, num_m_blocks, N,
         out = torch.empty((rows, N), dtype=torch.bfloat16, device=aq.device)
     _lib.call("moe_gg_mxfp8_gemm", aq.data_ptr(), sfa.data_ptr(), a_rows, rows, k, N,
               bq.data_ptr(), sfb.data_ptr(), num_experts, block_expert.data_ptr(),
-              num_m_blocks.data_ptr(), out.data_ptr(), _stream())
+              num_m_blocks.data_ptr(), out.data_ptr(), int(pair), _stream())
     return out
 
 
 def mxfp8_fc1(xq, sfx, w1q, sfw, num_experts, block_expert, num_m_blocks, m, max_rows=None,
-              want_act=True):
+              want_act=True, pair=False):
     """fc1 + SwiGLU on MXFP8 operands (w1q from interleave_gate_up_mx). Returns (preact bf16
     [rows, 2m] in the bf16 engine's layout, act bf16 [rows, m] or None, act codes [rows, m],
     act tiled scales) -- the last two are fc2's MXFP8 A operand."""
@@ -264,5 +264,5 @@ def mxfp8_fc1(xq, sfx, w1q, sfw, num_experts, block_expert, num_m_blocks, m, max
     _lib.call("moe_gg_mxfp8_fc1", xq.data_ptr(), sfx.data_ptr(), a_rows, rows, h, m,
               w1q.data_ptr(), sfw.data_ptr(), num_experts, block_expert.data_ptr(),
               num_m_blocks.data_ptr(), preact.data_ptr(), _ptr(act), act_q.data_ptr(),
-              act_sf.data_ptr(), _stream())
+              act_sf.data_ptr(), int(pair), _stream())
     return preact, act, act_q, act_sf

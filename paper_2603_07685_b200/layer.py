@@ -117,8 +117,9 @@ def _mxfp8_experts(xp, w1, w2, plan, e):
     w1q, w1sf = gemm.mxfp8_quantize_w1(w1)
     w2q, w2sf = gemm.mxfp8_quantize_weight(w2)
     preact, act, aq, asf = gemm.mxfp8_fc1(xq, xsf, w1q, w1sf, e, plan.block_expert,
-                                          plan.num_m_blocks, m)
-    o = gemm.mxfp8_gemm(aq, asf, w2q, w2sf, e, plan.block_expert, plan.num_m_blocks, h)
+                                          plan.num_m_blocks, m, pair=plan.pair)
+    o = gemm.mxfp8_gemm(aq, asf, w2q, w2sf, e, plan.block_expert, plan.num_m_blocks, h,
+                        pair=plan.pair)
     return preact, act, o
 
 

@@ -53,20 +53,21 @@ def _plan(rows_per_expert, dev):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("pair", [False, True], ids=["cta1", "pair"])
 @pytest.mark.parametrize("E,K,N", [(2, 256, 256), (3, 512, 384)])
-def test_mxfp8_grouped_gemm_matches_dequant_gemm(E, K, N):
+def test_mxfp8_grouped_gemm_matches_dequant_gemm(E, K, N, pair):
     from paper_2603_07685_b200 import gemm
 
     dev = torch.device("cuda", 0)
     g = torch.Generator().manual_seed(E * 7 + K)
-    rows_e = [256, 128, 384][:E]
+    rows_e = ([256, 512, 256] if pair else [256, 128, 384])[:E]
     be, nmb, rows = _plan(rows_e, dev)
     a = (torch.randn((rows, K), generator=g) * 3).to(torch.bfloat16)
     a[100:128] = 0  # padding-like rows
     w = (torch.randn((E, N, K), generator=g) * 0.05).to(torch.bfloat16)
     aq, asf, asp = gemm.mxfp8_quantize(a.to(dev), plain=True)
     wq, wsf, wsp = gemm.mxfp8_quantize(w.reshape(E * N, K).to(dev), plain=True)
-    out = gemm.mxfp8_gemm(aq, asf, wq, wsf, E, be, nmb, N).float().cpu().numpy()
+    out = gemm.mxfp8_gemm(aq, asf, wq, wsf, E, be, nmb, N, pair=pair).float().cpu().numpy()
     ad = M.dequantize_mxfp8(aq.cpu().numpy()[:rows], asp.cpu().numpy())
     wd = M.dequantize_mxfp8(wq.cpu().numpy(), wsp.cpu().numpy()).reshape(E, N, K)
     ref = np.concatenate([ad[sum(rows_e[:e]):sum(rows_e[:e + 1])] @ wd[e].T
@@ -76,13 +77,14 @@ def test_mxfp8_grouped_gemm_matches_dequant_gemm(E, K, N):
 
 
 @pytest.mark.gpu
-def test_mxfp8_fc1_swiglu_and_fused_act_quantisation():
+@pytest.mark.parametrize("pair", [False, True], ids=["cta1", "pair"])
+def test_mxfp8_fc1_swiglu_and_fused_act_quantisation(pair):
     from paper_2603_07685_b200 import gemm
 
     dev = torch.device("cuda", 0)
     g = torch.Generator().manual_seed(11)
     E, h, m = 2, 256, 256
-    rows_e = [128, 256]
+    rows_e = [256, 512] if pair else [128, 256]
     be, nmb, rows = _plan(rows_e, dev)
     x = torch.randn((rows, h), generator=g).to(torch.bfloat16)
     gate = (torch.randn((E, m, h), generator=g) * h ** -0.5).to(torch.bfloat16)
@@ -90,7 +92,7 @@ def test_mxfp8_fc1_swiglu_and_fused_act_quantisation():
     xq, xsf, xsp = gemm.mxfp8_quantize(x.to(dev), plain=True)
     w1 = gemm.interleave_gate_up_mx(gate.to(dev), up.to(dev))
     wq, wsf, wsp = gemm.mxfp8_quantize(w1.reshape(E * 2 * m, h), plain=True)
-    preact, act, act_q, act_sf = gemm.mxfp8_fc1(xq, xsf, wq, wsf, E, be, nmb, m)
+    preact, act, act_q, act_sf = gemm.mxfp8_fc1(xq, xsf, wq, wsf, E, be, nmb, m, pair=pair)
     torch.cuda.synchronize()
     xd = M.dequantize_mxfp8(xq.cpu().numpy()[:rows], xsp.cpu().numpy())
     wd = M.dequantize_mxfp8(wq.cpu().numpy(), wsp.cpu().numpy()).reshape(E, 2 * m, h)

@@ -52,8 +52,12 @@ def main():
     def mx_fc1():
         st["mx"] = gemm.mxfp8_fc1(xq, xsf, w1q, w1sf, E, be, nmb, m)
 
+    def mx_fc1_pair():
+        st["mx"] = gemm.mxfp8_fc1(xq, xsf, w1q, w1sf, E, be, nmb, m, pair=True)
+
     for _ in range(2):
-        for name, fn, fl in (("bf16_fc1", bf_fc1, fl1), ("mxfp8_fc1", mx_fc1, fl1)):
+        for name, fn, fl in (("bf16_fc1", bf_fc1, fl1), ("mxfp8_fc1", mx_fc1, fl1),
+                             ("mxfp8_fc1_pair", mx_fc1_pair, fl1)):
             ms = timed(fn)
             out[name] = {"ms": round(ms, 3), "TFLOPs": round(fl / ms / 1e9, 1)}
     act = st["pa"][1]
@@ -62,6 +66,8 @@ def main():
         for name, fn, fl in (
                 ("bf16_fc2", lambda: gemm.fc2_fwd(act, w2, be, nmb, pair=True), fl2),
                 ("mxfp8_fc2", lambda: gemm.mxfp8_gemm(aq, asf, w2q, w2sf, E, be, nmb, h), fl2),
+                ("mxfp8_fc2_pair", lambda: gemm.mxfp8_gemm(aq, asf, w2q, w2sf, E, be, nmb, h,
+                                                           pair=True), fl2),
                 ("mxfp8_quant_x", lambda: gemm.mxfp8_quantize(x), 0.0)):
             ms = timed(fn)
             out[name] = {"ms": round(ms, 3)}

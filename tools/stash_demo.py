@@ -1,4 +1,5 @@
-"""Paged Stashing at scale: L stacked EP MoE layers (sync-free p2p), all forwards then all
+"""Paged Stashing at scale: L stacked residual EP MoE layers (x + MoE(x), sync-free p2p), all
+forwards then all
 backwards, with (a) per-layer worst-case buffers and (b) one shared worst-case tmp set plus
 a paged stash of the actual rows. Reports device memory in use at the peak (after the last
 forward) and the fwd+bwd time of the L-layer stack, and checks (a) == (b) bit for bit.
@@ -69,8 +70,11 @@ def main():
         auxes = []
         t0 = time.time()
         for li, (w_r, w1, w2) in enumerate(layers):
-            y, aux = moe_forward_ep(y, w_r, w1, w2, cfg, ep, transport="p2p", sync_free=True,
-                                    tag=tag_of(li), stash=stash, layer_id=li)
+            # residual stream, as in a transformer block (keeps the routing of deep layers
+            # from collapsing onto one rank in this random-weight stack)
+            out, aux = moe_forward_ep(y, w_r, w1, w2, cfg, ep, transport="p2p", sync_free=True,
+                                      tag=tag_of(li), stash=stash, layer_id=li)
+            y = y + out
             auxes.append(aux)
             if stash is not None and os.environ.get("STASH_DEBUG") and rank == 0:
                 print("layer", li, [sb.stats() for sb in stash],
