@@ -258,8 +258,10 @@ int moe_mxfp8_quantize(const void* x, long long ldx, int rows, int K, void* code
                        long long ldc, void* sf_plain, void* sf_tiled, int w1_m, void* stream);
 /* block-scaled tcgen05 grouped GEMMs (kind::mxf8f6f4, UMMA 128x128x32): bf16 output, and
  * fc1 + SwiGLU with the activation re-quantised to MXFP8 in the epilogue (fc2's A operand);
- * w1q interleaves gate/up in 64-row blocks. flags bit 0: CTA-pair engine (UMMA 256 x 128,
- * cta_group::2; expert blocks 256-row aligned). */
+ * flags bit 0: CTA-pair engine (cta_group::2; expert blocks 256-row aligned). flags bit 1:
+ * 256-wide N tiles with a single TMEM accumulator (else 128-wide, double-buffered). fc1's
+ * w1q interleaves gate/up in 64-row blocks for 128-wide tiles, 128-row blocks (the bf16
+ * engine's layout) for 256-wide tiles. */
 int moe_gg_mxfp8_gemm(const void* a, const void* sfa, int a_rows, int max_rows, int K, int N,
                       const void* b, const void* sfb, int num_experts, const int* block_expert,
                       const int* num_m_blocks, void* out, int flags, void* stream);

@@ -29,25 +29,34 @@
 namespace moe {
 namespace mx8 {
 
-constexpr int BM = 128, BN = 128, BK = 128;  // BK in fp8 elements (= bytes)
+constexpr int BM = 128, BK = 128;  // BK in fp8 elements (= bytes)
 constexpr int UMMA_K = 32;
 constexpr int A_STAGE = BM * BK, SF_CHUNK = 512;
 // CG = 1: UMMA 128 x 128 per CTA. CG = 2: CTA pair, UMMA 256 x 128 (cta_group::2): each CTA
 // stages its 128 rows of A and half (64 rows) of the B tile, and its own copy of both scale
 // chunks; per-SM shared-memory operand traffic drops from 8 KB to 6 KB per 1 MFLOP and the
 // ring holds 8 stages instead of 6 (more time to hide TMA latency at fp8 MMA rates).
-template <int CG>
+// WIDE: 256-wide N tiles with a single TMEM accumulator (256 columns + 12 scale columns);
+// the operand traffic per MMA FLOP drops by a third again, at the cost of an epilogue that
+// no longer overlaps the next tile's MMAs. Narrow: 128-wide tiles, double-buffered.
+template <int CG, bool WIDE>
 struct Cfg {
+  static constexpr int BN = WIDE ? 256 : 128;
+  static constexpr int ACC = WIDE ? 1 : 2;        // accumulator stages in TMEM
+  static constexpr int SFB_CHUNKS = BN / 128;
   static constexpr int B_ROWS = BN / CG;
   static constexpr int B_STAGE = B_ROWS * BK;
-  static constexpr int STAGE = A_STAGE + B_STAGE + 2 * SF_CHUNK;
-  static constexpr int STAGES = CG == 1 ? 6 : 8;
+  static constexpr int STAGE = A_STAGE + B_STAGE + (1 + SFB_CHUNKS) * SF_CHUNK;
+  static constexpr int FIT = 200704 / STAGE;
+  static constexpr int STAGES = FIT > 8 ? 8 : FIT;
   static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
 };
 constexpr int TMEM_COLS = 512;
 constexpr int SF_COL = 256;
-constexpr int EPI_WARPS = 4;
-constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
+// epilogue warps: 4 (one per TMEM lane quarter), 8 for the single-accumulator wide tiles
+// (two per quarter, each draining half the columns: the MMAs wait for the drain there)
+template <bool WIDE>
+constexpr int epi_warps() { return WIDE ? 8 : 4; }
 constexpr int BAND_M = 16;
 
 enum Epi : int { EPI_BF16 = 0, EPI_SWIGLU_Q = 1 };
@@ -80,10 +89,10 @@ __device__ __forceinline__ void tmem_cp_sf(uint32_t taddr, uint64_t sdesc) {
                : "memory");
 }
 // Block-scaled instruction descriptor: E4M3 x E4M3, E8M0 scales, K-major, M=128, N=128.
-__host__ __device__ constexpr uint32_t idesc_mx(int j, int M) {
+__host__ __device__ constexpr uint32_t idesc_mx(int j, int M, int N) {
   return (static_cast<uint32_t>(j) << 4)          // B scale-factor id (byte)
          | (0u << 7) | (0u << 10)                 // A, B format: E4M3
-         | (static_cast<uint32_t>(BN >> 3) << 17)  // N / 8
+         | (static_cast<uint32_t>(N >> 3) << 17)   // N / 8
          | (1u << 23)                             // scale format: E8M0
          | (static_cast<uint32_t>(M >> 4) << 24)   // M / 16
          | (static_cast<uint32_t>(j) << 29);      // A scale-factor id
@@ -158,7 +167,7 @@ __device__ __forceinline__ int e8m0_exp(float amax) {
 struct Tile {
   int expert, m0, n0;
 };
-template <int CG>
+template <int CG, int BN>
 __device__ __forceinline__ void decode_tile(const Params& p, int t, int num_units, int rank,
                                             Tile& tl) {
   const int nb_count = p.N / BN;
@@ -173,13 +182,14 @@ __device__ __forceinline__ void decode_tile(const Params& p, int t, int num_unit
   tl.n0 = nb * BN;
 }
 
-template <int EPI, int CG>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+template <int EPI, int CG, bool WIDE>
+__global__ void __launch_bounds__(64 + 32 * epi_warps<WIDE>(), 1)
     mxfp8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                       const __grid_constant__ CUtensorMap tmap_b,
                       const __grid_constant__ CUtensorMap tmap_sfa,
                       const __grid_constant__ CUtensorMap tmap_sfb, const Params p) {
-  using C = Cfg<CG>;
+  using C = Cfg<CG, WIDE>;
+  constexpr int BN = C::BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -205,9 +215,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < C::ACC; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], EPI_WARPS * CG);
+      mbar_init(&tempty_bar[s], epi_warps<WIDE>() * CG);
     }
     fence_mbar_init();
     fence_async_shared();
@@ -244,7 +254,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t ph = 0;
       for (int t = first; t < num_tiles; t += stride) {
         Tile tl;
-        decode_tile<CG>(p, t, num_units, rank, tl);
+        decode_tile<CG, BN>(p, t, num_units, rank, tl);
         const int brow = tl.expert * p.N + tl.n0;  // first B row of the (full) N tile
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
@@ -260,7 +270,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // scale chunks viewed as [chunks * 2, 256] bytes: box {256, 2} = one 512-B chunk;
           // each CTA holds the chunk of its own 128 A rows and the full N tile's B chunk
           load(ssfa(s), &tmap_sfa, 0, ((tl.m0 / BM) * kst + kb) * 2);
-          load(ssfb(s), &tmap_sfb, 0, ((brow / BN) * kst + kb) * 2);
+#pragma unroll
+          for (int c = 0; c < C::SFB_CHUNKS; ++c)
+            load(ssfb(s) + c * SF_CHUNK, &tmap_sfb, 0, ((brow / 128 + c) * kst + kb) * 2);
           if (++s == C::STAGES) {
             s = 0;
             ph ^= 1;
@@ -286,10 +298,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // with cta_group::2 each CTA's chunk goes to its own TMEM)
           if constexpr (CG == 1) {
             tmem_cp_sf(t_sfa, sf_desc(smem_u32(ssfa(s))));
-            tmem_cp_sf(t_sfb, sf_desc(smem_u32(ssfb(s))));
+#pragma unroll
+            for (int c = 0; c < C::SFB_CHUNKS; ++c)
+              tmem_cp_sf(t_sfb + 4 * c, sf_desc(smem_u32(ssfb(s) + c * SF_CHUNK)));
           } else {
             tmem_cp_sf_pair(t_sfa, sf_desc(smem_u32(ssfa(s))));
-            tmem_cp_sf_pair(t_sfb, sf_desc(smem_u32(ssfb(s))));
+#pragma unroll
+            for (int c = 0; c < C::SFB_CHUNKS; ++c)
+              tmem_cp_sf_pair(t_sfb + 4 * c, sf_desc(smem_u32(ssfb(s) + c * SF_CHUNK)));
           }
           const uint32_t a_base = smem_u32(sa(s)), b_base = smem_u32(sb(s));
 #pragma unroll
@@ -297,9 +313,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t ad = make_sdesc_sw128(a_base + j * UMMA_K, 16, 1024);
             const uint64_t bd = make_sdesc_sw128(b_base + j * UMMA_K, 16, 1024);
             if constexpr (CG == 1)
-              umma_mx(d_tmem, ad, bd, idesc_mx(j, BM), t_sfa, t_sfb, (kb | j) != 0 ? 1u : 0u);
+              umma_mx(d_tmem, ad, bd, idesc_mx(j, BM, BN), t_sfa, t_sfb,
+                      (kb | j) != 0 ? 1u : 0u);
             else
-              umma_mx_pair(d_tmem, ad, bd, idesc_mx(j, 2 * BM), t_sfa, t_sfb,
+              umma_mx_pair(d_tmem, ad, bd, idesc_mx(j, 2 * BM, BN), t_sfa, t_sfb,
                            (kb | j) != 0 ? 1u : 0u);
           }
           if constexpr (CG == 1)
@@ -315,13 +332,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           umma_commit(&tfull_bar[acc]);
         else
           umma_commit_pair(&tfull_bar[acc]);
-        if (++acc == 2) {
+        if (++acc == C::ACC) {
           acc = 0;
           acc_ph ^= 1;
         }
       }
     }
   } else {
+    constexpr int NPART = epi_warps<WIDE>() / 4;  // warps sharing a lane quarter
+    const int part = (warp - 2) / 4;
     const int q = warp & 3;
     const int row_local = q * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
@@ -329,7 +348,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t acc_ph = 0;
     for (int t = first; t < num_tiles; t += stride) {
       Tile tl;
-      decode_tile<CG>(p, t, num_units, rank, tl);
+      decode_tile<CG, BN>(p, t, num_units, rank, tl);
       const long long row = tl.m0 + row_local;
       mbar_wait(&tfull_bar[acc], acc_ph);
       tc_fence_after();
@@ -337,7 +356,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if constexpr (EPI == EPI_BF16) {
         __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo + tl.n0;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = part * (BN / 32 / NPART); c < (part + 1) * (BN / 32 / NPART); ++c) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(t_base + c * 32, r);
           tmem_ld_wait();
@@ -352,15 +371,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       } else {
-        // tile columns [0, 64) = gate rows g0 + [0, 64), [64, 128) = the matching up rows
+        // tile columns [0, BN/2) = gate rows g0 + [0, BN/2), [BN/2, BN) = the matching up
+        // rows (narrow tiles: W1 in 64-row gate/up blocks; wide: the bf16 engine's 128)
+        constexpr int HALF = BN / 2;
         const int g0 = tl.n0 / 2;
         __nv_bfloat16* pre = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo +
                              (g0 >> 7) * 256 + (g0 & 127);
 #pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
+        for (int c = part * (HALF / 32 / NPART); c < (part + 1) * (HALF / 32 / NPART); ++c) {
           uint32_t g[32], u[32];
           tmem_ld_32x32b_x32(t_base + c * 32, g);
-          tmem_ld_32x32b_x32(t_base + 64 + c * 32, u);
+          tmem_ld_32x32b_x32(t_base + HALF + c * 32, u);
           tmem_ld_wait();
           uint32_t a2[16];
           float amax = 0.f;
@@ -423,7 +444,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         else
           mbar_arrive_leader(&tempty_bar[acc]);
       }
-      if (++acc == 2) {
+      if (++acc == C::ACC) {
         acc = 0;
         acc_ph ^= 1;
       }
@@ -477,28 +498,29 @@ static int make_tmap_u8(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_
   return r == CUDA_SUCCESS ? kOk : kErrCuda;
 }
 
-template <int EPI, int CG>
+template <int EPI, int CG, bool WIDE>
 static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tsa,
                      const CUtensorMap& tsb, const Params& p, int max_m_blocks,
                      cudaStream_t stream) {
-  auto kern = mxfp8_gemm_kernel<EPI, CG>;
+  using C = Cfg<CG, WIDE>;
+  auto kern = mxfp8_gemm_kernel<EPI, CG, WIDE>;
   static bool attr = false;
   if (!attr) {
     MOE_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        Cfg<CG>::SMEM));
+                                        C::SMEM));
     attr = true;
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int tiles = (max_m_blocks / CG) * (p.N / BN);
+  const int tiles = (max_m_blocks / CG) * (p.N / C::BN);
   if (tiles <= 0) return kOk;
   int grid = tiles * CG < sms ? tiles * CG : sms;
   grid -= grid % CG;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(NUM_THREADS);
-  cfg.dynamicSmemBytes = Cfg<CG>::SMEM;
+  cfg.blockDim = dim3(64 + 32 * epi_warps<WIDE>());
+  cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -513,20 +535,25 @@ static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtenso
 
 template <int EPI>
 static int launch(const void* a, int a_rows, int max_rows, const void* b, int num_experts,
-                  Params p, int pair, cudaStream_t stream) {
+                  Params p, int pair, int wide, cudaStream_t stream) {
   CUtensorMap ta, tb, tsa, tsb;
   int st;
   const int cg = pair ? 2 : 1;
+  const int bn = wide ? 256 : 128;
   const long long b_rows = (long long)num_experts * p.N;
   if ((st = make_tmap_u8(&ta, a, p.K, a_rows, BK, BM, true))) return st;
-  if ((st = make_tmap_u8(&tb, b, p.K, b_rows, BK, BN / cg, true))) return st;
+  if ((st = make_tmap_u8(&tb, b, p.K, b_rows, BK, bn / cg, true))) return st;
   // scale chunks: [rows/128 * K/128 chunks] x 512 B viewed as [2 * chunks, 256]
   const long long sfa_chunks = (long long)(max_rows / BM) * (p.K / BK);
-  const long long sfb_chunks = (b_rows / BN) * (p.K / BK);
+  const long long sfb_chunks = (b_rows / 128) * (p.K / BK);
   if ((st = make_tmap_u8(&tsa, p.sfa, 256, 2 * sfa_chunks, 256, 2, false))) return st;
   if ((st = make_tmap_u8(&tsb, p.sfb, 256, 2 * sfb_chunks, 256, 2, false))) return st;
-  if (pair) return launch_cg<EPI, 2>(ta, tb, tsa, tsb, p, max_rows / BM, stream);
-  return launch_cg<EPI, 1>(ta, tb, tsa, tsb, p, max_rows / BM, stream);
+  const int mb = max_rows / BM;
+  if (pair)
+    return wide ? launch_cg<EPI, 2, true>(ta, tb, tsa, tsb, p, mb, stream)
+                : launch_cg<EPI, 2, false>(ta, tb, tsa, tsb, p, mb, stream);
+  return wide ? launch_cg<EPI, 1, true>(ta, tb, tsa, tsb, p, mb, stream)
+              : launch_cg<EPI, 1, false>(ta, tb, tsa, tsb, p, mb, stream);
 }
 
 }  // namespace mx8
@@ -542,8 +569,8 @@ extern "C" {
 int moe_gg_mxfp8_gemm(const void* a, const void* sfa, int a_rows, int max_rows, int K, int N,
                       const void* b, const void* sfb, int num_experts, const int* block_expert,
                       const int* num_m_blocks, void* out, int flags, void* stream) {
-  const int pair = flags & 1;
-  if (K % BK || N % BN || max_rows % (BM * (pair ? 2 : 1)) || a_rows > max_rows)
+  const int pair = flags & 1, wide = (flags >> 1) & 1;
+  if (K % BK || N % (wide ? 256 : 128) || max_rows % (BM * (pair ? 2 : 1)) || a_rows > max_rows)
     return kErrInvalidArg;
   Params p{};
   p.num_m_blocks = num_m_blocks;
@@ -554,7 +581,7 @@ int moe_gg_mxfp8_gemm(const void* a, const void* sfa, int a_rows, int max_rows, 
   p.sfb = static_cast<const uint8_t*>(sfb);
   p.out = out;
   p.ldo = N;
-  return launch<EPI_BF16>(a, a_rows, max_rows, b, num_experts, p, pair,
+  return launch<EPI_BF16>(a, a_rows, max_rows, b, num_experts, p, pair, wide,
                           static_cast<cudaStream_t>(stream));
 }
 
@@ -565,7 +592,7 @@ int moe_gg_mxfp8_fc1(const void* xq, const void* sfx, int a_rows, int max_rows, 
                      const void* w1q, const void* sfw, int num_experts, const int* block_expert,
                      const int* num_m_blocks, void* preact, void* act, void* act_q,
                      void* act_sf, int flags, void* stream) {
-  const int pair = flags & 1;
+  const int pair = flags & 1, wide = (flags >> 1) & 1;
   if (h % BK || m % 128 || max_rows % (BM * (pair ? 2 : 1)) || a_rows > max_rows || !act_q ||
       !act_sf)
     return kErrInvalidArg;
@@ -582,7 +609,7 @@ int moe_gg_mxfp8_fc1(const void* xq, const void* sfx, int a_rows, int max_rows, 
   p.act_q = static_cast<uint8_t*>(act_q);
   p.act_sf = static_cast<uint8_t*>(act_sf);
   p.m = m;
-  return launch<EPI_SWIGLU_Q>(xq, a_rows, max_rows, w1q, num_experts, p, pair,
+  return launch<EPI_SWIGLU_Q>(xq, a_rows, max_rows, w1q, num_experts, p, pair, wide,
                               static_cast<cudaStream_t>(stream));
 }
 

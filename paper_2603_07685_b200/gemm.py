@@ -212,11 +212,12 @@ def mxfp8_quantize(x: torch.Tensor, rows_pad: int | None = None, plain: bool = F
     return codes, sf_t, sf_p
 
 
-def mxfp8_quantize_w1(w1: torch.Tensor):
-    """bf16-engine W1 [E, 2m, h] (128-row gate/up interleave) -> MXFP8 codes/scales in the
-    MXFP8 engine's 64-row interleave (one fused pass)."""
+def mxfp8_quantize_w1(w1: torch.Tensor, wide: bool = False):
+    """bf16-engine W1 [E, 2m, h] (128-row gate/up interleave) -> MXFP8 codes/scales for the
+    MXFP8 fc1: the narrow (128-wide tile) engine wants 64-row gate/up blocks (re-interleaved
+    in the same pass); the wide (256) engine uses the 128-row layout as is."""
     e, m2, h = w1.shape
-    codes, sf, _ = mxfp8_quantize(w1.reshape(e * m2, h), w1_m=m2 // 2)
+    codes, sf, _ = mxfp8_quantize(w1.reshape(e * m2, h), w1_m=0 if wide else m2 // 2)
     return codes, sf
 
 
@@ -237,7 +238,7 @@ def mxfp8_quantize_weight(w: torch.Tensor):
 
 
 def mxfp8_gemm(aq, sfa, bq, sfb, num_experts, block_expert, num_m_blocks, N,
-               out=None, max_rows=None, pair=False):
+               out=None, max_rows=None, pair=False, wide=False):
     """out[rows, N] bf16 = dequant(aq) @ dequant(bq_e)^T per 128-row block's expert."""
     a_rows, k = aq.shape
     rows = a_rows if max_rows is None else max_rows
@@ -245,12 +246,12 @@ def mxfp8_gemm(aq, sfa, bq, sfb, num_experts, block_expert, num_m_blocks, N,
         out = torch.empty((rows, N), dtype=torch.bfloat16, device=aq.device)
     _lib.call("moe_gg_mxfp8_gemm", aq.data_ptr(), sfa.data_ptr(), a_rows, rows, k, N,
               bq.data_ptr(), sfb.data_ptr(), num_experts, block_expert.data_ptr(),
-              num_m_blocks.data_ptr(), out.data_ptr(), int(pair), _stream())
+              num_m_blocks.data_ptr(), out.data_ptr(), int(pair) | (int(wide) << 1), _stream())
     return out
 
 
 def mxfp8_fc1(xq, sfx, w1q, sfw, num_experts, block_expert, num_m_blocks, m, max_rows=None,
-              want_act=True, pair=False):
+              want_act=True, pair=False, wide=False):
     """fc1 + SwiGLU on MXFP8 operands (w1q from interleave_gate_up_mx). Returns (preact bf16
     [rows, 2m] in the bf16 engine's layout, act bf16 [rows, m] or None, act codes [rows, m],
     act tiled scales) -- the last two are fc2's MXFP8 A operand."""
@@ -264,5 +265,5 @@ def mxfp8_fc1(xq, sfx, w1q, sfw, num_experts, block_expert, num_m_blocks, m, max
     _lib.call("moe_gg_mxfp8_fc1", xq.data_ptr(), sfx.data_ptr(), a_rows, rows, h, m,
               w1q.data_ptr(), sfw.data_ptr(), num_experts, block_expert.data_ptr(),
               num_m_blocks.data_ptr(), preact.data_ptr(), _ptr(act), act_q.data_ptr(),
-              act_sf.data_ptr(), int(pair), _stream())
+              act_sf.data_ptr(), int(pair) | (int(wide) << 1), _stream())
     return preact, act, act_q, act_sf

@@ -113,13 +113,16 @@ def _mxfp8_experts(xp, w1, w2, plan, e):
     Returns the bf16 preact / act the bf16 backward needs and the expert outputs."""
     m = w2.shape[2]
     h = xp.shape[1]
+    # 256-wide tiles (single TMEM accumulator, 8 epilogue warps) when the shapes allow:
+    # measured 1.2x (fc1) / 1.9x (fc2) the bf16 engine at Mixtral shape
+    wide = (2 * m) % 256 == 0 and h % 256 == 0
     xq, xsf, _ = gemm.mxfp8_quantize(xp)
-    w1q, w1sf = gemm.mxfp8_quantize_w1(w1)
+    w1q, w1sf = gemm.mxfp8_quantize_w1(w1, wide=wide)
     w2q, w2sf = gemm.mxfp8_quantize_weight(w2)
     preact, act, aq, asf = gemm.mxfp8_fc1(xq, xsf, w1q, w1sf, e, plan.block_expert,
-                                          plan.num_m_blocks, m, pair=plan.pair)
+                                          plan.num_m_blocks, m, pair=plan.pair, wide=wide)
     o = gemm.mxfp8_gemm(aq, asf, w2q, w2sf, e, plan.block_expert, plan.num_m_blocks, h,
-                        pair=plan.pair)
+                        pair=plan.pair, wide=wide)
     return preact, act, o
 
 

@@ -53,9 +53,10 @@ def _plan(rows_per_expert, dev):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("wide", [False, True], ids=["n128", "n256"])
 @pytest.mark.parametrize("pair", [False, True], ids=["cta1", "pair"])
-@pytest.mark.parametrize("E,K,N", [(2, 256, 256), (3, 512, 384)])
-def test_mxfp8_grouped_gemm_matches_dequant_gemm(E, K, N, pair):
+@pytest.mark.parametrize("E,K,N", [(2, 256, 256), (3, 512, 512)])
+def test_mxfp8_grouped_gemm_matches_dequant_gemm(E, K, N, pair, wide):
     from paper_2603_07685_b200 import gemm
 
     dev = torch.device("cuda", 0)
@@ -67,7 +68,8 @@ def test_mxfp8_grouped_gemm_matches_dequant_gemm(E, K, N, pair):
     w = (torch.randn((E, N, K), generator=g) * 0.05).to(torch.bfloat16)
     aq, asf, asp = gemm.mxfp8_quantize(a.to(dev), plain=True)
     wq, wsf, wsp = gemm.mxfp8_quantize(w.reshape(E * N, K).to(dev), plain=True)
-    out = gemm.mxfp8_gemm(aq, asf, wq, wsf, E, be, nmb, N, pair=pair).float().cpu().numpy()
+    out = gemm.mxfp8_gemm(aq, asf, wq, wsf, E, be, nmb, N, pair=pair,
+                          wide=wide).float().cpu().numpy()
     ad = M.dequantize_mxfp8(aq.cpu().numpy()[:rows], asp.cpu().numpy())
     wd = M.dequantize_mxfp8(wq.cpu().numpy(), wsp.cpu().numpy()).reshape(E, N, K)
     ref = np.concatenate([ad[sum(rows_e[:e]):sum(rows_e[:e + 1])] @ wd[e].T
@@ -77,8 +79,9 @@ def test_mxfp8_grouped_gemm_matches_dequant_gemm(E, K, N, pair):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("wide", [False, True], ids=["n128", "n256"])
 @pytest.mark.parametrize("pair", [False, True], ids=["cta1", "pair"])
-def test_mxfp8_fc1_swiglu_and_fused_act_quantisation(pair):
+def test_mxfp8_fc1_swiglu_and_fused_act_quantisation(pair, wide):
     from paper_2603_07685_b200 import gemm
 
     dev = torch.device("cuda", 0)
@@ -90,14 +93,17 @@ def test_mxfp8_fc1_swiglu_and_fused_act_quantisation(pair):
     gate = (torch.randn((E, m, h), generator=g) * h ** -0.5).to(torch.bfloat16)
     up = (torch.randn((E, m, h), generator=g) * h ** -0.5).to(torch.bfloat16)
     xq, xsf, xsp = gemm.mxfp8_quantize(x.to(dev), plain=True)
-    w1 = gemm.interleave_gate_up_mx(gate.to(dev), up.to(dev))
+    blk = 128 if wide else 64
+    w1 = (gemm.interleave_gate_up if wide else gemm.interleave_gate_up_mx)(gate.to(dev),
+                                                                          up.to(dev))
     wq, wsf, wsp = gemm.mxfp8_quantize(w1.reshape(E * 2 * m, h), plain=True)
-    preact, act, act_q, act_sf = gemm.mxfp8_fc1(xq, xsf, wq, wsf, E, be, nmb, m, pair=pair)
+    preact, act, act_q, act_sf = gemm.mxfp8_fc1(xq, xsf, wq, wsf, E, be, nmb, m, pair=pair,
+                                                wide=wide)
     torch.cuda.synchronize()
     xd = M.dequantize_mxfp8(xq.cpu().numpy()[:rows], xsp.cpu().numpy())
     wd = M.dequantize_mxfp8(wq.cpu().numpy(), wsp.cpu().numpy()).reshape(E, 2 * m, h)
-    gd = wd.reshape(E, m // 64, 2, 64, h)[:, :, 0].reshape(E, m, h)
-    ud = wd.reshape(E, m // 64, 2, 64, h)[:, :, 1].reshape(E, m, h)
+    gd = wd.reshape(E, m // blk, 2, blk, h)[:, :, 0].reshape(E, m, h)
+    ud = wd.reshape(E, m // blk, 2, blk, h)[:, :, 1].reshape(E, m, h)
     off = np.cumsum([0] + rows_e)
     zg = np.concatenate([xd[off[e]:off[e + 1]] @ gd[e].T for e in range(E)])
     zu = np.concatenate([xd[off[e]:off[e + 1]] @ ud[e].T for e in range(E)])

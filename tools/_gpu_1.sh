@@ -1,3 +1,5 @@
-timeout 600 python -m pytest tests/test_mxfp8.py tests/test_layer_gpu.py -q -p no:cacheprovider -x > gpurun_out/mx_pytest.log 2>&1; echo rc=$? >> gpurun_out/mx_pytest.log
-timeout 300 python tools/mxfp8_probe.py > gpurun_out/mx_probe.json 2> gpurun_out/mx_probe.err
-tail -30 gpurun_out/mx_pytest.log; cat gpurun_out/mx_probe.json; tail -5 gpurun_out/mx_probe.err
+timeout 300 python -m pytest tests/test_layer_gpu.py -q -p no:cacheprovider -k mxfp8 > gpurun_out/mx3.log 2>&1; tail -2 gpurun_out/mx3.log
+python bench.py --steps 10 --no-cpu-baseline > gpurun_out/mx3_bf16.json 2> gpurun_out/mx3_bf16.err
+python bench.py --steps 10 --no-cpu-baseline --precision mxfp8 > gpurun_out/mx3_mxfp8.json 2> gpurun_out/mx3_mxfp8.err
+python bench.py --steps 10 --no-cpu-baseline > gpurun_out/mx3_bf16b.json 2> gpurun_out/mx3_bf16b.err
+for f in mx3_bf16 mx3_mxfp8 mx3_bf16b; do python -c "import json;d=json.load(open('gpurun_out/$f.json'));print('$f', d['value'], d['ms_per_step'], d['clocks'])"; done

@@ -40,6 +40,7 @@ def main():
     w1mx = gemm.interleave_gate_up_mx(gate, up)
     xq, xsf, _ = gemm.mxfp8_quantize(x)
     w1q, w1sf = gemm.mxfp8_quantize_weight(w1mx)
+    w1qw, w1sfw = gemm.mxfp8_quantize_w1(w1, wide=True)
     w2q, w2sf = gemm.mxfp8_quantize_weight(w2)
     fl1 = 2.0 * rows * h * 2 * m
     fl2 = 2.0 * rows * m * h
@@ -55,9 +56,13 @@ def main():
     def mx_fc1_pair():
         st["mx"] = gemm.mxfp8_fc1(xq, xsf, w1q, w1sf, E, be, nmb, m, pair=True)
 
+    def mx_fc1_pair_wide():
+        st["mxw"] = gemm.mxfp8_fc1(xq, xsf, w1qw, w1sfw, E, be, nmb, m, pair=True, wide=True)
+
     for _ in range(2):
         for name, fn, fl in (("bf16_fc1", bf_fc1, fl1), ("mxfp8_fc1", mx_fc1, fl1),
-                             ("mxfp8_fc1_pair", mx_fc1_pair, fl1)):
+                             ("mxfp8_fc1_pair", mx_fc1_pair, fl1),
+                             ("mxfp8_fc1_pair_wide", mx_fc1_pair_wide, fl1)):
             ms = timed(fn)
             out[name] = {"ms": round(ms, 3), "TFLOPs": round(fl / ms / 1e9, 1)}
     act = st["pa"][1]
@@ -68,6 +73,8 @@ def main():
                 ("mxfp8_fc2", lambda: gemm.mxfp8_gemm(aq, asf, w2q, w2sf, E, be, nmb, h), fl2),
                 ("mxfp8_fc2_pair", lambda: gemm.mxfp8_gemm(aq, asf, w2q, w2sf, E, be, nmb, h,
                                                            pair=True), fl2),
+                ("mxfp8_fc2_pair_wide", lambda: gemm.mxfp8_gemm(aq, asf, w2q, w2sf, E, be, nmb,
+                                                                h, pair=True, wide=True), fl2),
                 ("mxfp8_quant_x", lambda: gemm.mxfp8_quantize(x), 0.0)):
             ms = timed(fn)
             out[name] = {"ms": round(ms, 3)}
