@@ -592,8 +592,9 @@ def main():
     ap.add_argument("--precision", default="bf16", choices=["bf16", "mxfp8"],
                     help="forward expert GEMMs: bf16 (headline) or MXFP8 (block-scaled "
                          "tcgen05; backward stays bf16)")
-    ap.add_argument("--sync-free", action="store_true",
-                    help="EP: plan the exchange on the device (no host read of the counts)")
+    ap.add_argument("--sync-free", action=argparse.BooleanOptionalAction, default=True,
+                    help="EP: plan the exchange on the device (no host read of the counts; "
+                         "worst-case static buffers). Default on: +2%% at EP=4 (measured)")
     ap.add_argument("--graph", action="store_true",
                     help="capture the whole fwd+bwd step in a CUDA graph (EP: implies "
                          "--sync-free)")

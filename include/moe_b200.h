@@ -256,6 +256,11 @@ int moe_gg_gemm_f32(const void* a, const void* b, int a_rows, int max_rows, int 
  * interleave (row remap fused into the quantisation). */
 int moe_mxfp8_quantize(const void* x, long long ldx, int rows, int K, void* codes,
                        long long ldc, void* sf_plain, void* sf_tiled, int w1_m, void* stream);
+/* transposing ("column twin", quant.py:195-200) quantisation: x [B, R, C] -> codes
+ * [B, C, R], 1x32 blocks along R (the dgrad / wgrad K dimension), tiled scales of the
+ * [B*C, R] operand (sf_plain optional [B*C, R/32]). */
+int moe_mxfp8_quantize_t(const void* x, int B, int R, int C, void* codes, void* sf_tiled,
+                         void* sf_plain, void* stream);
 /* block-scaled tcgen05 grouped GEMMs (kind::mxf8f6f4, UMMA 128x128x32): bf16 output, and
  * fc1 + SwiGLU with the activation re-quantised to MXFP8 in the epilogue (fc2's A operand);
  * flags bit 0: CTA-pair engine (cta_group::2; expert blocks 256-row aligned). flags bit 1:
@@ -265,6 +270,14 @@ int moe_mxfp8_quantize(const void* x, long long ldx, int rows, int K, void* code
 int moe_gg_mxfp8_gemm(const void* a, const void* sfa, int a_rows, int max_rows, int K, int N,
                       const void* b, const void* sfb, int num_experts, const int* block_expert,
                       const int* num_m_blocks, void* out, int flags, void* stream);
+/* fc2 dgrad + SwiGLU backward on MXFP8 operands (dO [rows, h], W2^T [E*m, h]); writes bf16
+ * d_preact and d_preact quantised along 2m (fc1 dgrad's A operand, then moe_gg_mxfp8_gemm
+ * with W1^T [E*h, 2m] codes from moe_mxfp8_quantize_t). */
+int moe_gg_mxfp8_fc2_dgrad(const void* doq, const void* sfd, int a_rows, int max_rows, int h,
+                           int m, const void* w2tq, const void* sfw, int num_experts,
+                           const int* block_expert, const int* num_m_blocks, const void* preact,
+                           void* d_preact, void* dpre_q, void* dpre_sf, int flags,
+                           void* stream);
 int moe_gg_mxfp8_fc1(const void* xq, const void* sfx, int a_rows, int max_rows, int h, int m,
                      const void* w1q, const void* sfw, int num_experts, const int* block_expert,
                      const int* num_m_blocks, void* preact, void* act, void* act_q,

@@ -73,8 +73,10 @@ SIGNATURES: dict[str, list] = {
     "moe_stash_copy": [P, L, P, I, L, P, P, I, I, I, P],
     # MXFP8 (csrc/mxfp8.cu, csrc/grouped_gemm_mxfp8.cu)
     "moe_mxfp8_quantize": [P, L, I, I, P, L, P, P, I, P],
+    "moe_mxfp8_quantize_t": [P, I, I, I, P, P, P, P],
     "moe_gg_mxfp8_gemm": [P, P, I, I, I, I, P, P, I, P, P, P, I, P],
     "moe_gg_mxfp8_fc1": [P, P, I, I, I, I, P, P, I, P, P, P, P, P, P, I, P],
+    "moe_gg_mxfp8_fc2_dgrad": [P, P, I, I, I, I, P, P, I, P, P, P, P, P, P, I, P],
     # grouped GEMM (csrc/grouped_gemm.cu)
     "moe_gg_fc1_fwd": [P, P, I, I, I, I, I, P, P, P, P, P, I, P],
     "moe_gg_fc2_fwd": [P, P, I, I, I, I, I, P, P, P, I, P],

@@ -42,8 +42,11 @@ constexpr int TMEM_COLS = 512;  // 2 accumulator stages x 256 fp32 columns
 // ~13% on fc1+SwiGLU (the extra warps share the MMA issuer's SMSP), so 4 it is.
 constexpr int EPI_WARPS = 4;
 constexpr int EPI_HALVES = EPI_WARPS / 4;
-constexpr int EPI_COLS = BN / EPI_HALVES;  // 128 columns per epilogue warp
-constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
+// Weight-gradient (grouped-K) kernels use 8 epilogue warps: with few token rows per expert
+// (DeepSeek-shape EP=1: 128) each output tile has almost no MMA work and the kernel is a
+// TMEM -> HBM drain, which 4 warps cannot keep busy.
+template <bool GROUPED_K>
+constexpr int epi_warps() { return GROUPED_K ? 8 : EPI_WARPS; }
 constexpr int BAND_M = 16;  // raster: 16 M units share each swept n-block (L2 reuse)
 
 template <int CG>
@@ -221,7 +224,7 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
 }
 
 template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI, int CG>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K>(), 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                         const __grid_constant__ CUtensorMap tmap_b, const Params p) {
   using C = Cfg<CG>;
@@ -250,7 +253,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], EPI_WARPS * CG);
+      mbar_init(&tempty_bar[s], epi_warps<GROUPED_K>() * CG);
     }
     fence_mbar_init();
     fence_async_shared();
@@ -389,7 +392,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int q = warp & 3;
     const int half = (warp - 2) / 4;
     uint8_t* stage = smem + C::STAGES * C::STAGE + 256 + (warp - 2) * SCATTER_STAGE;
-    const int cb = half * EPI_COLS;  // this warp's first tile column
+    constexpr int EC = BN / (epi_warps<GROUPED_K>() / 4);  // tile columns per epilogue warp
+    const int cb = half * EC;  // this warp's first tile column
     const int row_local = q * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     int acc = 0;
@@ -405,13 +409,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                              tl.expert * p.out_expert_stride + row * p.ldo + tl.n0 + cb;
           const int4 z = make_int4(0, 0, 0, 0);
 #pragma unroll 4
-          for (int c = 0; c < EPI_COLS / 8; ++c) reinterpret_cast<int4*>(o)[c] = z;
+          for (int c = 0; c < EC / 8; ++c) reinterpret_cast<int4*>(o)[c] = z;
         } else if constexpr (EPI == EPI_F32) {
           float* o = reinterpret_cast<float*>(p.out) + tl.expert * p.out_expert_stride +
                      row * p.ldo + tl.n0 + cb;
           const int4 z = make_int4(0, 0, 0, 0);
 #pragma unroll 4
-          for (int c = 0; c < EPI_COLS / 4; ++c) reinterpret_cast<int4*>(o)[c] = z;
+          for (int c = 0; c < EC / 4; ++c) reinterpret_cast<int4*>(o)[c] = z;
         }
         continue;
       }
@@ -435,7 +439,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if constexpr (EPI == EPI_BF16 || EPI == EPI_F32) {
         const long long ebase = GROUPED_K ? tl.expert * p.out_expert_stride : 0;
 #pragma unroll 1
-        for (int c = 0; c < EPI_COLS / 32; ++c) {
+        for (int c = 0; c < EC / 32; ++c) {
           const int col = cb + c * 32;
           uint32_t r[32];
           tmem_ld_32x32b_x32(t_base + col, r);
@@ -495,7 +499,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __nv_bfloat16* act =
             reinterpret_cast<__nv_bfloat16*>(p.out2) + row * p.ldo2 + (tl.n0 >> 1) + (cb >> 1);
 #pragma unroll 1
-        for (int c = 0; c < EPI_COLS / 64; ++c) {
+        for (int c = 0; c < EC / 64; ++c) {
           uint32_t g[32], u[32];
           tmem_ld_32x32b_x32(t_base + (cb >> 1) + c * 32, g);
           tmem_ld_32x32b_x32(t_base + 128 + (cb >> 1) + c * 32, u);
@@ -528,7 +532,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const __nv_bfloat16* pre_row = p.aux + row * p.ld_aux;
         __nv_bfloat16* dpre_row = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo;
 #pragma unroll 1
-        for (int c = 0; c < EPI_COLS / 32; ++c) {
+        for (int c = 0; c < EC / 32; ++c) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(t_base + cb + c * 32, r);
           const int j0 = tl.n0 + cb + c * 32;
@@ -539,7 +543,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             gv[v] = pre_g[v];
             uv[v] = pre_u[v];
           }
-          if (c + 1 < EPI_COLS / 32) {  // prefetch the next chunk's pre-activation
+          if (c + 1 < EC / 32) {  // prefetch the next chunk's pre-activation
             const int j1 = j0 + 32;
             const long long pos1 = (long long)(j1 >> 7) * 256 + (j1 & 127);
 #pragma unroll
@@ -676,7 +680,7 @@ static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params&
   grid -= grid % CG;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.blockDim = dim3(64 + 32 * epi_warps<GROUPED_K>());
   cfg.dynamicSmemBytes = smem_bytes<EPI, GROUPED_K, CG>();
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];

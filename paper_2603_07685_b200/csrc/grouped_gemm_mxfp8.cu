@@ -59,7 +59,16 @@ template <bool WIDE>
 constexpr int epi_warps() { return WIDE ? 8 : 4; }
 constexpr int BAND_M = 16;
 
-enum Epi : int { EPI_BF16 = 0, EPI_SWIGLU_Q = 1 };
+enum Epi : int { EPI_BF16 = 0, EPI_SWIGLU_Q = 1, EPI_DSWIGLU_Q = 2 };
+
+__device__ __forceinline__ int e8m0_exp(float amax) {
+  if (!(amax > 0.f)) return -127;
+  int q;
+  const float f = frexpf(amax, &q);
+  int e = q - 9 + (f > 0.875f ? 1 : 0);
+  return e < -127 ? -127 : (e > 127 ? 127 : e);
+}
+
 
 struct Params {
   const int* num_m_blocks;
@@ -73,7 +82,36 @@ struct Params {
   uint8_t* act_q;      // EPI_SWIGLU_Q: E4M3 codes [rows, m]
   uint8_t* act_sf;     // EPI_SWIGLU_Q: tiled scales for K = m
   int m;
+  // EPI_DSWIGLU_Q (fc2 dgrad): out = d_preact [rows, 2m] (interleaved like preact),
+  // aux = preact, act_q / act_sf = d_preact quantised along 2m (fc1 dgrad's A operand)
+  const __nv_bfloat16* aux;
 };
+
+// E4M3-quantise 32 values (one MX block), write 32 codes + the scale byte (tiled layout).
+__device__ __forceinline__ void quant_block32(const float (&v)[32], uint8_t* codes_dst,
+                                              uint8_t* sf, long long row, int kb,
+                                              int kblocks) {
+  float amax = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) amax = fmaxf(amax, fabsf(v[i]));
+  const int e = e8m0_exp(amax);
+  const float inv = __int_as_float((127 - e) << 23);
+  uint32_t qv[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
+        make_float2(v[4 * k] * inv, v[4 * k + 1] * inv), __NV_SATFINITE, __NV_E4M3);
+    const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
+        make_float2(v[4 * k + 2] * inv, v[4 * k + 3] * inv), __NV_SATFINITE, __NV_E4M3);
+    qv[k] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+  }
+  int4* qd = reinterpret_cast<int4*>(codes_dst);
+  qd[0] = make_int4(qv[0], qv[1], qv[2], qv[3]);
+  qd[1] = make_int4(qv[4], qv[5], qv[6], qv[7]);
+  const int rr = static_cast<int>(row & 127);
+  sf[((row >> 7) * (kblocks >> 2) + (kb >> 2)) * 512 + (rr & 31) * 16 + (rr >> 5) * 4 +
+     (kb & 3)] = static_cast<uint8_t>(e + 127);
+}
 
 // 32 rows x 16 B, no swizzle, rows contiguous (core matrices 8 x 16 B, SBO 128 B)
 __device__ __forceinline__ uint64_t sf_desc(uint32_t saddr) {
@@ -156,13 +194,6 @@ __device__ __forceinline__ void umma_mx(uint32_t tmem_d, uint64_t adesc, uint64_
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
 
-__device__ __forceinline__ int e8m0_exp(float amax) {
-  if (!(amax > 0.f)) return -127;
-  int q;
-  const float f = frexpf(amax, &q);
-  int e = q - 9 + (f > 0.875f ? 1 : 0);
-  return e < -127 ? -127 : (e > 127 ? 127 : e);
-}
 
 struct Tile {
   int expert, m0, n0;
@@ -369,6 +400,69 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<WIDE>(), 1)
             w.w = pack_bf16x2(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
             reinterpret_cast<int4*>(o + c * 32)[v] = w;
           }
+        }
+      } else if constexpr (EPI == EPI_DSWIGLU_Q) {
+        // accumulator = dL/d(act) for activation columns [n0, n0 + BN); recompute the SwiGLU
+        // derivative from the saved pre-activation (interleaved gate/up, 128-column blocks)
+        const __nv_bfloat16* pre_row = p.aux + row * (2LL * p.m);
+        __nv_bfloat16* dpre_row = reinterpret_cast<__nv_bfloat16*>(p.out) + row * (2LL * p.m);
+        const int kblocks = 2 * p.m / 32;
+#pragma unroll 1
+        for (int c = part * (BN / 32 / NPART); c < (part + 1) * (BN / 32 / NPART); ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_base + c * 32, r);
+          const int j0 = tl.n0 + c * 32;
+          const long long pos = (long long)(j0 >> 7) * 256 + (j0 & 127);
+          int4 gv[4], uv[4];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            gv[v] = reinterpret_cast<const int4*>(pre_row + pos)[v];
+            uv[v] = reinterpret_cast<const int4*>(pre_row + pos + 128)[v];
+          }
+          tmem_ld_wait();
+          float dg[32], du[32];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const uint32_t* sg = reinterpret_cast<const uint32_t*>(&gv[v]);
+            const uint32_t* su = reinterpret_cast<const uint32_t*>(&uv[v]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 gg = unpack_bf16x2(sg[j]);
+              const float2 uu = unpack_bf16x2(su[j]);
+              const int i = 8 * v + 2 * j;
+              const float a0 = __uint_as_float(r[i]), a1 = __uint_as_float(r[i + 1]);
+              const float s0 = 1.0f / (1.0f + __expf(-gg.x));
+              const float s1 = 1.0f / (1.0f + __expf(-gg.y));
+              dg[i] = a0 * uu.x * s0 * (1.0f + gg.x * (1.0f - s0));
+              dg[i + 1] = a1 * uu.y * s1 * (1.0f + gg.y * (1.0f - s1));
+              du[i] = a0 * gg.x * s0;
+              du[i + 1] = a1 * gg.y * s1;
+            }
+          }
+          // bf16 d_preact (the wgrad operand), then quantise the bf16 values
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            int4 wg, wu;
+            uint32_t* pg = reinterpret_cast<uint32_t*>(&wg);
+            uint32_t* pu = reinterpret_cast<uint32_t*>(&wu);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int i = 8 * v + 2 * j;
+              pg[j] = pack_bf16x2(dg[i], dg[i + 1]);
+              pu[j] = pack_bf16x2(du[i], du[i + 1]);
+              const float2 bg = unpack_bf16x2(pg[j]), bu = unpack_bf16x2(pu[j]);
+              dg[i] = bg.x;
+              dg[i + 1] = bg.y;
+              du[i] = bu.x;
+              du[i + 1] = bu.y;
+            }
+            reinterpret_cast<int4*>(dpre_row + pos)[v] = wg;
+            reinterpret_cast<int4*>(dpre_row + pos + 128)[v] = wu;
+          }
+          quant_block32(dg, p.act_q + row * (2LL * p.m) + pos, p.act_sf, row,
+                        static_cast<int>(pos / 32), kblocks);
+          quant_block32(du, p.act_q + row * (2LL * p.m) + pos + 128, p.act_sf, row,
+                        static_cast<int>((pos + 128) / 32), kblocks);
         }
       } else {
         // tile columns [0, BN/2) = gate rows g0 + [0, BN/2), [BN/2, BN) = the matching up
@@ -611,6 +705,40 @@ int moe_gg_mxfp8_fc1(const void* xq, const void* sfx, int a_rows, int max_rows, 
   p.m = m;
   return launch<EPI_SWIGLU_Q>(xq, a_rows, max_rows, w1q, num_experts, p, pair, wide,
                               static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// fc2 data-gradient fused with the SwiGLU backward, MXFP8 operands: A = dO codes [rows, h]
+// (1x32 along h), B = W2^T codes [E*m, h] (moe_mxfp8_quantize_t of W2 [E, h, m]). Writes
+// d_preact (bf16, preact's interleaved layout; the wgrad operand) and d_preact quantised
+// along 2m (codes + tiled scales: fc1 dgrad's A operand). Standard combine (no row scale).
+int moe_gg_mxfp8_fc2_dgrad(const void* doq, const void* sfd, int a_rows, int max_rows, int h,
+                           int m, const void* w2tq, const void* sfw, int num_experts,
+                           const int* block_expert, const int* num_m_blocks, const void* preact,
+                           void* d_preact, void* dpre_q, void* dpre_sf, int flags,
+                           void* stream) {
+  const int pair = flags & 1, wide = (flags >> 1) & 1;
+  if (h % BK || m % (wide ? 256 : 128) || max_rows % (BM * (pair ? 2 : 1)) ||
+      a_rows > max_rows || !dpre_q || !dpre_sf || !preact)
+    return kErrInvalidArg;
+  Params p{};
+  p.num_m_blocks = num_m_blocks;
+  p.block_expert = block_expert;
+  p.N = m;
+  p.K = h;
+  p.sfa = static_cast<const uint8_t*>(sfd);
+  p.sfb = static_cast<const uint8_t*>(sfw);
+  p.out = d_preact;
+  p.ldo = 2 * m;
+  p.aux = static_cast<const __nv_bfloat16*>(preact);
+  p.act_q = static_cast<uint8_t*>(dpre_q);
+  p.act_sf = static_cast<uint8_t*>(dpre_sf);
+  p.m = m;
+  return launch<EPI_DSWIGLU_Q>(doq, a_rows, max_rows, w2tq, num_experts, p, pair, wide,
+                               static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -88,6 +88,64 @@ __global__ void quant_kernel(const __nv_bfloat16* __restrict__ x, long long ldx,
   }
 }
 
+// Transposing quantisation ("column twin", the reference's with_column_twin quant.py:195-200):
+// x [B, R, C] bf16 -> codes [B, C, R] with 1x32 blocks along R, scales in the tiled layout
+// of the [B*C, R] operand. A CTA handles 32 rows x 256 columns of one batch: the tile is
+// staged in shared memory, then thread c quantises column c's 32 values and writes them as
+// one contiguous 32-byte run of the output row.
+__global__ void quant_t_kernel(const __nv_bfloat16* __restrict__ x, int B, int R, int C,
+                               uint8_t* __restrict__ codes, uint8_t* __restrict__ sf_tiled,
+                               uint8_t* __restrict__ sf_plain) {
+  __shared__ __nv_bfloat16 tile[32][256 + 8];
+  const int cblocks = (C + 255) / 256, rblocks = R / 32;
+  const long long nt = (long long)B * rblocks * cblocks;
+  for (long long id = blockIdx.x; id < nt; id += gridDim.x) {
+    const int b = static_cast<int>(id / ((long long)rblocks * cblocks));
+    const int rem = static_cast<int>(id % ((long long)rblocks * cblocks));
+    const int rb = rem / cblocks, cb = rem % cblocks;
+    const int r0 = rb * 32, c0 = cb * 256;
+    const __nv_bfloat16* src = x + ((long long)b * R + r0) * C + c0;
+    // 32 rows x 256 columns: each warp loads rows, 8 bf16 (16 B) per lane
+    for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
+      const int r = i / 32, v = i % 32;
+      if (c0 + v * 8 < C) {
+        const int4 w = ld_nc_v4(src + (long long)r * C + v * 8);
+        *reinterpret_cast<int4*>(&tile[r][v * 8]) = w;
+      }
+    }
+    __syncthreads();
+    const int c = c0 + threadIdx.x;
+    if (threadIdx.x < 256 && c < C) {
+      float f[32];
+      float amax = 0.f;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        f[r] = __bfloat162float(tile[r][threadIdx.x]);
+        amax = fmaxf(amax, fabsf(f[r]));
+      }
+      const int e = e8m0_exp(amax);
+      const float inv = __int_as_float((127 - e) << 23);
+      uint32_t out[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
+            make_float2(f[4 * q] * inv, f[4 * q + 1] * inv), __NV_SATFINITE, __NV_E4M3);
+        const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
+            make_float2(f[4 * q + 2] * inv, f[4 * q + 3] * inv), __NV_SATFINITE, __NV_E4M3);
+        out[q] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+      }
+      const long long orow = (long long)b * C + c;  // output row in [B*C, R]
+      int4* dst = reinterpret_cast<int4*>(codes + orow * R + r0);
+      dst[0] = make_int4(out[0], out[1], out[2], out[3]);
+      dst[1] = make_int4(out[4], out[5], out[6], out[7]);
+      const uint8_t sc = static_cast<uint8_t>(e + 127);
+      if (sf_tiled) sf_tiled[tiled_sf_offset(static_cast<int>(orow), rb, rblocks)] = sc;
+      if (sf_plain) sf_plain[orow * rblocks + rb] = sc;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace mx
 }  // namespace moe
 
@@ -109,6 +167,21 @@ extern "C" int moe_mxfp8_quantize(const void* x, long long ldx, int rows, int K,
   mx::quant_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const __nv_bfloat16*>(x), ldx, rows, K, static_cast<uint8_t*>(codes), ldc,
       static_cast<uint8_t*>(sf_plain), static_cast<uint8_t*>(sf_tiled), w1_m);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+extern "C" int moe_mxfp8_quantize_t(const void* x, int B, int R, int C, void* codes,
+                                    void* sf_tiled, void* sf_plain, void* stream) {
+  if (B < 1 || R % 128 || C % 8 || ((long long)B * C) % 128) return kErrInvalidArg;
+  const long long tiles = (long long)B * (R / 32) * ((C + 255) / 256);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = static_cast<int>(tiles < (long long)sms * 8 ? tiles : (long long)sms * 8);
+  mx::quant_t_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(x), B, R, C, static_cast<uint8_t*>(codes),
+      static_cast<uint8_t*>(sf_tiled), static_cast<uint8_t*>(sf_plain));
   MOE_LAUNCH_CHECK();
   return kOk;
 }

@@ -212,6 +212,19 @@ def mxfp8_quantize(x: torch.Tensor, rows_pad: int | None = None, plain: bool = F
     return codes, sf_t, sf_p
 
 
+def mxfp8_quantize_t(x: torch.Tensor, plain: bool = False):
+    """Transposing quantisation: x [B, R, C] (or [R, C]) bf16 -> (codes [B*C, R], tiled
+    scales, plain scales [B*C, R/32] or None), 1x32 blocks along R."""
+    x3 = x if x.dim() == 3 else x.unsqueeze(0)
+    b, r, c = x3.shape
+    codes = torch.empty((b * c, r), dtype=torch.uint8, device=x.device)
+    sf_t = torch.empty((b * c * r // 32,), dtype=torch.uint8, device=x.device)
+    sf_p = torch.empty((b * c, r // 32), dtype=torch.uint8, device=x.device) if plain else None
+    _lib.call("moe_mxfp8_quantize_t", x3.data_ptr(), b, r, c, codes.data_ptr(), sf_t.data_ptr(),
+              _ptr(sf_p), _stream())
+    return codes, sf_t, sf_p
+
+
 def mxfp8_quantize_w1(w1: torch.Tensor, wide: bool = False):
     """bf16-engine W1 [E, 2m, h] (128-row gate/up interleave) -> MXFP8 codes/scales for the
     MXFP8 fc1: the narrow (128-wide tile) engine wants 64-row gate/up blocks (re-interleaved
@@ -267,3 +280,21 @@ def mxfp8_fc1(xq, sfx, w1q, sfw, num_experts, block_expert, num_m_blocks, m, max
               num_m_blocks.data_ptr(), preact.data_ptr(), _ptr(act), act_q.data_ptr(),
               act_sf.data_ptr(), int(pair) | (int(wide) << 1), _stream())
     return preact, act, act_q, act_sf
+
+
+def mxfp8_fc2_dgrad(doq, sfd, w2tq, sfw, num_experts, block_expert, num_m_blocks, preact,
+                    max_rows=None, pair=False, wide=False):
+    """fc2 dgrad + SwiGLU backward on MXFP8 operands. Returns (d_preact bf16 [rows, 2m],
+    d_preact codes [rows, 2m], tiled scales) -- the last two are fc1 dgrad's A operand."""
+    a_rows, h = doq.shape
+    rows = a_rows if max_rows is None else max_rows
+    m2 = preact.shape[1]
+    dev = doq.device
+    d_pre = torch.empty((rows, m2), dtype=torch.bfloat16, device=dev)
+    dq = torch.empty((rows, m2), dtype=torch.uint8, device=dev)
+    dsf = torch.zeros((rows * m2 // 32,), dtype=torch.uint8, device=dev)
+    _lib.call("moe_gg_mxfp8_fc2_dgrad", doq.data_ptr(), sfd.data_ptr(), a_rows, rows, h, m2 // 2,
+              w2tq.data_ptr(), sfw.data_ptr(), num_experts, block_expert.data_ptr(),
+              num_m_blocks.data_ptr(), preact.data_ptr(), d_pre.data_ptr(), dq.data_ptr(),
+              dsf.data_ptr(), int(pair) | (int(wide) << 1), _stream())
+    return d_pre, dq, dsf

@@ -34,9 +34,10 @@ class MoEConfig:
     pad_to_capacity: bool = False     # --moe-pad-expert-input-to-capacity
     mem_efficient: bool = False       # combine_mem_efficient (prob folded into act)
     shared_ffn_hidden: int = 0        # DeepSeek shared expert width (0 = none)
-    # forward expert GEMMs: "bf16", or "mxfp8" (the paper's Blackwell recipe, 1x32 E8M0
-    # blocks, quant.py:62-64; block-scaled tcgen05 MMA, activations re-quantised in fc1's
-    # epilogue). The backward GEMMs stay bf16.
+    # expert GEMMs: "bf16", or "mxfp8" (the paper's Blackwell recipe, 1x32 E8M0 blocks,
+    # quant.py:62-64; block-scaled tcgen05 MMA): forward fc1/fc2 and the data-gradient
+    # GEMMs (operands re-quantised in the producing epilogues, weights transposed-quantised
+    # for dgrad); the weight-gradient GEMMs stay bf16.
     precision: str = "bf16"
 
     def capacity(self, num_tokens: int) -> int:
@@ -90,10 +91,17 @@ class _MoEFunction(torch.autograd.Function):
             dprob = ops.dprob_from_partials(plan, part)
         else:
             d_o, dprob = ops.combine_backward(dy, plan, o, r.topk_prob)
-            d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, plan.block_expert, plan.num_m_blocks,
-                                      pair=plan.pair)
+            if cfg.precision == "mxfp8":
+                d_pre, dq = _mxfp8_fc2_dgrad(d_o, w2, preact, plan, e)
+            else:
+                d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, plan.block_expert,
+                                          plan.num_m_blocks, pair=plan.pair)
         dw2 = gemm.wgrad(d_o, act, plan.off_pad, e)
-        dxp = gemm.fc1_dgrad(d_pre, w1, plan.block_expert, plan.num_m_blocks, pair=plan.pair)
+        if cfg.precision == "mxfp8":
+            dxp = _mxfp8_fc1_dgrad(dq, w1, plan, e)
+        else:
+            dxp = gemm.fc1_dgrad(d_pre, w1, plan.block_expert, plan.num_m_blocks,
+                                 pair=plan.pair)
         dw1 = gemm.wgrad(d_pre, xp, plan.off_pad, e)
         aux_scale = None if daux is None else daux.float()
         dw_r, dx_router = ops.router_backward(x, w_r_pad, r, dprob, cfg.score,
@@ -115,7 +123,7 @@ def _mxfp8_experts(xp, w1, w2, plan, e):
     h = xp.shape[1]
     # 256-wide tiles (single TMEM accumulator, 8 epilogue warps) when the shapes allow:
     # measured 1.2x (fc1) / 1.9x (fc2) the bf16 engine at Mixtral shape
-    wide = (2 * m) % 256 == 0 and h % 256 == 0
+    wide = _mxfp8_wide(m, h)
     xq, xsf, _ = gemm.mxfp8_quantize(xp)
     w1q, w1sf = gemm.mxfp8_quantize_w1(w1, wide=wide)
     w2q, w2sf = gemm.mxfp8_quantize_weight(w2)
@@ -124,6 +132,29 @@ def _mxfp8_experts(xp, w1, w2, plan, e):
     o = gemm.mxfp8_gemm(aq, asf, w2q, w2sf, e, plan.block_expert, plan.num_m_blocks, h,
                         pair=plan.pair, wide=wide)
     return preact, act, o
+
+
+def _mxfp8_wide(m, h):
+    return (2 * m) % 256 == 0 and m % 256 == 0 and h % 256 == 0
+
+
+def _mxfp8_fc2_dgrad(d_o, w2, preact, plan, e):
+    """fc2 dgrad + dSwiGLU in MXFP8 (dO quantised along h, W2 transposed-quantised along
+    h). Returns the bf16 d_preact (wgrad operand) and its MXFP8 copy (fc1 dgrad operand)."""
+    m, h = w2.shape[2], w2.shape[1]
+    wide = _mxfp8_wide(m, h)
+    doq, dosf, _ = gemm.mxfp8_quantize(d_o)
+    w2tq, w2tsf, _ = gemm.mxfp8_quantize_t(w2)
+    d_pre, dq, dsf = gemm.mxfp8_fc2_dgrad(doq, dosf, w2tq, w2tsf, e, plan.block_expert,
+                                          plan.num_m_blocks, preact, pair=plan.pair, wide=wide)
+    return d_pre, (dq, dsf)
+
+
+def _mxfp8_fc1_dgrad(dq, w1, plan, e):
+    h, m2 = w1.shape[2], w1.shape[1]
+    w1tq, w1tsf, _ = gemm.mxfp8_quantize_t(w1)
+    return gemm.mxfp8_gemm(dq[0], dq[1], w1tq, w1tsf, e, plan.block_expert, plan.num_m_blocks,
+                           h, pair=plan.pair, wide=_mxfp8_wide(m2 // 2, h))
 
 
 def shared_expert_forward(x, w1s, w2s):

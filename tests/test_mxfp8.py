@@ -131,3 +131,63 @@ def test_w1_remap_quantisation_equals_interleave_then_quantise():
     a = gemm.mxfp8_quantize_w1(gemm.interleave_gate_up(gate, up))
     b = gemm.mxfp8_quantize_weight(gemm.interleave_gate_up_mx(gate, up))
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+@pytest.mark.gpu
+def test_transposing_quantiser_equals_quantise_of_transpose():
+    from paper_2603_07685_b200 import gemm
+
+    dev = torch.device("cuda", 0)
+    g = torch.Generator().manual_seed(9)
+    x = (torch.randn((3, 256, 384), generator=g) * 2).to(torch.bfloat16)
+    codes, sf_t, sf_p = gemm.mxfp8_quantize_t(x.to(dev), plain=True)
+    xt = x.transpose(1, 2).reshape(3 * 384, 256).float().numpy().astype(np.float64)
+    want_c, want_s = M.quantize_mxfp8(xt)
+    assert np.array_equal(codes.cpu().numpy(), want_c)
+    assert np.array_equal(sf_p.cpu().numpy(), want_s)
+    assert np.array_equal(sf_t.cpu().numpy(), M.tile_scales(want_s, 3 * 384))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pair,wide", [(False, False), (True, True)], ids=["cta1", "pair_wide"])
+def test_mxfp8_dgrad_chain_matches_dequant_oracle(pair, wide):
+    """fc2 dgrad + dSwiGLU (fused d_preact quantisation) and fc1 dgrad on MXFP8 operands vs
+    the dequantise-then-multiply oracle; the fused quantisation is bit-exact."""
+    from paper_2603_07685_b200 import gemm
+
+    dev = torch.device("cuda", 0)
+    g = torch.Generator().manual_seed(17)
+    E, h, m = 2, 256, 256
+    rows_e = [256, 512] if pair else [128, 256]
+    be, nmb, rows = _plan(rows_e, dev)
+    d_o = torch.randn((rows, h), generator=g).to(torch.bfloat16)
+    preact = torch.randn((rows, 2 * m), generator=g).to(torch.bfloat16)
+    w2 = (torch.randn((E, h, m), generator=g) * m ** -0.5).to(torch.bfloat16)
+    w1 = (torch.randn((E, 2 * m, h), generator=g) * h ** -0.5).to(torch.bfloat16)
+    doq, dosf, dosp = gemm.mxfp8_quantize(d_o.to(dev), plain=True)
+    w2tq, w2tsf, w2tsp = gemm.mxfp8_quantize_t(w2.to(dev), plain=True)
+    d_pre, dq, dsf = gemm.mxfp8_fc2_dgrad(doq, dosf, w2tq, w2tsf, E, be, nmb, preact.to(dev),
+                                          pair=pair, wide=wide)
+    w1tq, w1tsf, w1tsp = gemm.mxfp8_quantize_t(w1.to(dev), plain=True)
+    dxp = gemm.mxfp8_gemm(dq, dsf, w1tq, w1tsf, E, be, nmb, h, pair=pair, wide=wide)
+    torch.cuda.synchronize()
+    off = np.cumsum([0] + rows_e)
+    dod = M.dequantize_mxfp8(doq.cpu().numpy()[:rows], dosp.cpu().numpy())
+    w2t = M.dequantize_mxfp8(w2tq.cpu().numpy(), w2tsp.cpu().numpy()).reshape(E, m, h)
+    G = np.concatenate([dod[off[e]:off[e + 1]] @ w2t[e].T for e in range(E)])
+    pg, pu = gemm.deinterleave_cols(preact)
+    gg, uu = pg.double().numpy(), pu.double().numpy()
+    s = 1 / (1 + np.exp(-gg))
+    dg_ref = G * uu * s * (1 + gg * (1 - s))
+    du_ref = G * gg * s
+    got_g, got_u = gemm.deinterleave_cols(d_pre)
+    rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)  # noqa: E731
+    assert rel(got_g.double().cpu().numpy(), dg_ref) < 5e-3
+    assert rel(got_u.double().cpu().numpy(), du_ref) < 5e-3
+    codes, scales = M.quantize_mxfp8(d_pre.float().cpu().numpy().astype(np.float64))
+    assert np.array_equal(dq.cpu().numpy(), codes)
+    assert np.array_equal(dsf.cpu().numpy(), M.tile_scales(scales, rows))
+    dpd = M.dequantize_mxfp8(codes, scales)
+    w1t = M.dequantize_mxfp8(w1tq.cpu().numpy(), w1tsp.cpu().numpy()).reshape(E, h, 2 * m)
+    dx_ref = np.concatenate([dpd[off[e]:off[e + 1]] @ w1t[e].T for e in range(E)])
+    assert rel(dxp.double().cpu().numpy(), dx_ref) < 5e-3
