@@ -78,8 +78,11 @@ class ClockSampler:
     def start(self):
         import shutil
 
+        ms = os.environ.get("MOE_BENCH_SMI_MS", "100")
+        if ms == "0":
+            return
         cmd = ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-               "-i", str(self.gpu), "-lms", "50"]
+               "-i", str(self.gpu), "-lms", ms]
         if shutil.which("stdbuf"):
             cmd = ["stdbuf", "-oL"] + cmd
         try:
