@@ -278,6 +278,12 @@ int moe_gg_mxfp8_fc2_dgrad(const void* doq, const void* sfd, int a_rows, int max
                            const int* block_expert, const int* num_m_blocks, const void* preact,
                            void* d_preact, void* dpre_q, void* dpre_sf, int flags,
                            void* stream);
+/* weight gradient on MXFP8 operands (grouped over experts along K = token rows):
+ * dw[e] (bf16 [M, N]) = sum_{r in [k_off[e], k_off[e+1])} A[r, :]^T B[r, :], with A^T / B^T
+ * as codes [M, K] / [N, K] from moe_mxfp8_quantize_t (blocks along the token rows). */
+int moe_gg_mxfp8_wgrad(const void* at, const void* sfa, const void* bt, const void* sfb, int K,
+                       int M, int N, int num_experts, const int* k_off, void* dw, int flags,
+                       void* stream);
 int moe_gg_mxfp8_fc1(const void* xq, const void* sfx, int a_rows, int max_rows, int h, int m,
                      const void* w1q, const void* sfw, int num_experts, const int* block_expert,
                      const int* num_m_blocks, void* preact, void* act, void* act_q,

@@ -85,6 +85,12 @@ struct Params {
   // EPI_DSWIGLU_Q (fc2 dgrad): out = d_preact [rows, 2m] (interleaved like preact),
   // aux = preact, act_q / act_sf = d_preact quantised along 2m (fc1 dgrad's A operand)
   const __nv_bfloat16* aux;
+  int num_experts_gk;
+  // grouped-K (weight gradients): expert e reduces K rows [k_off[e], k_off[e+1]) of the
+  // transposed operands A^T [M, K], B^T [N, K]; out[e] = M x N at out + e * out_stride
+  const int* k_off;
+  int M;
+  long long out_stride;
 };
 
 // E4M3-quantise 32 values (one MX block), write 32 codes + the scale byte (tiled layout).
@@ -196,12 +202,25 @@ __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)
 
 
 struct Tile {
-  int expert, m0, n0;
+  int expert, m0, n0, k0, nkb;
 };
-template <int CG, int BN>
+template <int CG, int BN, bool GK>
 __device__ __forceinline__ void decode_tile(const Params& p, int t, int num_units, int rank,
                                             Tile& tl) {
   const int nb_count = p.N / BN;
+  if constexpr (GK) {
+    const int per_e = (p.M / (BM * CG)) * nb_count;
+    const int e = t / per_e, rem = t - e * per_e;
+    const int mu = rem / nb_count, nb = rem - mu * nb_count;
+    tl.expert = e;
+    tl.m0 = mu * BM * CG + rank * BM;
+    tl.n0 = nb * BN;
+    tl.k0 = __ldg(p.k_off + e);
+    tl.nkb = (__ldg(p.k_off + e + 1) - tl.k0) / BK;
+    return;
+  }
+  tl.k0 = 0;
+  tl.nkb = p.K / BK;
   const int band = t / (BAND_M * nb_count);
   const int rem = t - band * BAND_M * nb_count;
   const int u0 = band * BAND_M;
@@ -213,7 +232,7 @@ __device__ __forceinline__ void decode_tile(const Params& p, int t, int num_unit
   tl.n0 = nb * BN;
 }
 
-template <int EPI, int CG, bool WIDE>
+template <int EPI, int CG, bool WIDE, bool GK>
 __global__ void __launch_bounds__(64 + 32 * epi_warps<WIDE>(), 1)
     mxfp8_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                       const __grid_constant__ CUtensorMap tmap_b,
@@ -273,9 +292,9 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<WIDE>(), 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int num_units = *p.num_m_blocks / CG;
-  const int num_tiles = num_units * (p.N / BN);
-  const int num_kb = p.K / BK;
+  const int num_units = GK ? 0 : *p.num_m_blocks / CG;
+  const int num_tiles = GK ? p.num_experts_gk * (p.M / (BM * CG)) * (p.N / BN)
+                           : num_units * (p.N / BN);
   const int kst = p.K / BK;  // K stages per 128-row scale tile
   const int first = blockIdx.x / CG, stride = gridDim.x / CG;
 
@@ -285,9 +304,11 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<WIDE>(), 1)
       uint32_t ph = 0;
       for (int t = first; t < num_tiles; t += stride) {
         Tile tl;
-        decode_tile<CG, BN>(p, t, num_units, rank, tl);
-        const int brow = tl.expert * p.N + tl.n0;  // first B row of the (full) N tile
-        for (int kb = 0; kb < num_kb; ++kb) {
+        decode_tile<CG, BN, GK>(p, t, num_units, rank, tl);
+        // first B row of the (full) N tile: stacked weights [E*N, K], or B^T [N, K] (GK)
+        const int brow = GK ? tl.n0 : tl.expert * p.N + tl.n0;
+        for (int kq = 0; kq < tl.nkb; ++kq) {
+          const int kb = tl.k0 / BK + kq;  // global K stage
           mbar_wait(&empty_bar[s], ph ^ 1);
           if (leader) mbar_arrive_expect_tx(&full_bar[s], C::STAGE * CG);
           auto load = [&](void* dst, const CUtensorMap* tm, int x, int y) {
@@ -319,10 +340,17 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<WIDE>(), 1)
       uint32_t acc_ph = 0;
       const uint32_t t_sfa = tmem_base + SF_COL, t_sfb = tmem_base + SF_COL + 4;
       for (int t = first; t < num_tiles; t += stride) {
+        int nkb = p.K / BK;
+        if constexpr (GK) {
+          Tile tl;
+          decode_tile<CG, BN, GK>(p, t, num_units, rank, tl);
+          nkb = tl.nkb;
+          if (nkb == 0) continue;  // expert without rows: the epilogue writes zeros
+        }
         mbar_wait(&tempty_bar[acc], acc_ph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full_bar[s], ph);
           tc_fence_after();
           // scale chunks smem -> TMEM (ordered before the MMAs below: same tcgen05 pipe;
@@ -379,13 +407,23 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<WIDE>(), 1)
     uint32_t acc_ph = 0;
     for (int t = first; t < num_tiles; t += stride) {
       Tile tl;
-      decode_tile<CG, BN>(p, t, num_units, rank, tl);
+      decode_tile<CG, BN, GK>(p, t, num_units, rank, tl);
       const long long row = tl.m0 + row_local;
+      if constexpr (GK) {
+        if (tl.nkb == 0) {  // weight gradient of an expert without rows: exactly zero
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) +
+                             tl.expert * p.out_stride + row * p.ldo + tl.n0;
+          for (int c = part * (BN / 8 / NPART); c < (part + 1) * (BN / 8 / NPART); ++c)
+            reinterpret_cast<int4*>(o)[c] = make_int4(0, 0, 0, 0);
+          continue;
+        }
+      }
       mbar_wait(&tfull_bar[acc], acc_ph);
       tc_fence_after();
       const uint32_t t_base = tmem_base + lane_off + acc * BN;
       if constexpr (EPI == EPI_BF16) {
-        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo + tl.n0;
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) +
+                           (GK ? tl.expert * p.out_stride : 0) + row * p.ldo + tl.n0;
 #pragma unroll 1
         for (int c = part * (BN / 32 / NPART); c < (part + 1) * (BN / 32 / NPART); ++c) {
           uint32_t r[32];
@@ -592,12 +630,12 @@ static int make_tmap_u8(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_
   return r == CUDA_SUCCESS ? kOk : kErrCuda;
 }
 
-template <int EPI, int CG, bool WIDE>
+template <int EPI, int CG, bool WIDE, bool GK>
 static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tsa,
                      const CUtensorMap& tsb, const Params& p, int max_m_blocks,
                      cudaStream_t stream) {
   using C = Cfg<CG, WIDE>;
-  auto kern = mxfp8_gemm_kernel<EPI, CG, WIDE>;
+  auto kern = mxfp8_gemm_kernel<EPI, CG, WIDE, GK>;
   static bool attr = false;
   if (!attr) {
     MOE_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -607,7 +645,8 @@ static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtenso
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int tiles = (max_m_blocks / CG) * (p.N / C::BN);
+  const int tiles = GK ? p.num_experts_gk * (p.M / (BM * CG)) * (p.N / C::BN)
+                     : (max_m_blocks / CG) * (p.N / C::BN);
   if (tiles <= 0) return kOk;
   int grid = tiles * CG < sms ? tiles * CG : sms;
   grid -= grid % CG;
@@ -644,10 +683,30 @@ static int launch(const void* a, int a_rows, int max_rows, const void* b, int nu
   if ((st = make_tmap_u8(&tsb, p.sfb, 256, 2 * sfb_chunks, 256, 2, false))) return st;
   const int mb = max_rows / BM;
   if (pair)
-    return wide ? launch_cg<EPI, 2, true>(ta, tb, tsa, tsb, p, mb, stream)
-                : launch_cg<EPI, 2, false>(ta, tb, tsa, tsb, p, mb, stream);
-  return wide ? launch_cg<EPI, 1, true>(ta, tb, tsa, tsb, p, mb, stream)
-              : launch_cg<EPI, 1, false>(ta, tb, tsa, tsb, p, mb, stream);
+    return wide ? launch_cg<EPI, 2, true, false>(ta, tb, tsa, tsb, p, mb, stream)
+                : launch_cg<EPI, 2, false, false>(ta, tb, tsa, tsb, p, mb, stream);
+  return wide ? launch_cg<EPI, 1, true, false>(ta, tb, tsa, tsb, p, mb, stream)
+              : launch_cg<EPI, 1, false, false>(ta, tb, tsa, tsb, p, mb, stream);
+}
+
+// grouped-K weight gradient: A^T codes [M, K], B^T codes [N, K], K = token rows
+static int launch_wgrad(const void* at, const void* bt, Params p, int pair, int wide,
+                        cudaStream_t stream) {
+  CUtensorMap ta, tb, tsa, tsb;
+  int st;
+  const int cg = pair ? 2 : 1;
+  const int bn = wide ? 256 : 128;
+  if ((st = make_tmap_u8(&ta, at, p.K, p.M, BK, BM, true))) return st;
+  if ((st = make_tmap_u8(&tb, bt, p.K, p.N, BK, bn / cg, true))) return st;
+  const long long sfa_chunks = (long long)(p.M / BM) * (p.K / BK);
+  const long long sfb_chunks = (long long)(p.N / 128) * (p.K / BK);
+  if ((st = make_tmap_u8(&tsa, p.sfa, 256, 2 * sfa_chunks, 256, 2, false))) return st;
+  if ((st = make_tmap_u8(&tsb, p.sfb, 256, 2 * sfb_chunks, 256, 2, false))) return st;
+  if (pair)
+    return wide ? launch_cg<EPI_BF16, 2, true, true>(ta, tb, tsa, tsb, p, 0, stream)
+                : launch_cg<EPI_BF16, 2, false, true>(ta, tb, tsa, tsb, p, 0, stream);
+  return wide ? launch_cg<EPI_BF16, 1, true, true>(ta, tb, tsa, tsb, p, 0, stream)
+              : launch_cg<EPI_BF16, 1, false, true>(ta, tb, tsa, tsb, p, 0, stream);
 }
 
 }  // namespace mx8
@@ -739,6 +798,34 @@ int moe_gg_mxfp8_fc2_dgrad(const void* doq, const void* sfd, int a_rows, int max
   p.m = m;
   return launch<EPI_DSWIGLU_Q>(doq, a_rows, max_rows, w2tq, num_experts, p, pair, wide,
                                static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// Weight gradient on MXFP8 operands: dw[e] (bf16 [M, N]) = sum over token rows
+// [k_off[e], k_off[e+1]) of A[r, 0:M]^T B[r, 0:N], with A^T / B^T given as codes [M, K] /
+// [N, K] quantised along the token rows (moe_mxfp8_quantize_t of the [K, M] / [K, N]
+// activations). k_off[] are multiples of 128 (the padded plan; padding rows are zero).
+int moe_gg_mxfp8_wgrad(const void* at, const void* sfa, const void* bt, const void* sfb, int K,
+                       int M, int N, int num_experts, const int* k_off, void* dw, int flags,
+                       void* stream) {
+  const int pair = flags & 1, wide = (flags >> 1) & 1;
+  if (K % BK || M % (BM * (pair ? 2 : 1)) || N % (wide ? 256 : 128) || !k_off)
+    return kErrInvalidArg;
+  Params p{};
+  p.N = N;
+  p.K = K;
+  p.M = M;
+  p.sfa = static_cast<const uint8_t*>(sfa);
+  p.sfb = static_cast<const uint8_t*>(sfb);
+  p.out = dw;
+  p.ldo = N;
+  p.out_stride = (long long)M * N;
+  p.k_off = k_off;
+  p.num_experts_gk = num_experts;
+  return launch_wgrad(at, bt, p, pair, wide, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

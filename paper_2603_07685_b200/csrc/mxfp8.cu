@@ -90,57 +90,70 @@ __global__ void quant_kernel(const __nv_bfloat16* __restrict__ x, long long ldx,
 
 // Transposing quantisation ("column twin", the reference's with_column_twin quant.py:195-200):
 // x [B, R, C] bf16 -> codes [B, C, R] with 1x32 blocks along R, scales in the tiled layout
-// of the [B*C, R] operand. A CTA handles 32 rows x 256 columns of one batch: the tile is
-// staged in shared memory, then thread c quantises column c's 32 values and writes them as
-// one contiguous 32-byte run of the output row.
-__global__ void quant_t_kernel(const __nv_bfloat16* __restrict__ x, int B, int R, int C,
-                               uint8_t* __restrict__ codes, uint8_t* __restrict__ sf_tiled,
-                               uint8_t* __restrict__ sf_plain) {
-  __shared__ __nv_bfloat16 tile[32][256 + 8];
-  const int cblocks = (C + 255) / 256, rblocks = R / 32;
+// of the [B*C, R] operand. A CTA handles 64 rows x 256 columns of one batch: the tile is
+// staged in shared memory (8 x 16-byte loads in flight per thread), then thread c quantises
+// column c's two 32-row blocks and writes them as one contiguous 64-byte run of the output
+// row.
+constexpr int QT_ROWS = 64;
+__global__ void __launch_bounds__(256) quant_t_kernel(const __nv_bfloat16* __restrict__ x,
+                                                      int B, int R, int C,
+                                                      uint8_t* __restrict__ codes,
+                                                      uint8_t* __restrict__ sf_tiled,
+                                                      uint8_t* __restrict__ sf_plain) {
+  __shared__ __nv_bfloat16 tile[QT_ROWS][256 + 8];
+  const int cblocks = (C + 255) / 256, rblocks = R / QT_ROWS;
   const long long nt = (long long)B * rblocks * cblocks;
   for (long long id = blockIdx.x; id < nt; id += gridDim.x) {
     const int b = static_cast<int>(id / ((long long)rblocks * cblocks));
     const int rem = static_cast<int>(id % ((long long)rblocks * cblocks));
     const int rb = rem / cblocks, cb = rem % cblocks;
-    const int r0 = rb * 32, c0 = cb * 256;
+    const int r0 = rb * QT_ROWS, c0 = cb * 256;
     const __nv_bfloat16* src = x + ((long long)b * R + r0) * C + c0;
-    // 32 rows x 256 columns: each warp loads rows, 8 bf16 (16 B) per lane
-    for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
-      const int r = i / 32, v = i % 32;
-      if (c0 + v * 8 < C) {
-        const int4 w = ld_nc_v4(src + (long long)r * C + v * 8);
-        *reinterpret_cast<int4*>(&tile[r][v * 8]) = w;
-      }
+    int4 v[QT_ROWS * 32 / 256];
+#pragma unroll
+    for (int k = 0; k < QT_ROWS * 32 / 256; ++k) {
+      const int i = threadIdx.x + k * 256;
+      const int r = i / 32, q = i % 32;
+      v[k] = c0 + q * 8 < C ? ld_nc_v4(src + (long long)r * C + q * 8) : make_int4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < QT_ROWS * 32 / 256; ++k) {
+      const int i = threadIdx.x + k * 256;
+      *reinterpret_cast<int4*>(&tile[i / 32][(i % 32) * 8]) = v[k];
     }
     __syncthreads();
     const int c = c0 + threadIdx.x;
-    if (threadIdx.x < 256 && c < C) {
-      float f[32];
-      float amax = 0.f;
-#pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        f[r] = __bfloat162float(tile[r][threadIdx.x]);
-        amax = fmaxf(amax, fabsf(f[r]));
-      }
-      const int e = e8m0_exp(amax);
-      const float inv = __int_as_float((127 - e) << 23);
-      uint32_t out[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
-            make_float2(f[4 * q] * inv, f[4 * q + 1] * inv), __NV_SATFINITE, __NV_E4M3);
-        const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
-            make_float2(f[4 * q + 2] * inv, f[4 * q + 3] * inv), __NV_SATFINITE, __NV_E4M3);
-        out[q] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
-      }
+    if (c < C) {
       const long long orow = (long long)b * C + c;  // output row in [B*C, R]
+      uint32_t out[16];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float f[32];
+        float amax = 0.f;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+          f[r] = __bfloat162float(tile[h * 32 + r][threadIdx.x]);
+          amax = fmaxf(amax, fabsf(f[r]));
+        }
+        const int e = e8m0_exp(amax);
+        const float inv = __int_as_float((127 - e) << 23);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
+              make_float2(f[4 * q] * inv, f[4 * q + 1] * inv), __NV_SATFINITE, __NV_E4M3);
+          const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
+              make_float2(f[4 * q + 2] * inv, f[4 * q + 3] * inv), __NV_SATFINITE, __NV_E4M3);
+          out[h * 8 + q] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+        }
+        const int kb = r0 / 32 + h;
+        const uint8_t sc = static_cast<uint8_t>(e + 127);
+        if (sf_tiled) sf_tiled[tiled_sf_offset(static_cast<int>(orow), kb, R / 32)] = sc;
+        if (sf_plain) sf_plain[orow * (R / 32) + kb] = sc;
+      }
       int4* dst = reinterpret_cast<int4*>(codes + orow * R + r0);
-      dst[0] = make_int4(out[0], out[1], out[2], out[3]);
-      dst[1] = make_int4(out[4], out[5], out[6], out[7]);
-      const uint8_t sc = static_cast<uint8_t>(e + 127);
-      if (sf_tiled) sf_tiled[tiled_sf_offset(static_cast<int>(orow), rb, rblocks)] = sc;
-      if (sf_plain) sf_plain[orow * rblocks + rb] = sc;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        dst[q] = make_int4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
     }
     __syncthreads();
   }
@@ -174,11 +187,11 @@ extern "C" int moe_mxfp8_quantize(const void* x, long long ldx, int rows, int K,
 extern "C" int moe_mxfp8_quantize_t(const void* x, int B, int R, int C, void* codes,
                                     void* sf_tiled, void* sf_plain, void* stream) {
   if (B < 1 || R % 128 || C % 8 || ((long long)B * C) % 128) return kErrInvalidArg;
-  const long long tiles = (long long)B * (R / 32) * ((C + 255) / 256);
+  const long long tiles = (long long)B * (R / mx::QT_ROWS) * ((C + 255) / 256);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = static_cast<int>(tiles < (long long)sms * 8 ? tiles : (long long)sms * 8);
+  const int grid = static_cast<int>(tiles < (long long)sms * 6 ? tiles : (long long)sms * 6);
   mx::quant_t_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const __nv_bfloat16*>(x), B, R, C, static_cast<uint8_t*>(codes),
       static_cast<uint8_t*>(sf_tiled), static_cast<uint8_t*>(sf_plain));

@@ -298,3 +298,22 @@ def mxfp8_fc2_dgrad(doq, sfd, w2tq, sfw, num_experts, block_expert, num_m_blocks
               num_m_blocks.data_ptr(), preact.data_ptr(), d_pre.data_ptr(), dq.data_ptr(),
               dsf.data_ptr(), int(pair) | (int(wide) << 1), _stream())
     return d_pre, dq, dsf
+
+
+def mxfp8_wgrad(a: torch.Tensor, b: torch.Tensor, k_off: torch.Tensor, num_experts: int,
+                out=None):
+    """dw[e] = a[rows_e]^T @ b[rows_e] (bf16 [E, M, N]) on MXFP8 operands: a [K, M] and
+    b [K, N] (K = padded token rows, k_off multiples of 128) are quantised along K by the
+    transposing quantiser, then one grouped-K block-scaled tcgen05 GEMM."""
+    k, m = a.shape
+    _, n = b.shape
+    at, asf, _ = mxfp8_quantize_t(a)
+    bt, bsf, _ = mxfp8_quantize_t(b)
+    if out is None:
+        out = torch.empty((num_experts, m, n), dtype=torch.bfloat16, device=a.device)
+    pair = m % 256 == 0
+    wide = n % 256 == 0
+    _lib.call("moe_gg_mxfp8_wgrad", at.data_ptr(), asf.data_ptr(), bt.data_ptr(),
+              bsf.data_ptr(), k, m, n, num_experts, k_off.data_ptr(), out.data_ptr(),
+              int(pair) | (int(wide) << 1), _stream())
+    return out

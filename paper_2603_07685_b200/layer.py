@@ -35,9 +35,10 @@ class MoEConfig:
     mem_efficient: bool = False       # combine_mem_efficient (prob folded into act)
     shared_ffn_hidden: int = 0        # DeepSeek shared expert width (0 = none)
     # expert GEMMs: "bf16", or "mxfp8" (the paper's Blackwell recipe, 1x32 E8M0 blocks,
-    # quant.py:62-64; block-scaled tcgen05 MMA): forward fc1/fc2 and the data-gradient
-    # GEMMs (operands re-quantised in the producing epilogues, weights transposed-quantised
-    # for dgrad); the weight-gradient GEMMs stay bf16.
+    # quant.py:62-64; block-scaled tcgen05 MMA) for all six: forward fc1/fc2, the
+    # data-gradient GEMMs (operands re-quantised in the producing epilogues, weights
+    # transposed-quantised along the dgrad K) and the weight-gradient GEMMs (activations and
+    # gradients transposed-quantised along the token rows, the reference's column twin).
     precision: str = "bf16"
 
     def capacity(self, num_tokens: int) -> int:
@@ -96,13 +97,15 @@ class _MoEFunction(torch.autograd.Function):
             else:
                 d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, plan.block_expert,
                                           plan.num_m_blocks, pair=plan.pair)
-        dw2 = gemm.wgrad(d_o, act, plan.off_pad, e)
         if cfg.precision == "mxfp8":
+            dw2 = gemm.mxfp8_wgrad(d_o, act, plan.off_pad, e)
             dxp = _mxfp8_fc1_dgrad(dq, w1, plan, e)
+            dw1 = gemm.mxfp8_wgrad(d_pre, xp, plan.off_pad, e)
         else:
+            dw2 = gemm.wgrad(d_o, act, plan.off_pad, e)
             dxp = gemm.fc1_dgrad(d_pre, w1, plan.block_expert, plan.num_m_blocks,
                                  pair=plan.pair)
-        dw1 = gemm.wgrad(d_pre, xp, plan.off_pad, e)
+            dw1 = gemm.wgrad(d_pre, xp, plan.off_pad, e)
         aux_scale = None if daux is None else daux.float()
         dw_r, dx_router = ops.router_backward(x, w_r_pad, r, dprob, cfg.score,
                                               aux_scale=aux_scale)

@@ -191,3 +191,30 @@ def test_mxfp8_dgrad_chain_matches_dequant_oracle(pair, wide):
     w1t = M.dequantize_mxfp8(w1tq.cpu().numpy(), w1tsp.cpu().numpy()).reshape(E, h, 2 * m)
     dx_ref = np.concatenate([dpd[off[e]:off[e + 1]] @ w1t[e].T for e in range(E)])
     assert rel(dxp.double().cpu().numpy(), dx_ref) < 5e-3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("Mo,No", [(256, 256), (128, 384)], ids=["pair_wide", "cta1_narrow"])
+def test_mxfp8_wgrad_matches_dequant_oracle(Mo, No):
+    """Grouped-K weight gradient on column-quantised operands, incl. an expert without rows."""
+    from paper_2603_07685_b200 import gemm
+
+    dev = torch.device("cuda", 0)
+    g = torch.Generator().manual_seed(23)
+    rows_e = [256, 0, 384]
+    K = sum(rows_e)
+    off = torch.tensor(np.cumsum([0] + rows_e), dtype=torch.int32, device=dev)
+    a = torch.randn((K, Mo), generator=g).to(torch.bfloat16)
+    b = torch.randn((K, No), generator=g).to(torch.bfloat16)
+    dw = gemm.mxfp8_wgrad(a.to(dev), b.to(dev), off, 3).double().cpu().numpy()
+    at, asf, asp = gemm.mxfp8_quantize_t(a.to(dev), plain=True)
+    bt, bsf, bsp = gemm.mxfp8_quantize_t(b.to(dev), plain=True)
+    ad = M.dequantize_mxfp8(at.cpu().numpy(), asp.cpu().numpy())  # [M, K]
+    bd = M.dequantize_mxfp8(bt.cpu().numpy(), bsp.cpu().numpy())  # [N, K]
+    o = np.cumsum([0] + rows_e)
+    for e in range(3):
+        ref = ad[:, o[e]:o[e + 1]] @ bd[:, o[e]:o[e + 1]].T
+        if rows_e[e] == 0:
+            assert not dw[e].any()
+        else:
+            assert np.linalg.norm(dw[e] - ref) / np.linalg.norm(ref) < 5e-3
