@@ -357,7 +357,7 @@ def run_gpu(args, c) -> None:
     # the step's aux loss is read back to the host. All copies are inside the timed region.
     x_host = x.cpu().pin_memory()
     dy_host = dy.cpu().pin_memory()
-    loss_host = torch.empty((args.steps,), dtype=torch.float32).pin_memory()
+    loss_host = torch.empty((max(args.steps, 2),), dtype=torch.float32).pin_memory()
     bufs = [(torch.empty_like(x), torch.empty_like(dy)) for _ in range(2)]
     copy_stream = torch.cuda.Stream(device=dev)
     landed = [torch.cuda.Event() for _ in range(2)]

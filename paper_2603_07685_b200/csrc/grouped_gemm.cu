@@ -106,7 +106,18 @@ struct Params {
   const uint32_t* block_need;
   const int* unit_order;
   int* wait_status;
+  // epilogue outputs stored with the streaming (evict-first) cache hint, so the output
+  // stream does not evict the operand tiles other CTAs still reuse from L2
+  int stream_stores;
+  int band_m;  // raster band: M units that sweep each n-block together (L2 reuse)
 };
+
+__device__ __forceinline__ void st_out(int4* p, int4 v, int cs) {
+  if (cs)
+    __stcs(p, v);
+  else
+    *p = v;
+}
 
 // Spin (bounded) until every source rank in `need` has published this epoch's rows. On a
 // timeout (2 s) the kernel records [1, block, missing sources, epoch, flags[0..3]] in
@@ -147,10 +158,11 @@ __device__ __forceinline__ void decode_tile(const Params& p, int t, int num_unit
                                             Tile& tl) {
   const int nb_count = p.N / BN;
   if constexpr (!GROUPED_K) {
-    const int band = t / (BAND_M * nb_count);
-    const int rem = t - band * BAND_M * nb_count;
-    const int u0 = band * BAND_M;
-    const int rows = min(BAND_M, num_units - u0);
+    const int bm = p.band_m;
+    const int band = t / (bm * nb_count);
+    const int rem = t - band * bm * nb_count;
+    const int u0 = band * bm;
+    const int rows = min(bm, num_units - u0);
     const int nb = rem / rows;
     int u = u0 + (rem - nb * rows);
     if (p.unit_order) u = __ldg(p.unit_order + u);
@@ -480,14 +492,15 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K>(), 1)
               w.y = pack_bf16x2(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3]));
               w.z = pack_bf16x2(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5]));
               w.w = pack_bf16x2(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
-              reinterpret_cast<int4*>(o)[v] = w;
+              st_out(reinterpret_cast<int4*>(o) + v, w, p.stream_stores);
             }
           } else {
             float* o = reinterpret_cast<float*>(p.out) + ebase + row * p.ldo + tl.n0 + col;
 #pragma unroll
             for (int v = 0; v < 8; ++v)
-              reinterpret_cast<int4*>(o)[v] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2],
-                                                        r[4 * v + 3]);
+              st_out(reinterpret_cast<int4*>(o) + v,
+                     make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]),
+                     p.stream_stores);
           }
         }
       } else if constexpr (EPI == EPI_SWIGLU) {
@@ -519,9 +532,9 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K>(), 1)
               pu[j] = pack_bf16x2(u0, u1);
               pa[j] = pack_bf16x2(silu_f(g0) * u0 * scale, silu_f(g1) * u1 * scale);
             }
-            reinterpret_cast<int4*>(pre + c * 32)[v] = wg;
-            reinterpret_cast<int4*>(pre + 128 + c * 32)[v] = wu;
-            reinterpret_cast<int4*>(act + c * 32)[v] = wa;
+            st_out(reinterpret_cast<int4*>(pre + c * 32) + v, wg, p.stream_stores);
+            st_out(reinterpret_cast<int4*>(pre + 128 + c * 32) + v, wu, p.stream_stores);
+            st_out(reinterpret_cast<int4*>(act + c * 32) + v, wa, p.stream_stores);
           }
         }
       } else if constexpr (EPI == EPI_DSWIGLU) {
@@ -576,8 +589,8 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K>(), 1)
               pg[j] = pack_bf16x2(dg0, dg1);
               pu[j] = pack_bf16x2(da0 * si0, da1 * si1);
             }
-            reinterpret_cast<int4*>(dpre_row + pos)[v] = wg;
-            reinterpret_cast<int4*>(dpre_row + pos + 128)[v] = wu;
+            st_out(reinterpret_cast<int4*>(dpre_row + pos) + v, wg, p.stream_stores);
+            st_out(reinterpret_cast<int4*>(dpre_row + pos + 128) + v, wu, p.stream_stores);
           }
         }
         if (p.row_partial)
@@ -699,10 +712,29 @@ constexpr int kFlagPair = 1;
 
 // Builds tensor maps for the chosen engine and launches. a_inner/a_outer/b_* describe the
 // 2-D global views; a/b K-major (box {64, rows}) or MN-major (box {64, 64}).
+static int stream_stores_default() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MOE_B200_EPI_CS");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v;
+}
+
 template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI>
 static int run(const void* a, uint64_t a_inner, uint64_t a_outer, const void* b,
                uint64_t b_inner, uint64_t b_outer, Params p, int units_m, int pair,
                cudaStream_t stream) {
+  p.stream_stores = stream_stores_default();
+  {
+    static int bm = -1;
+    if (bm < 0) {
+      const char* e = getenv("MOE_B200_BAND");
+      bm = e ? atoi(e) : BAND_M;
+      if (bm < 1) bm = BAND_M;
+    }
+    p.band_m = bm;
+  }
   CUtensorMap ta, tb;
   int st;
   const int cg = pair ? 2 : 1;
