@@ -58,6 +58,64 @@ def gemm_flops_per_token(c) -> float:
 
 
 # ----------------------------------------------------------------------------- clocks
+class NvmlClockSampler:
+    """In-process NVML sampling of the same fields nvidia-smi's clocks line reports (SM clock,
+    max SM clock, clock-event reasons), every 50 ms inside the timed window. NVML is the
+    library nvidia-smi itself calls; polling it from a thread avoids the driver contention
+    of a polling nvidia-smi process, which was measured to stall kernel launches on some
+    boxes (timed steps 1.6-1.9x their kernel time)."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, gpu_index: int = 0):
+        import pynvml
+
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+        self.samples: list[tuple[float, int, int, int]] = []
+        self.t0 = self.t1 = None
+        self.lines = [True]  # started immediately (ClockSampler interface)
+        self._stop = threading.Event()
+        self._reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def start(self):
+        self.t.start()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            if self.t0 is not None and self.t1 is None:
+                try:
+                    sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                    smax = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+                    rs = self._reasons(self.h)
+                    self.samples.append((time.time(), sm, smax, rs))
+                except Exception:  # noqa: BLE001
+                    pass
+            time.sleep(0.05)
+
+    def window(self, start: bool):
+        if start:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+
+    def stop(self) -> dict:
+        self._stop.set()
+        self.t.join(timeout=2)
+        sm = [x[1] for x in self.samples]
+        smax = [x[2] for x in self.samples]
+        reasons = sorted({nm for x in self.samples for nm, bit in self.REASONS.items()
+                          if x[3] & bit})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons,
+                "samples": len(sm), "source": "NVML (nvidia-smi's library), 50 ms"}
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md).
 
@@ -269,7 +327,12 @@ def run_gpu(args, c) -> None:
 
     # nvidia-smi start-up contends with the driver: start sampling before the warm-up and
     # wait for its first sample so the timed region only sees the steady 100 ms polling.
-    clocks = ClockSampler(dev.index if dev.index is not None else 0)
+    try:
+        if os.environ.get("MOE_BENCH_SMI") == "1":
+            raise ImportError
+        clocks = NvmlClockSampler(dev.index if dev.index is not None else 0)
+    except Exception:  # noqa: BLE001  (no pynvml / NVML: the nvidia-smi process)
+        clocks = ClockSampler(dev.index if dev.index is not None else 0)
     if rank == 0:
         clocks.start()
         t_wait = time.time()

@@ -62,11 +62,14 @@ struct Cfg {
 // rows x 128 columns (half a tile row) in shared memory and writes every row with one
 // 256-byte TMA bulk store to its destination (often a peer GPU over NVLink) instead of 16-B
 // per-thread stores, which NVLink serves poorly.
-constexpr int SCATTER_COLS = 128;
-constexpr int SCATTER_STAGE = 32 * SCATTER_COLS * 2;  // per epilogue warp
+// The weight-gradient kernels (8 epilogue warps) can use the same staged bulk stores for
+// their local output rows (bulk_out; 64-column pieces, 128-byte rows).
+constexpr int SCATTER_BYTES = 32 * 1024;  // staging for all epilogue warps
+template <bool GROUPED_K>
+constexpr int scatter_cols() { return GROUPED_K ? 64 : 128; }
 template <int EPI, bool GROUPED_K, int CG>
 constexpr int smem_bytes() {
-  return Cfg<CG>::SMEM + ((EPI == 0 && !GROUPED_K) ? EPI_WARPS * SCATTER_STAGE : 0);
+  return Cfg<CG>::SMEM + (EPI == 0 ? SCATTER_BYTES : 0);
 }
 
 enum Epi : int { EPI_BF16 = 0, EPI_SWIGLU = 1, EPI_DSWIGLU = 2, EPI_F32 = 3 };
@@ -110,6 +113,7 @@ struct Params {
   // stream does not evict the operand tiles other CTAs still reuse from L2
   int stream_stores;
   int band_m;  // raster band: M units that sweep each n-block together (L2 reuse)
+  int bulk_out;  // grouped-K EPI_BF16: staged TMA bulk stores for the output rows
 };
 
 __device__ __forceinline__ void st_out(int4* p, int4 v, int cs) {
@@ -403,7 +407,8 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K>(), 1)
     // ===================== epilogue (warps 2..9: lane quarter x column half) ===========
     const int q = warp & 3;
     const int half = (warp - 2) / 4;
-    uint8_t* stage = smem + C::STAGES * C::STAGE + 256 + (warp - 2) * SCATTER_STAGE;
+    constexpr int SC = scatter_cols<GROUPED_K>();
+    uint8_t* stage = smem + C::STAGES * C::STAGE + 256 + (warp - 2) * (32 * SC * 2);
     constexpr int EC = BN / (epi_warps<GROUPED_K>() / 4);  // tile columns per epilogue warp
     const int cb = half * EC;  // this warp's first tile column
     const int row_local = q * 32 + lane;
@@ -457,10 +462,10 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K>(), 1)
           tmem_ld_32x32b_x32(t_base + col, r);
           tmem_ld_wait();
           if constexpr (EPI == EPI_BF16) {
-            if (!GROUPED_K && p.row_dst) {
-              // stage this lane's row chunk; one bulk store per (row, 128 columns)
-              const int hc = col % SCATTER_COLS;
-              uint8_t* srow = stage + lane * (SCATTER_COLS * 2);
+            if ((!GROUPED_K && p.row_dst) || (GROUPED_K && p.bulk_out)) {
+              // stage this lane's row chunk; one bulk store per (row, SC columns)
+              const int hc = col % SC;
+              uint8_t* srow = stage + lane * (SC * 2);
               if (hc == 0) bulk_wait_read_all();  // slot free again (previous half read)
 #pragma unroll
               for (int v = 0; v < 4; ++v) {
@@ -471,13 +476,15 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K>(), 1)
                 w.w = pack_bf16x2(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
                 reinterpret_cast<int4*>(srow + hc * 2)[v] = w;
               }
-              if (hc + 32 == SCATTER_COLS) {
-                const unsigned long long dst = __ldg(p.row_dst + row);
+              if (hc + 32 == SC) {
+                const unsigned long long dst =
+                    GROUPED_K ? reinterpret_cast<unsigned long long>(
+                                    reinterpret_cast<__nv_bfloat16*>(p.out) + ebase + row * p.ldo)
+                              : __ldg(p.row_dst + row);
                 fence_async_shared();
                 if (dst) {
-                  bulk_store_s2g(reinterpret_cast<__nv_bfloat16*>(dst) + tl.n0 + col + 32 -
-                                     SCATTER_COLS,
-                                 srow, SCATTER_COLS * 2);
+                  bulk_store_s2g(reinterpret_cast<__nv_bfloat16*>(dst) + tl.n0 + col + 32 - SC,
+                                 srow, SC * 2);
                   bulk_commit();
                 }
               }
@@ -613,7 +620,8 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K>(), 1)
 
   // scattered rows may be in peer memory: complete the bulk stores and make them visible
   // system-wide before the stream-ordered collective that publishes them
-  if (EPI == EPI_BF16 && !GROUPED_K && p.row_dst && warp >= 2) {
+  if (EPI == EPI_BF16 && ((!GROUPED_K && p.row_dst) || (GROUPED_K && p.bulk_out)) &&
+      warp >= 2) {
     bulk_wait_all();
     __threadfence_system();
   }
@@ -734,6 +742,14 @@ static int run(const void* a, uint64_t a_inner, uint64_t a_outer, const void* b,
       if (bm < 1) bm = BAND_M;
     }
     p.band_m = bm;
+  }
+  {
+    static int bo = -1;
+    if (bo < 0) {
+      const char* e = getenv("MOE_B200_WGRAD_BULK");
+      bo = (e && e[0] == '1') ? 1 : 0;
+    }
+    p.bulk_out = bo;
   }
   CUtensorMap ta, tb;
   int st;
