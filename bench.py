@@ -344,6 +344,9 @@ def run_gpu(args, c) -> None:
 
     run = step
     graph_launches = None
+    if args.graph and n == 1:
+        raise SystemExit("--graph captures the sync-free EP step (--gpus >= 2); the EP=1 "
+                         "layer is launch-bound only at small token counts")
     if args.graph:
         # whole fwd+bwd step (router, EP planning on the device, exchanges, GEMMs, NCCL
         # all-gather / barriers) captured once and replayed: no host work per step

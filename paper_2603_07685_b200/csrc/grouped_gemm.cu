@@ -744,12 +744,16 @@ static int run(const void* a, uint64_t a_inner, uint64_t a_outer, const void* b,
     p.band_m = bm;
   }
   {
-    static int bo = -1;
-    if (bo < 0) {
+    // grouped-K: staged bulk stores pay off when the tiles are output-bound, i.e. few token
+    // rows per expert (DeepSeek-shape EP=1, 128 rows: wgrad 12.0 -> 10.8 ms); with long K
+    // the per-thread stores are as fast (Mixtral 9.52 vs 9.61 ms, Qwen3 7.87 vs 8.64 ms)
+    static int bo = -2;
+    if (bo == -2) {
       const char* e = getenv("MOE_B200_WGRAD_BULK");
-      bo = (e && e[0] == '1') ? 1 : 0;
+      bo = e ? (e[0] == '1' ? 1 : 0) : -1;
     }
-    p.bulk_out = bo;
+    const long long avg_k = p.num_experts > 0 ? (long long)a_outer / p.num_experts : 0;
+    p.bulk_out = bo >= 0 ? bo : (GROUPED_K && avg_k > 0 && avg_k <= 512 ? 1 : 0);
   }
   CUtensorMap ta, tb;
   int st;
