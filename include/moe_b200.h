@@ -126,6 +126,10 @@ int moe_ep_dispatch_push_dest(const void* x, int T, int K, int h, const int* top
                               const int* inv_c, const int* base, int el,
                               const unsigned long long* peers, const float* prob,
                               const unsigned long long* prob_peers, int dest, void* stream);
+/* rows[r] -> *row_dst[r] (0 = skip): the return transfer as a standalone NVLink push, for
+ * GEMMs without the scatter epilogue (the MXFP8 engine). */
+int moe_ep_scatter_rows(const void* src, int rows, int h, const unsigned long long* row_dst,
+                        void* stream);
 int moe_ep_signal(const unsigned long long* flag_peers, int dest, int slot,
                   const unsigned int* epoch, void* stream);
 /* *epoch += 1 in stream order (the dispatch epoch is a device scalar, so a captured CUDA

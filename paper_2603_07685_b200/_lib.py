@@ -57,6 +57,7 @@ SIGNATURES: dict[str, list] = {
     "moe_ep_combine_bwd_push_dest": [P, P, P, I, I, I, P, P, P, I, P, P, I, P],
     "moe_ep_dispatch_push_dest": [P, I, I, I, P, P, P, I, P, P, P, I, P],
     "moe_ep_signal": [P, I, I, P, P],
+    "moe_ep_scatter_rows": [P, I, I, P, P],
     "moe_ep_epoch_bump": [P, P],
     "moe_ep_prepare": [],
     "moe_ep_block_need": [P, I, I, I, I, I, P, P, P],

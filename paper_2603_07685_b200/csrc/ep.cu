@@ -625,6 +625,34 @@ int moe_ep_epoch_bump(unsigned int* epoch, void* stream) {
   return kOk;
 }
 
+// rows[r] -> *row_dst[r] (0 = skip) for r < rows: the EP return transfer as a standalone
+// NVLink push (warp per row, 512 contiguous bytes per instruction) for GEMMs without a
+// scatter epilogue (the MXFP8 engine).
+__global__ void scatter_rows_kernel(const int4* __restrict__ src, int rows, int hv,
+                                    const unsigned long long* __restrict__ row_dst) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = lane_id();
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = warp; r < rows; r += nwarps) {
+    const unsigned long long d = __ldg(row_dst + r);
+    if (!d) continue;
+    int4* dst = reinterpret_cast<int4*>(d);
+    const int4* s = src + (long long)r * hv;
+    for (int c = lane; c < hv; c += 32) dst[c] = ld_nc_v4(s + c);
+  }
+  __threadfence_system();
+}
+
+int moe_ep_scatter_rows(const void* src, int rows, int h, const unsigned long long* row_dst,
+                        void* stream) {
+  if (h % 8 || rows < 0) return kErrInvalidArg;
+  if (rows == 0) return kOk;
+  scatter_rows_kernel<<<warp_grid(rows), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const int4*>(src), rows, h / 8, row_dst);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
 // Per 128-row block of this rank's padded plan: bitmask of the source ranks whose rows it
 // holds (table of moe_ep_regroup_map), and the schedule of GEMM units (unit = `cg` blocks)
 // sorted by the arrival position of their latest source: source s pushes to ranks

@@ -550,6 +550,10 @@ class _MoEEPP2PFunction(torch.autograd.Function):
                 layer_id: int = 0):
         t, h = x.shape
         E, K = cfg.num_experts, cfg.top_k
+        mx = cfg.precision == "mxfp8"
+        if mx and (cfg.mem_efficient or overlap or echo_slots or stash is not None):
+            raise ValueError("MXFP8 experts under EP: standard combine, p2p / p2p_pull "
+                             "transport, no ECHO / stash")
         n = ep.n
         dev = x.device
         pool = _pool(ep, dev, tag)
@@ -674,9 +678,13 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         else:
             _lib.call("moe_ep_dispatch_push", *push_args, stream)
             pool.barrier()
-            preact, act = gemm.fc1_fwd(xp, w1, be_d, nmb, row_prob, pair=pair,
-                                       **_tmp_preact_act(pool, stash, rows_alloc, w1))
+            if not mx:
+                preact, act = gemm.fc1_fwd(xp, w1, be_d, nmb, row_prob, pair=pair,
+                                           **_tmp_preact_act(pool, stash, rows_alloc, w1))
         ctx.overlap = overlap
+        o_mx = None
+        if mx:  # MXFP8 experts: fc1 + SwiGLU and fc2 into a local buffer
+            preact, act, o_mx = gemm.mxfp8_experts_fwd(xp, w1, w2, be_d, nmb, pair)
         y = torch.empty_like(x)
         row_dst_dx = None
         if scatter:
@@ -692,7 +700,11 @@ class _MoEEPP2PFunction(torch.autograd.Function):
                           dst_off_d.data_ptr(), pp.data_ptr(), h * 2, row_dst[i].data_ptr(),
                           stream)
             row_dst_dx = row_dst[1]
-            gemm.fc2_fwd_scatter(act, w2, be_d, nmb, row_dst[0], pair=pair)
+            if mx:  # the MXFP8 engine has no scatter epilogue: push the rows afterwards
+                _lib.call("moe_ep_scatter_rows", o_mx.data_ptr(), rows_bound, h,
+                          row_dst[0].data_ptr(), stream)
+            else:
+                gemm.fc2_fwd_scatter(act, w2, be_d, nmb, row_dst[0], pair=pair)
             shared = shared_expert_forward(x, w1s, w2s) if w1s is not None else None
             pool.barrier()
             _lib.call("moe_combine", o_local.data_ptr(), t, K, h, splan.inv_map.data_ptr(),
@@ -703,7 +715,10 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         else:
             o, o_peers = pool.get("o", rows_alloc * h, torch.bfloat16)
             o = o[: rows_alloc * h].view(rows_alloc, h)
-            gemm.fc2_fwd(act, w2, be_d, nmb, out=o, pair=pair)
+            if mx:
+                o.copy_(o_mx)
+            else:
+                gemm.fc2_fwd(act, w2, be_d, nmb, out=o, pair=pair)
             shared = shared_expert_forward(x, w1s, w2s) if w1s is not None else None
             pool.barrier()
             # local compact copy of the pulled expert outputs: the backward's dprob = <dY, O>
@@ -730,6 +745,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
             st_out.stash(2 * layer_id + 1, {"o": o_local}, rows_dev=splan.meta[2:3])
             preact = act = None
         ctx.stash, ctx.layer_id = stash, layer_id
+        ctx.rows_bound = rows_bound
         ctx.scatter, ctx.tag, ctx.row_dst_dx = scatter, tag, row_dst_dx
         ctx.cfg, ctx.ep, ctx.r, ctx.splan, ctx.cap, ctx.pair = cfg, ep, r, splan, cap, pair
         ctx.topk_use, ctx.layout, ctx.el_own = topk_use, layout, E // n
@@ -789,21 +805,34 @@ class _MoEEPP2PFunction(torch.autograd.Function):
             _lib.call("moe_ep_combine_bwd_push", *push_args,
                       None if cfg.mem_efficient else dprob.data_ptr(), stream)
             pool.barrier()
-        if cfg.mem_efficient:
+        mx = cfg.precision == "mxfp8"
+        dxp_mx = None
+        if mx:
+            d_pre, dxp_mx = gemm.mxfp8_experts_dgrad(d_o, w1, w2, preact, be_d, nmb, ctx.pair)
+        elif cfg.mem_efficient:
             d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, be_d, nmb, row_prob=ctx.row_prob,
                                       pair=ctx.pair, part=part, wait=wait)
         else:
             d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, be_d, nmb, pair=ctx.pair, wait=wait)
         if ctx.overlap:
             main.wait_stream(pool.comm)
-        dw2 = gemm.wgrad(d_o, act, off_pad_d, el)
+        dw2 = gemm.mxfp8_wgrad(d_o, act, off_pad_d, el) if mx else gemm.wgrad(d_o, act,
+                                                                                off_pad_d, el)
         if ctx.scatter:  # dX rows return from fc1_dgrad's epilogue into the source ranks
-            gemm.fc1_dgrad_scatter(d_pre, w1, be_d, nmb, ctx.row_dst_dx, pair=ctx.pair)
+            if mx:
+                _lib.call("moe_ep_scatter_rows", dxp_mx.data_ptr(), ctx.rows_bound, h,
+                          ctx.row_dst_dx.data_ptr(), stream)
+            else:
+                gemm.fc1_dgrad_scatter(d_pre, w1, be_d, nmb, ctx.row_dst_dx, pair=ctx.pair)
         else:
             dxp, dxp_peers = pool.get("dxp", rows_alloc * h, torch.bfloat16)
             dxp = dxp[: rows_alloc * h].view(rows_alloc, h)
-            gemm.fc1_dgrad(d_pre, w1, be_d, nmb, out=dxp, pair=ctx.pair)
-        dw1 = gemm.wgrad(d_pre, xp, off_pad_d, el)
+            if mx:
+                dxp.copy_(dxp_mx)
+            else:
+                gemm.fc1_dgrad(d_pre, w1, be_d, nmb, out=dxp, pair=ctx.pair)
+        dw1 = gemm.mxfp8_wgrad(d_pre, xp, off_pad_d, el) if mx else gemm.wgrad(d_pre, xp,
+                                                                                 off_pad_d, el)
         # also orders every rank's reads of its symmetric buffers (xp, d_o) before any
         # peer's next write into them
         pool.barrier()
@@ -1109,6 +1138,8 @@ def moe_forward_ep(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
         return _MoEEPP2PFunction.apply(*args, int(echo_slots), transport != "p2p_pull", tag,
                                        transport == "p2p_overlap",
                                        sync_free and not echo_slots, stash, int(layer_id))
+    if cfg.precision != "bf16":
+        raise ValueError(f"precision {cfg.precision!r} runs on the p2p / p2p_pull transports")
     if transport == "p2p_dedup":
         return _MoEEPDedupFunction.apply(*args, tag)
     if transport == "nccl":

@@ -317,3 +317,40 @@ def mxfp8_wgrad(a: torch.Tensor, b: torch.Tensor, k_off: torch.Tensor, num_exper
               bsf.data_ptr(), k, m, n, num_experts, k_off.data_ptr(), out.data_ptr(),
               int(pair) | (int(wide) << 1), _stream())
     return out
+
+
+# ---- MXFP8 expert-GEMM chain (shared by layer.py at EP = 1 and the EP dispatcher)
+
+def mxfp8_wide(m: int, h: int) -> bool:
+    """256-wide N tiles (single TMEM accumulator, 8 epilogue warps) when the shapes allow."""
+    return (2 * m) % 256 == 0 and m % 256 == 0 and h % 256 == 0
+
+
+def mxfp8_experts_fwd(xp, w1, w2, block_expert, num_m_blocks, pair, out=None):
+    """fc1 + SwiGLU and fc2 on MXFP8 operands (x rows and weights quantised here, the
+    activation re-quantised in fc1's epilogue). Returns (preact, act, o) in bf16."""
+    e, m2, h = w1.shape
+    m = m2 // 2
+    wide = mxfp8_wide(m, h)
+    xq, xsf, _ = mxfp8_quantize(xp)
+    w1q, w1sf = mxfp8_quantize_w1(w1, wide=wide)
+    w2q, w2sf = mxfp8_quantize_weight(w2)
+    preact, act, aq, asf = mxfp8_fc1(xq, xsf, w1q, w1sf, e, block_expert, num_m_blocks, m,
+                                     pair=pair, wide=wide)
+    o = mxfp8_gemm(aq, asf, w2q, w2sf, e, block_expert, num_m_blocks, h, out=out, pair=pair,
+                   wide=wide)
+    return preact, act, o
+
+
+def mxfp8_experts_dgrad(d_o, w1, w2, preact, block_expert, num_m_blocks, pair, dx_out=None):
+    """fc2 dgrad + dSwiGLU and fc1 dgrad on MXFP8 operands. Returns (d_preact bf16, dxp)."""
+    e, h, m = w2.shape
+    wide = mxfp8_wide(m, h)
+    doq, dosf, _ = mxfp8_quantize(d_o)
+    w2tq, w2tsf, _ = mxfp8_quantize_t(w2)
+    d_pre, dq, dsf = mxfp8_fc2_dgrad(doq, dosf, w2tq, w2tsf, e, block_expert, num_m_blocks,
+                                     preact, pair=pair, wide=wide)
+    w1tq, w1tsf, _ = mxfp8_quantize_t(w1)
+    dxp = mxfp8_gemm(dq, dsf, w1tq, w1tsf, e, block_expert, num_m_blocks, h, out=dx_out,
+                     pair=pair, wide=wide)
+    return d_pre, dxp

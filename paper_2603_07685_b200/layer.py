@@ -62,7 +62,8 @@ class _MoEFunction(torch.autograd.Function):
         xp = ops.permute_gather(x, plan)
         row_prob = plan.row_prob if cfg.mem_efficient else None
         if cfg.precision == "mxfp8":
-            preact, act, o = _mxfp8_experts(xp, w1, w2, plan, e)
+            preact, act, o = gemm.mxfp8_experts_fwd(xp, w1, w2, plan.block_expert,
+                                                    plan.num_m_blocks, plan.pair)
         else:
             preact, act = gemm.fc1_fwd(xp, w1, plan.block_expert, plan.num_m_blocks, row_prob,
                                        pair=plan.pair)
@@ -93,13 +94,14 @@ class _MoEFunction(torch.autograd.Function):
         else:
             d_o, dprob = ops.combine_backward(dy, plan, o, r.topk_prob)
             if cfg.precision == "mxfp8":
-                d_pre, dq = _mxfp8_fc2_dgrad(d_o, w2, preact, plan, e)
+                d_pre, dxp_mx = gemm.mxfp8_experts_dgrad(d_o, w1, w2, preact, plan.block_expert,
+                                                         plan.num_m_blocks, plan.pair)
             else:
                 d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, plan.block_expert,
                                           plan.num_m_blocks, pair=plan.pair)
         if cfg.precision == "mxfp8":
             dw2 = gemm.mxfp8_wgrad(d_o, act, plan.off_pad, e)
-            dxp = _mxfp8_fc1_dgrad(dq, w1, plan, e)
+            dxp = dxp_mx
             dw1 = gemm.mxfp8_wgrad(d_pre, xp, plan.off_pad, e)
         else:
             dw2 = gemm.wgrad(d_o, act, plan.off_pad, e)
@@ -116,48 +118,6 @@ class _MoEFunction(torch.autograd.Function):
         dx = ops.combine(dxp, plan, None, resid=dy if cap >= 0 else None, extra=dx_router,
                          extra2=dx_shared)
         return (dx, dw_r.to(torch.bfloat16), dw1, dw2, None, dw1s, dw2s, None)
-
-
-def _mxfp8_experts(xp, w1, w2, plan, e):
-    """MXFP8 forward experts: quantise the permuted rows and the (current) weights, fc1 +
-    SwiGLU with the activation re-quantised in its epilogue, fc2 -- all block-scaled tcgen05.
-    Returns the bf16 preact / act the bf16 backward needs and the expert outputs."""
-    m = w2.shape[2]
-    h = xp.shape[1]
-    # 256-wide tiles (single TMEM accumulator, 8 epilogue warps) when the shapes allow:
-    # measured 1.2x (fc1) / 1.9x (fc2) the bf16 engine at Mixtral shape
-    wide = _mxfp8_wide(m, h)
-    xq, xsf, _ = gemm.mxfp8_quantize(xp)
-    w1q, w1sf = gemm.mxfp8_quantize_w1(w1, wide=wide)
-    w2q, w2sf = gemm.mxfp8_quantize_weight(w2)
-    preact, act, aq, asf = gemm.mxfp8_fc1(xq, xsf, w1q, w1sf, e, plan.block_expert,
-                                          plan.num_m_blocks, m, pair=plan.pair, wide=wide)
-    o = gemm.mxfp8_gemm(aq, asf, w2q, w2sf, e, plan.block_expert, plan.num_m_blocks, h,
-                        pair=plan.pair, wide=wide)
-    return preact, act, o
-
-
-def _mxfp8_wide(m, h):
-    return (2 * m) % 256 == 0 and m % 256 == 0 and h % 256 == 0
-
-
-def _mxfp8_fc2_dgrad(d_o, w2, preact, plan, e):
-    """fc2 dgrad + dSwiGLU in MXFP8 (dO quantised along h, W2 transposed-quantised along
-    h). Returns the bf16 d_preact (wgrad operand) and its MXFP8 copy (fc1 dgrad operand)."""
-    m, h = w2.shape[2], w2.shape[1]
-    wide = _mxfp8_wide(m, h)
-    doq, dosf, _ = gemm.mxfp8_quantize(d_o)
-    w2tq, w2tsf, _ = gemm.mxfp8_quantize_t(w2)
-    d_pre, dq, dsf = gemm.mxfp8_fc2_dgrad(doq, dosf, w2tq, w2tsf, e, plan.block_expert,
-                                          plan.num_m_blocks, preact, pair=plan.pair, wide=wide)
-    return d_pre, (dq, dsf)
-
-
-def _mxfp8_fc1_dgrad(dq, w1, plan, e):
-    h, m2 = w1.shape[2], w1.shape[1]
-    w1tq, w1tsf, _ = gemm.mxfp8_quantize_t(w1)
-    return gemm.mxfp8_gemm(dq[0], dq[1], w1tq, w1tsf, e, plan.block_expert, plan.num_m_blocks,
-                           h, pair=plan.pair, wide=_mxfp8_wide(m2 // 2, h))
 
 
 def shared_expert_forward(x, w1s, w2s):

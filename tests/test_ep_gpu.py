@@ -24,6 +24,11 @@ CASES = {
                           mem=True),
     "top8": dict(E=16, K=8, h=256, m=256, T=160, score="softmax", cf=None, pad=False),
 }
+# MXFP8 expert GEMMs under EP (tolerance of the recipe: tests/test_layer_gpu.py)
+MX_CASES = {
+    "mxfp8": dict(E=8, K=2, h=256, m=256, T=256, score="softmax", cf=None, pad=False,
+                  precision="mxfp8", y_tol=0.1, g_tol=0.12),
+}
 # ECHO hot-expert cloning (dropless, a strongly preferred expert): the cloned computation
 # must equal the un-cloned global oracle exactly as any other EP run.
 ECHO_CASES = {
@@ -80,7 +85,8 @@ def _worker(rank, world, port, case, q, transport):
         E, K, h, m, T = case["E"], case["K"], case["h"], case["m"], case["T"]
         cfg = MoEConfig(E, K, h, m, score=case["score"], aux_loss_coeff=1e-2,
                         capacity_factor=case["cf"], pad_to_capacity=case["pad"],
-                        mem_efficient=case.get("mem", False))
+                        mem_efficient=case.get("mem", False),
+                        precision=case.get("precision", "bf16"))
         g = torch.Generator().manual_seed(11)
         bf = torch.bfloat16
         x_g = torch.randn((world * T, h), generator=g).to(bf)
@@ -185,7 +191,8 @@ def _worker(rank, world, port, case, q, transport):
             errs[f"dup{e}"] = rel(f64(du[j]), ref["dw1"][e])
             errs[f"dw2_{e}"] = rel(f64(w2d.grad[j]), ref["dw2"][e])
         aux_err = abs(float(aux.detach()) - ref["aux"]) / max(abs(ref["aux"]), 1e-9)
-        bad = {k: v for k, v in errs.items() if v > (1e-2 if k == "y" else 2e-2)}
+        y_tol, g_tol = case.get("y_tol", 1e-2), case.get("g_tol", 2e-2)
+        bad = {k: v for k, v in errs.items() if v > (y_tol if k == "y" else g_tol)}
         if aux_err > 1e-4:
             bad["aux"] = aux_err
         q.put((rank, "ok" if not bad else f"errors {bad}"))
@@ -201,6 +208,12 @@ def _worker(rank, world, port, case, q, transport):
 @pytest.mark.parametrize("name", list(CASES))
 def test_ep_layer_matches_global_oracle(name, transport):
     _run(CASES[name], transport)
+
+
+@pytest.mark.parametrize("transport", ["p2p", "p2p_sync_free", "p2p_pull"])
+@pytest.mark.parametrize("name", list(MX_CASES))
+def test_ep_mxfp8_matches_global_oracle(name, transport):
+    _run(MX_CASES[name], transport)
 
 
 @pytest.mark.parametrize("name", list(ECHO_CASES))
