@@ -137,7 +137,7 @@ class ClockSampler:
         import shutil
 
         ms = os.environ.get("MOE_BENCH_SMI_MS", "100")
-        if ms == "0":
+        if ms == "0" or os.environ.get("MOE_BENCH_CLOCKS") == "0":
             return
         cmd = ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                "-i", str(self.gpu), "-lms", ms]
@@ -328,7 +328,7 @@ def run_gpu(args, c) -> None:
     # nvidia-smi start-up contends with the driver: start sampling before the warm-up and
     # wait for its first sample so the timed region only sees the steady 100 ms polling.
     try:
-        if os.environ.get("MOE_BENCH_SMI") == "1":
+        if os.environ.get("MOE_BENCH_SMI") == "1" or os.environ.get("MOE_BENCH_CLOCKS") == "0":
             raise ImportError
         clocks = NvmlClockSampler(dev.index if dev.index is not None else 0)
     except Exception:  # noqa: BLE001  (no pynvml / NVML: the nvidia-smi process)
