@@ -292,6 +292,19 @@ int moe_gg_mxfp8_fc1(const void* xq, const void* sfx, int a_rows, int max_rows, 
                      const void* w1q, const void* sfw, int num_experts, const int* block_expert,
                      const int* num_m_blocks, void* preact, void* act, void* act_q,
                      void* act_sf, int flags, void* stream);
+/* _t variants: the epilogue also writes its activation (act / d_preact) quantised along the
+ * token rows -- codes [C, max_rows] (C = m / 2m), tiled scales: the weight-gradient GEMM's
+ * operand, block amax by warp shuffles over the 32 TMEM lanes (one lane per row). */
+int moe_gg_mxfp8_fc1_t(const void* xq, const void* sfx, int a_rows, int max_rows, int h, int m,
+                       const void* w1q, const void* sfw, int num_experts,
+                       const int* block_expert, const int* num_m_blocks, void* preact,
+                       void* act, void* act_q, void* act_sf, void* act_t, void* act_t_sf,
+                       int flags, void* stream);
+int moe_gg_mxfp8_fc2_dgrad_t(const void* doq, const void* sfd, int a_rows, int max_rows,
+                             int h, int m, const void* w2tq, const void* sfw, int num_experts,
+                             const int* block_expert, const int* num_m_blocks,
+                             const void* preact, void* d_preact, void* dpre_q, void* dpre_sf,
+                             void* dpre_t, void* dpre_t_sf, int flags, void* stream);
 
 #ifdef __cplusplus
 }

@@ -78,6 +78,8 @@ SIGNATURES: dict[str, list] = {
     "moe_gg_mxfp8_gemm": [P, P, I, I, I, I, P, P, I, P, P, P, I, P],
     "moe_gg_mxfp8_fc1": [P, P, I, I, I, I, P, P, I, P, P, P, P, P, P, I, P],
     "moe_gg_mxfp8_fc2_dgrad": [P, P, I, I, I, I, P, P, I, P, P, P, P, P, P, I, P],
+    "moe_gg_mxfp8_fc1_t": [P, P, I, I, I, I, P, P, I, P, P, P, P, P, P, P, P, I, P],
+    "moe_gg_mxfp8_fc2_dgrad_t": [P, P, I, I, I, I, P, P, I, P, P, P, P, P, P, P, P, I, P],
     "moe_gg_mxfp8_wgrad": [P, P, P, P, I, I, I, I, P, P, I, P],
     # grouped GEMM (csrc/grouped_gemm.cu)
     "moe_gg_fc1_fwd": [P, P, I, I, I, I, I, P, P, P, P, P, I, P],

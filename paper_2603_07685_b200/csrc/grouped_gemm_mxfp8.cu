@@ -91,7 +91,41 @@ struct Params {
   const int* k_off;
   int M;
   long long out_stride;
+  // transposed MXFP8 copy of the epilogue's activation (EPI_SWIGLU_Q: act, EPI_DSWIGLU_Q:
+  // d_preact), quantised along the token rows for the weight-gradient GEMM: codes [C, ldT]
+  // (C = m or 2m columns become rows), tiled scales; nullable
+  uint8_t* qt;
+  uint8_t* qt_sf;
+  long long qt_ld;
 };
+
+// Column-wise (token-row) quantisation from registers: the 32 lanes of a warp hold 32
+// consecutive rows (TMEM lanes), lane l has v[j] = value of (row0 + l, col0 + j). For each
+// column, a 5-step butterfly gives the block amax over the 32 rows; each lane then writes its
+// code byte (the 32 lanes write 32 contiguous bytes of output row col0 + j).
+__device__ __forceinline__ void quant_t_cols(const float (&v)[32], int col0, long long row0,
+                                             uint8_t* qt, uint8_t* qt_sf, long long ldT) {
+  const int lane = threadIdx.x & 31;
+  const int kblocks = static_cast<int>(ldT / 32);
+  const int kb = static_cast<int>(row0 / 32);
+#pragma unroll 4
+  for (int j = 0; j < 32; ++j) {
+    float a = fabsf(v[j]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+    const int e = e8m0_exp(a);
+    const float inv = __int_as_float((127 - e) << 23);
+    const __nv_fp8x2_storage_t c2 =
+        __nv_cvt_float2_to_fp8x2(make_float2(v[j] * inv, 0.f), __NV_SATFINITE, __NV_E4M3);
+    const long long orow = col0 + j;
+    qt[orow * ldT + row0 + lane] = static_cast<uint8_t>(c2 & 0xFF);
+    if (lane == 0) {
+      const int r = static_cast<int>(orow);
+      qt_sf[((long long)(r >> 7) * (kblocks >> 2) + (kb >> 2)) * 512 + (r & 31) * 16 +
+            ((r & 127) >> 5) * 4 + (kb & 3)] = static_cast<uint8_t>(e + 127);
+    }
+  }
+}
 
 // E4M3-quantise 32 values (one MX block), write 32 codes + the scale byte (tiled layout).
 __device__ __forceinline__ void quant_block32(const float (&v)[32], uint8_t* codes_dst,
@@ -497,6 +531,11 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<WIDE>(), 1)
             reinterpret_cast<int4*>(dpre_row + pos)[v] = wg;
             reinterpret_cast<int4*>(dpre_row + pos + 128)[v] = wu;
           }
+          if (p.qt) {
+            quant_t_cols(dg, static_cast<int>(pos), tl.m0 + q * 32, p.qt, p.qt_sf, p.qt_ld);
+            quant_t_cols(du, static_cast<int>(pos + 128), tl.m0 + q * 32, p.qt, p.qt_sf,
+                         p.qt_ld);
+          }
           quant_block32(dg, p.act_q + row * (2LL * p.m) + pos, p.act_sf, row,
                         static_cast<int>(pos / 32), kblocks);
           quant_block32(du, p.act_q + row * (2LL * p.m) + pos + 128, p.act_sf, row,
@@ -540,6 +579,16 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<WIDE>(), 1)
             reinterpret_cast<int4*>(pre + 128 + c * 32)[v] = wu;
           }
           const int col = g0 + c * 32;  // activation column = MX block col / 32
+          if (p.qt) {
+            float vt[32];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float2 ab = unpack_bf16x2(a2[i]);
+              vt[2 * i] = ab.x;
+              vt[2 * i + 1] = ab.y;
+            }
+            quant_t_cols(vt, col, tl.m0 + q * 32, p.qt, p.qt_sf, p.qt_ld);
+          }
           if (p.act) {
             int4* ad = reinterpret_cast<int4*>(reinterpret_cast<__nv_bfloat16*>(p.act) +
                                                row * p.m + col);
@@ -741,10 +790,39 @@ int moe_gg_mxfp8_gemm(const void* a, const void* sfa, int a_rows, int max_rows, 
 // fc1 forward + SwiGLU with MXFP8 operands: B = W1 codes [E, 2m, h] interleaved gate/up in
 // 64-row blocks (moe_mxfp8_interleave_w1). Writes preact (bf16, the bf16 engine's
 // 128-interleaved layout), act (bf16, nullable) and act as MXFP8 (codes + tiled scales).
+static int mxfp8_fc1_impl(const void* xq, const void* sfx, int a_rows, int max_rows, int h,
+                          int m, const void* w1q, const void* sfw, int num_experts,
+                          const int* block_expert, const int* num_m_blocks, void* preact,
+                          void* act, void* act_q, void* act_sf, void* act_t, void* act_t_sf,
+                          int flags, void* stream);
+
 int moe_gg_mxfp8_fc1(const void* xq, const void* sfx, int a_rows, int max_rows, int h, int m,
                      const void* w1q, const void* sfw, int num_experts, const int* block_expert,
                      const int* num_m_blocks, void* preact, void* act, void* act_q,
                      void* act_sf, int flags, void* stream) {
+  return mxfp8_fc1_impl(xq, sfx, a_rows, max_rows, h, m, w1q, sfw, num_experts, block_expert,
+                        num_m_blocks, preact, act, act_q, act_sf, nullptr, nullptr, flags,
+                        stream);
+}
+
+// ... and act quantised along the token rows too (act_t: codes [m, max_rows], tiled scales):
+// the weight-gradient GEMM's operand straight from the epilogue (warp-shuffle block amax).
+int moe_gg_mxfp8_fc1_t(const void* xq, const void* sfx, int a_rows, int max_rows, int h, int m,
+                       const void* w1q, const void* sfw, int num_experts,
+                       const int* block_expert, const int* num_m_blocks, void* preact,
+                       void* act, void* act_q, void* act_sf, void* act_t, void* act_t_sf,
+                       int flags, void* stream) {
+  if (!act_t || !act_t_sf) return kErrInvalidArg;
+  return mxfp8_fc1_impl(xq, sfx, a_rows, max_rows, h, m, w1q, sfw, num_experts, block_expert,
+                        num_m_blocks, preact, act, act_q, act_sf, act_t, act_t_sf, flags,
+                        stream);
+}
+
+static int mxfp8_fc1_impl(const void* xq, const void* sfx, int a_rows, int max_rows, int h,
+                          int m, const void* w1q, const void* sfw, int num_experts,
+                          const int* block_expert, const int* num_m_blocks, void* preact,
+                          void* act, void* act_q, void* act_sf, void* act_t, void* act_t_sf,
+                          int flags, void* stream) {
   const int pair = flags & 1, wide = (flags >> 1) & 1;
   if (h % BK || m % 128 || max_rows % (BM * (pair ? 2 : 1)) || a_rows > max_rows || !act_q ||
       !act_sf)
@@ -762,6 +840,9 @@ int moe_gg_mxfp8_fc1(const void* xq, const void* sfx, int a_rows, int max_rows, 
   p.act_q = static_cast<uint8_t*>(act_q);
   p.act_sf = static_cast<uint8_t*>(act_sf);
   p.m = m;
+  p.qt = static_cast<uint8_t*>(act_t);
+  p.qt_sf = static_cast<uint8_t*>(act_t_sf);
+  p.qt_ld = max_rows;
   return launch<EPI_SWIGLU_Q>(xq, a_rows, max_rows, w1q, num_experts, p, pair, wide,
                               static_cast<cudaStream_t>(stream));
 }
@@ -774,11 +855,28 @@ extern "C" {
 // (1x32 along h), B = W2^T codes [E*m, h] (moe_mxfp8_quantize_t of W2 [E, h, m]). Writes
 // d_preact (bf16, preact's interleaved layout; the wgrad operand) and d_preact quantised
 // along 2m (codes + tiled scales: fc1 dgrad's A operand). Standard combine (no row scale).
+int moe_gg_mxfp8_fc2_dgrad_t(const void* doq, const void* sfd, int a_rows, int max_rows,
+                             int h, int m, const void* w2tq, const void* sfw, int num_experts,
+                             const int* block_expert, const int* num_m_blocks,
+                             const void* preact, void* d_preact, void* dpre_q, void* dpre_sf,
+                             void* dpre_t, void* dpre_t_sf, int flags, void* stream);
+
 int moe_gg_mxfp8_fc2_dgrad(const void* doq, const void* sfd, int a_rows, int max_rows, int h,
                            int m, const void* w2tq, const void* sfw, int num_experts,
                            const int* block_expert, const int* num_m_blocks, const void* preact,
                            void* d_preact, void* dpre_q, void* dpre_sf, int flags,
                            void* stream) {
+  return moe_gg_mxfp8_fc2_dgrad_t(doq, sfd, a_rows, max_rows, h, m, w2tq, sfw, num_experts,
+                                  block_expert, num_m_blocks, preact, d_preact, dpre_q,
+                                  dpre_sf, nullptr, nullptr, flags, stream);
+}
+
+// ... and d_preact quantised along the token rows too (dpre_t: codes [2m, max_rows]).
+int moe_gg_mxfp8_fc2_dgrad_t(const void* doq, const void* sfd, int a_rows, int max_rows,
+                             int h, int m, const void* w2tq, const void* sfw, int num_experts,
+                             const int* block_expert, const int* num_m_blocks,
+                             const void* preact, void* d_preact, void* dpre_q, void* dpre_sf,
+                             void* dpre_t, void* dpre_t_sf, int flags, void* stream) {
   const int pair = flags & 1, wide = (flags >> 1) & 1;
   if (h % BK || m % (wide ? 256 : 128) || max_rows % (BM * (pair ? 2 : 1)) ||
       a_rows > max_rows || !dpre_q || !dpre_sf || !preact)
@@ -796,6 +894,9 @@ int moe_gg_mxfp8_fc2_dgrad(const void* doq, const void* sfd, int a_rows, int max
   p.act_q = static_cast<uint8_t*>(dpre_q);
   p.act_sf = static_cast<uint8_t*>(dpre_sf);
   p.m = m;
+  p.qt = static_cast<uint8_t*>(dpre_t);
+  p.qt_sf = static_cast<uint8_t*>(dpre_t_sf);
+  p.qt_ld = max_rows;
   return launch<EPI_DSWIGLU_Q>(doq, a_rows, max_rows, w2tq, num_experts, p, pair, wide,
                                static_cast<cudaStream_t>(stream));
 }

@@ -683,8 +683,10 @@ class _MoEEPP2PFunction(torch.autograd.Function):
                                            **_tmp_preact_act(pool, stash, rows_alloc, w1))
         ctx.overlap = overlap
         o_mx = None
+        ctx.act_t = None
         if mx:  # MXFP8 experts: fc1 + SwiGLU and fc2 into a local buffer
-            preact, act, o_mx = gemm.mxfp8_experts_fwd(xp, w1, w2, be_d, nmb, pair)
+            preact, ctx.act_t, o_mx = gemm.mxfp8_experts_fwd(xp, w1, w2, be_d, nmb, pair)
+            act = None
         y = torch.empty_like(x)
         row_dst_dx = None
         if scatter:
@@ -808,7 +810,8 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         mx = cfg.precision == "mxfp8"
         dxp_mx = None
         if mx:
-            d_pre, dxp_mx = gemm.mxfp8_experts_dgrad(d_o, w1, w2, preact, be_d, nmb, ctx.pair)
+            dxp_mx, dw1, dw2 = gemm.mxfp8_experts_bwd(d_o, xp, w1, w2, preact, ctx.act_t, be_d,
+                                                      nmb, off_pad_d, ctx.pair)
         elif cfg.mem_efficient:
             d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, be_d, nmb, row_prob=ctx.row_prob,
                                       pair=ctx.pair, part=part, wait=wait)
@@ -816,8 +819,8 @@ class _MoEEPP2PFunction(torch.autograd.Function):
             d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, be_d, nmb, pair=ctx.pair, wait=wait)
         if ctx.overlap:
             main.wait_stream(pool.comm)
-        dw2 = gemm.mxfp8_wgrad(d_o, act, off_pad_d, el) if mx else gemm.wgrad(d_o, act,
-                                                                                off_pad_d, el)
+        if not mx:
+            dw2 = gemm.wgrad(d_o, act, off_pad_d, el)
         if ctx.scatter:  # dX rows return from fc1_dgrad's epilogue into the source ranks
             if mx:
                 _lib.call("moe_ep_scatter_rows", dxp_mx.data_ptr(), ctx.rows_bound, h,
@@ -831,8 +834,8 @@ class _MoEEPP2PFunction(torch.autograd.Function):
                 dxp.copy_(dxp_mx)
             else:
                 gemm.fc1_dgrad(d_pre, w1, be_d, nmb, out=dxp, pair=ctx.pair)
-        dw1 = gemm.mxfp8_wgrad(d_pre, xp, off_pad_d, el) if mx else gemm.wgrad(d_pre, xp,
-                                                                                 off_pad_d, el)
+        if not mx:
+            dw1 = gemm.wgrad(d_pre, xp, off_pad_d, el)
         # also orders every rank's reads of its symmetric buffers (xp, d_o) before any
         # peer's next write into them
         pool.barrier()

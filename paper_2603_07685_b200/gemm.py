@@ -264,7 +264,7 @@ def mxfp8_gemm(aq, sfa, bq, sfb, num_experts, block_expert, num_m_blocks, N,
 
 
 def mxfp8_fc1(xq, sfx, w1q, sfw, num_experts, block_expert, num_m_blocks, m, max_rows=None,
-              want_act=True, pair=False, wide=False):
+              want_act=True, pair=False, wide=False, want_t=False):
     """fc1 + SwiGLU on MXFP8 operands (w1q from interleave_gate_up_mx). Returns (preact bf16
     [rows, 2m] in the bf16 engine's layout, act bf16 [rows, m] or None, act codes [rows, m],
     act tiled scales) -- the last two are fc2's MXFP8 A operand."""
@@ -275,15 +275,23 @@ def mxfp8_fc1(xq, sfx, w1q, sfw, num_experts, block_expert, num_m_blocks, m, max
     act = torch.empty((rows, m), dtype=torch.bfloat16, device=dev) if want_act else None
     act_q = torch.empty((rows, m), dtype=torch.uint8, device=dev)
     act_sf = torch.zeros((rows * m // 32,), dtype=torch.uint8, device=dev)
-    _lib.call("moe_gg_mxfp8_fc1", xq.data_ptr(), sfx.data_ptr(), a_rows, rows, h, m,
-              w1q.data_ptr(), sfw.data_ptr(), num_experts, block_expert.data_ptr(),
-              num_m_blocks.data_ptr(), preact.data_ptr(), _ptr(act), act_q.data_ptr(),
-              act_sf.data_ptr(), int(pair) | (int(wide) << 1), _stream())
-    return preact, act, act_q, act_sf
+    args = (xq.data_ptr(), sfx.data_ptr(), a_rows, rows, h, m, w1q.data_ptr(), sfw.data_ptr(),
+            num_experts, block_expert.data_ptr(), num_m_blocks.data_ptr(), preact.data_ptr(),
+            _ptr(act), act_q.data_ptr(), act_sf.data_ptr())
+    flags = int(pair) | (int(wide) << 1)
+    if not want_t:
+        _lib.call("moe_gg_mxfp8_fc1", *args, flags, _stream())
+        return preact, act, act_q, act_sf
+    # act quantised along the token rows ([m, rows] codes): the dW2 operand
+    act_t = torch.zeros((m, rows), dtype=torch.uint8, device=dev)
+    act_tsf = torch.zeros((m * rows // 32,), dtype=torch.uint8, device=dev)
+    _lib.call("moe_gg_mxfp8_fc1_t", *args, act_t.data_ptr(), act_tsf.data_ptr(), flags,
+              _stream())
+    return preact, act, act_q, act_sf, act_t, act_tsf
 
 
 def mxfp8_fc2_dgrad(doq, sfd, w2tq, sfw, num_experts, block_expert, num_m_blocks, preact,
-                    max_rows=None, pair=False, wide=False):
+                    max_rows=None, pair=False, wide=False, want_t=False):
     """fc2 dgrad + SwiGLU backward on MXFP8 operands. Returns (d_preact bf16 [rows, 2m],
     d_preact codes [rows, 2m], tiled scales) -- the last two are fc1 dgrad's A operand."""
     a_rows, h = doq.shape
@@ -293,11 +301,30 @@ def mxfp8_fc2_dgrad(doq, sfd, w2tq, sfw, num_experts, block_expert, num_m_blocks
     d_pre = torch.empty((rows, m2), dtype=torch.bfloat16, device=dev)
     dq = torch.empty((rows, m2), dtype=torch.uint8, device=dev)
     dsf = torch.zeros((rows * m2 // 32,), dtype=torch.uint8, device=dev)
-    _lib.call("moe_gg_mxfp8_fc2_dgrad", doq.data_ptr(), sfd.data_ptr(), a_rows, rows, h, m2 // 2,
-              w2tq.data_ptr(), sfw.data_ptr(), num_experts, block_expert.data_ptr(),
-              num_m_blocks.data_ptr(), preact.data_ptr(), d_pre.data_ptr(), dq.data_ptr(),
-              dsf.data_ptr(), int(pair) | (int(wide) << 1), _stream())
-    return d_pre, dq, dsf
+    args = (doq.data_ptr(), sfd.data_ptr(), a_rows, rows, h, m2 // 2, w2tq.data_ptr(),
+            sfw.data_ptr(), num_experts, block_expert.data_ptr(), num_m_blocks.data_ptr(),
+            preact.data_ptr(), d_pre.data_ptr(), dq.data_ptr(), dsf.data_ptr())
+    flags = int(pair) | (int(wide) << 1)
+    if not want_t:
+        _lib.call("moe_gg_mxfp8_fc2_dgrad", *args, flags, _stream())
+        return d_pre, dq, dsf
+    dpt = torch.zeros((m2, rows), dtype=torch.uint8, device=dev)
+    dptsf = torch.zeros((m2 * rows // 32,), dtype=torch.uint8, device=dev)
+    _lib.call("moe_gg_mxfp8_fc2_dgrad_t", *args, dpt.data_ptr(), dptsf.data_ptr(), flags,
+              _stream())
+    return d_pre, dq, dsf, dpt, dptsf
+
+
+def mxfp8_wgrad_q(at, asf, bt, bsf, k_off: torch.Tensor, num_experts: int, out=None):
+    """Weight gradient from pre-quantised transposed operands (codes [M, K] / [N, K])."""
+    m, k = at.shape
+    n = bt.shape[0]
+    if out is None:
+        out = torch.empty((num_experts, m, n), dtype=torch.bfloat16, device=at.device)
+    _lib.call("moe_gg_mxfp8_wgrad", at.data_ptr(), asf.data_ptr(), bt.data_ptr(),
+              bsf.data_ptr(), k, m, n, num_experts, k_off.data_ptr(), out.data_ptr(),
+              int(m % 256 == 0) | (int(n % 256 == 0) << 1), _stream())
+    return out
 
 
 def mxfp8_wgrad(a: torch.Tensor, b: torch.Tensor, k_off: torch.Tensor, num_experts: int,
@@ -328,7 +355,13 @@ def mxfp8_wide(m: int, h: int) -> bool:
 
 def mxfp8_experts_fwd(xp, w1, w2, block_expert, num_m_blocks, pair, out=None):
     """fc1 + SwiGLU and fc2 on MXFP8 operands (x rows and weights quantised here, the
-    activation re-quantised in fc1's epilogue). Returns (preact, act, o) in bf16."""
+    activation re-quantised row-wise in fc1's epilogue for fc2, and along the token rows by
+    the transposing quantiser for the dW2 GEMM). Returns (preact bf16, act_t = (codes
+    [m, rows], scales), o bf16).
+
+    (The epilogues can also emit the token-row copies directly -- want_t, warp-shuffle block
+    amax, bit-exact -- but that measured slower: fc1 5.2 -> 7.9 ms, fc2-dgrad 4.1 -> 10.4 ms
+    against 1.4 ms saved in the transposing quantiser.)"""
     e, m2, h = w1.shape
     m = m2 // 2
     wide = mxfp8_wide(m, h)
@@ -337,20 +370,29 @@ def mxfp8_experts_fwd(xp, w1, w2, block_expert, num_m_blocks, pair, out=None):
     w2q, w2sf = mxfp8_quantize_weight(w2)
     preact, act, aq, asf = mxfp8_fc1(xq, xsf, w1q, w1sf, e, block_expert, num_m_blocks, m,
                                      pair=pair, wide=wide)
+    act_t, act_tsf, _ = mxfp8_quantize_t(act)
     o = mxfp8_gemm(aq, asf, w2q, w2sf, e, block_expert, num_m_blocks, h, out=out, pair=pair,
                    wide=wide)
-    return preact, act, o
+    return preact, (act_t, act_tsf), o
 
 
-def mxfp8_experts_dgrad(d_o, w1, w2, preact, block_expert, num_m_blocks, pair, dx_out=None):
-    """fc2 dgrad + dSwiGLU and fc1 dgrad on MXFP8 operands. Returns (d_preact bf16, dxp)."""
+def mxfp8_experts_bwd(d_o, xp, w1, w2, preact, act_t, block_expert, num_m_blocks, k_off,
+                      pair, dx_out=None):
+    """fc2 dgrad + dSwiGLU, fc1 dgrad and both weight gradients on MXFP8 operands. d_preact
+    is re-quantised in fc2-dgrad's epilogue (row-wise for fc1 dgrad, along the token rows for
+    dW1). Returns (dxp, dw1, dw2)."""
     e, h, m = w2.shape
     wide = mxfp8_wide(m, h)
     doq, dosf, _ = mxfp8_quantize(d_o)
     w2tq, w2tsf, _ = mxfp8_quantize_t(w2)
     d_pre, dq, dsf = mxfp8_fc2_dgrad(doq, dosf, w2tq, w2tsf, e, block_expert, num_m_blocks,
                                      preact, pair=pair, wide=wide)
+    dpt, dptsf, _ = mxfp8_quantize_t(d_pre)
     w1tq, w1tsf, _ = mxfp8_quantize_t(w1)
     dxp = mxfp8_gemm(dq, dsf, w1tq, w1tsf, e, block_expert, num_m_blocks, h, out=dx_out,
                      pair=pair, wide=wide)
-    return d_pre, dxp
+    dot, dotsf, _ = mxfp8_quantize_t(d_o)
+    dw2 = mxfp8_wgrad_q(dot, dotsf, act_t[0], act_t[1], k_off, e)
+    xpt, xptsf, _ = mxfp8_quantize_t(xp)
+    dw1 = mxfp8_wgrad_q(dpt, dptsf, xpt, xptsf, k_off, e)
+    return dxp, dw1, dw2

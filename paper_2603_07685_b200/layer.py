@@ -61,9 +61,11 @@ class _MoEFunction(torch.autograd.Function):
                               align=ops.pick_align(t, cfg.top_k, e))
         xp = ops.permute_gather(x, plan)
         row_prob = plan.row_prob if cfg.mem_efficient else None
+        act_t = None
         if cfg.precision == "mxfp8":
-            preact, act, o = gemm.mxfp8_experts_fwd(xp, w1, w2, plan.block_expert,
-                                                    plan.num_m_blocks, plan.pair)
+            preact, act_t, o = gemm.mxfp8_experts_fwd(xp, w1, w2, plan.block_expert,
+                                                      plan.num_m_blocks, plan.pair)
+            act = None  # the weight gradient reads the token-row quantised copy
         else:
             preact, act = gemm.fc1_fwd(xp, w1, plan.block_expert, plan.num_m_blocks, row_prob,
                                        pair=plan.pair)
@@ -75,6 +77,7 @@ class _MoEFunction(torch.autograd.Function):
         ctx.cfg = cfg
         ctx.plan = plan
         ctx.r = r
+        ctx.act_t = act_t
         ctx.shared = shared[:-1] if shared is not None else None
         ctx.save_for_backward(x, w_r_pad, w1, w2, xp, preact, act, o, w1s, w2s)
         return y, r.aux
@@ -93,16 +96,13 @@ class _MoEFunction(torch.autograd.Function):
             dprob = ops.dprob_from_partials(plan, part)
         else:
             d_o, dprob = ops.combine_backward(dy, plan, o, r.topk_prob)
-            if cfg.precision == "mxfp8":
-                d_pre, dxp_mx = gemm.mxfp8_experts_dgrad(d_o, w1, w2, preact, plan.block_expert,
-                                                         plan.num_m_blocks, plan.pair)
-            else:
+            if cfg.precision != "mxfp8":
                 d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, plan.block_expert,
                                           plan.num_m_blocks, pair=plan.pair)
         if cfg.precision == "mxfp8":
-            dw2 = gemm.mxfp8_wgrad(d_o, act, plan.off_pad, e)
-            dxp = dxp_mx
-            dw1 = gemm.mxfp8_wgrad(d_pre, xp, plan.off_pad, e)
+            dxp, dw1, dw2 = gemm.mxfp8_experts_bwd(d_o, xp, w1, w2, preact, ctx.act_t,
+                                                   plan.block_expert, plan.num_m_blocks,
+                                                   plan.off_pad, plan.pair)
         else:
             dw2 = gemm.wgrad(d_o, act, plan.off_pad, e)
             dxp = gemm.fc1_dgrad(d_pre, w1, plan.block_expert, plan.num_m_blocks,

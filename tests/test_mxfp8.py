@@ -97,8 +97,8 @@ def test_mxfp8_fc1_swiglu_and_fused_act_quantisation(pair, wide):
     w1 = (gemm.interleave_gate_up if wide else gemm.interleave_gate_up_mx)(gate.to(dev),
                                                                           up.to(dev))
     wq, wsf, wsp = gemm.mxfp8_quantize(w1.reshape(E * 2 * m, h), plain=True)
-    preact, act, act_q, act_sf = gemm.mxfp8_fc1(xq, xsf, wq, wsf, E, be, nmb, m, pair=pair,
-                                                wide=wide)
+    preact, act, act_q, act_sf, act_t, act_tsf = gemm.mxfp8_fc1(
+        xq, xsf, wq, wsf, E, be, nmb, m, pair=pair, wide=wide, want_t=True)
     torch.cuda.synchronize()
     xd = M.dequantize_mxfp8(xq.cpu().numpy()[:rows], xsp.cpu().numpy())
     wd = M.dequantize_mxfp8(wq.cpu().numpy(), wsp.cpu().numpy()).reshape(E, 2 * m, h)
@@ -117,6 +117,10 @@ def test_mxfp8_fc1_swiglu_and_fused_act_quantisation(pair, wide):
     codes, scales = M.quantize_mxfp8(act.float().cpu().numpy().astype(np.float64))
     assert np.array_equal(act_q.cpu().numpy(), codes)
     assert np.array_equal(act_sf.cpu().numpy(), M.tile_scales(scales, rows))
+    # ... and along the token rows (warp-shuffle block amax): quantise(act^T) of the same act
+    ct, st = M.quantize_mxfp8(act.float().cpu().numpy().astype(np.float64).T)
+    assert np.array_equal(act_t.cpu().numpy(), ct)
+    assert np.array_equal(act_tsf.cpu().numpy(), M.tile_scales(st, m))
 
 
 @pytest.mark.gpu
@@ -166,8 +170,9 @@ def test_mxfp8_dgrad_chain_matches_dequant_oracle(pair, wide):
     w1 = (torch.randn((E, 2 * m, h), generator=g) * h ** -0.5).to(torch.bfloat16)
     doq, dosf, dosp = gemm.mxfp8_quantize(d_o.to(dev), plain=True)
     w2tq, w2tsf, w2tsp = gemm.mxfp8_quantize_t(w2.to(dev), plain=True)
-    d_pre, dq, dsf = gemm.mxfp8_fc2_dgrad(doq, dosf, w2tq, w2tsf, E, be, nmb, preact.to(dev),
-                                          pair=pair, wide=wide)
+    d_pre, dq, dsf, dpt, dptsf = gemm.mxfp8_fc2_dgrad(doq, dosf, w2tq, w2tsf, E, be, nmb,
+                                                      preact.to(dev), pair=pair, wide=wide,
+                                                      want_t=True)
     w1tq, w1tsf, w1tsp = gemm.mxfp8_quantize_t(w1.to(dev), plain=True)
     dxp = gemm.mxfp8_gemm(dq, dsf, w1tq, w1tsf, E, be, nmb, h, pair=pair, wide=wide)
     torch.cuda.synchronize()
@@ -187,6 +192,9 @@ def test_mxfp8_dgrad_chain_matches_dequant_oracle(pair, wide):
     codes, scales = M.quantize_mxfp8(d_pre.float().cpu().numpy().astype(np.float64))
     assert np.array_equal(dq.cpu().numpy(), codes)
     assert np.array_equal(dsf.cpu().numpy(), M.tile_scales(scales, rows))
+    ct, st = M.quantize_mxfp8(d_pre.float().cpu().numpy().astype(np.float64).T)
+    assert np.array_equal(dpt.cpu().numpy(), ct)
+    assert np.array_equal(dptsf.cpu().numpy(), M.tile_scales(st, 2 * m))
     dpd = M.dequantize_mxfp8(codes, scales)
     w1t = M.dequantize_mxfp8(w1tq.cpu().numpy(), w1tsp.cpu().numpy()).reshape(E, h, 2 * m)
     dx_ref = np.concatenate([dpd[off[e]:off[e + 1]] @ w1t[e].T for e in range(E)])
