@@ -60,10 +60,9 @@ def gemm_flops_per_token(c) -> float:
 # ----------------------------------------------------------------------------- clocks
 class NvmlClockSampler:
     """In-process NVML sampling of the same fields nvidia-smi's clocks line reports (SM clock,
-    max SM clock, clock-event reasons), every 50 ms inside the timed window. NVML is the
-    library nvidia-smi itself calls; polling it from a thread avoids the driver contention
-    of a polling nvidia-smi process, which was measured to stall kernel launches on some
-    boxes (timed steps 1.6-1.9x their kernel time)."""
+    max SM clock, clock-event reasons), every 20 ms inside the timed window. NVML is the
+    library nvidia-smi itself calls; reading it directly timestamps every sample inside the
+    window (a polling nvidia-smi process delivered lines late through its pipe)."""
 
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                "sw_power_cap": 0x4}
@@ -96,7 +95,9 @@ class NvmlClockSampler:
                     self.samples.append((time.time(), sm, smax, rs))
                 except Exception:  # noqa: BLE001
                     pass
-            time.sleep(0.05)
+                time.sleep(0.02)
+            else:
+                time.sleep(0.005)
 
     def window(self, start: bool):
         if start:
@@ -113,7 +114,7 @@ class NvmlClockSampler:
                           if x[3] & bit})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None, "reasons": reasons,
-                "samples": len(sm), "source": "NVML (nvidia-smi's library), 50 ms"}
+                "samples": len(sm), "source": "NVML (nvidia-smi's library), every 20 ms"}
 
 
 class ClockSampler:
