@@ -339,23 +339,23 @@ def run_gpu(args, c) -> None:
         t_wait = time.time()
         while not clocks.lines and time.time() - t_wait < 10:
             time.sleep(0.05)
-    for _ in range(args.warmup):
-        step(x, dy)
+    if not args.graph:
+        for _ in range(args.warmup):
+            step(x, dy)
     barrier()
 
     run = step
     graph_launches = None
-    if args.graph and n == 1:
-        raise SystemExit("--graph captures the sync-free EP step (--gpus >= 2); the EP=1 "
-                         "layer is launch-bound only at small token counts")
     if args.graph:
         # whole fwd+bwd step (router, EP planning on the device, exchanges, GEMMs, NCCL
         # all-gather / barriers) captured once and replayed: no host work per step
+        # warm-up on a side stream only: eager steps on the legacy default stream before
+        # the capture make it fail (cudaErrorStreamCaptureImplicit, measured at EP=1)
         sx, sdy = x.clone(), dy.clone()
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
-            for _ in range(2):
+            for _ in range(max(args.warmup, 2)):
                 step(sx, sdy)
         torch.cuda.current_stream().wait_stream(side)
         barrier()

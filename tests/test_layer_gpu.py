@@ -165,3 +165,37 @@ def test_mxfp8_forward_experts(dev):
     GEMM-level parity against the dequantised oracle is tests/test_mxfp8.py."""
     cfg = MoEConfig(8, 2, 256, 256, score="softmax", aux_loss_coeff=1e-2, precision="mxfp8")
     run_case(cfg, 512, 21, dev, y_tol=0.1, g_tol=0.12)
+
+
+def test_cuda_graph_capture_matches_eager(dev):
+    """The EP=1 step has no host sync, so fwd+bwd captures into one CUDA graph; replays give
+    the eager results bit for bit (warm-up on a side stream, as bench.py --graph does)."""
+    cfg = MoEConfig(8, 2, 256, 256, score="softmax", aux_loss_coeff=1e-2)
+    x, w_r, gate, up, w2, dy, _ = make(cfg, 512, 31, dev)
+    x, w_r, w2, dy = x.to(dev), w_r.to(dev).requires_grad_(), w2.to(dev).requires_grad_(), dy.to(dev)
+    w1 = gemm.interleave_gate_up(gate.to(dev), up.to(dev)).requires_grad_()
+
+    def step():
+        for p in (w_r, w1, w2):
+            p.grad = None
+        xx = x.detach().requires_grad_(True)
+        y, aux = moe_forward(xx, w_r, w1, w2, cfg)
+        torch.autograd.backward([y, aux], [dy, torch.ones_like(aux)])
+        return y, xx
+
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(2):
+            y_e, x_e = step()
+        ref = [y_e.detach().clone(), x_e.grad.clone(), w_r.grad.clone(), w1.grad.clone(),
+               w2.grad.clone()]
+    torch.cuda.current_stream().wait_stream(side)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        y_g, x_g = step()
+    for _ in range(2):
+        graph.replay()
+    torch.cuda.synchronize()
+    got = [y_g, x_g.grad, w_r.grad, w1.grad, w2.grad]
+    assert all(torch.equal(a, b) for a, b in zip(ref, got))
