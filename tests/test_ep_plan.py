@@ -152,3 +152,47 @@ def test_ep_plan_single_process_world4():
     sent = sum(sum(ep_host_plan(counts_all, r, -1).send_splits) -
                ep_host_plan(counts_all, r, -1).send_splits[r] for r in range(n))
     assert sent <= n * T * K
+
+
+def test_static_rows_bound_every_plan():
+    """Sync-free EP buffers (dispatcher.ep_static_rows) bound every rank's padded plan,
+    including all-to-one routing and capacity with pad."""
+    from paper_2603_07685_b200 import ops
+    from paper_2603_07685_b200.dispatcher import ep_static_rows, p2p_tables
+
+    rng = np.random.default_rng(41)
+    for _ in range(200):
+        n = int(rng.choice([2, 4, 8]))
+        el = int(rng.integers(1, 5))
+        E, T, K = n * el, int(rng.integers(1, 300)), int(rng.integers(1, min(4, n * el) + 1))
+        cf = [None, 0.5, 1.0, 2.0][int(rng.integers(0, 4))]
+        pad = bool(rng.integers(0, 2))
+        cap = -1 if cf is None else -(-int(round(cf * n * T * K)) // E)
+        align = ops.pick_align(n * T, K, E)
+        if rng.random() < 0.3:  # everything onto rank 0's first expert
+            counts = np.zeros((n, E), dtype=np.int64)
+            counts[:, 0] = T * K
+        else:
+            counts = np.stack([rng.multinomial(T * K, rng.dirichlet(np.ones(E) * 0.3))
+                               for _ in range(n)])
+        bound = ep_static_rows(n, T, K, E, cap, align)
+        for me in range(n):
+            _, rows_all, hp = p2p_tables(counts, me, cap, pad, align)
+            assert max(rows_all) <= bound, (n, E, T, K, cf, pad)
+            assert hp.rows_pad % align == 0
+
+
+def test_mx_interleave_layouts():
+    """The MXFP8 fc1 weight layouts (64-row gate/up blocks, or the bf16 engine's 128) keep
+    every (gate, up) pair inside one GEMM tile of the matching width."""
+    from paper_2603_07685_b200 import gemm
+
+    E, m, h = 2, 256, 8
+    gate = torch.arange(E * m * h, dtype=torch.float32).reshape(E, m, h)
+    up = -gate
+    w64 = gemm.interleave_gate_up_mx(gate, up)
+    w128 = gemm.interleave_gate_up(gate, up)
+    for w, blk in ((w64, 64), (w128, 128)):
+        v = w.reshape(E, m // blk, 2, blk, h)
+        assert torch.equal(v[:, :, 0].reshape(E, m, h), gate)
+        assert torch.equal(v[:, :, 1].reshape(E, m, h), up)
