@@ -547,7 +547,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
     def forward(ctx, x, w_r, w1, w2, sel_bias, w1s, w2s, cfg: MoEConfig, ep: EPGroup,
                 echo_slots: int = 0, scatter: bool = True, tag: str = "",
                 overlap: bool = True, sync_free: bool = False, stash=None,
-                layer_id: int = 0):
+                layer_id: int = 0, stash_overlap: bool = False):
         t, h = x.shape
         E, K = cfg.num_experts, cfg.top_k
         mx = cfg.precision == "mxfp8"
@@ -562,6 +562,12 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         r = ops.router_forward(x, w_r, K, cfg.score, sel_bias, 0.0, w_r_t=w_r_t)
         stats = torch.cat([r.counts.float(), r.mean_scores])
         gathered = torch.empty((n, 2 * E), dtype=torch.float32, device=dev)
+        if stash is not None and stash_overlap:
+            # this tag's tmp buffers are free once the stash of its previous layer (on the
+            # pack stream) has read them; ordering the all-gather after that also keeps
+            # peers from pushing into xp early
+            for ev in getattr(pool, "stash_done", ()):
+                torch.cuda.current_stream().wait_event(ev)
         dist.all_gather_into_tensor(gathered, stats, group=ep.group)  # also the reuse barrier
         cap = cfg.capacity(n * t)
         layout = None
@@ -742,11 +748,18 @@ class _MoEEPP2PFunction(torch.autograd.Function):
                 raise ValueError("paged stashing needs the sync-free p2p transport with the "
                                  "standard combine")
             st_plan, st_out = _stash_pair(stash)
-            st_plan.stash(2 * layer_id, {"xp": xp, "preact": preact, "act": act},
-                          rows_dev=meta_d[1:2])
-            st_out.stash(2 * layer_id + 1, {"o": o_local}, rows_dev=splan.meta[2:3])
+            if stash_overlap:  # copies on the pack stream, overlapping the next layer
+                pool.stash_done = (
+                    st_plan.stash_async(2 * layer_id, {"xp": xp, "preact": preact, "act": act},
+                                        rows_dev=meta_d[1:2]),
+                    st_out.stash_async(2 * layer_id + 1, {"o": o_local},
+                                       rows_dev=splan.meta[2:3]))
+            else:
+                st_plan.stash(2 * layer_id, {"xp": xp, "preact": preact, "act": act},
+                              rows_dev=meta_d[1:2])
+                st_out.stash(2 * layer_id + 1, {"o": o_local}, rows_dev=splan.meta[2:3])
             preact = act = None
-        ctx.stash, ctx.layer_id = stash, layer_id
+        ctx.stash, ctx.layer_id, ctx.stash_overlap = stash, layer_id, stash_overlap
         ctx.rows_bound = rows_bound
         ctx.scatter, ctx.tag, ctx.row_dst_dx = scatter, tag, row_dst_dx
         ctx.cfg, ctx.ep, ctx.r, ctx.splan, ctx.cap, ctx.pair = cfg, ep, r, splan, cap, pair
@@ -779,6 +792,11 @@ class _MoEEPP2PFunction(torch.autograd.Function):
             st_plan.reload(2 * ctx.layer_id, {"xp": xp, "preact": preact, "act": act},
                            rows_dev=meta_d[1:2])
             st_out.reload(2 * ctx.layer_id + 1, {"o": ctx.o_local}, rows_dev=splan.meta[2:3])
+            if ctx.stash_overlap and ctx.layer_id > 0:
+                # prefetch the previous layer's rows (other tag: its buffers were last used
+                # by the backward that just finished) while this layer's backward computes
+                st_plan.prefetch(2 * (ctx.layer_id - 1))
+                st_out.prefetch(2 * (ctx.layer_id - 1) + 1)
         d_o, d_peers = pool.get("do", rows_alloc * h, torch.bfloat16)
         d_o = d_o[: rows_alloc * h].view(rows_alloc, h)
         _lib.call("moe_zero_pad_rows", meta_d.data_ptr(), map_pad.data_ptr(), h, d_o.data_ptr(),
@@ -870,7 +888,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
             dw1 = _echo_reduce(pool, ep, dw1, ctx.layout, ctx.el_own, "echo_dw1")
             dw2 = _echo_reduce(pool, ep, dw2, ctx.layout, ctx.el_own, "echo_dw2")
         return (dx, dw_r.to(torch.bfloat16), dw1, dw2, None, dw1s, dw2s, None, None, None, None,
-                None, None, None, None, None)
+                None, None, None, None, None, None)
 
 
 def _stash_pair(stash):
@@ -1094,7 +1112,7 @@ class _MoEEPDedupFunction(torch.autograd.Function):
 def moe_forward_ep(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
                    selection_bias=None, w1_shared=None, w2_shared=None, transport: str = "auto",
                    echo_slots: int = 0, tag: str = "", sync_free: bool = False,
-                   stash=None, layer_id: int = 0):
+                   stash=None, layer_id: int = 0, stash_overlap: bool = False):
     """EP MoE layer: w1_local [E/EP, 2m, h], w2_local [E/EP, h, m] are this rank's experts
     (global experts [rank*E/EP, (rank+1)*E/EP)). Returns (y [T,h], global aux).
 
@@ -1124,6 +1142,10 @@ def moe_forward_ep(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
       actual rows are copied into pages after its forward and back before its backward, so
       memory is O(worst case + sum of actual rows) instead of O(layers x worst case).
       layer_id: this layer's stash record key (unique among live layers).
+    stash_overlap: run the stash copies on a pack stream while the next layer computes and
+      prefetch reloads on an unpack stream during the later layer's backward.
+      Needs two alternating tags (layer i uses tag of parity i % 2: double-buffered tmp
+      sets) and layer ids 0, 1, 2, ... in forward order.
 
     The router weight gradient returned is this rank's partial sum over its own tokens;
     W_r is replicated, so its all-reduce belongs to the data-parallel gradient sync.
@@ -1140,7 +1162,8 @@ def moe_forward_ep(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
         # ECHO hot-expert cloning runs on the p2p transport (virtual experts)
         return _MoEEPP2PFunction.apply(*args, int(echo_slots), transport != "p2p_pull", tag,
                                        transport == "p2p_overlap",
-                                       sync_free and not echo_slots, stash, int(layer_id))
+                                       sync_free and not echo_slots, stash, int(layer_id),
+                                       bool(stash_overlap))
     if cfg.precision != "bf16":
         raise ValueError(f"precision {cfg.precision!r} runs on the p2p / p2p_pull transports")
     if transport == "p2p_dedup":

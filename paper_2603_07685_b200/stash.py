@@ -44,11 +44,57 @@ class PagedStashBuffer:
         self.records = torch.zeros((max_records, 1 + self.max_pages), **i32)
         self._slot: dict[int, int] = {}  # live layer id -> record slot (host bookkeeping)
         self._free_slots = list(range(max_records))
+        # overlap: stash copies on a "pack" stream while the next layer
+        # computes, reloads prefetched on an "unpack" stream during the later layer's
+        # backward; _dest keeps each record's reload destination + row count
+        self.pack = torch.cuda.Stream(device=dev)
+        self.unpack = torch.cuda.Stream(device=dev)
+        self._dest: dict[int, tuple] = {}
+        self._prefetched: dict[int, torch.cuda.Event] = {}
+        self._stashed: dict[int, torch.cuda.Event] = {}  # pack-stream completion per record
         _lib.call("moe_stash_init", self.state.data_ptr(), self.ring.data_ptr(), num_pages,
                   _stream())
 
     def pages_needed(self, rows: int) -> int:
         return -(-rows // self.page_rows)
+
+    def stash_async(self, layer_id: int, tensors: dict[str, torch.Tensor], rows_dev=None,
+                    rows: int = 0) -> torch.cuda.Event:
+        """stash() on the pack stream, ordered after the current stream's work so far.
+        Returns the event after which the tensors may be overwritten (the caller must make
+        the next writer of these buffers wait on it)."""
+        cur = torch.cuda.current_stream()
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        self.pack.wait_event(ev)
+        with torch.cuda.stream(self.pack):
+            self.stash(layer_id, tensors, rows_dev, rows)
+            done = torch.cuda.Event()
+            done.record(self.pack)
+        self._stashed[layer_id] = done
+        return done
+
+    def prefetch(self, layer_id: int) -> bool:
+        """Start the reload of a stashed record on the unpack stream, into the tensors it
+        was stashed from (stash(..., keep_dest=True)), ordered after the current stream's
+        work so far. reload() of that record then only waits for it."""
+        if layer_id not in self._slot or layer_id not in self._dest or \
+                layer_id in self._prefetched:
+            return False
+        tensors, rows_dev, rows = self._dest[layer_id]
+        cur = torch.cuda.current_stream()
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        self.unpack.wait_event(ev)
+        st = self._stashed.pop(layer_id, None)
+        if st is not None:  # the pages must have been written
+            self.unpack.wait_event(st)
+        with torch.cuda.stream(self.unpack):
+            self._reload_now(layer_id, tensors, rows_dev, rows)
+            done = torch.cuda.Event()
+            done.record(self.unpack)
+        self._prefetched[layer_id] = done
+        return True
 
     def stash(self, layer_id: int, tensors: dict[str, torch.Tensor], rows_dev=None,
               rows: int = 0) -> torch.Tensor:
@@ -67,14 +113,27 @@ class PagedStashBuffer:
                   self.page_rows, rd, int(rows), rec.data_ptr(), self.max_pages, _stream())
         for nm, t in tensors.items():
             self._copy(nm, t, rec, rd, rows, to_pages=True)
+        self._dest[layer_id] = (dict(tensors), rows_dev, rows)
         return rec
 
     def reload(self, layer_id: int, tensors: dict[str, torch.Tensor], rows_dev=None,
                rows: int = 0) -> None:
-        """Copy the layer's rows back into the given dense tensors, then free its pages."""
+        """Copy the layer's rows back into the given dense tensors, then free its pages (or,
+        if prefetch() already did that into the same tensors, wait for it)."""
+        ev = self._prefetched.pop(layer_id, None)
+        if ev is not None:
+            torch.cuda.current_stream().wait_event(ev)
+            return
+        st = self._stashed.pop(layer_id, None)
+        if st is not None:  # a stash_async record: its pages must have been written
+            torch.cuda.current_stream().wait_event(st)
+        self._reload_now(layer_id, tensors, rows_dev, rows)
+
+    def _reload_now(self, layer_id, tensors, rows_dev, rows):
         slot = self._slot.pop(layer_id, None)
         if slot is None:
             raise KeyError(f"no stash record for layer {layer_id}")
+        self._dest.pop(layer_id, None)
         rec = self.records[slot]
         rd = rows_dev.data_ptr() if rows_dev is not None else None
         for nm, t in tensors.items():
@@ -86,6 +145,7 @@ class PagedStashBuffer:
     def release(self, layer_id: int) -> None:
         """Free a record's pages without copying (e.g. a failed or abandoned stash)."""
         slot = self._slot.pop(layer_id)
+        self._dest.pop(layer_id, None)
         _lib.call("moe_stash_release", self.state.data_ptr(), self.ring.data_ptr(),
                   self.num_pages, self.records[slot].data_ptr(), _stream())
         self._free_slots.append(slot)

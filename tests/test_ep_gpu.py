@@ -276,7 +276,7 @@ def _stash_worker(rank, world, port, q):
         ep = EPGroup()
         rows_w = {"xp": h * 2, "preact": 4 * m, "act": 2 * m, "o": h * 2}
 
-        def run(stash):
+        def run(stash, overlap=False):
             for ws in layers:
                 for w in ws:
                     w.grad = None
@@ -284,9 +284,13 @@ def _stash_worker(rank, world, port, q):
             y = x
             auxes = []
             for li, (w_r, w1, w2) in enumerate(layers):
-                tag = "shared" if stash is not None else f"layer{li}"
+                if stash is None:
+                    tag = f"layer{li}"
+                else:  # overlapped stashing double-buffers the tmp set (two tags)
+                    tag = f"ov{li % 2}" if overlap else "shared"
                 y, aux = moe_forward_ep(y, w_r, w1, w2, cfg, ep, transport="p2p", sync_free=True,
-                                        tag=tag, stash=stash, layer_id=li)
+                                        tag=tag, stash=stash, layer_id=li,
+                                        stash_overlap=overlap)
                 auxes.append(aux)
             torch.autograd.backward([y] + auxes, [dy] + [torch.ones_like(a) for a in auxes])
             torch.cuda.synchronize()
@@ -296,10 +300,13 @@ def _stash_worker(rank, world, port, q):
         ref = run(None)
         buf = PagedStashBuffer(256, rows_w, page_rows=64, device=dev)
         got = run(buf)
+        got_ov = run(buf, overlap=True)
         buf.check()
         check_ep_status()
         st = buf.stats()
         bad = [i for i, (a, b) in enumerate(zip(ref, got)) if not torch.equal(a, b)]
+        bad += [f"overlap {i}" for i, (a, b) in enumerate(zip(ref, got_ov))
+                if not torch.equal(a, b)]
         if st["free_pages"] != 256 or st["peak_pages_used"] == 0:
             bad.append(f"pages {st}")
         q.put((rank, "ok" if not bad else f"mismatch {bad}"))

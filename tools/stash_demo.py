@@ -30,7 +30,7 @@ def main():
     ap.add_argument("--config", default="mixtral")
     ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--mode", default="both", choices=["both", "plain", "stash"])
+    ap.add_argument("--mode", default="both", choices=["both", "plain", "stash", "stash_overlap"])
     a = ap.parse_args()
     rank = int(os.environ["RANK"])
     torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
@@ -60,7 +60,7 @@ def main():
     plan_pages = int(1.25 * a.layers * -(-(T * K + el * align) // page_rows))
     out_pages = int(1.25 * a.layers * -(-(T * K) // page_rows))
 
-    def run(stash, tag_of):
+    def run(stash, tag_of, overlap=False):
         for ws in layers:
             for w in ws:
                 w.grad = None
@@ -73,7 +73,8 @@ def main():
             # residual stream, as in a transformer block (keeps the routing of deep layers
             # from collapsing onto one rank in this random-weight stack)
             out, aux = moe_forward_ep(y, w_r, w1, w2, cfg, ep, transport="p2p", sync_free=True,
-                                      tag=tag_of(li), stash=stash, layer_id=li)
+                                      tag=tag_of(li), stash=stash, layer_id=li,
+                                      stash_overlap=overlap)
             y = y + out
             auxes.append(aux)
             if stash is not None and os.environ.get("STASH_DEBUG") and rank == 0:
@@ -94,16 +95,17 @@ def main():
     results = {}
     for mode in (["plain", "stash"] if a.mode == "both" else [a.mode]):
         stash = None
-        if mode == "stash":
+        if mode in ("stash", "stash_overlap"):
             stash = (PagedStashBuffer(plan_pages, {"xp": 2 * h, "preact": 4 * m, "act": 2 * m},
                                       page_rows=page_rows, device=dev),
                      PagedStashBuffer(out_pages, {"o": 2 * h}, page_rows=page_rows, device=dev))
-            tag_of = lambda li: "shared"  # noqa: E731
+            tag_of = ((lambda li: f"ov{li % 2}") if mode == "stash_overlap"  # noqa: E731
+                      else (lambda li: "shared"))
         else:
             tag_of = lambda li: f"layer{li}"  # noqa: E731
         best = None
         for _ in range(a.steps):
-            used, tf, tb, res = run(stash, tag_of)
+            used, tf, tb, res = run(stash, tag_of, overlap=mode == "stash_overlap")
             best = (used, tf, tb) if best is None or tf + tb < best[1] + best[2] else best
         check_ep_status()
         entry = {"device_mem_in_use_at_peak_GB": round(best[0] / 1e9, 2),
