@@ -55,3 +55,26 @@ def test_missing_library_fails_loudly(tmp_path, monkeypatch):
     monkeypatch.setattr(_lib, "LIB_PATH", tmp_path / "missing.so")
     with pytest.raises(_lib.MoEKernelError, match="no CPU fallback"):
         _lib.load()
+
+
+def _declared_arity():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    out = {}
+    for m in re.finditer(r"^\s*(?:int|long long)\s+(moe_\w+)\s*\(([^)]*)\)\s*;", text,
+                         flags=re.M | re.S):
+        params = m.group(2).strip()
+        out[m.group(1)] = 0 if params in ("", "void") else params.count(",") + 1
+    return out
+
+
+def test_ctypes_signatures_match_header_arity():
+    """Every ctypes argtypes list has as many entries as the header declaration has
+    parameters (catches ABI drift between include/moe_b200.h and _lib.py)."""
+    arity = _declared_arity()
+    assert arity, "no declarations parsed"
+    for name, argtypes in _lib.SIGNATURES.items():
+        assert name in arity, f"{name} bound in _lib.py but not declared"
+        assert len(argtypes) == arity[name], (name, len(argtypes), arity[name])
+    for name, (argtypes, _) in _lib.QUERIES.items():
+        assert len(argtypes) == arity[name], (name, len(argtypes), arity[name])
