@@ -36,10 +36,41 @@ from .layer import MoEConfig, shared_expert_backward, shared_expert_forward
 
 
 class EPGroup:
+    """The EP process group (one rank per GPU, NCCL). Every collective the dispatcher
+    issues goes through these methods, so another group implementation (the single-GPU
+    loopback group of :mod:`paper_2603_07685_b200.loopback`) can stand in for it."""
+
     def __init__(self, group=None):
         self.group = group if group is not None else dist.group.WORLD
         self.n = dist.get_world_size(self.group)
         self.rank = dist.get_rank(self.group)
+
+    @property
+    def key(self):
+        return id(self.group)
+
+    def all_gather_into_tensor(self, out, inp):
+        dist.all_gather_into_tensor(out, inp, group=self.group)
+
+    def all_reduce(self, t):
+        dist.all_reduce(t, group=self.group)
+
+    def all_to_all_single(self, out, inp, out_splits, in_splits):
+        dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
+
+    def symm_empty(self, numel: int, dtype, dev):
+        """A symmetric (peer-mapped over NVLink) buffer: (tensor, [n] peer base pointers,
+        handle with get_remote_tensor(peer, shape, dtype)). Collective."""
+        import torch.distributed._symmetric_memory as symm
+
+        t = symm.empty(numel, dtype=dtype, device=dev)
+        h = symm.rendezvous(t, self.group)
+        ptrs = [int(p) for p in h.buffer_ptrs]
+        off = int(getattr(h, "offset", 0))
+        if ptrs[self.rank] != t.data_ptr():
+            ptrs = [p + off for p in ptrs]
+        assert ptrs[self.rank] == t.data_ptr(), "symmetric-memory peer pointers"
+        return t, ptrs, h
 
 
 @dataclass
@@ -167,8 +198,8 @@ class _Exchange:
         out_rows = self.total_recv if forward else self.total_send
         out = torch.empty((out_rows,) + tuple(send.shape[1:]), dtype=send.dtype,
                           device=send.device)
-        dist.all_to_all_single(out, send, hp.recv_splits if forward else hp.send_splits,
-                               hp.send_splits if forward else hp.recv_splits, group=group)
+        group.all_to_all_single(out, send, hp.recv_splits if forward else hp.send_splits,
+                                hp.send_splits if forward else hp.recv_splits)
         return out
 
     def to_padded(self, recv):
@@ -196,7 +227,7 @@ class _MoEEPFunction(torch.autograd.Function):
         r = ops.router_forward(x, w_r, K, cfg.score, sel_bias, 0.0, w_r_t=w_r_t)
         stats = torch.cat([r.counts.float(), r.mean_scores])
         gathered = torch.empty((n, 2 * E), dtype=torch.float32, device=dev)
-        dist.all_gather_into_tensor(gathered, stats, group=ep.group)
+        ep.all_gather_into_tensor(gathered, stats)
         g = gathered.cpu().numpy()  # the one host sync of the EP forward
         counts_all = np.rint(g[:, :E]).astype(np.int64)
         cap = cfg.capacity(n * t)  # global capacity on the global batch
@@ -217,11 +248,11 @@ class _MoEEPFunction(torch.autograd.Function):
         splan = ops.build_plan(r.topk_idx, r.topk_prob, E, -1, False, cap_e=cap_e, compact=True)
         send = ops.permute_gather(x, splan, out=torch.empty((max(xc.total_send, 1), h),
                                                             dtype=x.dtype, device=dev))
-        recv = xc.a2a(send[: xc.total_send], True, ep.group)
+        recv = xc.a2a(send[: xc.total_send], True, ep)
         xp = xc.to_padded(recv)
         row_prob = None
         if cfg.mem_efficient:
-            prob_recv = xc.a2a(splan.row_prob[: xc.total_send].contiguous(), True, ep.group)
+            prob_recv = xc.a2a(splan.row_prob[: xc.total_send].contiguous(), True, ep)
             mp = xc.map_pad.long()
             row_prob = torch.where(mp >= 0, prob_recv[mp.clamp(min=0)] if xc.total_recv else
                                    torch.zeros_like(mp, dtype=torch.float32),
@@ -229,7 +260,7 @@ class _MoEEPFunction(torch.autograd.Function):
         preact, act = gemm.fc1_fwd(xp, w1, xc.block_expert, xc.num_m_blocks, row_prob,
                                    pair=pair)
         o = gemm.fc2_fwd(act, w2, xc.block_expert, xc.num_m_blocks, pair=pair)
-        o_local = xc.a2a(xc.from_padded(o), False, ep.group)
+        o_local = xc.a2a(xc.from_padded(o), False, ep)
         shared = shared_expert_forward(x, w1s, w2s) if w1s is not None else None
         y = ops.combine(o_local, splan, None if cfg.mem_efficient else r.topk_prob,
                         resid=x if cap >= 0 else None,
@@ -254,13 +285,13 @@ class _MoEEPFunction(torch.autograd.Function):
             d_send, _ = ops.combine_backward(dy, splan, None, None, d_rows=d_send)
         else:
             d_send, dprob = ops.combine_backward(dy, splan, o_local, r.topk_prob, d_rows=d_send)
-        d_o = xc.to_padded(xc.a2a(d_send[: xc.total_send], True, ep.group))
+        d_o = xc.to_padded(xc.a2a(d_send[: xc.total_send], True, ep))
         if cfg.mem_efficient:
             d_pre, part = gemm.fc2_dgrad(d_o, w2, preact, xc.block_expert, xc.num_m_blocks,
                                          row_prob=ctx.row_prob, want_dprob=True, pair=ctx.pair)
             dp_pad = part.sum(dim=1)
             dp_recv = dp_pad[xc.map_recv.long()] if xc.total_recv else dp_pad[:0]
-            dp_send = xc.a2a(dp_recv.contiguous(), False, ep.group)
+            dp_send = xc.a2a(dp_recv.contiguous(), False, ep)
             inv = splan.inv_map.long()
             dprob = torch.where(inv >= 0, dp_send[inv.clamp(min=0)] if xc.total_send else
                                 torch.zeros_like(inv, dtype=torch.float32),
@@ -271,7 +302,7 @@ class _MoEEPFunction(torch.autograd.Function):
         dw2 = gemm.wgrad(d_o, act, xc.off_pad, el)
         dxp = gemm.fc1_dgrad(d_pre, w1, xc.block_expert, xc.num_m_blocks, pair=ctx.pair)
         dw1 = gemm.wgrad(d_pre, xp, xc.off_pad, el)
-        dxp_local = xc.a2a(xc.from_padded(dxp), False, ep.group)
+        dxp_local = xc.a2a(xc.from_padded(dxp), False, ep)
         aux_scale = None if daux is None else daux.float()
         dw_r, dx_router = ops.router_backward(x, w_r_pad, r, dprob, cfg.score,
                                               aux_scale=aux_scale)
@@ -295,9 +326,6 @@ class SymmPool:
     in the same order (sizes come from the all-gathered counts), so growth is collective."""
 
     def __init__(self, ep: EPGroup, dev):
-        import torch.distributed._symmetric_memory as symm
-
-        self._symm = symm
         self.ep = ep
         self.dev = dev
         self.bufs = {}
@@ -318,13 +346,7 @@ class SymmPool:
         cur = self.bufs.get(name)
         if cur is None or cur[0].numel() < numel or cur[0].dtype != dtype:
             cap = int(numel * 1.25) + 4096
-            t = self._symm.empty(cap, dtype=dtype, device=self.dev)
-            h = self._symm.rendezvous(t, self.ep.group)
-            ptrs = [int(p) for p in h.buffer_ptrs]
-            off = int(getattr(h, "offset", 0))
-            if ptrs[self.ep.rank] != t.data_ptr():
-                ptrs = [p + off for p in ptrs]
-            assert ptrs[self.ep.rank] == t.data_ptr(), "symmetric-memory peer pointers"
+            t, ptrs, h = self.ep.symm_empty(cap, dtype, self.dev)
             peers = torch.tensor(ptrs, dtype=torch.int64, device=self.dev)
             # start from zeros (no NaN garbage in rows that are never pushed) before any
             # peer can write into it
@@ -351,7 +373,7 @@ class SymmPool:
 
     def barrier(self):
         """Stream-ordered cross-rank barrier (an NCCL all-reduce of one float)."""
-        dist.all_reduce(self.bar, group=self.ep.group)
+        self.ep.all_reduce(self.bar)
 
 
 _POOLS: dict = {}
@@ -443,7 +465,7 @@ def _pool(ep: EPGroup, dev, tag: str = "") -> SymmPool:
     """Symmetric buffers per (EP group, device, tag). Layers that are alive at the same time
     (several MoE layers before their backward) must use distinct tags: a layer's received
     rows stay in its pool until its backward has run."""
-    key = (id(ep.group), dev.index, tag)
+    key = (ep.key, dev.index, tag)
     if key not in _POOLS:
         _POOLS[key] = SymmPool(ep, dev)
     return _POOLS[key]
@@ -568,7 +590,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
             # peers from pushing into xp early
             for ev in getattr(pool, "stash_done", ()):
                 torch.cuda.current_stream().wait_event(ev)
-        dist.all_gather_into_tensor(gathered, stats, group=ep.group)  # also the reuse barrier
+        ep.all_gather_into_tensor(gathered, stats)  # also the reuse barrier
         cap = cfg.capacity(n * t)
         layout = None
         topk_use, E_use = r.topk_idx, E
@@ -948,14 +970,14 @@ class _MoEEPDedupFunction(torch.autograd.Function):
             rank_idx, sel_j, sel_pos, rplan = token_ranks(splan)
             stats = torch.cat([r.counts.float(), r.mean_scores, rplan.counts.float()])
             gathered = torch.empty((n, 2 * E + n), dtype=torch.float32, device=dev)
-            dist.all_gather_into_tensor(gathered, stats, group=ep.group)
+            ep.all_gather_into_tensor(gathered, stats)
             g = gathered.cpu().numpy()  # the one host sync of the forward
             counts_all = np.rint(g[:, :E]).astype(np.int64)
             ntok = np.rint(g[:, 2 * E:]).astype(np.int64)
         else:
             stats = torch.cat([r.counts.float(), r.mean_scores])
             gathered = torch.empty((n, 2 * E), dtype=torch.float32, device=dev)
-            dist.all_gather_into_tensor(gathered, stats, group=ep.group)
+            ep.all_gather_into_tensor(gathered, stats)
             g = gathered.cpu().numpy()
             counts_all = np.rint(g[:, :E]).astype(np.int64)
         align = ops.pick_align(n * t, K, E)
@@ -970,7 +992,7 @@ class _MoEEPDedupFunction(torch.autograd.Function):
             rank_idx, sel_j, sel_pos, rplan = token_ranks(splan)
             tc = rplan.counts.float()
             gat2 = torch.empty((n, n), dtype=torch.float32, device=dev)
-            dist.all_gather_into_tensor(gat2, tc, group=ep.group)
+            ep.all_gather_into_tensor(gat2, tc)
             ntok = np.rint(gat2.cpu().numpy()).astype(np.int64)
         aux_v, aux_g = global_aux(counts_all, g[:, E:2 * E], t, K, cfg.aux_loss_coeff)
         # token-slot tables: this rank as source (tbase) and as destination (tok rows)
@@ -1150,6 +1172,17 @@ def moe_forward_ep(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
     The router weight gradient returned is this rank's partial sum over its own tokens;
     W_r is replicated, so its all-reduce belongs to the data-parallel gradient sync.
     """
+    fn, args = ep_function(x, w_r, w1_local, w2_local, cfg, ep, selection_bias, w1_shared,
+                           w2_shared, transport, echo_slots, tag, sync_free, stash, layer_id,
+                           stash_overlap)
+    return fn.apply(*args)
+
+
+def ep_function(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
+                selection_bias=None, w1_shared=None, w2_shared=None, transport: str = "auto",
+                echo_slots: int = 0, tag: str = "", sync_free: bool = False,
+                stash=None, layer_id: int = 0, stash_overlap: bool = False):
+    """(autograd.Function, apply-args) of moe_forward_ep's transport (same arguments)."""
     if cfg.num_experts % ep.n:
         raise ValueError(f"num_experts {cfg.num_experts} not divisible by EP {ep.n}")
     if transport == "auto":
@@ -1160,14 +1193,13 @@ def moe_forward_ep(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
     args = (x, w_r, w1_local, w2_local, selection_bias, w1_shared, w2_shared, cfg, ep)
     if echo_slots or transport in ("p2p", "p2p_overlap", "p2p_pull"):
         # ECHO hot-expert cloning runs on the p2p transport (virtual experts)
-        return _MoEEPP2PFunction.apply(*args, int(echo_slots), transport != "p2p_pull", tag,
-                                       transport == "p2p_overlap",
-                                       sync_free and not echo_slots, stash, int(layer_id),
-                                       bool(stash_overlap))
+        return _MoEEPP2PFunction, (*args, int(echo_slots), transport != "p2p_pull", tag,
+                                   transport == "p2p_overlap", sync_free and not echo_slots,
+                                   stash, int(layer_id), bool(stash_overlap))
     if cfg.precision != "bf16":
         raise ValueError(f"precision {cfg.precision!r} runs on the p2p / p2p_pull transports")
     if transport == "p2p_dedup":
-        return _MoEEPDedupFunction.apply(*args, tag)
+        return _MoEEPDedupFunction, (*args, tag)
     if transport == "nccl":
-        return _MoEEPFunction.apply(*args)
+        return _MoEEPFunction, args
     raise ValueError(f"unknown transport {transport!r}")

@@ -77,7 +77,8 @@ def run_case(cfg: MoEConfig, T, seed, dev, y_tol=Y_TOL, g_tol=G_TOL):
     # the decision at the logits boundary
     r = ops.router_forward(x.to(dev), w_r.to(dev), cfg.top_k, cfg.score, None, cfg.aux_loss_coeff)
     cap = cfg.capacity(T)
-    plan = ops.build_plan(r.topk_idx, r.topk_prob, cfg.num_experts, cap, cfg.pad_to_capacity)
+    plan = ops.build_plan(r.topk_idx, r.topk_prob, cfg.num_experts, cap, cfg.pad_to_capacity,
+                          align=ops.pick_align(T, cfg.top_k, cfg.num_experts))
     rmap_gpu, _ = ops.compact_row_id_map(plan)
     logits = f64(r.logits[:T, :cfg.num_experts])
     dec = R.route(logits, np.eye(cfg.num_experts), score=cfg.score, top_k=cfg.top_k)
@@ -155,6 +156,24 @@ def test_shared_expert_sigmoid(dev):
 
 def test_experts_128_top8(dev):
     run_case(MoEConfig(128, 8, 256, 256, aux_loss_coeff=1e-2), 1024, 6, dev)
+
+
+def test_baseline_tiny_config_T4096(dev):
+    """BASELINE.json configs[0] exactly: 8 experts top-2, hidden 256, ffn 512, 4096 tokens,
+    aux-loss router, against the fp64 numpy oracle."""
+    run_case(MoEConfig(8, 2, 256, 512, aux_loss_coeff=1e-2), 4096, 8, dev)
+
+
+def test_cta_pair_engine_multi_tile(dev):
+    """The 256-row CTA-pair plan (ops.pick_align) with more tiles than SM pairs (fc1: 8 n-tiles
+    x 32 units = 256 cluster tiles over 74 pairs), so every persistent CTA runs several tiles
+    (accumulator phase flips, raster bands), against the fp64 numpy oracle."""
+    T, E, K = 4096, 4, 2
+    assert ops.pick_align(T, K, E) == 256
+    run_case(MoEConfig(E, K, 512, 1024, aux_loss_coeff=1e-2), T, 9, dev)
+    run_case(MoEConfig(E, K, 512, 1024, aux_loss_coeff=1e-2, mem_efficient=True), T, 10, dev)
+    run_case(MoEConfig(E, K, 512, 1024, aux_loss_coeff=1e-2, capacity_factor=1.0,
+                       pad_to_capacity=True), T, 11, dev)
 
 
 def test_mxfp8_forward_experts(dev):
