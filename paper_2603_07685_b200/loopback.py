@@ -66,7 +66,8 @@ class LoopbackEPGroup:
 
     # every collective: drain this rank's stream, publish, meet, read, drain, meet
     def _sync(self):
-        torch.cuda.current_stream().synchronize()
+        if self.world.dev.type == "cuda":
+            torch.cuda.current_stream().synchronize()
 
     def _meet(self):
         self.world.barrier.wait()
@@ -147,6 +148,9 @@ def run_ranks(n: int, fn, dev=None):
 
     def body(r):
         try:
+            if dev.type != "cuda":  # host tensors (tests of the collectives themselves)
+                results[r] = fn(LoopbackEPGroup(world, r))
+                return
             torch.cuda.set_device(dev)
             s = torch.cuda.Stream(device=dev)
             with torch.cuda.stream(s):
