@@ -546,7 +546,8 @@ def run_gpu(args, c) -> None:
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
-            "dtype": "bf16" if args.precision == "bf16" else "mxfp8 fwd GEMMs, bf16 bwd",
+            "dtype": ("bf16" if args.precision == "bf16" else
+                      "mxfp8 (all six expert GEMMs: E4M3 with 1x32 E8M0 block scales)"),
             "data": "synthetic (seeded N(0,1) tokens, N(0,1/fan_in) random-init weights)",
             "config": {
                 "workload": f"{c['name']}: E={E}, top-{K}, h={h}, ffn={m}, {T} tokens/GPU, "
@@ -660,8 +661,9 @@ def main():
                     choices=["auto", "p2p", "p2p_overlap", "p2p_pull", "p2p_dedup", "nccl"],
                     help="EP exchange: fused NVLink peer-memory kernels (p2p) or NCCL a2a")
     ap.add_argument("--precision", default="bf16", choices=["bf16", "mxfp8"],
-                    help="forward expert GEMMs: bf16 (headline) or MXFP8 (block-scaled "
-                         "tcgen05; backward stays bf16)")
+                    help="expert GEMMs: bf16 (headline) or MXFP8 (block-scaled tcgen05 for "
+                         "all six: fc1/fc2 forward, both data gradients, both weight "
+                         "gradients)")
     ap.add_argument("--sync-free", action=argparse.BooleanOptionalAction, default=True,
                     help="EP: plan the exchange on the device (no host read of the counts; "
                          "worst-case static buffers). Default on: +2%% at EP=4 (measured)")

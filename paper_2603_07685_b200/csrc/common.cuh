@@ -9,6 +9,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "moe_b200.h"
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
@@ -41,6 +45,38 @@ enum Status : int {
     if (_e != cudaSuccess) return ::moe::kErrCuda;           \
   } while (0)
 
+// ---------------------------------------------------------------- per-device host state
+// Launch geometry and kernel attributes are per device (a process may drive several GPUs,
+// e.g. the loopback EP ranks or a multi-GPU host thread): cache them by device ordinal.
+inline int device_sms() {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  int d = 0;
+  cudaGetDevice(&d);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(d);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+  if (n <= 0) n = 148;
+  cache[d] = n;
+  return n;
+}
+// Raise a kernel's dynamic shared-memory limit on the current device (once per device).
+inline cudaError_t ensure_dyn_smem(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  int d = 0;
+  cudaGetDevice(&d);
+  std::lock_guard<std::mutex> g(mu);
+  int& cur = done[{kern, d}];
+  if (cur >= bytes) return cudaSuccess;
+  const cudaError_t e =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
+
 __host__ __device__ __forceinline__ int ceil_div_i(int a, int b) { return (a + b - 1) / b; }
 __host__ __device__ __forceinline__ long long ceil_div_ll(long long a, long long b) {
   return (a + b - 1) / b;
@@ -55,6 +91,16 @@ __device__ __forceinline__ float warp_sum(float v) {
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 __device__ __forceinline__ int warp_sum_i(int v) {

@@ -19,6 +19,10 @@
 //
 // Push kernels end with __threadfence_system(); cross-rank completion is established by a
 // stream-ordered NCCL collective between the push and the consumer (no spin-waits).
+// A negative destination row (base[e] + inv_c < 0) is skipped by every push and pull: the
+// device planner poisons base[] that way when the EP group is inconsistent (token counts
+// differ across ranks, or a plan exceeds the static buffers), so no rank ever stores past
+// a peer's allocation; the status word it sets makes check_ep_status() raise.
 #include "common.cuh"
 
 namespace moe {
@@ -77,6 +81,7 @@ __global__ void dispatch_push_kernel(const int4* __restrict__ x, int T, int K, i
         const int r = e / el;
         if (dest >= 0 && r != dest) continue;
         const long long row = (long long)__ldg(base + e) + d;
+        if (row < 0) continue;  // poisoned plan (moe_ep_plan_device: inconsistent EP group)
         if (!loaded) {
 #pragma unroll
           for (int u = 0; u < VPL; ++u) {
@@ -127,8 +132,8 @@ __global__ void combine_pull_kernel(const unsigned long long* __restrict__ peers
       w[k] = 0.f;
       if (k < K) {
         const int d = __ldg(inv_c + (long long)t * K + k);
-        if (d >= 0) {
-          const int e = __ldg(topk_idx + (long long)t * K + k);
+        const int e = d >= 0 ? __ldg(topk_idx + (long long)t * K + k) : 0;
+        if (d >= 0 && __ldg(base + e) + d >= 0) {  // (a poisoned plan pulls nothing)
           rows[k] = reinterpret_cast<const int4*>(peers[e / el]) +
                     ((long long)__ldg(base + e) + d) * hv;
           if (rows_copy) copy[k] = rows_copy + (long long)d * hv;
@@ -205,7 +210,7 @@ __global__ void combine_bwd_push_kernel(const int4* __restrict__ dy,
         const long long i = (long long)t * K + k;
         const int d = __ldg(inv_c + i);
         const int e = d >= 0 ? __ldg(topk_idx + i) : -1;
-        if (d >= 0 && (dest < 0 || e / el == dest)) {
+        if (d >= 0 && (dest < 0 || e / el == dest) && __ldg(base + e) + d >= 0) {
           any = true;
           const long long row = (long long)__ldg(base + e) + d;
           if (o_local) orow[k] = o_local + (long long)d * hv;
@@ -289,6 +294,7 @@ __global__ void __launch_bounds__(128) combine_bwd_push_sel_kernel(
       const int e = __ldg(topk_idx + i);
       if (e / el != dest) continue;
       const long long row = (long long)__ldg(base + e) + d;
+      if (row < 0) continue;
       int4* drow = reinterpret_cast<int4*>(d_peers[dest]) + row * hv;
       const int4* orow = o_local ? o_local + (long long)d * hv : nullptr;
       const float p = prob ? __ldg(prob + i) : 1.f;
@@ -340,8 +346,8 @@ __global__ void dprob_pull_kernel(const unsigned long long* __restrict__ part_pe
   if (i >= n) return;
   const int d = inv_c[i];
   float s = 0.f;
-  if (d >= 0) {
-    const int e = topk_idx[i];
+  const int e = d >= 0 ? topk_idx[i] : 0;
+  if (d >= 0 && (long long)base[e] + d >= 0) {
     const long long row = (long long)base[e] + d;
     const float* pr = reinterpret_cast<const float*>(part_peers[e / el]) + row * ldp;
     for (int j = 0; j < ldp; ++j) s += pr[j];
@@ -539,15 +545,7 @@ __global__ void echo_rewrite_kernel(const int* __restrict__ topk_idx,
   topk_v[i] = v;
 }
 
-static int sms() {
-  static int n = 0;
-  if (!n) {
-    int d = 0;
-    cudaGetDevice(&d);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
-  }
-  return n;
-}
+static int sms() { return device_sms(); }
 // Kernels that must run beside a persistent grouped GEMM (the overlapped dispatch) use the
 // GEMM's L1/shared split: an SM only hosts CTAs of kernels whose carve-out matches its
 // current configuration, so with the default (L1-preferring) carve-out a push CTA would wait

@@ -119,12 +119,30 @@ __global__ void ep_plan_kernel(const float* __restrict__ g, int ldg, int n, int 
     }
     block_expert[b] = lo;
   }
+  // Consistency of the group: every rank routed T*K selections (equal T per rank: the
+  // symmetric buffers and the capacity are sized from T), and no rank's plan exceeds the
+  // static rows. Otherwise poison base[] (pushes / pulls skip negative rows), run no GEMM
+  // block and flag the status, so nothing is written past a peer's allocation.
+  __shared__ int bad;
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int s = tid; s < n; s += nt) {
+    long long tot = 0, rows_s = 0;
+    for (int e = 0; e < E; ++e) tot += counts[s * E + e];
+    for (int j = 0; j < el; ++j) rows_s += padded[s * el + j];
+    if (tot != (long long)T * K || rows_s > rows_cap) atomicOr(&bad, 1);
+  }
+  __syncthreads();
+  if (bad) {
+    for (int e = tid; e < E; e += nt) base[e] = -(1 << 30);
+    // and an empty local plan: no regroup rows, no scatter rows, zero-row weight gradients
+    for (int i = tid; i < 2 * n * el + 2 * el + 1; i += nt) table[i] = 0;
+  }
   if (tid == 0) {
-    const bool over = rows_pad > rows_cap;
-    meta[0] = over ? 0 : nblocks;  // an overflowing plan runs no GEMM blocks
-    meta[1] = rows_pad;
+    meta[0] = bad ? 0 : nblocks;  // an inconsistent / overflowing plan runs no GEMM blocks
+    meta[1] = bad ? 0 : rows_pad;
     meta[2] = 0;
-    if (over && status) atomicExch(status, 1);
+    if (bad && status) atomicExch(status, 1);
   }
 }
 
@@ -142,12 +160,9 @@ extern "C" int moe_ep_plan_device(const float* gathered, int ldg, int n, int E, 
       ldg < 2 * E)
     return kErrInvalidArg;
   const int smem = (2 * n * E + E + E / n + 1) * static_cast<int>(sizeof(int));
-  static int smem_set = 0;
-  if (smem > 48 * 1024 && smem > smem_set) {
-    MOE_CUDA_CHECK(cudaFuncSetAttribute(epplan::ep_plan_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    smem_set = smem;
-  }
+  if (smem > 48 * 1024)
+    MOE_CUDA_CHECK(
+        ensure_dyn_smem(reinterpret_cast<const void*>(epplan::ep_plan_kernel), smem));
   epplan::ep_plan_kernel<<<1, 1024, smem, static_cast<cudaStream_t>(stream)>>>(
       gathered, ldg, n, E, me, T, K, capacity, pad, align, coeff, rows_cap, base, cap_local,
       table, block_expert, max_blocks, meta, dst_off, aux, aux_grad, status);

@@ -103,7 +103,8 @@ struct Params {
   // EP dispatch overlap (grouped-M): source rank s's rows of the A operand are pushed over
   // NVLink while this GEMM runs; s then stores `epoch` into src_flag[s]. A tile's A rows are
   // loaded only once every source in block_need[128-row block] has signalled; units run in
-  // unit_order (rows of early-arriving sources first). wait_status <- 1 on a 10 s timeout.
+  // unit_order (rows of early-arriving sources first). A 2 s timeout records wait_status
+  // and traps (wait_sources).
   const uint32_t* src_flag;
   const uint32_t* epoch;  // device scalar (bumped in stream order before the dispatch)
   const uint32_t* block_need;
@@ -125,7 +126,8 @@ __device__ __forceinline__ void st_out(int4* p, int4 v, int cs) {
 
 // Spin (bounded) until every source rank in `need` has published this epoch's rows. On a
 // timeout (2 s) the kernel records [1, block, missing sources, epoch, flags[0..3]] in
-// wait_status[0..7] and stops waiting (later waits of any CTA fail fast).
+// wait_status[0..7], makes it visible system-wide and traps: the launch fails with a CUDA
+// error instead of multiplying rows that never arrived (check_ep_status() decodes the record).
 __device__ __forceinline__ void wait_sources(const Params& p, uint32_t need, int blk,
                                              uint32_t epoch) {
   if (!need) return;
@@ -136,7 +138,6 @@ __device__ __forceinline__ void wait_sources(const Params& p, uint32_t need, int
       need &= need - 1;
       continue;
     }
-    if (p.wait_status && *reinterpret_cast<volatile int*>(p.wait_status)) break;
     if (globaltimer_ns() - t0 > 2000000000ull) {
       if (p.wait_status && atomicCAS(p.wait_status, 0, 1) == 0) {
         p.wait_status[1] = blk;
@@ -145,7 +146,8 @@ __device__ __forceinline__ void wait_sources(const Params& p, uint32_t need, int
         for (int i = 0; i < 4; ++i)
           p.wait_status[4 + i] = static_cast<int>(ld_acquire_sys_u32(p.src_flag + i));
       }
-      break;
+      __threadfence_system();
+      __trap();
     }
     __nanosleep(128);
   }
@@ -675,27 +677,14 @@ static int make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t o
   return r == CUDA_SUCCESS ? kOk : kErrCuda;
 }
 
-static int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+static int num_sms() { return device_sms(); }
 
 template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI, int CG>
 static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
                      int max_tiles, cudaStream_t stream) {
   auto kern = grouped_gemm_kernel<A_MN, B_MN, GROUPED_K, EPI, CG>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    MOE_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        smem_bytes<EPI, GROUPED_K, CG>()));
-    attr_set = true;
-  }
+  MOE_CUDA_CHECK(ensure_dyn_smem(reinterpret_cast<const void*>(kern),
+                                 smem_bytes<EPI, GROUPED_K, CG>()));
   if (max_tiles <= 0) return kOk;
   int grid = max_tiles * CG < num_sms() ? max_tiles * CG : num_sms();
   grid -= grid % CG;

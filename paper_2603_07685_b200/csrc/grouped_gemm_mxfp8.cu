@@ -685,15 +685,8 @@ static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtenso
                      cudaStream_t stream) {
   using C = Cfg<CG, WIDE>;
   auto kern = mxfp8_gemm_kernel<EPI, CG, WIDE, GK>;
-  static bool attr = false;
-  if (!attr) {
-    MOE_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        C::SMEM));
-    attr = true;
-  }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  MOE_CUDA_CHECK(ensure_dyn_smem(reinterpret_cast<const void*>(kern), C::SMEM));
+  const int sms = device_sms();
   const int tiles = GK ? p.num_experts_gk * (p.M / (BM * CG)) * (p.N / C::BN)
                      : (max_m_blocks / CG) * (p.N / C::BN);
   if (tiles <= 0) return kOk;

@@ -498,15 +498,7 @@ __global__ void dprob_from_partials_kernel(const int* __restrict__ inv_map, long
   dprob[i] = s;
 }
 
-static int sms() {
-  static int n = 0;
-  if (!n) {
-    int d = 0;
-    cudaGetDevice(&d);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
-  }
-  return n;
-}
+static int sms() { return device_sms(); }
 
 static int warp_grid(long long items, int warps_per_block = 8) {
   const long long blocks = ceil_div_ll(items > 0 ? items : 1, warps_per_block);

@@ -9,9 +9,15 @@
 //   aux_loss     :111-120 (coeff * E * sum_i f_i P_i, f = counts / (T*K))
 //   gradients    SURVEY Appendix C (score Jacobians; aux term with f constant).
 //
-// Selection without a bias is done on the fp32 LOGITS: softmax and sigma/sum-sigma are
-// strictly monotone per row, so the chosen set equals the oracle's (fp64 scores) choice
-// with ties going to the lower expert index; this is what makes the indices bit-exact.
+// Selection keys are the oracle's fp64 scores (routing.py:85-95): exp(l - max) for softmax
+// (the common 1/sum factor is monotone and dropped), sigma(l) = 1/(1+exp(-l)) for
+// sigma/sum-sigma, computed in double from the fp32 logits the oracle is given, plus the
+// selection bias when present. Distinct fp32 logits give distinct keys except where the fp64
+// scores themselves collide (sigmoid saturation to 1.0 from l ~ 34, exp underflow), and
+// there the oracle's stable argsort picks the lower expert index, as `better` does; this is
+// what makes the indices bit-exact. Non-finite keys (NaN / inf logits: status bit 0, route()
+// raises the reference's ValueError) are mapped to -inf so every token still selects K
+// valid experts and no index leaves [0, E).
 #include "common.cuh"
 
 namespace moe {
@@ -20,7 +26,7 @@ namespace router {
 constexpr int WARPS = 8;
 
 struct Cand {
-  float v;
+  double v;
   int i;
 };
 __device__ __forceinline__ bool better(const Cand& a, const Cand& b) {
@@ -85,17 +91,41 @@ __global__ void __launch_bounds__(WARPS * 32) topk_kernel(
 #pragma unroll
     for (int j = 0; j < EPL; ++j) part[j] += s[j];
 
-    // selection key (routing.py:95): logits when unbiased (monotone), scores + bias else
-    float key[EPL];
+    // selection key (routing.py:95-97): the fp64 score (up to the common positive factor
+    // 1/sum), + bias on the normalised score when a bias is given
+    double key[EPL];
+    double kmx = -INFINITY, ksum = 0.0;
+    if (score_fn == 0) {
+#pragma unroll
+      for (int j = 0; j < EPL; ++j) kmx = fmax(kmx, (double)l[j]);
+      kmx = warp_max_d(kmx);
+    }
 #pragma unroll
     for (int j = 0; j < EPL; ++j) {
       const int e = j * 32 + lane;
-      key[j] = sel_bias ? (e < E ? s[j] + __ldg(sel_bias + e) : -INFINITY) : l[j];
+      double k64 = -INFINITY;
+      if (e < E) {
+        const double ld = (double)l[j];
+        k64 = score_fn == 0 ? exp(ld - kmx) : 1.0 / (1.0 + exp(-ld));
+        ksum += k64;
+      }
+      key[j] = k64;
     }
+    if (sel_bias) {
+      ksum = warp_sum_d(ksum);
+#pragma unroll
+      for (int j = 0; j < EPL; ++j) {
+        const int e = j * 32 + lane;
+        if (e < E) key[j] = key[j] / ksum + (double)__ldg(sel_bias + e);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < EPL; ++j)
+      if (isnan(key[j])) key[j] = -INFINITY;
     unsigned taken = 0u;  // bit j: expert j*32+lane already selected
     int my_sel = -1;      // lane k keeps the k-th winner
     for (int k = 0; k < K; ++k) {
-      Cand c{-INFINITY, 0x7fffffff};
+      Cand c{-INFINITY, 0x7fffffff};  // loses to any real expert, even one keyed -inf
 #pragma unroll
       for (int j = 0; j < EPL; ++j) {
         const int e = j * 32 + lane;
@@ -109,6 +139,7 @@ __global__ void __launch_bounds__(WARPS * 32) topk_kernel(
         Cand o{__shfl_xor_sync(0xffffffffu, c.v, off), __shfl_xor_sync(0xffffffffu, c.i, off)};
         if (better(o, c)) c = o;
       }
+      if (c.i >= E) break;  // unreachable (K <= E leaves a candidate); keeps indices valid
       if ((c.i & 31) == lane) taken |= 1u << (c.i >> 5);
       if (lane == k) my_sel = c.i;
     }
@@ -127,7 +158,7 @@ __global__ void __launch_bounds__(WARPS * 32) topk_kernel(
       if (my_sel >= 0 && (my_sel >> 5) == j) sel_score = v;
       (void)e;
     }
-    if (lane < K) {
+    if (lane < K && my_sel >= 0 && my_sel < E) {
       topk_idx[(long long)t * K + rank] = my_sel;
       topk_prob[(long long)t * K + rank] = sel_score;
       atomicAdd(&s_counts[my_sel], 1);
@@ -253,15 +284,7 @@ __global__ void __launch_bounds__(WARPS * 32) bwd_kernel(
   }
 }
 
-static int sms() {
-  static int n = 0;
-  if (!n) {
-    int d = 0;
-    cudaGetDevice(&d);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
-  }
-  return n;
-}
+static int sms() { return device_sms(); }
 
 }  // namespace router
 }  // namespace moe

@@ -60,13 +60,24 @@ __global__ void release_kernel(int* state, int* ring, int num_pages, int* record
 __global__ void copy_kernel(uint8_t* dense, long long ld_bytes, uint8_t* pool, int page_rows,
                             long long row_bytes, const int* record, const int* rows_dev,
                             int rows_host, int max_rows, int to_pages) {
-  if (record[0] < 0) return;  // failed stash: nothing recorded
   int rows = rows_dev ? *rows_dev : rows_host;
   rows = rows < max_rows ? rows : max_rows;
   const int vpr = static_cast<int>(row_bytes / 16);
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  if (record[0] < 0) {
+    // failed stash (out of pages, planners.py:441-446 MemoryError): nothing was recorded.
+    // The reload poisons the destination rows with all-ones bytes (bf16 / fp32 NaN, int
+    // -1) so the backward cannot silently compute on another layer's activations; the
+    // sticky state[3] makes PagedStashBuffer.check() raise MemoryError.
+    if (!to_pages)
+      for (int r = warp; r < rows; r += nwarps) {
+        int4* d = reinterpret_cast<int4*>(dense + (long long)r * ld_bytes);
+        for (int c = lane; c < vpr; c += 32) d[c] = make_int4(-1, -1, -1, -1);
+      }
+    return;
+  }
   for (int r = warp; r < rows; r += nwarps) {
     const int page = __ldg(record + 1 + r / page_rows);
     int4* p = reinterpret_cast<int4*>(pool + ((long long)page * page_rows + r % page_rows) *
@@ -80,15 +91,7 @@ __global__ void copy_kernel(uint8_t* dense, long long ld_bytes, uint8_t* pool, i
   }
 }
 
-static int sms() {
-  static int n = 0;
-  if (!n) {
-    int d = 0;
-    cudaGetDevice(&d);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
-  }
-  return n;
-}
+static int sms() { return device_sms(); }
 
 }  // namespace stash
 }  // namespace moe

@@ -92,6 +92,15 @@ class EPHostPlan:
     eff: np.ndarray            # [el] real + phantom
 
 
+def check_uniform_tokens(counts_all: np.ndarray, t: int, K: int) -> None:
+    """Every rank must route the same T tokens (capacity, buffer sizes and the symmetric
+    pools are derived from the local T): each rank's pre-drop counts sum to T*K."""
+    tot = np.asarray(counts_all, dtype=np.int64).sum(axis=1)
+    if not np.all(tot == t * K):
+        raise ValueError(f"EP ranks must hold the same number of tokens: per-rank "
+                         f"selections {tot.tolist()}, expected {t * K} each")
+
+
 def _excl_cumsum(a, axis=-1):
     c = np.cumsum(a, axis=axis)
     return c - a
@@ -230,6 +239,7 @@ class _MoEEPFunction(torch.autograd.Function):
         ep.all_gather_into_tensor(gathered, stats)
         g = gathered.cpu().numpy()  # the one host sync of the EP forward
         counts_all = np.rint(g[:, :E]).astype(np.int64)
+        check_uniform_tokens(counts_all, t, K)
         cap = cfg.capacity(n * t)  # global capacity on the global batch
         align = ops.pick_align(n * t, K, E)
         hp = ep_host_plan(counts_all, ep.rank, cap, cfg.pad_to_capacity, align)
@@ -414,6 +424,34 @@ def ep_static_rows(n: int, t: int, K: int, E: int, capacity: int, align: int) ->
     return max(-(-rows // align) * align, 2 * ops.ALIGN)
 
 
+def sync_free_bytes(n: int, t: int, K: int, E: int, h: int, m: int, capacity: int = -1,
+                    mem_efficient: bool = False) -> dict:
+    """Per-rank HBM of one sync-free p2p layer (worst-case static buffers, the default
+    transport of bench.py at EP > 1), by buffer: the symmetric pools (allocated at 1.25x
+    their request, SymmPool.get), the fc1 / dSwiGLU outputs and the rank's expert weights and
+    their gradients. Activations of the caller (x, dY, dX) are included once each."""
+    align = ops.pick_align(n * t, K, E)
+    rows = ep_static_rows(n, t, K, E, capacity, align)
+    el = E // n
+    sym = lambda numel, w: int(numel * 1.25 + 4096) * w  # noqa: E731
+    b = {
+        "xp (symmetric)": sym(rows * h, 2),
+        "d_o (symmetric)": sym(rows * h, 2),
+        "orecv + dxrecv (symmetric)": 2 * sym(t * K * h, 2),
+        "preact": rows * 2 * m * 2,
+        "act": rows * m * 2,
+        "d_preact": rows * 2 * m * 2,
+        "row tables": rows * (2 * 8 + 4) + 4 * E * n,
+        "expert weights + grads": 2 * el * 3 * h * m * 2,
+        "x, dY, dX, y": 4 * t * h * 2,
+    }
+    if mem_efficient:
+        b["prob + dprob partials (symmetric)"] = sym(rows, 4) + sym(rows * (m // 256), 4)
+    b["total"] = sum(b.values())
+    b["rows_static"] = rows
+    return b
+
+
 def exchange_stats_from_device():
     """Fill last_exchange from the last sync-free forward's gathered counts (syncs)."""
     d = last_plan_inputs
@@ -430,7 +468,9 @@ def check_ep_status():
     for key, pool in _POOLS.items():
         st = pool.status.tolist()
         if st[7]:
-            raise _lib.MoEKernelError(f"EP plan exceeds the static buffers (pool {key})")
+            raise _lib.MoEKernelError(
+                f"EP plan inconsistent (pool {key}): token counts differ across ranks or a "
+                "plan exceeds the static buffers; no rows were exchanged")
         if st[0]:
             raise _lib.MoEKernelError(
                 f"EP dispatch wait timed out (pool {key}): block {st[1]}, missing sources "
@@ -621,6 +661,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         else:
             g = gathered.cpu().numpy()  # the one host sync of the EP forward
             counts_all = np.rint(g[:, :E]).astype(np.int64)
+            check_uniform_tokens(counts_all, t, K)
             # ECHO: route to virtual experts (expert segments on their serving ranks)
             counts_use = counts_all
             if echo_slots:
@@ -973,6 +1014,7 @@ class _MoEEPDedupFunction(torch.autograd.Function):
             ep.all_gather_into_tensor(gathered, stats)
             g = gathered.cpu().numpy()  # the one host sync of the forward
             counts_all = np.rint(g[:, :E]).astype(np.int64)
+            check_uniform_tokens(counts_all, t, K)
             ntok = np.rint(g[:, 2 * E:]).astype(np.int64)
         else:
             stats = torch.cat([r.counts.float(), r.mean_scores])
@@ -980,6 +1022,7 @@ class _MoEEPDedupFunction(torch.autograd.Function):
             ep.all_gather_into_tensor(gathered, stats)
             g = gathered.cpu().numpy()
             counts_all = np.rint(g[:, :E]).astype(np.int64)
+            check_uniform_tokens(counts_all, t, K)
         align = ops.pick_align(n * t, K, E)
         pair = align == 2 * ops.ALIGN
         base, rows_all, hp = p2p_tables(counts_all, me, cap, cfg.pad_to_capacity, align)
@@ -1164,6 +1207,10 @@ def moe_forward_ep(x, w_r, w1_local, w2_local, cfg: MoEConfig, ep: EPGroup,
       actual rows are copied into pages after its forward and back before its backward, so
       memory is O(worst case + sum of actual rows) instead of O(layers x worst case).
       layer_id: this layer's stash record key (unique among live layers).
+      Out of pages (the reference's MemoryError, planners.py:441-446): a stash that finds
+      too few free pages records nothing and its reload fills the layer's rows with NaN, so
+      the gradients come out NaN rather than silently wrong; PagedStashBuffer.check()
+      (a host sync) raises the MemoryError.
     stash_overlap: run the stash copies on a pack stream while the next layer computes and
       prefetch reloads on an unpack stream during the later layer's backward.
       Needs two alternating tags (layer i uses tag of parity i % 2: double-buffered tmp

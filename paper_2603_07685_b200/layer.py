@@ -40,6 +40,10 @@ class MoEConfig:
     # transposed-quantised along the dgrad K) and the weight-gradient GEMMs (activations and
     # gradients transposed-quantised along the token rows, the reference's column twin).
     precision: str = "bf16"
+    # raise the reference's ValueError("router logits are not finite") (routing.py:80-81) when
+    # a token's router logits are NaN / inf. Costs one host sync per forward, so it is off by
+    # default; the kernels stay memory-safe either way (non-finite keys select valid experts)
+    check_finite: bool = False
 
     def capacity(self, num_tokens: int) -> int:
         """expert_capacity() routing.py:250-251 (k = top_k since every token selects K)."""
@@ -56,6 +60,8 @@ class _MoEFunction(torch.autograd.Function):
         w_r_t, w_r_pad = ops.stage_router_weight(w_r)
         r = ops.router_forward(x, w_r, cfg.top_k, cfg.score, sel_bias, cfg.aux_loss_coeff,
                                w_r_t=w_r_t)
+        if cfg.check_finite and int(r.status.item()) & 1:
+            raise ValueError("router logits are not finite")
         cap = cfg.capacity(t)
         plan = ops.build_plan(r.topk_idx, r.topk_prob, e, cap, cfg.pad_to_capacity,
                               align=ops.pick_align(t, cfg.top_k, e))

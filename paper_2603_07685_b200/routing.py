@@ -241,8 +241,10 @@ def apply_capacity(decision: RoutingDecision, capacity_factor: float, pad: bool 
     plan = ops.build_plan(idx, prob, e, cap, pad)
     dropped_sel = (plan.inv_map < 0) & (idx >= 0)
     dropped = torch.zeros((t, e), dtype=torch.bool, device=rm.device)
-    if t:
-        dropped.scatter_(1, idx.long().clamp(min=0), dropped_sel)
+    valid = idx >= 0  # ragged decisions pad idx with -1: scatter only real selections
+    if t and bool(valid.any()):
+        rows = torch.arange(t, device=rm.device).unsqueeze(1).expand_as(idx)
+        dropped[rows[valid], idx[valid].long()] = dropped_sel[valid]
     phantom = None
     if pad:
         phantom = (cap - torch.clamp(rm.sum(0), max=cap)).to(torch.int64)

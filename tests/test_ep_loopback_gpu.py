@@ -128,3 +128,48 @@ def test_loopback_paged_stash_two_layers(dev):
 
     res = run_ranks(N, body, dev)
     assert all(r == "ok" for r in res), res
+
+
+@pytest.mark.parametrize("sync_free", [False, True])
+def test_loopback_ep_unequal_tokens_rejected(sync_free, dev):
+    """Ranks with different token counts: the host-planned transports raise on
+    every rank before any exchange; the sync-free device planner poisons the plan (no
+    push, pull or scatter touches a peer's buffers) and check_ep_status() raises."""
+    from paper_2603_07685_b200 import _lib
+    from paper_2603_07685_b200.dispatcher import check_ep_status
+    from paper_2603_07685_b200.layer import MoEConfig
+    from paper_2603_07685_b200.loopback import forward_backward, run_ranks
+
+    E, K, h, m = 8, 2, 256, 256
+    cfg = MoEConfig(E, K, h, m, aux_loss_coeff=1e-2)
+
+    def body(ep):
+        T = 256 if ep.rank == 0 else 192
+        g = torch.Generator(device=dev).manual_seed(ep.rank)
+        bf = torch.bfloat16
+        el = E // ep.n
+        x = torch.randn((T, h), device=dev, generator=g).to(bf)
+        w_r = (torch.randn((h, E), device=dev, generator=g) / 16).to(bf)
+        w1 = (torch.randn((el, 2 * m, h), device=dev, generator=g) / 16).to(bf)
+        w2 = (torch.randn((el, h, m), device=dev, generator=g) / 16).to(bf)
+        forward_backward(x, w_r, w1, w2, cfg, ep, torch.ones_like(x), transport="p2p",
+                         sync_free=sync_free, tag=f"unequal{int(sync_free)}")
+        torch.cuda.current_stream().synchronize()
+        try:
+            check_ep_status()
+        except _lib.MoEKernelError as exc:
+            return str(exc)
+        return "no error"
+
+    from paper_2603_07685_b200 import dispatcher as D
+
+    try:
+        if sync_free:
+            res = run_ranks(2, body, dev)
+            assert all("inconsistent" in r for r in res), res
+        else:
+            with pytest.raises(RuntimeError, match="same number of tokens"):
+                run_ranks(2, body, dev)
+    finally:  # drop the poisoned pools: later check_ep_status() calls look at every pool
+        for key in [k for k in D._POOLS if str(k[2]).startswith("unequal")]:
+            del D._POOLS[key]

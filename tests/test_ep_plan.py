@@ -196,3 +196,25 @@ def test_mx_interleave_layouts():
         v = w.reshape(E, m // blk, 2, blk, h)
         assert torch.equal(v[:, :, 0].reshape(E, m, h), gate)
         assert torch.equal(v[:, :, 1].reshape(E, m, h), up)
+
+
+def test_sync_free_worst_case_buffers_fit_hbm_at_ep8():
+    """The sync-free transport sizes its buffers for the worst case (every selection of the
+    group on one rank: n*T*K rows). At EP=2/4/8 for every BASELINE.json config the per-rank
+    total must fit the 180 GB of one B200 with margin (<= 75%)."""
+    from paper_2603_07685_b200.dispatcher import sync_free_bytes
+
+    configs = {  # BASELINE.json configs[1..4] (T per GPU; DeepSeek T per SURVEY §8 table)
+        "mixtral": dict(E=8, K=2, h=4096, m=14336, T=16384, cap=-1),
+        "qwen3": dict(E=128, K=8, h=4096, m=1536, T=32768, cap=-1),
+        "deepseek": dict(E=256, K=8, h=7168, m=2048, T=4096, cap=-1),
+        "capacity": dict(E=8, K=2, h=4096, m=14336, T=16384, cap=1),
+    }
+    hbm = 180e9
+    for name, c in configs.items():
+        for n in (2, 4, 8):
+            if c["E"] % n:
+                continue
+            cap = -(-(n * c["T"] * c["K"]) // c["E"]) if c["cap"] > 0 else -1
+            b = sync_free_bytes(n, c["T"], c["K"], c["E"], c["h"], c["m"], cap)
+            assert b["total"] <= 0.75 * hbm, (name, n, {k: v / 1e9 for k, v in b.items()})

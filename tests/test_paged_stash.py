@@ -111,3 +111,26 @@ def test_device_stash_reload_identity_device_rows():
         assert torch.equal(a[:rows], a0[:rows]) and torch.equal(b[:rows], b0[:rows])
         assert not a[rows:].any()
     assert buf.stats()["free_pages"] == 64
+
+
+@pytest.mark.gpu
+def test_device_stash_out_of_pages_poisons_reload():
+    """A stash that runs out of pages (the reference's MemoryError) records nothing; its
+    reload fills the destination rows with NaN instead of leaving stale activations, and
+    check() raises MemoryError."""
+    from paper_2603_07685_b200.stash import PagedStashBuffer
+
+    dev = torch.device("cuda", 0)
+    buf = PagedStashBuffer(4, {"a": 256 * 2}, page_rows=64, device=dev)
+    a0 = torch.randn((512, 256), device=dev).to(torch.bfloat16)
+    buf.stash(0, {"a": a0}, rows=200)          # 4 pages: fits exactly
+    buf.stash(1, {"a": a0}, rows=10)           # no page left: fails
+    with pytest.raises(MemoryError, match="out of pages"):
+        buf.check()
+    a = torch.zeros_like(a0)
+    buf.reload(1, {"a": a}, rows=10)
+    assert torch.isnan(a[:10].float()).all() and not a[10:].any()
+    b = torch.zeros_like(a0)
+    buf.reload(0, {"a": b}, rows=200)
+    assert torch.equal(b[:200], a0[:200])
+    assert buf.stats()["free_pages"] == 4

@@ -260,3 +260,65 @@ def test_torch_in_torch_out():
     assert isinstance(d.routing_map, torch.Tensor) and d.routing_map.is_cuda
     rows, rmap = G.permute(x, d)
     assert rows.is_cuda and rmap.dtype == torch.int64
+
+
+# -- edge cases of the top-k kernel (non-finite keys, fp64 score ties) ---------
+
+def test_nonfinite_rows_raise_and_select_valid_experts():
+    """A NaN hidden row (and an inf one with a selection bias) makes route() raise the
+    reference's ValueError; the kernel itself still writes K valid, distinct experts per
+    token and leaves the counts consistent (no out-of-range index, no stray writes)."""
+    from paper_2603_07685_b200 import ops
+
+    E, K = 8, 2
+    logits = np.random.default_rng(3).normal(size=(64, E))
+    logits[5] = np.nan
+    with pytest.raises(ValueError, match="finite"):
+        from_logits(logits, k=K)
+    bias = np.linspace(0, 0.1, E)
+    inf_row = np.random.default_rng(4).normal(size=(16, E))
+    inf_row[3, 2] = np.inf
+    with pytest.raises(ValueError, match="finite"):
+        G.route(inf_row, np.eye(E), score="sigmoid", top_k=K, selection_bias=bias)
+    # kernel level: every row keeps K distinct in-range experts, counts sum to T*K
+    x = torch.as_tensor(logits, dtype=torch.float32).to(torch.bfloat16).cuda()
+    x = torch.nn.functional.pad(x, (0, 64 - E))
+    w = torch.eye(64, E, dtype=torch.bfloat16, device="cuda")
+    for bias_t in (None, torch.as_tensor(bias, dtype=torch.float32, device="cuda")):
+        r = ops.router_forward(x, w, K, "softmax", bias_t)
+        idx = r.topk_idx.cpu().numpy()
+        assert idx.min() >= 0 and idx.max() < E
+        assert np.all(np.diff(idx, axis=1) > 0)
+        assert int(r.counts.sum()) == 64 * K
+        assert int(r.status.item()) & 1
+    # the device is still healthy
+    d = from_logits([[2.0, 1.0, 0.0, -1.0]], k=2)
+    assert set(np.nonzero(d.routing_map[0])[0]) == {0, 1}
+
+
+@pytest.mark.parametrize("score,row", [
+    # fp64 sigmoid saturates to exactly 1.0 from l = 36.7368: experts 1..3 tie, the oracle's
+    # stable argsort takes the lowest indices (fp32-logit order would take 2 and 3)
+    ("sigmoid", [0.0, 36.75, 40.0, 38.0, -1.0]),
+    # fp64 exp underflows to 0 below max - 745.13: experts 1..3 tie at probability 0
+    ("softmax", [0.0, -1000.0, -800.0, -896.0, -2000.0]),
+])
+def test_selection_ties_of_saturated_fp64_scores(score, row):
+    logits = np.asarray([row], dtype=np.float64)
+    d = from_logits(logits, k=2, score=score)
+    ref = R.route(logits, np.eye(logits.shape[1]), score=score, top_k=2)
+    assert np.array_equal(d.routing_map, ref.routing_map), (d.routing_map, ref.routing_map)
+    assert list(np.nonzero(d.routing_map[0])[0]) == ([0, 1] if score == "softmax" else [1, 2])
+
+
+def test_layer_check_finite_raises():
+    from paper_2603_07685_b200.layer import MoEConfig, moe_forward
+
+    cfg = MoEConfig(8, 2, 256, 256, check_finite=True)
+    x = torch.randn((128, 256), device="cuda").to(torch.bfloat16)
+    x[7, 3] = float("nan")
+    w_r = (torch.randn((256, 8), device="cuda") / 16).to(torch.bfloat16)
+    w1 = (torch.randn((8, 512, 256), device="cuda") / 16).to(torch.bfloat16)
+    w2 = (torch.randn((8, 256, 256), device="cuda") / 16).to(torch.bfloat16)
+    with pytest.raises(ValueError, match="finite"):
+        moe_forward(x, w_r, w1, w2, cfg)
