@@ -421,12 +421,17 @@ def run_gpu(args, c) -> None:
     # ---- e2e: host buffers through the public API ----------------------------------
     # Each step's x and dY come from pinned host memory (H2D on a copy stream, double
     # buffered so step i+1's copy overlaps step i's compute, like a data-loader prefetch);
-    # the step's aux loss is read back to the host. All copies are inside the timed region.
+    # the step's results go back to pinned host memory: the output y (the activation the
+    # layer hands on) and the aux loss, D2H on a second copy stream that overlaps the next
+    # step. All copies are inside the timed region; the region ends when the last y is on
+    # the host.
     x_host = x.cpu().pin_memory()
     dy_host = dy.cpu().pin_memory()
     loss_host = torch.empty((max(args.steps, 2),), dtype=torch.float32).pin_memory()
+    y_host = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for _ in range(2)]
     bufs = [(torch.empty_like(x), torch.empty_like(dy)) for _ in range(2)]
     copy_stream = torch.cuda.Stream(device=dev)
+    d2h_stream = torch.cuda.Stream(device=dev)
     landed = [torch.cuda.Event() for _ in range(2)]
     released = [torch.cuda.Event() for _ in range(2)]
     main = torch.cuda.current_stream()
@@ -447,9 +452,19 @@ def run_gpu(args, c) -> None:
             if i + 1 < steps:
                 h2d(1 - slot)
             main.wait_event(landed[slot])
-            _, aux = run(*bufs[slot])
+            if args.graph:  # the replay overwrites the graph's static y: previous D2H first
+                main.wait_stream(d2h_stream)
+            y, aux = run(*bufs[slot])
             released[slot].record(main)
-            loss_host[i].copy_(aux.detach(), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(main)
+            with torch.cuda.stream(d2h_stream):
+                d2h_stream.wait_event(ev)
+                yd = y.detach()
+                yd.record_stream(d2h_stream)
+                y_host[slot].copy_(yd, non_blocking=True)
+                loss_host[i].copy_(aux.detach(), non_blocking=True)
+        main.wait_stream(d2h_stream)
 
     e2e_run(2)
     barrier()
@@ -463,6 +478,45 @@ def run_gpu(args, c) -> None:
     if n > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
+
+    # ---- drop-in function API (the reference's moelab.routing surface): numpy in, numpy
+    # out, forward only (the reference API has no backward). route() + combine_standard() on
+    # this step's x with the same expert weights, host<->device copies included.
+    dropin = None
+    if n == 1 and not args.no_dropin and c.get("shared", 0) == 0:
+        import numpy as np
+
+        from paper_2603_07685_b200 import routing as G
+
+        gate_w, up_w = gemm.split_gate_up(w1.detach())
+        params_np = G.ExpertParams(w1=list(up_w.float().cpu().numpy()),
+                                   w2=list(w2.detach().float().cpu().numpy()),
+                                   gate=list(gate_w.float().cpu().numpy()))
+        x_np = x.float().cpu().numpy()
+        w_r_np = w_r.detach().float().cpu().numpy()
+
+        def dropin_call():
+            dec = G.route(x_np, w_r_np, score=c["score"], top_k=K)
+            if cfg.capacity_factor is not None:
+                dec = G.apply_capacity(dec, cfg.capacity_factor, pad=cfg.pad_to_capacity)
+                return G.moe_output_with_residual(x_np, dec, params_np)
+            return G.combine_standard(x_np, dec, params_np)
+
+        dropin_call()  # warm-up: uploads and stacks the expert weights once (then cached)
+        times = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            y_np = dropin_call()
+            times.append(time.perf_counter() - t0)
+        assert isinstance(y_np, np.ndarray) and y_np.shape == (T, h)
+        dsec = statistics.median(times)
+        dropin = {"value": round(T / dsec, 1), "unit": "tokens/s", "ms_per_call": round(dsec * 1e3, 2),
+                  "api": "paper_2603_07685_b200.routing.route + combine_standard (numpy fp32 "
+                         "in, float64 out; forward only, as the reference API); host wall clock "
+                         "with the host<->device copies, median of 3 after a warm-up call",
+                  "h2d_bytes_per_call": int(x_np.nbytes), "d2h_bytes_per_call": int(T * h * 8)}
+        del params_np, x_np
 
     # ---- routing statistics of this workload (global counts; config 5 drop fraction) ----
     from paper_2603_07685_b200 import ops
@@ -584,7 +638,9 @@ def run_gpu(args, c) -> None:
                 "unit": "tokens/s",
                 "ms_per_step": round(e2e_ms, 4),
                 "h2d_bytes_per_step": int(x.numel() * 2 + dy.numel() * 2),
-                "d2h_bytes_per_step": 4,
+                "d2h_bytes_per_step": int(x.numel() * 2 + 4),
+                "copies": "x, dY pinned H2D (copy stream, prefetched one step ahead); y and "
+                          "the aux loss D2H to pinned host (second copy stream)",
             },
             "gpu_launches": launches,
             "gpu_launches_per_step": launches / args.steps,
@@ -597,6 +653,7 @@ def run_gpu(args, c) -> None:
                 "paper_2603_07685_b200.dispatcher", fromlist=["x"]).last_echo)
                 if args.echo_slots and n > 1 else None),
             "nvlink": nvlink_stats,
+            "dropin": dropin,
         }
         if n == 1 and not args.no_cpu_baseline:
             thr = cpu_threads()
@@ -657,6 +714,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-tokens", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dropin", action="store_true",
+                    help="skip timing the numpy-in/numpy-out drop-in function API")
     ap.add_argument("--ep-transport", default="auto",
                     choices=["auto", "p2p", "p2p_overlap", "p2p_pull", "p2p_dedup", "nccl"],
                     help="EP exchange: fused NVLink peer-memory kernels (p2p) or NCCL a2a")

@@ -234,6 +234,9 @@ int moe_gg_fc2_dgrad_ep(const void* dout, const void* w2, const void* preact, in
                         float* dprob_partial, int flags, const unsigned int* src_flag,
                         const unsigned int* epoch, const unsigned int* block_need,
                         const int* unit_order, int* status, void* stream);
+/* Columns of the per-row dprob partials moe_gg_fc2_dgrad writes for ffn width m (workspace
+ * query: one partial per (256-column tile, epilogue column half)). */
+int moe_gg_dprob_partials(int m);
 int moe_gg_fc2_dgrad(const void* dout, const void* w2, const void* preact, int a_rows,
                      int max_rows, int h, int m, int num_experts, const int* block_expert,
                      const int* num_m_blocks, const float* row_prob, void* d_preact,

@@ -98,6 +98,7 @@ SIGNATURES: dict[str, list] = {
 QUERIES: dict[str, tuple] = {
     "moe_router_num_partials": ([I], c_int),
     "moe_permute_workspace_ints": ([I, I, I], c_int64),
+    "moe_gg_dprob_partials": ([I], c_int),
 }
 
 _lib = None

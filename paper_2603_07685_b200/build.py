@@ -50,6 +50,11 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in _sources() + _headers())
 
 
+def _extra_flags() -> list[str]:
+    """MOE_NVCC_EXTRA: extra nvcc flags for A/B builds (e.g. -DMOE_DSWIGLU_WARPS=4)."""
+    return os.environ.get("MOE_NVCC_EXTRA", "").split()
+
+
 def build_lib(force: bool = False, verbose: bool = False) -> Path:
     if not force and not needs_build():
         return LIB
@@ -59,7 +64,7 @@ def build_lib(force: bool = False, verbose: bool = False) -> Path:
 
     def compile_one(src: Path) -> Path:
         obj = OBJ_DIR / (src.stem + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        cmd = [nvcc, *NVCC_FLAGS, *_extra_flags(), "-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src.name}:\n{r.stderr}")

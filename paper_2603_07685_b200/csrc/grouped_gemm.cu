@@ -41,12 +41,25 @@ constexpr int TMEM_COLS = 512;  // 2 accumulator stages x 256 fp32 columns
 // tile's columns). Measured on B200: 8 warps did not speed up the dSwiGLU epilogue and cost
 // ~13% on fc1+SwiGLU (the extra warps share the MMA issuer's SMSP), so 4 it is.
 constexpr int EPI_WARPS = 4;
-constexpr int EPI_HALVES = EPI_WARPS / 4;
+enum Epi : int { EPI_BF16 = 0, EPI_SWIGLU = 1, EPI_DSWIGLU = 2, EPI_F32 = 3 };
+// The dSwiGLU epilogue (fc2 dgrad) reads the saved pre-activation and writes d_preact, 4
+// bytes in and out per accumulator element plus the SwiGLU-backward math. In round 1 it
+// kept the MMA issuer waiting on the accumulator release (ncu: 4.7M tempty spins per launch,
+// tensor pipe 73%, 42 warp-instructions per element from the IEEE division;
+// profiles/r02_ncu_gemm_mixtral_before.txt). With the fast-math sigmoid (dswiglu8) 4 warps
+// (one per TMEM lane quarter) measured faster than 8 on B200: Mixtral fc2 dgrad 3.07 ms
+// (1252 TFLOP/s) vs 3.61 ms, Qwen3 2.95 vs 3.20 ms. -DMOE_DSWIGLU_WARPS=8 rebuilds the other.
+#ifndef MOE_DSWIGLU_WARPS
+#define MOE_DSWIGLU_WARPS 4
+#endif
+constexpr int DSW_HALVES = MOE_DSWIGLU_WARPS / 4;  // dprob partials per (row, n-tile)
 // Weight-gradient (grouped-K) kernels use 8 epilogue warps: with few token rows per expert
 // (DeepSeek-shape EP=1: 128) each output tile has almost no MMA work and the kernel is a
 // TMEM -> HBM drain, which 4 warps cannot keep busy.
-template <bool GROUPED_K>
-constexpr int epi_warps() { return GROUPED_K ? 8 : EPI_WARPS; }
+template <bool GROUPED_K, int EPI>
+constexpr int epi_warps() {
+  return GROUPED_K ? 8 : (EPI == EPI_DSWIGLU ? MOE_DSWIGLU_WARPS : EPI_WARPS);
+}
 constexpr int BAND_M = 16;  // raster: 16 M units share each swept n-block (L2 reuse)
 
 template <int CG>
@@ -72,7 +85,6 @@ constexpr int smem_bytes() {
   return Cfg<CG>::SMEM + (EPI == 0 ? SCATTER_BYTES : 0);
 }
 
-enum Epi : int { EPI_BF16 = 0, EPI_SWIGLU = 1, EPI_DSWIGLU = 2, EPI_F32 = 3 };
 
 struct Params {
   // grouped-M
@@ -194,7 +206,43 @@ __device__ __forceinline__ void decode_tile(const Params& p, int t, int num_unit
   }
 }
 
-__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+// Fast-math SwiGLU pieces for the epilogues: MUFU ex2 + MUFU rcp (rcp.approx.ftz, <= 1 ulp)
+// instead of the IEEE division, whose refinement and slow-path checks made the dSwiGLU
+// epilogue ~3x longer than the math needs. Saturates correctly: g -> -inf gives
+// exp -> inf, rcp -> 0; g -> +inf gives exp -> 0, rcp -> 1. The outputs are bf16.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float sigmoid_f(float g) { return rcp_approx(1.0f + __expf(-g)); }
+__device__ __forceinline__ float silu_f(float g) { return g * sigmoid_f(g); }
+
+// dSwiGLU of 8 accumulator columns: a = dL/d(act) (fp32), g / u = the saved gate / up
+// pre-activations (bf16 x8 each). Writes d_gate = a*scale*u*s*(1 + g*(1-s)) and
+// d_up = a*scale*silu(g) (bf16 x8 each); DP: also accumulates <a, silu(g)*u> (the dprob
+// partial of the memory-efficient combine).
+template <bool DP>
+__device__ __forceinline__ void dswiglu8(const uint32_t* a, int4 gv, int4 uv, float scale,
+                                         int4& dg_out, int4& du_out, float& dp) {
+  const uint32_t* sg = reinterpret_cast<const uint32_t*>(&gv);
+  const uint32_t* su = reinterpret_cast<const uint32_t*>(&uv);
+  uint32_t* pg = reinterpret_cast<uint32_t*>(&dg_out);
+  uint32_t* pu = reinterpret_cast<uint32_t*>(&du_out);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 gg = unpack_bf16x2(sg[j]);
+    const float2 uu = unpack_bf16x2(su[j]);
+    const float a0 = __uint_as_float(a[2 * j]), a1 = __uint_as_float(a[2 * j + 1]);
+    const float s0 = sigmoid_f(gg.x), s1 = sigmoid_f(gg.y);
+    const float si0 = gg.x * s0, si1 = gg.y * s1;
+    if constexpr (DP) dp = fmaf(a0 * si0, uu.x, fmaf(a1 * si1, uu.y, dp));
+    const float da0 = a0 * scale, da1 = a1 * scale;
+    const float t0 = fmaf(gg.x, 1.0f - s0, 1.0f), t1 = fmaf(gg.y, 1.0f - s1, 1.0f);
+    pg[j] = pack_bf16x2((da0 * uu.x) * (s0 * t0), (da1 * uu.y) * (s1 * t1));
+    pu[j] = pack_bf16x2(da0 * si0, da1 * si1);
+  }
+}
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -242,7 +290,7 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
 }
 
 template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI, int CG>
-__global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K>(), 1)
+__global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                         const __grid_constant__ CUtensorMap tmap_b, const Params p) {
   using C = Cfg<CG>;
@@ -271,7 +319,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K>(), 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], epi_warps<GROUPED_K>() * CG);
+      mbar_init(&tempty_bar[s], epi_warps<GROUPED_K, EPI>() * CG);
     }
     fence_mbar_init();
     fence_async_shared();
@@ -411,7 +459,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K>(), 1)
     const int half = (warp - 2) / 4;
     constexpr int SC = scatter_cols<GROUPED_K>();
     uint8_t* stage = smem + C::STAGES * C::STAGE + 256 + (warp - 2) * (32 * SC * 2);
-    constexpr int EC = BN / (epi_warps<GROUPED_K>() / 4);  // tile columns per epilogue warp
+    constexpr int EC = BN / (epi_warps<GROUPED_K, EPI>() / 4);  // tile columns per epilogue warp
     const int cb = half * EC;  // this warp's first tile column
     const int row_local = q * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
@@ -575,35 +623,26 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K>(), 1)
             }
           }
           tmem_ld_wait();
+          if (p.row_partial) {
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            int4 wg, wu;
-            uint32_t* pg = reinterpret_cast<uint32_t*>(&wg);
-            uint32_t* pu = reinterpret_cast<uint32_t*>(&wu);
-            const uint32_t* sg = reinterpret_cast<const uint32_t*>(&gv[v]);
-            const uint32_t* su = reinterpret_cast<const uint32_t*>(&uv[v]);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float2 gg = unpack_bf16x2(sg[j]);
-              const float2 uu = unpack_bf16x2(su[j]);
-              const int i = 8 * v + 2 * j;
-              const float a0 = __uint_as_float(r[i]), a1 = __uint_as_float(r[i + 1]);
-              const float s0 = 1.0f / (1.0f + __expf(-gg.x));
-              const float s1 = 1.0f / (1.0f + __expf(-gg.y));
-              const float si0 = gg.x * s0, si1 = gg.y * s1;
-              dp_acc += a0 * si0 * uu.x + a1 * si1 * uu.y;
-              const float da0 = a0 * scale, da1 = a1 * scale;
-              const float dg0 = da0 * uu.x * s0 * (1.0f + gg.x * (1.0f - s0));
-              const float dg1 = da1 * uu.y * s1 * (1.0f + gg.y * (1.0f - s1));
-              pg[j] = pack_bf16x2(dg0, dg1);
-              pu[j] = pack_bf16x2(da0 * si0, da1 * si1);
+            for (int v = 0; v < 4; ++v) {
+              int4 wg, wu;
+              dswiglu8<true>(r + 8 * v, gv[v], uv[v], scale, wg, wu, dp_acc);
+              st_out(reinterpret_cast<int4*>(dpre_row + pos) + v, wg, p.stream_stores);
+              st_out(reinterpret_cast<int4*>(dpre_row + pos + 128) + v, wu, p.stream_stores);
             }
-            st_out(reinterpret_cast<int4*>(dpre_row + pos) + v, wg, p.stream_stores);
-            st_out(reinterpret_cast<int4*>(dpre_row + pos + 128) + v, wu, p.stream_stores);
+          } else {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              int4 wg, wu;
+              dswiglu8<false>(r + 8 * v, gv[v], uv[v], scale, wg, wu, dp_acc);
+              st_out(reinterpret_cast<int4*>(dpre_row + pos) + v, wg, p.stream_stores);
+              st_out(reinterpret_cast<int4*>(dpre_row + pos + 128) + v, wu, p.stream_stores);
+            }
           }
         }
         if (p.row_partial)
-          p.row_partial[row * p.ld_partial + (tl.n0 / BN) * EPI_HALVES + half] = dp_acc;
+          p.row_partial[row * p.ld_partial + (tl.n0 / BN) * DSW_HALVES + half] = dp_acc;
       }
       tc_fence_before();
       __syncwarp();
@@ -690,7 +729,7 @@ static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params&
   grid -= grid % CG;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(64 + 32 * epi_warps<GROUPED_K>());
+  cfg.blockDim = dim3(64 + 32 * epi_warps<GROUPED_K, EPI>());
   cfg.dynamicSmemBytes = smem_bytes<EPI, GROUPED_K, CG>();
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -898,11 +937,13 @@ static int fc2_dgrad_impl(const void* dout, const void* w2, const void* preact, 
   p.ld_aux = 2 * m;
   p.row_scale = row_prob;
   p.row_partial = dprob_partial;
-  p.ld_partial = (m / BN) * EPI_HALVES;  // one partial per (n-tile, epilogue half)
+  p.ld_partial = (m / BN) * DSW_HALVES;  // one partial per (n-tile, epilogue half)
   return run<false, true, false, EPI_DSWIGLU>(dout, h, a_rows, w2, m, (uint64_t)num_experts * h,
                                               p, p.max_m_blocks, pair,
                                               static_cast<cudaStream_t>(stream));
 }
+
+int moe_gg_dprob_partials(int m) { return (m / BN) * DSW_HALVES; }
 
 int moe_gg_fc2_dgrad(const void* dout, const void* w2, const void* preact, int a_rows,
                      int max_rows, int h, int m, int num_experts, const int* block_expert,

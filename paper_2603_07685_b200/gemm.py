@@ -13,12 +13,12 @@ from . import _lib
 
 BLOCK_M = 128
 GATE_UP_BLOCK = 128  # gate/up rows interleave granularity inside the stacked W1
-EPI_HALVES = 1       # epilogue warps per TMEM lane quarter (csrc/grouped_gemm.cu EPI_WARPS/4)
 
 
 def dprob_partials(m: int) -> int:
-    """Per-row dprob partials the fc2-dgrad epilogue writes: one per (256-col tile, half)."""
-    return (m // 256) * EPI_HALVES
+    """Per-row dprob partials the fc2-dgrad epilogue writes: one per (256-col tile, epilogue
+    column half), as the library was built (moe_gg_dprob_partials)."""
+    return int(_lib.query("moe_gg_dprob_partials", m))
 
 
 def _ptr(t):

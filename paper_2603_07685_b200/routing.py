@@ -345,6 +345,52 @@ class _Stacked:
         return xp
 
 
+# Stacked device weights per ExpertParams object: the function API is stateless like the
+# reference's, but re-uploading and re-stacking every expert on every combine call would make
+# the weight copy dominate. An entry is reused only for the same params object whose arrays
+# are unchanged (same objects and buffers; torch tensors by their in-place version counter,
+# numpy arrays by a 1024-element strided sample); clear_weight_cache() drops everything.
+_STACK_CACHE: list = []  # [(weakref(params), h_in, fingerprint, _Stacked)], most recent last
+_STACK_CACHE_SIZE = 2
+
+
+def _fingerprint(params: ExpertParams):
+    fp = []
+    for lst in (params.w1, params.w2, params.gate or ()):
+        for w in lst:
+            if isinstance(w, torch.Tensor):
+                fp.append((id(w), w.data_ptr(), tuple(w.shape), w._version))
+            else:
+                a = np.asarray(w)
+                flat = a.reshape(-1)
+                step = max(flat.size // 1024, 1)
+                fp.append((id(w), a.__array_interface__["data"][0], a.shape,
+                           flat[::step][:1024].tobytes()))
+    return tuple(fp)
+
+
+def _stacked(params: ExpertParams, h_in: int) -> _Stacked:
+    import weakref
+
+    fp = _fingerprint(params)
+    for i, (ref, h, f, st) in enumerate(_STACK_CACHE):
+        if ref() is params and h == h_in and f == fp:
+            _STACK_CACHE.append(_STACK_CACHE.pop(i))
+            return st
+    st = _Stacked(params, h_in)
+    try:
+        ref = weakref.ref(params)
+    except TypeError:
+        return st
+    _STACK_CACHE.append((ref, h_in, fp, st))
+    del _STACK_CACHE[:-_STACK_CACHE_SIZE]
+    return st
+
+
+def clear_weight_cache() -> None:
+    _STACK_CACHE.clear()
+
+
 def _experts_padded(xp_rows, st: _Stacked, plan, row_prob=None):
     """fc1+SwiGLU then fc2 on a padded plan -> expert output rows [max_rows, hop]."""
     _, act = gemm.fc1_fwd(xp_rows, st.w1, plan.block_expert, plan.num_m_blocks, row_prob)
@@ -394,7 +440,7 @@ def _combine(tokens, decision: RoutingDecision, params: ExpertParams, mem_effici
     np_io = _is_np(tokens)
     x = _t(tokens)
     t = x.shape[0]
-    st = _Stacked(params, x.shape[1])
+    st = _stacked(params, x.shape[1])
     plan, prob = _plan(decision)
     xp = ops.permute_gather(st.pad_x(x), plan)
     o = _experts_padded(xp, st, plan, plan.row_prob if mem_efficient else None)
