@@ -36,6 +36,27 @@ extern "C" {
  * replaces route() routing.py:71-108 (score :85-91, bias on scores :95, stable top-k with
  * lowest-index ties :96-101, unnormalised probs :102, counts :106) and aux_loss()
  * routing.py:111-120. The logits GEMM x @ W_r (routing.py:79) runs on moe_gg_gemm_f32. */
+/* Small-E router (E <= 16, e.g. Mixtral E = 8): the logits x . W_r (routing.py:79) are
+ * computed on the CUDA cores inside the scoring / top-k kernel (x read once, W_r^T in shared
+ * memory) instead of a tensor-core tile padded to 256 columns; same outputs as
+ * moe_router_topk plus logits[T, E] fp32. moe_router_small_ok(E, h) says whether a shape is
+ * eligible (else: moe_gg_gemm_f32 + moe_router_topk). */
+int moe_router_small_ok(int E, int h);
+int moe_router_fused(const void* x, int T, int h, const void* w_r, int E, int K, int score_fn,
+                     const float* sel_bias, float* logits, int* topk_idx, float* topk_prob,
+                     float* scores_out, int* counts, float* score_partials, int* status,
+                     void* stream);
+/* Its backward (aux part = aux_loss_grad_wr routing.py:123-137): dlogits
+ * as compact fp32 [T, E]; dW_r = x^T dl with a fixed-order reduction over token groups
+ * (workspace moe_router_wgrad_small_ws floats); router dX = dl . W_r^T as bf16 [T, h]. */
+int moe_router_bwd_f32(const float* logits, int ld, int T, int E, int K, int score_fn,
+                       const int* topk_idx, const float* dprob, const float* aux_grad,
+                       float* dlogits, void* stream);
+long long moe_router_wgrad_small_ws(int T, int h, int E);
+int moe_router_wgrad_small(const void* x, int T, int h, const float* dl, int E, float* ws,
+                           float* dw, void* stream);
+int moe_router_dx_small(const float* dl, int T, int E, const void* w_r, int h, void* dx,
+                        void* stream);
 int moe_router_num_partials(int T);
 int moe_router_topk(const float* logits, int ld, int T, int E, int K, int score_fn,
                     const float* sel_bias, int* topk_idx, float* topk_prob, float* scores_out,

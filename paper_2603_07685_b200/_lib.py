@@ -37,6 +37,10 @@ SIGNATURES: dict[str, list] = {
     "moe_router_bwd": [P, I, I, I, I, I, P, P, P, P, I, P],
     "moe_stage_router_weight": [P, I, I, I, P, P, P],
     "moe_reduce_groups_f32": [P, I, I, I, I, P, P],
+    "moe_router_fused": [P, I, I, P, I, I, I, P, P, P, P, P, P, P, P, P],
+    "moe_router_bwd_f32": [P, I, I, I, I, I, P, P, P, P, P],
+    "moe_router_wgrad_small": [P, I, I, P, I, P, P, P],
+    "moe_router_dx_small": [P, I, I, P, I, P, P],
     # permutation / combine (csrc/permute.cu)
     "moe_permute_plan": [P, P, I, I, I, I, P, I, P, I, I, P, P, P, P, P, P, P, P, P, P, P, P,
                          P],
@@ -97,6 +101,8 @@ SIGNATURES: dict[str, list] = {
 # non-status query functions: name -> (argtypes, restype)
 QUERIES: dict[str, tuple] = {
     "moe_router_num_partials": ([I], c_int),
+    "moe_router_small_ok": ([I, I], c_int),
+    "moe_router_wgrad_small_ws": ([I, I, I], c_int64),
     "moe_permute_workspace_ints": ([I, I, I], c_int64),
     "moe_gg_dprob_partials": ([I], c_int),
 }
@@ -153,7 +159,8 @@ def check(status: int, what: str) -> None:
 
 # kernels of ours launched by one call of each entry point (cudaMemsetAsync not counted)
 KERNELS_PER_CALL = {name: 1 for name in SIGNATURES}
-KERNELS_PER_CALL.update({"moe_permute_plan": 5, "moe_permute_gather": 2, "moe_ep_prepare": 0})
+KERNELS_PER_CALL.update({"moe_permute_plan": 5, "moe_permute_gather": 2, "moe_ep_prepare": 0,
+                         "moe_router_wgrad_small": 2})
 
 
 class _Stats:

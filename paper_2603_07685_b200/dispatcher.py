@@ -232,7 +232,7 @@ class _MoEEPFunction(torch.autograd.Function):
         E, K = cfg.num_experts, cfg.top_k
         n = ep.n
         dev = x.device
-        w_r_t, w_r_pad = ops.stage_router_weight(w_r)
+        w_r_t, w_r_pad = ops.stage_router(w_r)
         r = ops.router_forward(x, w_r, K, cfg.score, sel_bias, 0.0, w_r_t=w_r_t)
         stats = torch.cat([r.counts.float(), r.mean_scores])
         gathered = torch.empty((n, 2 * E), dtype=torch.float32, device=dev)
@@ -620,7 +620,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         dev = x.device
         pool = _pool(ep, dev, tag)
         stream = torch.cuda.current_stream().cuda_stream
-        w_r_t, w_r_pad = ops.stage_router_weight(w_r)
+        w_r_t, w_r_pad = ops.stage_router(w_r)
         r = ops.router_forward(x, w_r, K, cfg.score, sel_bias, 0.0, w_r_t=w_r_t)
         stats = torch.cat([r.counts.float(), r.mean_scores])
         gathered = torch.empty((n, 2 * E), dtype=torch.float32, device=dev)
@@ -992,7 +992,7 @@ class _MoEEPDedupFunction(torch.autograd.Function):
         pool = _pool(ep, dev, tag)
         stream = torch.cuda.current_stream().cuda_stream
         i32 = dict(dtype=torch.int32, device=dev)
-        w_r_t, w_r_pad = ops.stage_router_weight(w_r)
+        w_r_t, w_r_pad = ops.stage_router(w_r)
         r = ops.router_forward(x, w_r, K, cfg.score, sel_bias, 0.0, w_r_t=w_r_t)
         cap = cfg.capacity(n * t)
         el = E // n

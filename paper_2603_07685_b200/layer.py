@@ -57,7 +57,7 @@ class _MoEFunction(torch.autograd.Function):
     def forward(ctx, x, w_r, w1, w2, sel_bias, w1s, w2s, cfg: MoEConfig):
         t, h = x.shape
         e = cfg.num_experts
-        w_r_t, w_r_pad = ops.stage_router_weight(w_r)
+        w_r_t, w_r_pad = ops.stage_router(w_r)
         r = ops.router_forward(x, w_r, cfg.top_k, cfg.score, sel_bias, cfg.aux_loss_coeff,
                                w_r_t=w_r_t)
         if cfg.check_finite and int(r.status.item()) & 1:

@@ -44,6 +44,31 @@ class RouterOut:
     mean_scores: torch.Tensor  # [E] fp32, P_e
     status: torch.Tensor       # [1] int32, bit0 = non-finite logits
     scores: torch.Tensor | None = None  # [T, E] fp32 when requested
+    w_r: torch.Tensor | None = None     # [h, E] bf16: set on the small-E path (backward operand)
+
+
+# Small-E CUDA-core router (moe_router_fused + CUDA-core backward) instead of the tcgen05
+# logits / gradient GEMMs padded to 256 columns. Correct (tests/test_router_gpu.py) but measured
+# SLOWER on B200 (tools/router_probe.py, profiles/r02_router_probe.txt: Mixtral shape fwd+bwd
+# chain 289 us vs 244 us): the x . W_r product at E = 8 is ~32 FLOP per x element over three
+# passes, which is CUDA-core instruction bound, while the padded tensor-core tiles stay near
+# the HBM floor. Opt-in with MOE_ROUTER_SMALL=1.
+ROUTER_SMALL = os.environ.get("MOE_ROUTER_SMALL", "0") == "1"
+
+
+def router_small(num_experts: int, hidden: int) -> bool:
+    """True when the small-E CUDA-core router is enabled (ROUTER_SMALL) and eligible
+    (E <= 16, W_r^T fits shared memory); else the tcgen05 logits GEMM path runs."""
+    return ROUTER_SMALL and bool(_lib.query("moe_router_small_ok", num_experts, hidden))
+
+
+def stage_router(w_r: torch.Tensor):
+    """Per-forward router-weight operands: (W_r^T padded, W_r padded) for the tcgen05 path,
+    (None, None) on the small-E path (which reads W_r [h, E] as is)."""
+    h, e = w_r.shape
+    if router_small(e, h):
+        return None, None
+    return stage_router_weight(w_r)
 
 
 def stage_router_weight(w_r: torch.Tensor, want_t=True, want_pad=True):
@@ -67,6 +92,8 @@ def router_forward(x: torch.Tensor, w_r: torch.Tensor, top_k: int, score: str = 
     t, h = x.shape
     e = w_r.shape[1]
     dev = x.device
+    if w_r_t is None and router_small(e, h):
+        return _router_forward_small(x, w_r, top_k, score, selection_bias, coeff, want_scores)
     if w_r_t is None:
         w_r_t, _ = stage_router_weight(w_r, want_pad=False)
     epad = w_r_t.shape[1]
@@ -98,14 +125,74 @@ def router_forward(x: torch.Tensor, w_r: torch.Tensor, top_k: int, score: str = 
                      scores)
 
 
-def router_backward(x: torch.Tensor, w_r_pad: torch.Tensor, r: RouterOut, dprob: torch.Tensor,
-                    score: str, aux_scale: float | torch.Tensor | None = 1.0,
-                    num_splits: int = 8):
+def _router_forward_small(x, w_r, top_k, score, selection_bias, coeff, want_scores):
+    """route() + aux_loss() for E <= 16: one kernel computes the logits (CUDA cores, x read
+    once), scores, top-k, counts and score partials (moe_router_fused)."""
+    t, h = x.shape
+    e = w_r.shape[1]
+    dev = x.device
+    w_r = w_r.to(torch.bfloat16).contiguous()
+    logits = torch.empty((t, e), dtype=torch.float32, device=dev)
+    topk_idx = torch.empty((t, top_k), dtype=torch.int32, device=dev)
+    topk_prob = torch.empty((t, top_k), dtype=torch.float32, device=dev)
+    counts = torch.empty((e,), dtype=torch.int32, device=dev)
+    npart = _lib.query("moe_router_num_partials", t)
+    partials = torch.empty((max(npart, 1), e), dtype=torch.float32, device=dev)
+    status = torch.empty((1,), dtype=torch.int32, device=dev)
+    scores = torch.empty((t, e), dtype=torch.float32, device=dev) if want_scores else None
+    bias = None
+    if selection_bias is not None:
+        bias = selection_bias.to(device=dev, dtype=torch.float32).contiguous()
+    _lib.call("moe_router_fused", x.data_ptr(), t, h, w_r.data_ptr(), e, top_k, SCORE_FN[score],
+              _p(bias), logits.data_ptr(), topk_idx.data_ptr(), topk_prob.data_ptr(),
+              _p(scores), counts.data_ptr(), partials.data_ptr(), status.data_ptr(), _stream())
+    aux = torch.empty((), dtype=torch.float32, device=dev)
+    aux_grad = torch.empty((e,), dtype=torch.float32, device=dev)
+    mean_scores = torch.empty((e,), dtype=torch.float32, device=dev)
+    _lib.call("moe_router_finalize", counts.data_ptr(), partials.data_ptr(), t, top_k, e,
+              float(coeff), aux.data_ptr(), aux_grad.data_ptr(), mean_scores.data_ptr(), _stream())
+    return RouterOut(logits, topk_idx, topk_prob, counts, aux, aux_grad, mean_scores, status,
+                     scores, w_r)
+
+
+def _router_backward_small(x, r: RouterOut, dprob, score, aux_g, want_dx=True):
+    t, h = x.shape
+    e = r.counts.shape[0]
+    k = r.topk_idx.shape[1]
+    dev = x.device
+    dl = torch.empty((t, e), dtype=torch.float32, device=dev)
+    _lib.call("moe_router_bwd_f32", r.logits.data_ptr(), r.logits.shape[1], t, e, k,
+              SCORE_FN[score], r.topk_idx.data_ptr(), dprob.data_ptr(), _p(aux_g),
+              dl.data_ptr(), _stream())
+    ws = torch.empty((max(int(_lib.query("moe_router_wgrad_small_ws", t, h, e)), 1),),
+                     dtype=torch.float32, device=dev)
+    dw = torch.empty((h, e), dtype=torch.float32, device=dev)
+    _lib.call("moe_router_wgrad_small", x.data_ptr(), t, h, dl.data_ptr(), e, ws.data_ptr(),
+              dw.data_ptr(), _stream())
+    dx = None
+    if want_dx:
+        dx = torch.empty((t, h), dtype=torch.bfloat16, device=dev)
+        _lib.call("moe_router_dx_small", dl.data_ptr(), t, e, r.w_r.data_ptr(), h, dx.data_ptr(),
+                  _stream())
+    return dw, dx
+
+
+def router_backward(x: torch.Tensor, w_r_pad: torch.Tensor | None, r: RouterOut,
+                    dprob: torch.Tensor, score: str,
+                    aux_scale: float | torch.Tensor | None = 1.0, num_splits: int = 8):
     """Router backward (aux part = routing.py:123-137).
 
-    Returns (dW_r [h, E] fp32, dX_router [ceil128(T), h] bf16 or None).
+    Returns (dW_r [h, E] fp32, dX_router [>= T, h] bf16 or None).
     aux_scale multiplies the aux-loss gradient (the upstream grad of the aux output).
+    w_r_pad: the staged [h, 256k] router weight of the tcgen05 path (None on the small-E path,
+    which uses r.w_r).
     """
+    if r.w_r is not None:
+        aux_g = None
+        if aux_scale is not None:
+            aux_g = r.aux_grad if (isinstance(aux_scale, float) and aux_scale == 1.0) else (
+                r.aux_grad * aux_scale)
+        return _router_backward_small(x, r, dprob, score, aux_g)
     t, h = x.shape
     e = r.counts.shape[0]
     k = r.topk_idx.shape[1]

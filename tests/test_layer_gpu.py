@@ -218,3 +218,13 @@ def test_cuda_graph_capture_matches_eager(dev):
     torch.cuda.synchronize()
     got = [y_g, x_g.grad, w_r.grad, w1.grad, w2.grad]
     assert all(torch.equal(a, b) for a, b in zip(ref, got))
+
+
+def test_small_e_cuda_core_router_path(dev, monkeypatch):
+    """The opt-in small-E router (moe_router_fused + CUDA-core backward, ops.ROUTER_SMALL)
+    through the whole layer, against the fp64 oracle."""
+    monkeypatch.setattr(ops, "ROUTER_SMALL", True)
+    assert ops.router_small(8, 256)
+    run_case(MoEConfig(8, 2, 256, 512, aux_loss_coeff=1e-2), 1000, 12, dev)
+    run_case(MoEConfig(16, 4, 256, 256, score="sigmoid", aux_loss_coeff=1e-2,
+                       capacity_factor=0.8, pad_to_capacity=True), 512, 13, dev)
