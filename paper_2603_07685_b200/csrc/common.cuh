@@ -288,6 +288,19 @@ __device__ __forceinline__ void bulk_store_s2g(void* gdst, const void* ssrc, uin
                "r"(smem_u32(ssrc)), "r"(bytes)
                : "memory");
 }
+// TMA tensor store of a shared-memory box (same swizzle as the tensor map) to global.
+__device__ __forceinline__ void tma_store_2d(const void* tmap, const void* smem_src, int x,
+                                             int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(tmap)),
+      "r"(smem_u32(smem_src)), "r"(x), "r"(y)
+      : "memory");
+}
+// wait until at most one committed bulk group of this thread still reads shared memory
+__device__ __forceinline__ void bulk_wait_read_1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }

@@ -62,15 +62,20 @@ constexpr int epi_warps() {
 }
 constexpr int BAND_M = 16;  // raster: 16 M units share each swept n-block (L2 reuse)
 
-template <int CG>
+// SK: the small-K weight-gradient variant (few token rows per expert, e.g. DeepSeek-shape
+// EP=1 with ~128): tiles are output-bound, so it trades operand stages for a 64 KB output
+// staging area (two 4 KB TMA-store boxes per epilogue warp).
+template <int CG, bool SK = false>
 struct Cfg {
   static constexpr int A_STAGE = BM * BK * 2;           // this CTA's 128 rows of A
   static constexpr int B_ROWS = BN / CG;                // rows of the B tile this CTA stages
   static constexpr int B_STAGE = B_ROWS * BK * 2;
   static constexpr int STAGE = A_STAGE + B_STAGE;
-  static constexpr int STAGES = CG == 1 ? 4 : 6;
+  static constexpr int STAGES = SK ? (CG == 1 ? 3 : 4) : (CG == 1 ? 4 : 6);
   static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
 };
+constexpr int SK_BOX_BYTES = 32 * 64 * 2;              // 32 rows x 64 bf16 columns
+constexpr int SK_STAGING = 8 * 2 * SK_BOX_BYTES;       // 8 warps x double buffer
 // Row-scatter epilogue (EPI_BF16, grouped-M, row_dst set): each epilogue warp stages its 32
 // rows x 128 columns (half a tile row) in shared memory and writes every row with one
 // 256-byte TMA bulk store to its destination (often a peer GPU over NVLink) instead of 16-B
@@ -80,9 +85,10 @@ struct Cfg {
 constexpr int SCATTER_BYTES = 32 * 1024;  // staging for all epilogue warps
 template <bool GROUPED_K>
 constexpr int scatter_cols() { return GROUPED_K ? 64 : 128; }
-template <int EPI, bool GROUPED_K, int CG>
+template <int EPI, bool GROUPED_K, int CG, bool SK>
 constexpr int smem_bytes() {
-  return Cfg<CG>::SMEM + (EPI == 0 ? SCATTER_BYTES : 0);
+  // SK staging starts 1024-aligned after the barrier block (SWIZZLE_128B TMA boxes)
+  return Cfg<CG, SK>::SMEM + (EPI == 0 ? (SK ? 768 + SK_STAGING : SCATTER_BYTES) : 0);
 }
 
 
@@ -126,7 +132,7 @@ struct Params {
   // stream does not evict the operand tiles other CTAs still reuse from L2
   int stream_stores;
   int band_m;  // raster band: M units that sweep each n-block together (L2 reuse)
-  int bulk_out;  // grouped-K EPI_BF16: staged TMA bulk stores for the output rows
+  int bulk_out;  // grouped-K EPI_BF16: the SK variant (TMA tensor stores of staged boxes)
 };
 
 __device__ __forceinline__ void st_out(int4* p, int4 v, int cs) {
@@ -289,11 +295,12 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
       : "memory");
 }
 
-template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI, int CG>
+template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI, int CG, bool SK>
 __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
-                        const __grid_constant__ CUtensorMap tmap_b, const Params p) {
-  using C = Cfg<CG>;
+                        const __grid_constant__ CUtensorMap tmap_b,
+                        const __grid_constant__ CUtensorMap tmap_c, const Params p) {
+  using C = Cfg<CG, SK>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -459,6 +466,9 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
     const int half = (warp - 2) / 4;
     constexpr int SC = scatter_cols<GROUPED_K>();
     uint8_t* stage = smem + C::STAGES * C::STAGE + 256 + (warp - 2) * (32 * SC * 2);
+    // SK: two 4 KB boxes per warp, 1024-aligned; boxes alternate across the warp's pieces
+    uint8_t* sk_box = smem + C::STAGES * C::STAGE + 1024 + (warp - 2) * (2 * SK_BOX_BYTES);
+    int sk_piece = 0;
     constexpr int EC = BN / (epi_warps<GROUPED_K, EPI>() / 4);  // tile columns per epilogue warp
     const int cb = half * EC;  // this warp's first tile column
     const int row_local = q * 32 + lane;
@@ -503,7 +513,41 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
       tc_fence_after();
       const uint32_t t_base = tmem_base + lane_off + acc * BN;
 
-      if constexpr (EPI == EPI_BF16 || EPI == EPI_F32) {
+      if constexpr (EPI == EPI_BF16 && GROUPED_K && SK) {
+        // 64-column pieces: this warp's 32 rows x 64 columns go to a SWIZZLE_128B box in
+        // shared memory (lane = row; 16-byte chunk j stored at j ^ (row & 7): the 16-byte
+        // stores of a warp hit distinct bank groups) and leave with one TMA tensor store; two
+        // boxes alternate so a store drains while the next piece is staged. Both 32-column
+        // TMEM loads of a piece are in flight before the single wait.
+#pragma unroll 1
+        for (int pc = 0; pc < EC / 64; ++pc) {
+          const int col = cb + pc * 64;
+          uint32_t r[2][32];
+          tmem_ld_32x32b_x32(t_base + col, r[0]);
+          tmem_ld_32x32b_x32(t_base + col + 32, r[1]);
+          uint8_t* box = sk_box + (sk_piece & 1) * SK_BOX_BYTES;
+          if (lane == 0) bulk_wait_read_1();  // the store that last used this box has read it
+          __syncwarp();
+          tmem_ld_wait();
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            const uint32_t* rv = r[v >> 2] + 8 * (v & 3);
+            int4 w;
+            w.x = pack_bf16x2(__uint_as_float(rv[0]), __uint_as_float(rv[1]));
+            w.y = pack_bf16x2(__uint_as_float(rv[2]), __uint_as_float(rv[3]));
+            w.z = pack_bf16x2(__uint_as_float(rv[4]), __uint_as_float(rv[5]));
+            w.w = pack_bf16x2(__uint_as_float(rv[6]), __uint_as_float(rv[7]));
+            *reinterpret_cast<int4*>(box + lane * 128 + ((v ^ (lane & 7)) * 16)) = w;
+          }
+          fence_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmap_c, box, tl.n0 + col, tl.expert * p.M + tl.m0 + q * 32);
+            bulk_commit();
+          }
+          ++sk_piece;
+        }
+      } else if constexpr (EPI == EPI_BF16 || EPI == EPI_F32) {
         const long long ebase = GROUPED_K ? tl.expert * p.out_expert_stride : 0;
 #pragma unroll 1
         for (int c = 0; c < EC / 32; ++c) {
@@ -512,7 +556,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
           tmem_ld_32x32b_x32(t_base + col, r);
           tmem_ld_wait();
           if constexpr (EPI == EPI_BF16) {
-            if ((!GROUPED_K && p.row_dst) || (GROUPED_K && p.bulk_out)) {
+            if (!GROUPED_K && p.row_dst) {
               // stage this lane's row chunk; one bulk store per (row, SC columns)
               const int hc = col % SC;
               uint8_t* srow = stage + lane * (SC * 2);
@@ -527,10 +571,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
                 reinterpret_cast<int4*>(srow + hc * 2)[v] = w;
               }
               if (hc + 32 == SC) {
-                const unsigned long long dst =
-                    GROUPED_K ? reinterpret_cast<unsigned long long>(
-                                    reinterpret_cast<__nv_bfloat16*>(p.out) + ebase + row * p.ldo)
-                              : __ldg(p.row_dst + row);
+                const unsigned long long dst = __ldg(p.row_dst + row);
                 fence_async_shared();
                 if (dst) {
                   bulk_store_s2g(reinterpret_cast<__nv_bfloat16*>(dst) + tl.n0 + col + 32 - SC,
@@ -661,8 +702,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
 
   // scattered rows may be in peer memory: complete the bulk stores and make them visible
   // system-wide before the stream-ordered collective that publishes them
-  if (EPI == EPI_BF16 && ((!GROUPED_K && p.row_dst) || (GROUPED_K && p.bulk_out)) &&
-      warp >= 2) {
+  if (EPI == EPI_BF16 && ((!GROUPED_K && p.row_dst) || (GROUPED_K && SK)) && warp >= 2) {
     bulk_wait_all();
     __threadfence_system();
   }
@@ -718,19 +758,19 @@ static int make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t o
 
 static int num_sms() { return device_sms(); }
 
-template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI, int CG>
-static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
-                     int max_tiles, cudaStream_t stream) {
-  auto kern = grouped_gemm_kernel<A_MN, B_MN, GROUPED_K, EPI, CG>;
+template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI, int CG, bool SK>
+static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                     const Params& p, int max_tiles, cudaStream_t stream) {
+  auto kern = grouped_gemm_kernel<A_MN, B_MN, GROUPED_K, EPI, CG, SK>;
   MOE_CUDA_CHECK(ensure_dyn_smem(reinterpret_cast<const void*>(kern),
-                                 smem_bytes<EPI, GROUPED_K, CG>()));
+                                 smem_bytes<EPI, GROUPED_K, CG, SK>()));
   if (max_tiles <= 0) return kOk;
   int grid = max_tiles * CG < num_sms() ? max_tiles * CG : num_sms();
   grid -= grid % CG;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(64 + 32 * epi_warps<GROUPED_K, EPI>());
-  cfg.dynamicSmemBytes = smem_bytes<EPI, GROUPED_K, CG>();
+  cfg.dynamicSmemBytes = smem_bytes<EPI, GROUPED_K, CG, SK>();
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -739,7 +779,7 @@ static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params&
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  MOE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
+  MOE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p));
   return kOk;
 }
 
@@ -772,9 +812,9 @@ static int run(const void* a, uint64_t a_inner, uint64_t a_outer, const void* b,
     p.band_m = bm;
   }
   {
-    // grouped-K: staged bulk stores pay off when the tiles are output-bound, i.e. few token
-    // rows per expert (DeepSeek-shape EP=1, 128 rows: wgrad 12.0 -> 10.8 ms); with long K
-    // the per-thread stores are as fast (Mixtral 9.52 vs 9.61 ms, Qwen3 7.87 vs 8.64 ms)
+    // grouped-K with few token rows per expert (avg <= 512: DeepSeek-shape EP=1 has 128) is
+    // output-bound: the SK variant (staged boxes + TMA tensor stores). With long K the
+    // per-thread stores of the 6-stage engine are as fast (Mixtral, Qwen3).
     static int bo = -2;
     if (bo == -2) {
       const char* e = getenv("MOE_B200_WGRAD_BULK");
@@ -783,14 +823,28 @@ static int run(const void* a, uint64_t a_inner, uint64_t a_outer, const void* b,
     const long long avg_k = p.num_experts > 0 ? (long long)a_outer / p.num_experts : 0;
     p.bulk_out = bo >= 0 ? bo : (GROUPED_K && avg_k > 0 && avg_k <= 512 ? 1 : 0);
   }
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tc;
   int st;
   const int cg = pair ? 2 : 1;
   if ((st = make_tmap(&ta, a, a_inner, a_outer, a_inner, 64, A_MN ? BK : BM))) return st;
   if ((st = make_tmap(&tb, b, b_inner, b_outer, b_inner, 64, B_MN ? BK : BN / cg))) return st;
   const int nb = p.N / BN;
-  if (pair) return launch_cg<A_MN, B_MN, GROUPED_K, EPI, 2>(ta, tb, p, (units_m / 2) * nb, stream);
-  return launch_cg<A_MN, B_MN, GROUPED_K, EPI, 1>(ta, tb, p, units_m * nb, stream);
+  if constexpr (GROUPED_K && EPI == EPI_BF16) {
+    if (p.bulk_out) {
+      // output dW [E*M rows, N] bf16, boxes of 32 rows x 64 columns, SWIZZLE_128B
+      if ((st = make_tmap(&tc, p.out, p.N, (uint64_t)p.num_experts * p.M, p.ldo, 64, 32)))
+        return st;
+      if (pair)
+        return launch_cg<A_MN, B_MN, true, EPI, 2, true>(ta, tb, tc, p, (units_m / 2) * nb,
+                                                         stream);
+      return launch_cg<A_MN, B_MN, true, EPI, 1, true>(ta, tb, tc, p, units_m * nb, stream);
+    }
+  }
+  tc = tb;  // unused by the other variants
+  if (pair)
+    return launch_cg<A_MN, B_MN, GROUPED_K, EPI, 2, false>(ta, tb, tc, p, (units_m / 2) * nb,
+                                                           stream);
+  return launch_cg<A_MN, B_MN, GROUPED_K, EPI, 1, false>(ta, tb, tc, p, units_m * nb, stream);
 }
 
 }  // namespace gg
