@@ -242,6 +242,52 @@ def cpu_baseline(c, sample_tokens: int, threads: int, reps: int = 1) -> dict:
                        f"fwd+bwd, oracle/backward_ref.py numpy fp32, best of {reps}")}
 
 
+def gemm_traffic(config: str, n: int):
+    """DRAM bytes of the routed grouped-GEMM launches of one step (ncu --metrics pass over
+    tools/layer_step.py, reduced by tools/step_traffic.py into profiles/), next to their
+    algorithmic bytes. EP=1 captures only (the per-rank GEMMs at EP>1 see the same shapes
+    per expert but fewer experts)."""
+    if n != 1:
+        return None
+    f = ROOT / "profiles" / f"r02_step_traffic_{config}.json"
+    if not f.exists():
+        return None
+    d = json.loads(f.read_text())
+    g = d["routed_gemm_traffic"]
+    tot = sum(v["traffic_GB"] for v in g.values())
+    alg = sum(v["algorithmic_GB"] for v in g.values())
+    return {"bytes": int(tot * 1e9), "bytes_per_launch": int(tot * 1e9 / max(len(g), 1)),
+            "algorithmic_bytes": int(alg * 1e9), "ratio": round(tot / alg, 2),
+            "per_gemm_GB": {k: v["traffic_GB"] for k, v in g.items()},
+            "source": f"profiles/{f.name} (ncu dram__bytes_read.sum + dram__bytes_write.sum, "
+                      "one step of tools/layer_step.py)"}
+
+
+def hbm_kernels(c, per_kernel: dict, steps: int, hbm_gbs: float):
+    """Event-timed bandwidth of the HBM-bound data-movement kernels (SURVEY §8(d) bytes):
+    permute gather (x read, R rows written), combine (forward y and backward dX), combine
+    backward (dY + O rows read, dO rows written)."""
+    T, K, h = c["T"], c["K"], c["h"]
+    R, w = T * K, 2
+    alg = {
+        "moe_permute_gather": T * h * w + R * h * w + R * 4,
+        # forward: R rows + probs + map read, y written (+ the shared-expert output read);
+        # backward dX: R rows + map + the router dX (+ shared-expert dX) read, dX written
+        "moe_combine": (R * h * w + R * 8 + T * h * w + (T * h * w if c.get("shared") else 0))
+                       + (R * h * w + R * 4 + T * h * w + (T * h * w if c.get("shared") else 0)
+                          + T * h * w),
+        "moe_combine_bwd": T * h * w + 2 * R * h * w + R * 12,
+    }
+    out = {}
+    for k, b in alg.items():
+        if k in per_kernel:
+            ms = sum(per_kernel[k]) / steps
+            gbs = b / (ms / 1e3) / 1e9
+            out[k] = {"ms_per_step": round(ms, 4), "algorithmic_MB": round(b / 1e6, 1),
+                      "achieved_GBps": round(gbs, 1), "frac_of_measured_hbm": round(gbs / hbm_gbs, 3)}
+    return out
+
+
 def cpu_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -587,6 +633,10 @@ def run_gpu(args, c) -> None:
         peak_src = ("measured sustained cuBLAS bf16 (MEASURED_PEAKS.json bf16_tflops_sustained)"
                     if peaks else "fallback ~1.4 PF sustained (B200_PROFILING.md)")
         gemm_flops_step = gemm_flops_per_token(c) * T  # per rank
+        burst_tf = peaks.get("bf16_tflops", 1590.0)
+        hbm_gbs = peaks.get("hbm_gbs", 6650.0)
+        traffic = gemm_traffic(args.config, n)
+        hbm = hbm_kernels(c, per_kernel, args.steps, hbm_gbs)
         gemm_tflops = gemm_flops_step * args.steps / (gemm_ms / 1e3) / 1e12 if gemm_ms else None
         gemm_launches = sum(len(v) for k_, v in per_kernel.items() if k_.startswith("moe_gg_"))
         out = {
@@ -628,11 +678,17 @@ def run_gpu(args, c) -> None:
                 "peak_source": peak_src,
                 "unit": "TFLOP/s",
                 "frac": round(gemm_tflops / peak_tf, 4) if gemm_tflops else None,
-                "traffic": None,
+                "frac_vs": ({"sustained_measured": round(gemm_tflops / peak_tf, 4),
+                             "burst_measured": round(gemm_tflops / burst_tf, 4),
+                             "datasheet_dense_2250": round(gemm_tflops / 2250.0, 4)}
+                            if gemm_tflops else None),
+                "traffic": traffic["bytes"] if traffic else None,
+                "traffic_detail": traffic,
                 "algorithmic": f"18*K*h*m FLOP/token = {gemm_flops_per_token(c) / 1e9:.3f} "
                                "GFLOP/token (fwd 6, dgrad 6, wgrad 6)",
                 "gemm_share_of_step": round(gemm_ms / args.steps / ms_step, 4) if gemm_ms else None,
             },
+            "hbm_kernels": hbm,
             "e2e": {
                 "value": round(tokens / (e2e_ms / 1e3), 1),
                 "unit": "tokens/s",
