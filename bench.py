@@ -222,12 +222,19 @@ def cpu_baseline(c, sample_tokens: int, threads: int, reps: int = 1) -> dict:
     f32 = np.float32
     x = rng.standard_normal((sample_tokens, h), dtype=f32)
     w_r = (rng.standard_normal((h, e), dtype=f32) * h ** -0.5).astype(f32)
-    # one expert's weights shared by reference across all experts: identical FLOPs and
-    # memory traffic per expert, without generating E x 3 x m x h random numbers.
-    up = (rng.standard_normal((m, h), dtype=f32) * h ** -0.5).astype(f32)
-    gate = (rng.standard_normal((m, h), dtype=f32) * h ** -0.5).astype(f32)
-    w2 = (rng.standard_normal((h, m), dtype=f32) * m ** -0.5).astype(f32)
-    params = R.ExpertParams(w1=[up] * e, w2=[w2] * e, gate=[gate] * e)
+    # every expert has its own weights (the layer's full parameter set, E x 3 x m x h fp32)
+    # up to 8 GB of host memory; beyond that (DeepSeek shape: 45 GB) the experts share one
+    # set -- same FLOPs per expert, stated in the sample description
+    def expert_w(shape, fan_in):
+        return (rng.standard_normal(shape, dtype=f32) * fan_in ** -0.5).astype(f32)
+
+    distinct = e * 3 * m * h * 4 <= 8e9
+    nw = e if distinct else 1
+    up = [expert_w((m, h), h) for _ in range(nw)]
+    w2 = [expert_w((h, m), m) for _ in range(nw)]
+    gate = [expert_w((m, h), h) for _ in range(nw)]
+    params = R.ExpertParams(w1=(up if distinct else up * e), w2=(w2 if distinct else w2 * e),
+                            gate=(gate if distinct else gate * e))
     dy = rng.standard_normal((sample_tokens, h), dtype=f32)
     def one_step() -> float:
         t0 = time.perf_counter()
@@ -238,8 +245,12 @@ def cpu_baseline(c, sample_tokens: int, threads: int, reps: int = 1) -> dict:
     best = min(times)
     return {"value": sample_tokens / best, "unit": "tokens/s", "cores": threads,
             "kind": "port", "seconds": best, "times": times, "step": one_step,
-            "sample": (f"{sample_tokens} tokens of the {c['name']} (E={e},K={k},h={h},m={m}), "
-                       f"fwd+bwd, oracle/backward_ref.py numpy fp32, best of {reps}")}
+            "sample": (f"{sample_tokens} tokens of the {c['name']} (E={e},K={k},h={h},m={m}, "
+                       + (f"all {e} experts' own weights" if distinct else
+                          "experts sharing one weight set (host memory)")
+                       + "), fwd+bwd, oracle/backward_ref.py "
+                       f"(the pinned numpy restatement of moelab.routing + its analytic "
+                       f"backward) fp32, best of {reps}")}
 
 
 def gemm_traffic(config: str, n: int):
