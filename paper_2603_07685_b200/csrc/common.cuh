@@ -297,6 +297,10 @@ __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* smem_
       "r"(smem_u32(smem_src)), "r"(x), "r"(y)
       : "memory");
 }
+// wait until no committed bulk group of this thread still reads shared memory
+__device__ __forceinline__ void bulk_wait_read_0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
 // wait until at most one committed bulk group of this thread still reads shared memory
 __device__ __forceinline__ void bulk_wait_read_1() {
   asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");

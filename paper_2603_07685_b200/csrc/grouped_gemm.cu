@@ -53,6 +53,15 @@ enum Epi : int { EPI_BF16 = 0, EPI_SWIGLU = 1, EPI_DSWIGLU = 2, EPI_F32 = 3 };
 #define MOE_DSWIGLU_WARPS 4
 #endif
 constexpr int DSW_HALVES = MOE_DSWIGLU_WARPS / 4;  // dprob partials per (row, n-tile)
+// dSwiGLU operands through shared memory: per epilogue warp and 32-column chunk, the gate /
+// up pre-activation (32 rows x 32 columns each) arrive by TMA into a SWIZZLE_64B box one chunk
+// ahead, d_gate / d_up overwrite them in place and leave by TMA tensor store (coalesced
+// 64-byte row segments both ways instead of 16-byte per-thread accesses across 32 rows).
+#ifndef MOE_DSWIGLU_TMA
+#define MOE_DSWIGLU_TMA 1
+#endif
+constexpr int DSW_BOX = 32 * 32 * 2;                          // 32 rows x 32 bf16 columns
+constexpr int DSW_STAGING = MOE_DSWIGLU_WARPS * 2 * 2 * DSW_BOX;  // warps x 2 bufs x (g, u)
 // Weight-gradient (grouped-K) kernels use 8 epilogue warps: with few token rows per expert
 // (DeepSeek-shape EP=1: 128) each output tile has almost no MMA work and the kernel is a
 // TMEM -> HBM drain, which 4 warps cannot keep busy.
@@ -87,8 +96,10 @@ template <bool GROUPED_K>
 constexpr int scatter_cols() { return GROUPED_K ? 64 : 128; }
 template <int EPI, bool GROUPED_K, int CG, bool SK>
 constexpr int smem_bytes() {
-  // SK staging starts 1024-aligned after the barrier block (SWIZZLE_128B TMA boxes)
-  return Cfg<CG, SK>::SMEM + (EPI == 0 ? (SK ? 768 + SK_STAGING : SCATTER_BYTES) : 0);
+  // SK / dSwiGLU staging starts 1024-aligned after the barrier block (swizzled TMA boxes)
+  return Cfg<CG, SK>::SMEM +
+         (EPI == 0 ? (SK ? 768 + SK_STAGING : SCATTER_BYTES)
+                   : (EPI == 2 && MOE_DSWIGLU_TMA ? 768 + DSW_STAGING : 0));
 }
 
 
@@ -299,7 +310,8 @@ template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI, int CG, bool SK>
 __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                         const __grid_constant__ CUtensorMap tmap_b,
-                        const __grid_constant__ CUtensorMap tmap_c, const Params p) {
+                        const __grid_constant__ CUtensorMap tmap_c,
+                        const __grid_constant__ CUtensorMap tmap_d, const Params p) {
   using C = Cfg<CG, SK>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -311,6 +323,9 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
   uint64_t* tfull_bar = empty_bar + C::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  // dSwiGLU operand boxes: 2 mbarriers per epilogue warp at +192 of the barrier block
+  uint64_t* dsw_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE + 192);
+  constexpr bool DSW_TMA = EPI == EPI_DSWIGLU && MOE_DSWIGLU_TMA;
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -327,6 +342,11 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
       mbar_init(&tempty_bar[s], epi_warps<GROUPED_K, EPI>() * CG);
+    }
+    if constexpr (DSW_TMA) {
+      tma_prefetch_desc(&tmap_c);
+      tma_prefetch_desc(&tmap_d);
+      for (int i = 0; i < 2 * epi_warps<GROUPED_K, EPI>(); ++i) mbar_init(&dsw_bar[i], 1);
     }
     fence_mbar_init();
     fence_async_shared();
@@ -475,6 +495,27 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     int acc = 0;
     uint32_t acc_ph = 0;
+    // dSwiGLU boxes of this warp: buffer b holds gate at +0 and up at +DSW_BOX
+    uint8_t* dsw_buf = smem + C::STAGES * C::STAGE + 1024 + (warp - 2) * (4 * DSW_BOX);
+    uint64_t* dbar = dsw_bar + (warp - 2) * 2;
+    uint32_t dsw_ph = 0;  // bit b: parity of buffer b's next completion
+    int dsw_seq = 0;      // chunks consumed by this warp (buffer = dsw_seq & 1)
+    auto dsw_load = [&](const Tile& tn, int c, int b) {
+      const int j0 = tn.n0 + cb + c * 32;
+      const int gpos = (j0 >> 7) * 256 + (j0 & 127);
+      const int y = tn.m0 + q * 32;
+      uint8_t* dst = dsw_buf + b * (2 * DSW_BOX);
+      mbar_arrive_expect_tx(&dbar[b], 2 * DSW_BOX);
+      tma_load_2d(dst, &tmap_d, &dbar[b], gpos, y);
+      tma_load_2d(dst + DSW_BOX, &tmap_d, &dbar[b], gpos + 128, y);
+    };
+    if constexpr (DSW_TMA) {
+      if (first < num_tiles && lane == 0) {
+        Tile t0;
+        decode_tile<GROUPED_K, CG>(p, first, num_units, rank, t0);
+        dsw_load(t0, 0, 0);
+      }
+    }
     for (int t = first; t < num_tiles; t += stride) {
       Tile tl;
       decode_tile<GROUPED_K, CG>(p, t, num_units, rank, tl);
@@ -499,7 +540,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
       // dSwiGLU: the first chunk's pre-activation (DRAM/L2 latency) is fetched while the
       // tile's MMAs are still running; later chunks are prefetched one chunk ahead.
       int4 pre_g[4], pre_u[4];
-      if constexpr (EPI == EPI_DSWIGLU) {
+      if constexpr (EPI == EPI_DSWIGLU && !DSW_TMA) {
         const __nv_bfloat16* pr = p.aux + row * p.ld_aux;
         const int jc = tl.n0 + cb;
         const long long pos0 = (long long)(jc >> 7) * 256 + (jc & 127);
@@ -635,6 +676,61 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
             st_out(reinterpret_cast<int4*>(act + c * 32) + v, wa, p.stream_stores);
           }
         }
+      } else if constexpr (DSW_TMA) {
+        // Accumulator = dL/d(act) (or dL/d(p*act) for the mem-efficient combine) for this
+        // warp's columns of the m-wide activation; phi is recomputed from the preact box.
+        const float scale = p.row_scale ? __ldg(p.row_scale + row) : 1.0f;
+        float dp_acc = 0.0f;
+        const int sw = (lane >> 1) & 3;  // SWIZZLE_64B: 16-byte chunk j of row r at j ^ sw
+#pragma unroll 1
+        for (int c = 0; c < EC / 32; ++c) {
+          const int b = dsw_seq & 1;
+          if (lane == 0) {
+            // next chunk (this tile, or chunk 0 of this warp's next tile) into the other box,
+            // once the store that last read that box has drained
+            bulk_wait_read_0();
+            if (c + 1 < EC / 32) {
+              dsw_load(tl, c + 1, b ^ 1);
+            } else if (t + stride < num_tiles) {
+              Tile tn;
+              decode_tile<GROUPED_K, CG>(p, t + stride, num_units, rank, tn);
+              dsw_load(tn, 0, b ^ 1);
+            }
+          }
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_base + cb + c * 32, r);
+          mbar_wait(&dbar[b], (dsw_ph >> b) & 1);
+          dsw_ph ^= 1u << b;
+          tmem_ld_wait();
+          uint8_t* gbox = dsw_buf + b * (2 * DSW_BOX) + lane * 64;
+          uint8_t* ubox = gbox + DSW_BOX;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            int4* gp = reinterpret_cast<int4*>(gbox + ((v ^ sw) << 4));
+            int4* up = reinterpret_cast<int4*>(ubox + ((v ^ sw) << 4));
+            int4 wg, wu;
+            if (p.row_partial)
+              dswiglu8<true>(r + 8 * v, *gp, *up, scale, wg, wu, dp_acc);
+            else
+              dswiglu8<false>(r + 8 * v, *gp, *up, scale, wg, wu, dp_acc);
+            *gp = wg;
+            *up = wu;
+          }
+          fence_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            const int j0 = tl.n0 + cb + c * 32;
+            const int gpos = (j0 >> 7) * 256 + (j0 & 127);
+            const int y = tl.m0 + q * 32;
+            uint8_t* box = dsw_buf + b * (2 * DSW_BOX);
+            tma_store_2d(&tmap_c, box, gpos, y);
+            tma_store_2d(&tmap_c, box + DSW_BOX, gpos + 128, y);
+            bulk_commit();
+          }
+          ++dsw_seq;
+        }
+        if (p.row_partial)
+          p.row_partial[row * p.ld_partial + (tl.n0 / BN) * DSW_HALVES + half] = dp_acc;
       } else if constexpr (EPI == EPI_DSWIGLU) {
         // Accumulator = dL/d(act) (or dL/d(p*act) for the mem-efficient combine) for
         // columns [n0, n0+256) of the m-wide activation. Recompute phi from preact.
@@ -702,7 +798,8 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
 
   // scattered rows may be in peer memory: complete the bulk stores and make them visible
   // system-wide before the stream-ordered collective that publishes them
-  if (EPI == EPI_BF16 && ((!GROUPED_K && p.row_dst) || (GROUPED_K && SK)) && warp >= 2) {
+  if ((DSW_TMA || (EPI == EPI_BF16 && ((!GROUPED_K && p.row_dst) || (GROUPED_K && SK)))) &&
+      warp >= 2) {
     bulk_wait_all();
     __threadfence_system();
   }
@@ -742,7 +839,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2-D bf16 tensor [outer, inner] with row stride `ld` elements, 128B-swizzled boxes.
 static int make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
-                     uint64_t ld, uint32_t box_inner, uint32_t box_outer) {
+                     uint64_t ld, uint32_t box_inner, uint32_t box_outer,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (!fn) return kErrCuda;
   if ((reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * 2) & 15)) return kErrInvalidArg;
@@ -751,7 +849,7 @@ static int make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t o
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? kOk : kErrCuda;
 }
@@ -760,7 +858,8 @@ static int num_sms() { return device_sms(); }
 
 template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI, int CG, bool SK>
 static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
-                     const Params& p, int max_tiles, cudaStream_t stream) {
+                     const CUtensorMap& td, const Params& p, int max_tiles,
+                     cudaStream_t stream) {
   auto kern = grouped_gemm_kernel<A_MN, B_MN, GROUPED_K, EPI, CG, SK>;
   MOE_CUDA_CHECK(ensure_dyn_smem(reinterpret_cast<const void*>(kern),
                                  smem_bytes<EPI, GROUPED_K, CG, SK>()));
@@ -779,7 +878,7 @@ static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtenso
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  MOE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p));
+  MOE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, td, p));
   return kOk;
 }
 
@@ -823,7 +922,7 @@ static int run(const void* a, uint64_t a_inner, uint64_t a_outer, const void* b,
     const long long avg_k = p.num_experts > 0 ? (long long)a_outer / p.num_experts : 0;
     p.bulk_out = bo >= 0 ? bo : (GROUPED_K && avg_k > 0 && avg_k <= 512 ? 1 : 0);
   }
-  CUtensorMap ta, tb, tc;
+  CUtensorMap ta, tb, tc, td;
   int st;
   const int cg = pair ? 2 : 1;
   if ((st = make_tmap(&ta, a, a_inner, a_outer, a_inner, 64, A_MN ? BK : BM))) return st;
@@ -835,16 +934,27 @@ static int run(const void* a, uint64_t a_inner, uint64_t a_outer, const void* b,
       if ((st = make_tmap(&tc, p.out, p.N, (uint64_t)p.num_experts * p.M, p.ldo, 64, 32)))
         return st;
       if (pair)
-        return launch_cg<A_MN, B_MN, true, EPI, 2, true>(ta, tb, tc, p, (units_m / 2) * nb,
+        return launch_cg<A_MN, B_MN, true, EPI, 2, true>(ta, tb, tc, tc, p, (units_m / 2) * nb,
                                                          stream);
-      return launch_cg<A_MN, B_MN, true, EPI, 1, true>(ta, tb, tc, p, units_m * nb, stream);
+      return launch_cg<A_MN, B_MN, true, EPI, 1, true>(ta, tb, tc, tc, p, units_m * nb, stream);
     }
   }
   tc = tb;  // unused by the other variants
+  td = tb;
+  if constexpr (EPI == EPI_DSWIGLU && MOE_DSWIGLU_TMA) {
+    // d_preact (store) and preact (load): [rows, 2m] bf16, 32 x 32 boxes, SWIZZLE_64B
+    const uint64_t rows = (uint64_t)p.max_m_blocks * BM;
+    if ((st = make_tmap(&tc, p.out, p.ldo, rows, p.ldo, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)))
+      return st;
+    if ((st = make_tmap(&td, p.aux, p.ld_aux, rows, p.ld_aux, 32, 32,
+                        CU_TENSOR_MAP_SWIZZLE_64B)))
+      return st;
+  }
   if (pair)
-    return launch_cg<A_MN, B_MN, GROUPED_K, EPI, 2, false>(ta, tb, tc, p, (units_m / 2) * nb,
-                                                           stream);
-  return launch_cg<A_MN, B_MN, GROUPED_K, EPI, 1, false>(ta, tb, tc, p, units_m * nb, stream);
+    return launch_cg<A_MN, B_MN, GROUPED_K, EPI, 2, false>(ta, tb, tc, td, p,
+                                                           (units_m / 2) * nb, stream);
+  return launch_cg<A_MN, B_MN, GROUPED_K, EPI, 1, false>(ta, tb, tc, td, p, units_m * nb,
+                                                         stream);
 }
 
 }  // namespace gg
