@@ -62,6 +62,13 @@ constexpr int DSW_HALVES = MOE_DSWIGLU_WARPS / 4;  // dprob partials per (row, n
 #endif
 constexpr int DSW_BOX = 32 * 32 * 2;                          // 32 rows x 32 bf16 columns
 constexpr int DSW_STAGING = MOE_DSWIGLU_WARPS * 2 * 2 * DSW_BOX;  // warps x 2 bufs x (g, u)
+// SwiGLU forward epilogue (fc1): gate / up pre-activation and act leave by TMA tensor stores
+// of SWIZZLE_64B boxes (one (g, u, act) box set per epilogue warp) instead of 16-byte
+// per-thread stores spread over 32 rows.
+#ifndef MOE_SWIGLU_TMA
+#define MOE_SWIGLU_TMA 1
+#endif
+constexpr int SWG_STAGING = EPI_WARPS * 4 * DSW_BOX;  // per-warp stride of the dSwiGLU boxes
 // Weight-gradient (grouped-K) kernels use 8 epilogue warps: with few token rows per expert
 // (DeepSeek-shape EP=1: 128) each output tile has almost no MMA work and the kernel is a
 // TMEM -> HBM drain, which 4 warps cannot keep busy.
@@ -99,7 +106,9 @@ constexpr int smem_bytes() {
   // SK / dSwiGLU staging starts 1024-aligned after the barrier block (swizzled TMA boxes)
   return Cfg<CG, SK>::SMEM +
          (EPI == 0 ? (SK ? 768 + SK_STAGING : SCATTER_BYTES)
-                   : (EPI == 2 && MOE_DSWIGLU_TMA ? 768 + DSW_STAGING : 0));
+          : EPI == 2 ? (MOE_DSWIGLU_TMA ? 768 + DSW_STAGING : 0)
+          : EPI == 1 ? (MOE_SWIGLU_TMA ? 768 + SWG_STAGING : 0)
+                     : 0);
 }
 
 
@@ -326,6 +335,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
   // dSwiGLU operand boxes: 2 mbarriers per epilogue warp at +192 of the barrier block
   uint64_t* dsw_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE + 192);
   constexpr bool DSW_TMA = EPI == EPI_DSWIGLU && MOE_DSWIGLU_TMA;
+  constexpr bool SWG_TMA = EPI == EPI_SWIGLU && MOE_SWIGLU_TMA;
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -343,9 +353,11 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
       mbar_init(&tfull_bar[s], 1);
       mbar_init(&tempty_bar[s], epi_warps<GROUPED_K, EPI>() * CG);
     }
-    if constexpr (DSW_TMA) {
+    if constexpr (DSW_TMA || SWG_TMA) {
       tma_prefetch_desc(&tmap_c);
       tma_prefetch_desc(&tmap_d);
+    }
+    if constexpr (DSW_TMA) {
       for (int i = 0; i < 2 * epi_warps<GROUPED_K, EPI>(); ++i) mbar_init(&dsw_bar[i], 1);
     }
     fence_mbar_init();
@@ -642,6 +654,52 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
                      p.stream_stores);
           }
         }
+      } else if constexpr (SWG_TMA) {
+        // Tile columns [0,128) = gate rows, [128,256) = up rows of the interleaved W1; 32
+        // gate columns and the matching up columns per chunk -> (g, u, act) boxes.
+        const float scale = p.row_scale ? __ldg(p.row_scale + row) : 1.0f;
+        const int sw = (lane >> 1) & 3;  // SWIZZLE_64B
+        uint8_t* box = dsw_buf;          // this warp's 3 boxes: g, u, act
+        uint8_t* grow = box + lane * 64;
+#pragma unroll 1
+        for (int c = 0; c < EC / 64; ++c) {
+          uint32_t g[32], u[32];
+          tmem_ld_32x32b_x32(t_base + (cb >> 1) + c * 32, g);
+          tmem_ld_32x32b_x32(t_base + 128 + (cb >> 1) + c * 32, u);
+          if (lane == 0) bulk_wait_read_0();  // the previous chunk's stores have read the boxes
+          __syncwarp();
+          tmem_ld_wait();
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            int4 wg, wu, wa;
+            uint32_t* pg = reinterpret_cast<uint32_t*>(&wg);
+            uint32_t* pu = reinterpret_cast<uint32_t*>(&wu);
+            uint32_t* pa = reinterpret_cast<uint32_t*>(&wa);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int i = 8 * v + 2 * j;
+              const float g0 = __uint_as_float(g[i]), g1 = __uint_as_float(g[i + 1]);
+              const float u0 = __uint_as_float(u[i]), u1 = __uint_as_float(u[i + 1]);
+              pg[j] = pack_bf16x2(g0, g1);
+              pu[j] = pack_bf16x2(u0, u1);
+              pa[j] = pack_bf16x2(silu_f(g0) * u0 * scale, silu_f(g1) * u1 * scale);
+            }
+            const int off = (v ^ sw) << 4;
+            *reinterpret_cast<int4*>(grow + off) = wg;
+            *reinterpret_cast<int4*>(grow + DSW_BOX + off) = wu;
+            *reinterpret_cast<int4*>(grow + 2 * DSW_BOX + off) = wa;
+          }
+          fence_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            const int x = tl.n0 + (cb >> 1) + c * 32;
+            const int y = tl.m0 + q * 32;
+            tma_store_2d(&tmap_c, box, x, y);
+            tma_store_2d(&tmap_c, box + DSW_BOX, x + 128, y);
+            tma_store_2d(&tmap_d, box + 2 * DSW_BOX, (tl.n0 >> 1) + (cb >> 1) + c * 32, y);
+            bulk_commit();
+          }
+        }
       } else if constexpr (EPI == EPI_SWIGLU) {
         // Tile columns [0,128) = gate rows, [128,256) = up rows of the interleaved W1; this
         // warp takes gate columns [half*64, +64) and the matching up columns.
@@ -798,7 +856,8 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
 
   // scattered rows may be in peer memory: complete the bulk stores and make them visible
   // system-wide before the stream-ordered collective that publishes them
-  if ((DSW_TMA || (EPI == EPI_BF16 && ((!GROUPED_K && p.row_dst) || (GROUPED_K && SK)))) &&
+  if ((DSW_TMA || SWG_TMA ||
+       (EPI == EPI_BF16 && ((!GROUPED_K && p.row_dst) || (GROUPED_K && SK)))) &&
       warp >= 2) {
     bulk_wait_all();
     __threadfence_system();
@@ -941,6 +1000,14 @@ static int run(const void* a, uint64_t a_inner, uint64_t a_outer, const void* b,
   }
   tc = tb;  // unused by the other variants
   td = tb;
+  if constexpr (EPI == EPI_SWIGLU && MOE_SWIGLU_TMA) {
+    // preact [rows, 2m] and act [rows, m] bf16 (stores), 32 x 32 boxes, SWIZZLE_64B
+    const uint64_t rows = (uint64_t)p.max_m_blocks * BM;
+    if ((st = make_tmap(&tc, p.out, p.ldo, rows, p.ldo, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)))
+      return st;
+    if ((st = make_tmap(&td, p.out2, p.ldo2, rows, p.ldo2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)))
+      return st;
+  }
   if constexpr (EPI == EPI_DSWIGLU && MOE_DSWIGLU_TMA) {
     // d_preact (store) and preact (load): [rows, 2m] bf16, 32 x 32 boxes, SWIZZLE_64B
     const uint64_t rows = (uint64_t)p.max_m_blocks * BM;
