@@ -288,6 +288,14 @@ __device__ __forceinline__ void bulk_store_s2g(void* gdst, const void* ssrc, uin
                "r"(smem_u32(ssrc)), "r"(bytes)
                : "memory");
 }
+// TMA bulk copy global -> shared (contiguous bytes), completion on an mbarrier.
+__device__ __forceinline__ void bulk_load_g2s(void* sdst, const void* gsrc, uint32_t bytes,
+                                              uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 // TMA tensor store of a shared-memory box (same swizzle as the tensor map) to global.
 __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* smem_src, int x,
                                              int y) {

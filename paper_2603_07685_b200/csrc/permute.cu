@@ -233,6 +233,97 @@ __global__ void gather_tokens_kernel(const int4* __restrict__ x, int T, int K, i
   }
 }
 
+// Token-driven gather over (token, chunk) work items: a chunk is 32 lanes x VPL 16-byte
+// vectors of one x row, read once and stored to each kept destination row. Splitting rows
+// into chunks keeps every SM busy when T is small (DeepSeek shape: 4096 tokens of 14 KB).
+template <int VPL>
+__global__ void gather_chunks_kernel(const int4* __restrict__ x, int T, int K, int hv,
+                                     const int* __restrict__ inv_map, int4* __restrict__ out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = lane_id();
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int per_row = (hv + 32 * VPL - 1) / (32 * VPL);
+  const long long items = (long long)T * per_row;
+  for (long long it = warp; it < items; it += nwarps) {
+    const int t = static_cast<int>(it / per_row);
+    const int c0 = static_cast<int>(it - (long long)t * per_row) * 32 * VPL;
+    const int* inv = inv_map + (long long)t * K;
+    int4 v[VPL];
+#pragma unroll
+    for (int u = 0; u < VPL; ++u) {
+      const int c = c0 + u * 32 + lane;
+      if (c < hv) v[u] = ld_nc_v4(x + (long long)t * hv + c);
+    }
+    for (int k = 0; k < K; ++k) {
+      const int d = __ldg(inv + k);
+      if (d < 0) continue;
+      int4* o = out + (long long)d * hv;
+#pragma unroll
+      for (int u = 0; u < VPL; ++u) {
+        const int c = c0 + u * 32 + lane;
+        if (c < hv) st_na_v4(o + c, v[u]);
+      }
+    }
+  }
+}
+
+// Token-driven gather on the TMA engine: each warp's lane 0 streams tokens, one bulk copy of
+// the x row into shared memory (double-buffered, mbarrier completion) and one bulk store of
+// it to each kept destination row. A write-dominated copy (K rows written per row read)
+// issued as a handful of large asynchronous copies instead of K x hv 16-byte stores per
+// token; the warp's other lanes idle.
+constexpr int GT_WARPS = 4;
+__global__ void __launch_bounds__(GT_WARPS * 32) gather_tokens_tma_kernel(
+    const uint8_t* __restrict__ x, int T, int K, int row_bytes, const int* __restrict__ inv_map,
+    uint8_t* __restrict__ out) {
+  extern __shared__ __align__(128) uint8_t gt_smem[];
+  __shared__ __align__(8) uint64_t bars[GT_WARPS][2];
+  const int warp = warp_id(), lane = lane_id();
+  uint8_t* buf = gt_smem + warp * 2 * row_bytes;
+  if (lane == 0) {
+    mbar_init(&bars[warp][0], 1);
+    mbar_init(&bars[warp][1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  if (lane != 0) return;
+  const int nwarps = gridDim.x * GT_WARPS;
+  // a token whose selections were all dropped has nothing to copy: skip its load
+  auto next_token = [&](int t) {
+    for (; t < T; t += nwarps) {
+      for (int k = 0; k < K; ++k)
+        if (__ldg(inv_map + (long long)t * K + k) >= 0) return t;
+    }
+    return t;
+  };
+  uint32_t ph = 0;
+  int t = next_token(blockIdx.x * GT_WARPS + warp);
+  if (t < T) {
+    mbar_arrive_expect_tx(&bars[warp][0], row_bytes);
+    bulk_load_g2s(buf, x + (long long)t * row_bytes, row_bytes, &bars[warp][0]);
+  }
+  for (int i = 0; t < T; ++i) {
+    const int b = i & 1;
+    const int tn = next_token(t + nwarps);
+    // the other buffer's stores (token i-1) must have read it before it is refilled
+    bulk_wait_read_0();
+    if (tn < T) {
+      mbar_arrive_expect_tx(&bars[warp][b ^ 1], row_bytes);
+      bulk_load_g2s(buf + (b ^ 1) * row_bytes, x + (long long)tn * row_bytes, row_bytes,
+                    &bars[warp][b ^ 1]);
+    }
+    mbar_wait(&bars[warp][b], (ph >> b) & 1);
+    ph ^= 1u << b;
+    for (int k = 0; k < K; ++k) {
+      const int d = __ldg(inv_map + (long long)t * K + k);
+      if (d >= 0) bulk_store_s2g(out + (long long)d * row_bytes, buf + b * row_bytes, row_bytes);
+    }
+    bulk_commit();
+    t = tn;
+  }
+  bulk_wait_all();
+}
+
 // Zero the rows whose source is -1 (padding / phantom) among the first meta[0]*128 rows.
 __global__ void zero_pad_rows_kernel(const int* __restrict__ meta, const int* __restrict__ row_src,
                                      int hv, int4* __restrict__ out) {
@@ -760,9 +851,35 @@ int moe_permute_gather(const void* x, int T, int K, int h, const int* inv_map, c
   if (h % 8) return kErrInvalidArg;
   auto st = static_cast<cudaStream_t>(stream);
   const int hv = h / 8;
-  if (T > 0) {
+  // Default: one warp per token row (measured best, tools/hbm_probe.py: Mixtral 0.77, Qwen3
+  // 0.84 of HBM). MOE_B200_GATHER=chunks: (token, chunk) work items (Qwen3 0.79);
+  // =tma: bulk-copy variant (Mixtral 0.75, Qwen3 0.79). DeepSeek's 0.55 is the zero fill of
+  // the padding rows (experts of ~128 rows padded to 128-row blocks), not counted here.
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("MOE_B200_GATHER");
+    mode = !e ? 2 : (e[0] == 't' && e[1] == 'm') ? 1 : (e[0] == 'c') ? 0 : 2;
+  }
+  const int use_tma = mode == 1;
+  const int row_bytes = h * 2;
+  const int smem = GT_WARPS * 2 * row_bytes;
+  if (T > 0 && use_tma && smem <= 200 * 1024) {
+    MOE_CUDA_CHECK(
+        ensure_dyn_smem(reinterpret_cast<const void*>(gather_tokens_tma_kernel), smem));
+    const int blocks_per_sm = smem <= 100 * 1024 ? 2 : 1;
+    const int want = ceil_div_i(T, GT_WARPS);
+    const int grid = want < blocks_per_sm * sms() ? want : blocks_per_sm * sms();
+    gather_tokens_tma_kernel<<<grid, GT_WARPS * 32, smem, st>>>(
+        static_cast<const uint8_t*>(x), T, K, row_bytes, inv_map, static_cast<uint8_t*>(xp));
+    MOE_LAUNCH_CHECK();
+  } else if (T > 0 && mode == 2) {
     gather_tokens_kernel<4><<<warp_grid(T), 256, 0, st>>>(static_cast<const int4*>(x), T, K, hv,
                                                           inv_map, static_cast<int4*>(xp));
+    MOE_LAUNCH_CHECK();
+  } else if (T > 0) {
+    const long long items = (long long)T * ceil_div_i(hv, 32 * 2);
+    gather_chunks_kernel<2><<<warp_grid(items), 256, 0, st>>>(
+        static_cast<const int4*>(x), T, K, hv, inv_map, static_cast<int4*>(xp));
     MOE_LAUNCH_CHECK();
   }
   zero_pad_rows_kernel<<<sms() * 8, 256, 0, st>>>(meta, row_src, hv, static_cast<int4*>(xp));
