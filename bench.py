@@ -439,7 +439,10 @@ def run_gpu(args, c) -> None:
     if rank == 0:
         clocks.lines.clear()
     _lib.stats.launches = 0
-    _lib.stats.timing = not args.graph
+    # per-launch CUDA events ride inside the timed region (the roofline's "achieved" is
+    # measured live); MOE_BENCH_KERNEL_EVENTS=0 moves them to an instrumented pass after it
+    live_events = os.environ.get("MOE_BENCH_KERNEL_EVENTS", "1") != "0"
+    _lib.stats.timing = live_events and not args.graph
     _lib.stats.events = []
     barrier()
     t_start = torch.cuda.Event(enable_timing=True)
@@ -453,7 +456,7 @@ def run_gpu(args, c) -> None:
     clocks.window(False)
     launches = _lib.stats.launches if graph_launches is None else graph_launches * args.steps
     ms_total = t_start.elapsed_time(t_end)
-    if args.graph:
+    if args.graph or not live_events:
         # per-kernel timings (roofline) from eager instrumented steps outside the timed region
         _lib.stats.timing = True
         for _ in range(args.steps):

@@ -173,3 +173,11 @@ def test_loopback_ep_unequal_tokens_rejected(sync_free, dev):
     finally:  # drop the poisoned pools: later check_ep_status() calls look at every pool
         for key in [k for k in D._POOLS if str(k[2]).startswith("unequal")]:
             del D._POOLS[key]
+
+
+@pytest.mark.parametrize("transport", ["p2p", "p2p_sync_free", "nccl"])
+@pytest.mark.parametrize("name", ["dropless_softmax", "capacity_pad", "top8"])
+def test_loopback_ep8(name, transport, dev):
+    """EP = 8, the whole EP group of a B200 box (one expert per rank at E = 8): the layout the
+    8-GPU scaling run uses, here as 8 loopback ranks on one GPU."""
+    _run(CASES[name], transport, dev, n=8)
