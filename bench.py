@@ -444,6 +444,7 @@ def run_gpu(args, c) -> None:
     live_events = os.environ.get("MOE_BENCH_KERNEL_EVENTS", "1") != "0"
     _lib.stats.timing = live_events and not args.graph
     _lib.stats.events = []
+    _lib.stats.prepare(64 * args.steps)  # event pairs created before the clock starts
     barrier()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
@@ -458,6 +459,7 @@ def run_gpu(args, c) -> None:
     ms_total = t_start.elapsed_time(t_end)
     if args.graph or not live_events:
         # per-kernel timings (roofline) from eager instrumented steps outside the timed region
+        _lib.stats.prepare(64 * args.steps)
         _lib.stats.timing = True
         for _ in range(args.steps):
             step(x, dy)

@@ -169,6 +169,13 @@ class _Stats:
     launches = 0
     timing = False
     events: list = []  # (name, start_event, end_event)
+    pool: list = []    # pre-created event pairs (prepare()): no event creation while timing
+
+    def prepare(self, n: int) -> None:
+        import torch
+
+        self.pool = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                     for _ in range(n)]
 
 
 stats = _Stats()
@@ -178,9 +185,12 @@ def call(name: str, *args) -> None:
     lib = load()
     fn = getattr(lib, name)
     if stats.timing:
-        import torch
+        if stats.pool:
+            s, e = stats.pool.pop()
+        else:
+            import torch
 
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         st = fn(*args)
         e.record()
