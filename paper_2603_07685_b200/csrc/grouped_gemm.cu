@@ -68,6 +68,11 @@ constexpr int DSW_STAGING = MOE_DSWIGLU_WARPS * 2 * 2 * DSW_BOX;  // warps x 2 b
 #ifndef MOE_SWIGLU_TMA
 #define MOE_SWIGLU_TMA 1
 #endif
+// epilogue TMA traffic (preact / act / d_preact / dW boxes: streamed once) with an L2
+// evict-first policy
+#ifndef MOE_EPI_EVICT_FIRST
+#define MOE_EPI_EVICT_FIRST 1
+#endif
 constexpr int SWG_STAGING = EPI_WARPS * 4 * DSW_BOX;  // per-warp stride of the dSwiGLU boxes
 // Weight-gradient (grouped-K) kernels use 8 epilogue warps: with few token rows per expert
 // (DeepSeek-shape EP=1: 128) each output tile has almost no MMA work and the kernel is a
@@ -519,6 +524,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
     // dSwiGLU boxes of this warp: buffer b holds gate at +0 and up at +DSW_BOX
     uint8_t* dsw_buf = smem + C::STAGES * C::STAGE + 1024 + (warp - 2) * (4 * DSW_BOX);
     uint64_t* dbar = dsw_bar + (warp - 2) * 2;
+    const uint64_t epi_pol = l2_evict_first_policy();
     uint32_t dsw_ph = 0;  // bit b: parity of buffer b's next completion
     int dsw_seq = 0;      // chunks consumed by this warp (buffer = dsw_seq & 1)
     auto dsw_load = [&](const Tile& tn, int c, int b) {
@@ -527,8 +533,13 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
       const int y = tn.m0 + q * 32;
       uint8_t* dst = dsw_buf + b * (2 * DSW_BOX);
       mbar_arrive_expect_tx(&dbar[b], 2 * DSW_BOX);
-      tma_load_2d(dst, &tmap_d, &dbar[b], gpos, y);
-      tma_load_2d(dst + DSW_BOX, &tmap_d, &dbar[b], gpos + 128, y);
+      if (MOE_EPI_EVICT_FIRST) {
+        tma_load_2d_hint(dst, &tmap_d, &dbar[b], gpos, y, epi_pol);
+        tma_load_2d_hint(dst + DSW_BOX, &tmap_d, &dbar[b], gpos + 128, y, epi_pol);
+      } else {
+        tma_load_2d(dst, &tmap_d, &dbar[b], gpos, y);
+        tma_load_2d(dst + DSW_BOX, &tmap_d, &dbar[b], gpos + 128, y);
+      }
     };
     if constexpr (DSW_TMA) {
       if (first < num_tiles && lane == 0) {
@@ -604,7 +615,11 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
           fence_async_shared();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmap_c, box, tl.n0 + col, tl.expert * p.M + tl.m0 + q * 32);
+            if (MOE_EPI_EVICT_FIRST)
+              tma_store_2d_hint(&tmap_c, box, tl.n0 + col, tl.expert * p.M + tl.m0 + q * 32,
+                                epi_pol);
+            else
+              tma_store_2d(&tmap_c, box, tl.n0 + col, tl.expert * p.M + tl.m0 + q * 32);
             bulk_commit();
           }
           ++sk_piece;
@@ -703,9 +718,16 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
           if (lane == 0) {
             const int x = tl.n0 + (cb >> 1) + c * 32;
             const int y = tl.m0 + q * 32;
-            tma_store_2d(&tmap_c, box, x, y);
-            tma_store_2d(&tmap_c, box + DSW_BOX, x + 128, y);
-            tma_store_2d(&tmap_d, box + 2 * DSW_BOX, (tl.n0 >> 1) + (cb >> 1) + c * 32, y);
+            if (MOE_EPI_EVICT_FIRST) {
+              tma_store_2d_hint(&tmap_c, box, x, y, epi_pol);
+              tma_store_2d_hint(&tmap_c, box + DSW_BOX, x + 128, y, epi_pol);
+              tma_store_2d_hint(&tmap_d, box + 2 * DSW_BOX, (tl.n0 >> 1) + (cb >> 1) + c * 32, y,
+                                epi_pol);
+            } else {
+              tma_store_2d(&tmap_c, box, x, y);
+              tma_store_2d(&tmap_c, box + DSW_BOX, x + 128, y);
+              tma_store_2d(&tmap_d, box + 2 * DSW_BOX, (tl.n0 >> 1) + (cb >> 1) + c * 32, y);
+            }
             bulk_commit();
           }
         }
@@ -790,8 +812,13 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
             const int gpos = (j0 >> 7) * 256 + (j0 & 127);
             const int y = tl.m0 + q * 32;
             uint8_t* box = dsw_buf + b * (2 * DSW_BOX);
-            tma_store_2d(&tmap_c, box, gpos, y);
-            tma_store_2d(&tmap_c, box + DSW_BOX, gpos + 128, y);
+            if (MOE_EPI_EVICT_FIRST) {
+              tma_store_2d_hint(&tmap_c, box, gpos, y, epi_pol);
+              tma_store_2d_hint(&tmap_c, box + DSW_BOX, gpos + 128, y, epi_pol);
+            } else {
+              tma_store_2d(&tmap_c, box, gpos, y);
+              tma_store_2d(&tmap_c, box + DSW_BOX, gpos + 128, y);
+            }
             bulk_commit();
           }
           ++dsw_seq;
