@@ -274,28 +274,57 @@ def gemm_traffic(config: str, n: int):
                       "one step of tools/layer_step.py)"}
 
 
-def hbm_kernels(c, per_kernel: dict, steps: int, hbm_gbs: float):
+def measure_write_gbs(nbytes: int = 1 << 31, iters: int = 10) -> float:
+    """HBM write-only bandwidth of this GPU (torch zero_ over 2 GiB, CUDA events, best of
+    `iters`): the bound of write-dominated kernels, which B200 serves well below the copy
+    rate (measured ~3.95 TB/s write-only vs ~6.5 TB/s copy, tools/hbm_probe.py)."""
+    import torch
+
+    buf = torch.empty((nbytes // 2,), dtype=torch.bfloat16, device="cuda")
+    buf.zero_()
+    best = None
+    for _ in range(iters):
+        s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+        s.record()
+        buf.zero_()
+        e.record()
+        e.synchronize()
+        ms = s.elapsed_time(e)
+        best = ms if best is None else min(best, ms)
+    del buf
+    return nbytes / (best / 1e3) / 1e9
+
+
+def hbm_kernels(c, per_kernel: dict, steps: int, hbm_gbs: float, write_gbs: float | None = None):
     """Event-timed bandwidth of the HBM-bound data-movement kernels (SURVEY §8(d) bytes):
     permute gather (x read, R rows written), combine (forward y and backward dX), combine
-    backward (dY + O rows read, dO rows written)."""
+    backward (dY + O rows read, dO rows written), and the small-N router (x read in the
+    forward and in dW_r). `frac_of_bound`: the kernel's time floor max(bytes / copy
+    bandwidth, written bytes / write-only bandwidth) over its measured time."""
     T, K, h = c["T"], c["K"], c["h"]
     R, w = T * K, 2
+    sh = T * h * w if c.get("shared") else 0
+    # (algorithmic bytes, of which written)
     alg = {
-        "moe_permute_gather": T * h * w + R * h * w + R * 4,
+        "moe_permute_gather": (T * h * w + R * h * w + R * 4, R * h * w),
         # forward: R rows + probs + map read, y written (+ the shared-expert output read);
         # backward dX: R rows + map + the router dX (+ shared-expert dX) read, dX written
-        "moe_combine": (R * h * w + R * 8 + T * h * w + (T * h * w if c.get("shared") else 0))
-                       + (R * h * w + R * 4 + T * h * w + (T * h * w if c.get("shared") else 0)
-                          + T * h * w),
-        "moe_combine_bwd": T * h * w + 2 * R * h * w + R * 12,
+        "moe_combine": ((R * h * w + R * 8 + T * h * w + sh)
+                        + (R * h * w + R * 4 + T * h * w + sh + T * h * w), 2 * T * h * w),
+        "moe_combine_bwd": (T * h * w + 2 * R * h * w + R * 12, R * h * w),
+        "moe_router_tc_fwd": (T * h * w + T * c["E"] * 4, T * c["E"] * 4),
+        "moe_router_tc_wgrad": (T * h * w, 0),
     }
     out = {}
-    for k, b in alg.items():
+    for k, (b, wb) in alg.items():
         if k in per_kernel:
             ms = sum(per_kernel[k]) / steps
             gbs = b / (ms / 1e3) / 1e9
+            floor_ms = max(b / hbm_gbs, wb / write_gbs if write_gbs else 0.0) / 1e6
             out[k] = {"ms_per_step": round(ms, 4), "algorithmic_MB": round(b / 1e6, 1),
-                      "achieved_GBps": round(gbs, 1), "frac_of_measured_hbm": round(gbs / hbm_gbs, 3)}
+                      "written_MB": round(wb / 1e6, 1),
+                      "achieved_GBps": round(gbs, 1), "frac_of_measured_hbm": round(gbs / hbm_gbs, 3),
+                      "frac_of_bound": round(floor_ms / ms, 3)}
     return out
 
 
@@ -652,7 +681,11 @@ def run_gpu(args, c) -> None:
         burst_tf = peaks.get("bf16_tflops", 1590.0)
         hbm_gbs = peaks.get("hbm_gbs", 6650.0)
         traffic = gemm_traffic(args.config, n)
-        hbm = hbm_kernels(c, per_kernel, args.steps, hbm_gbs)
+        write_gbs = measure_write_gbs()
+        hbm = hbm_kernels(c, per_kernel, args.steps, hbm_gbs, write_gbs)
+        hbm["_peaks"] = {"copy_GBps": hbm_gbs, "write_only_GBps": round(write_gbs, 1),
+                         "copy_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
+                         "write_source": "measured in this run (torch zero_ over 2 GiB)"}
         gemm_tflops = gemm_flops_step * args.steps / (gemm_ms / 1e3) / 1e12 if gemm_ms else None
         gemm_launches = sum(len(v) for k_, v in per_kernel.items() if k_.startswith("moe_gg_"))
         out = {

@@ -69,6 +69,29 @@ int moe_router_finalize(const int* counts, const float* score_partials, int T, i
 int moe_router_bwd(const float* logits, int ld, int T, int E, int K, int score_fn,
                    const int* topk_idx, const float* dprob, const float* aux_grad,
                    void* dlogits, int ldd, void* stream);
+/* Small-N tensor-core router (the default path; csrc/router_tc.cu). replaces route()
+ * routing.py:71-108 + aux_loss() :111-120 in one tcgen05 GEMM whose epilogue scores, selects
+ * and counts (thread per token, logits read from TMEM) + the finalize: x[T,h] bf16,
+ * w_t[moe_router_tc_npad(E), h] bf16 = W_r^T zero-padded; logits out compact [T, E] fp32;
+ * ws: moe_router_tc_fwd_ws(T, h, E) floats (score partials first). K <= 8. */
+int moe_router_tc_npad(int E);
+long long moe_router_tc_fwd_ws(int T, int h, int E);
+int moe_router_tc_fwd(const void* x, int T, int h, const void* w_t, int E, int K, int score_fn,
+                      const float* sel_bias, float coeff, float* logits, int* topk_idx,
+                      float* topk_prob, float* scores_out, int* counts, float* ws, int* status,
+                      float* aux_out, float* aux_grad, float* mean_scores, void* stream);
+int moe_router_finalize_p(const int* counts, const float* score_partials, int P, int T, int K,
+                          int E, float coeff, float* aux_out, float* aux_grad,
+                          float* mean_scores, void* stream);
+/* Its backward: dl row-major bf16 [T, ldd] (dX GEMM operand) and/or dl^T bf16 [npad, ldt]
+ * (moe_router_bwd semantics), and dW_r[h, E] fp32 = x^T dl on a small-N tcgen05 tile with a
+ * fixed-order split-K sum (ws: moe_router_tc_wgrad_ws floats; h % 128 == 0). */
+int moe_router_bwd2(const float* logits, int ld, int T, int E, int K, int score_fn,
+                    const int* topk_idx, const float* dprob, const float* aux_grad,
+                    void* dlogits, int ldd, void* dlt, int ldt, int npad, void* stream);
+long long moe_router_tc_wgrad_ws(int T, int h, int E);
+int moe_router_tc_wgrad(const void* x, int T, int h, const void* dlt, int ldt, int E, float* ws,
+                        float* dw, void* stream);
 /* W_r [h,E] bf16 -> W_r^T zero-padded [Epad,h] and/or W_r zero-padded [h,Epad] */
 int moe_stage_router_weight(const void* w, int h, int E, int Epad, void* wt_pad, void* w_pad,
                             void* stream);

@@ -38,6 +38,11 @@ SIGNATURES: dict[str, list] = {
     "moe_stage_router_weight": [P, I, I, I, P, P, P],
     "moe_reduce_groups_f32": [P, I, I, I, I, P, P],
     "moe_router_fused": [P, I, I, P, I, I, I, P, P, P, P, P, P, P, P, P],
+    # small-N tensor-core router (csrc/router_tc.cu)
+    "moe_router_tc_fwd": [P, I, I, P, I, I, I, P, F, P, P, P, P, P, P, P, P, P, P, P],
+    "moe_router_finalize_p": [P, P, I, I, I, I, F, P, P, P, P],
+    "moe_router_bwd2": [P, I, I, I, I, I, P, P, P, P, I, P, I, I, P],
+    "moe_router_tc_wgrad": [P, I, I, P, I, I, P, P, P],
     "moe_router_bwd_f32": [P, I, I, I, I, I, P, P, P, P, P],
     "moe_router_wgrad_small": [P, I, I, P, I, P, P, P],
     "moe_router_dx_small": [P, I, I, P, I, P, P],
@@ -103,6 +108,9 @@ QUERIES: dict[str, tuple] = {
     "moe_router_num_partials": ([I], c_int),
     "moe_router_small_ok": ([I, I], c_int),
     "moe_router_wgrad_small_ws": ([I, I, I], c_int64),
+    "moe_router_tc_npad": ([I], c_int),
+    "moe_router_tc_fwd_ws": ([I, I, I], c_int64),
+    "moe_router_tc_wgrad_ws": ([I, I, I], c_int64),
     "moe_permute_workspace_ints": ([I, I, I], c_int64),
     "moe_gg_dprob_partials": ([I], c_int),
 }
@@ -160,7 +168,8 @@ def check(status: int, what: str) -> None:
 # kernels of ours launched by one call of each entry point (cudaMemsetAsync not counted)
 KERNELS_PER_CALL = {name: 1 for name in SIGNATURES}
 KERNELS_PER_CALL.update({"moe_permute_plan": 5, "moe_permute_gather": 2, "moe_ep_prepare": 0,
-                         "moe_router_wgrad_small": 2})
+                         "moe_router_wgrad_small": 2, "moe_router_tc_fwd": 2,
+                         "moe_router_tc_wgrad": 2})
 
 
 class _Stats:

@@ -77,6 +77,25 @@ inline cudaError_t ensure_dyn_smem(const void* kern, int bytes) {
   return e;
 }
 
+// Wave-sync slots for the persistent GEMMs (see wave_sync below): one slot per (device,
+// stream), so GEMMs running concurrently on different streams never share a counter. Slot
+// s is g_wave_sync[s * 32 ..]: [0] arrivals, [1] exits, [2] disabled (a wait timed out).
+constexpr int kWaveSyncSlots = 64;
+inline int wave_sync_slot(cudaStream_t stream) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, int> slots;
+  static std::map<int, int> next;
+  int d = 0;
+  cudaGetDevice(&d);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = slots.find({d, stream});
+  if (it != slots.end()) return it->second;
+  int& n = next[d];
+  if (n >= kWaveSyncSlots) return -1;  // out of slots: this stream runs unsynchronised
+  slots[{d, stream}] = n;
+  return n++;
+}
+
 __host__ __device__ __forceinline__ int ceil_div_i(int a, int b) { return (a + b - 1) / b; }
 __host__ __device__ __forceinline__ long long ceil_div_ll(long long a, long long b) {
   return (a + b - 1) / b;
@@ -169,6 +188,20 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// try_wait with a suspend-time hint: the thread sleeps in the barrier unit (up to the hint)
+// instead of spinning, so a long wait issues no instructions.
+__device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
   }
 }
 
@@ -281,6 +314,45 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+// ---- wave sync of persistent-GEMM producers
+// The persistent GEMMs stride over tiles (CTA pair c takes tiles c, c + S, c + 2S, ...).
+// Tiles that share an operand strip only hit in L2 when they load it at about the same time;
+// without a sync the pairs drift apart by whole tiles over a launch and every tile streams
+// its strips from DRAM (ncu: Mixtral fc1 dgrad 26.7 GB for 4.0 GB algorithmic). Each TMA
+// producer arrives at a grid-wide counter at its sync points and waits (bounded) until every
+// CTA has reached the same point. Only the loads wait: the MMA keeps draining the staged
+// k-blocks, so a wait shorter than the ring costs nothing. Results never depend on it: a wait
+// that exceeds `timeout_ns` (CTAs not co-resident, a concurrent kernel) disables the sync for
+// the rest of the launch.
+__device__ __forceinline__ uint32_t ld_relaxed_gpu_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wave_sync(uint32_t* ctr, uint32_t target, uint64_t timeout_ns) {
+  atomicAdd(ctr, 1u);
+  if (target == 0 || ld_relaxed_gpu_u32(ctr + 2)) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (static_cast<int>(ld_relaxed_gpu_u32(ctr) - target) < 0) {
+    if (globaltimer_ns() - t0 > timeout_ns) {
+      atomicExch(ctr + 2, 1u);
+      return;
+    }
+    if (ld_relaxed_gpu_u32(ctr + 2)) return;
+    __nanosleep(256);
+  }
+}
+// Called once per CTA after its last sync point: the last CTA out resets the slot for the
+// next launch on the stream (kernel boundaries order the reset before that launch).
+__device__ __forceinline__ void wave_sync_exit(uint32_t* ctr) {
+  __threadfence();
+  if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+    ctr[0] = 0;
+    ctr[2] = 0;
+    ctr[1] = 0;
+    __threadfence();
+  }
 }
 // TMA bulk store shared -> global (any generic global address, including peer memory)
 __device__ __forceinline__ void bulk_store_s2g(void* gdst, const void* ssrc, uint32_t bytes) {

@@ -159,7 +159,16 @@ struct Params {
   int band_m;  // raster band: M units that sweep each n-block together (L2 reuse)
   int bulk_out;  // grouped-K EPI_BF16: the SK variant (TMA tensor stores of staged boxes)
   int gk_mu_fast;  // grouped-K raster: M units fastest (when M < N), else n-blocks fastest
+  // wave sync of the TMA producers (common.cuh wave_sync): off when sync_on == 0; sync points
+  // at every tile start and, grouped-M only, every sync_kb k-blocks inside a tile (0 = none)
+  int sync_on;
+  int sync_slot;
+  int sync_kb;
+  int sync_lag;  // a producer at sync point g waits for every CTA to reach g - sync_lag
 };
+
+// per-(device, stream) wave-sync counters (common.cuh wave_sync_slot)
+__device__ uint32_t g_wave_sync[kWaveSyncSlots * 32];
 
 __device__ __forceinline__ void st_out(int4* p, int4 v, int cs) {
   if (cs)
@@ -414,13 +423,36 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
       int s = 0;
       uint32_t ph = 0;
       const uint32_t epoch = p.src_flag ? *reinterpret_cast<const volatile uint32_t*>(p.epoch) : 0u;
-      for (int t = first; t < num_tiles; t += stride) {
+      // wave sync: sync point (it, q) = phase q of this CTA's it-th tile, linear index
+      // g = it * Q + q. Every CTA with a tile at iteration it arrives Q times there, so the
+      // arrivals through g are CG * (it * S * Q + (q + 1) * P_it), P_it = CTA slots busy at
+      // iteration it. A producer at g waits for the arrivals through g - lag (lag 0: a full
+      // barrier; lag 1: nobody runs more than one phase ahead of the slowest CTA).
+      uint32_t* wctr = p.sync_on ? g_wave_sync + p.sync_slot * 32 : nullptr;
+      const int skb = GROUPED_K ? 0 : p.sync_kb;
+      int it = 0;
+      auto wsync = [&](int q, int num_kb) {
+        const int nq = skb > 0 ? (num_kb + skb - 1) / skb : 1;
+        const int g = it * nq + q - p.sync_lag;
+        uint32_t target = 0;
+        if (g >= 0) {
+          const int it2 = g / nq, q2 = g - (g / nq) * nq;
+          const int busy = min(stride, num_tiles - it2 * stride);
+          target = static_cast<uint32_t>(CG * (it2 * stride * nq + (q2 + 1) * busy));
+        }
+        wave_sync(wctr, target, 100000ull);
+      };
+      for (int t = first; t < num_tiles; t += stride, ++it) {
         Tile tl;
         decode_tile<GROUPED_K, CG>(p, t, num_units, rank, tl);
+        if (wctr) wsync(0, tl.num_kb);
         if constexpr (!GROUPED_K) {
           if (p.src_flag) wait_sources(p, __ldg(p.block_need + tl.m0 / BM), tl.m0 / BM, epoch);
         }
         for (int kb = 0; kb < tl.num_kb; ++kb) {
+          if constexpr (!GROUPED_K) {
+            if (wctr && skb > 0 && kb > 0 && kb % skb == 0) wsync(kb / skb, tl.num_kb);
+          }
           mbar_wait(&empty_bar[s], ph ^ 1);
           if (leader) mbar_arrive_expect_tx(&full_bar[s], C::STAGE * CG);
           uint8_t* sa = smem_a + s * C::A_STAGE;
@@ -453,6 +485,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
           }
         }
       }
+      if (wctr) wave_sync_exit(wctr);
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (single thread of the leader CTA) =================
@@ -1026,6 +1059,33 @@ static int run(const void* a, uint64_t a_inner, uint64_t a_outer, const void* b,
       gr = e ? (e[0] == 'm' ? 1 : 0) : -1;
     }
     p.gk_mu_fast = GROUPED_K ? (gr >= 0 ? gr : (p.M < p.N ? 1 : 0)) : 0;
+  }
+  {
+    // wave sync of the producers (common.cuh wave_sync). MOE_B200_WAVE_SYNC=0 turns it off;
+    // MOE_B200_SYNC_KB sets the in-tile sync period (k-blocks, grouped-M; 0 = tile starts only)
+    static int on = -1, kb = -1, lag = 0, min_kb = 0;
+    if (on < 0) {
+      const char* e = getenv("MOE_B200_WAVE_SYNC");
+      on = (e && e[0] == '0') ? 0 : 1;
+      const char* k = getenv("MOE_B200_SYNC_KB");
+      kb = k ? atoi(k) : 32;
+      if (kb < 0) kb = 0;
+      const char* l = getenv("MOE_B200_SYNC_LAG");
+      lag = l ? atoi(l) : 1;
+      if (lag < 0) lag = 0;
+      const char* m = getenv("MOE_B200_SYNC_MIN_KB");
+      min_kb = m ? atoi(m) : 256;
+    }
+    // Measured on B200 (profiles/r02_wave_sync.txt): the sync cuts DRAM reads (Mixtral fc1
+    // dgrad 15.5 -> 10.3 GB, dW1 5.0 -> 2.6 GB) and raises the power-capped clock, but its
+    // waits cost more than that wins except on very long K (Mixtral fc1 dgrad, K = 28672:
+    // 6.05 -> 5.88 ms with 32-k-block phases, lag 1). Default: grouped-M only, K >= 256
+    // k-blocks. Grouped-K (weight gradients) measured slower with it at every setting.
+    const bool want = on && !GROUPED_K && p.K / BK >= min_kb;
+    p.sync_slot = want ? wave_sync_slot(stream) : -1;
+    p.sync_on = p.sync_slot >= 0 ? 1 : 0;
+    p.sync_kb = kb;
+    p.sync_lag = lag;
   }
   CUtensorMap ta, tb, tc, td;
   int st;

@@ -355,7 +355,8 @@ template <int EPL, typename OutT>
 __global__ void __launch_bounds__(WARPS * 32) bwd_kernel(
     const float* __restrict__ logits, int ld, int T, int E, int K, int score_fn,
     const int* __restrict__ topk_idx, const float* __restrict__ dprob,
-    const float* __restrict__ aux_grad, OutT* __restrict__ dlogits, int ldd) {
+    const float* __restrict__ aux_grad, OutT* __restrict__ dlogits, int ldd,
+    __nv_bfloat16* __restrict__ dlt = nullptr, int ldt = 0, int npad = 0) {
   const int warp = warp_id(), lane = lane_id();
   const int stride = gridDim.x * WARPS;
   for (int t = blockIdx.x * WARPS + warp; t < T; t += stride) {
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(WARPS * 32) bwd_kernel(
       inner += ds[j] * s[j];
     }
     inner = warp_sum(inner);
-    OutT* out = dlogits + (long long)t * ldd;
+    OutT* out = dlogits ? dlogits + (long long)t * ldd : nullptr;
 #pragma unroll
     for (int j = 0; j < EPL; ++j) {
       const int e = j * 32 + lane;
@@ -416,9 +417,14 @@ __global__ void __launch_bounds__(WARPS * 32) bwd_kernel(
         dl = s[j] * (ds[j] - inner);
       else
         dl = sig[j] * (1.0f - sig[j]) * inv * (ds[j] - inner);
-      if (e < E) out[e] = static_cast<OutT>(dl);
+      if (e < E && out) out[e] = static_cast<OutT>(dl);
+      // transposed copy dl^T [npad, ldt] (B operand of the small-N router weight gradient)
+      if (e < E && dlt) dlt[(long long)e * ldt + t] = __float2bfloat16_rn(dl);
     }
-    for (int e = E + lane; e < ldd; e += 32) out[e] = static_cast<OutT>(0.f);
+    if (out)
+      for (int e = E + lane; e < ldd; e += 32) out[e] = static_cast<OutT>(0.f);
+    if (dlt)
+      for (int e = E + lane; e < npad; e += 32) dlt[(long long)e * ldt + t] = __float2bfloat16_rn(0.f);
   }
 }
 
@@ -600,6 +606,46 @@ int moe_router_finalize(const int* counts, const float* score_partials, int T, i
   const int P = moe_router_num_partials(T);
   finalize_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(
       counts, score_partials, T == 0 ? 0 : P, T, K, E, coeff, aux_out, aux_grad, mean_scores);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+// moe_router_finalize over P explicit score-partial rows (the small-N tensor-core router
+// writes one row per 128-token tile).
+int moe_router_finalize_p(const int* counts, const float* score_partials, int P, int T, int K,
+                          int E, float coeff, float* aux_out, float* aux_grad,
+                          float* mean_scores, void* stream) {
+  if (E < 1 || E > 256) return kErrInvalidArg;
+  finalize_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(
+      counts, score_partials, T == 0 ? 0 : P, T, K, E, coeff, aux_out, aux_grad, mean_scores);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+// Router backward for the small-N tensor-core router: dl written row-major bf16 [T, ldd]
+// (zero beyond E; the dX GEMM's A operand, ldd a multiple of 64) and/or transposed bf16
+// dlt[npad, ldt] (rows >= E zero; the weight-gradient B operand). Either may be NULL.
+int moe_router_bwd2(const float* logits, int ld, int T, int E, int K, int score_fn,
+                    const int* topk_idx, const float* dprob, const float* aux_grad,
+                    void* dlogits, int ldd, void* dlt, int ldt, int npad, void* stream) {
+  if (E < 1 || E > 256 || K > 32 || (dlogits && ldd < E) || (dlt && (ldt < T || npad < E)))
+    return kErrInvalidArg;
+  if (T == 0) return kOk;
+  const int blocks = moe_router_num_partials(T);
+  auto st = static_cast<cudaStream_t>(stream);
+  auto out = static_cast<__nv_bfloat16*>(dlogits);
+  auto ot = static_cast<__nv_bfloat16*>(dlt);
+  const int epl = E <= 32 ? 1 : E <= 64 ? 2 : E <= 128 ? 4 : 8;
+#define LAUNCH_BWD2(N)                                                                       \
+  bwd_kernel<N, __nv_bfloat16><<<blocks, WARPS * 32, 0, st>>>(                               \
+      logits, ld, T, E, K, score_fn, topk_idx, dprob, aux_grad, out, ldd, ot, ldt, npad)
+  switch (epl) {
+    case 1: LAUNCH_BWD2(1); break;
+    case 2: LAUNCH_BWD2(2); break;
+    case 4: LAUNCH_BWD2(4); break;
+    default: LAUNCH_BWD2(8); break;
+  }
+#undef LAUNCH_BWD2
   MOE_LAUNCH_CHECK();
   return kOk;
 }

@@ -45,6 +45,8 @@ class RouterOut:
     status: torch.Tensor       # [1] int32, bit0 = non-finite logits
     scores: torch.Tensor | None = None  # [T, E] fp32 when requested
     w_r: torch.Tensor | None = None     # [h, E] bf16: set on the small-E path (backward operand)
+    w_pad: torch.Tensor | None = None   # [1, h, KPAD] bf16: set on the tensor-core (tc) path
+    path: str = "gemm"                  # "tc" (default), "gemm" (256-padded), "small"
 
 
 # Small-E CUDA-core router (moe_router_fused + CUDA-core backward) instead of the tcgen05
@@ -62,11 +64,71 @@ def router_small(num_experts: int, hidden: int) -> bool:
     return ROUTER_SMALL and bool(_lib.query("moe_router_small_ok", num_experts, hidden))
 
 
-def stage_router(w_r: torch.Tensor):
-    """Per-forward router-weight operands: (W_r^T padded, W_r padded) for the tcgen05 path,
-    (None, None) on the small-E path (which reads W_r [h, E] as is)."""
+# Small-N tensor-core router (csrc/router_tc.cu): the logits GEMM with N = E padded to 16
+# and route() fused into its epilogue, and the weight gradient on the same small-N tile. The
+# default for K <= 8 and h % 128 == 0; MOE_ROUTER_TC=0 selects the round-1 chain (logits
+# GEMM padded to 256 columns + warp-per-token top-k) for A/B measurements.
+ROUTER_TC = os.environ.get("MOE_ROUTER_TC", "1") != "0"
+
+
+def router_tc(num_experts: int, hidden: int, top_k: int) -> bool:
+    return (ROUTER_TC and 1 <= num_experts <= 256 and 1 <= top_k <= min(8, num_experts)
+            and hidden >= 128 and hidden % 128 == 0)
+
+
+_TC_STAGE: dict = {}
+
+
+def tc_kpad(e: int) -> int:
+    """Router dX GEMM K (= the row stride of the row-major dlogits): E rounded up to 64 when the
+    weight gradient runs on the small-N tile (E <= 32), else to 256 (the grouped-K split GEMM
+    the larger-E backward uses needs N % 256 == 0)."""
+    return ceil_to(e, 64) if e <= 32 else ceil_to(e, ROUTER_NPAD)
+
+
+def stage_router_tc(w_r: torch.Tensor):
+    """W_r [h, E] -> (W_r^T [1, NPAD, h], W_r [1, h, KPAD]) zero-padded bf16 for the small-N
+    router (NPAD = moe_router_tc_npad(E), KPAD = E rounded up to 64: the dX GEMM's K).
+
+    Cached on the tensor object and its version counter (an in-place optimizer update bumps
+    it), so repeated forwards with unchanged weights stage nothing; never cached while a CUDA
+    graph is being captured (a replay must re-stage weights updated in place)."""
     h, e = w_r.shape
-    if router_small(e, h):
+    capturing = torch.cuda.is_current_stream_capturing()
+    key = id(w_r)
+    if not capturing:
+        hit = _TC_STAGE.get(key)
+        if (hit is not None and hit[0]() is w_r and hit[1] == w_r._version
+                and hit[2] == w_r.data_ptr()):
+            return hit[3], hit[4]
+    npad = int(_lib.query("moe_router_tc_npad", e))
+    kpad = tc_kpad(e)
+    w_r = w_r.contiguous() if w_r.dtype == torch.bfloat16 else w_r.to(torch.bfloat16)
+    wt = torch.empty((1, npad, h), dtype=torch.bfloat16, device=w_r.device)
+    wp = torch.empty((1, h, kpad), dtype=torch.bfloat16, device=w_r.device)
+    _lib.call("moe_stage_router_weight", w_r.data_ptr(), h, e, npad, wt.data_ptr(), None,
+              _stream())
+    _lib.call("moe_stage_router_weight", w_r.data_ptr(), h, e, kpad, None, wp.data_ptr(),
+              _stream())
+    if not capturing:
+        import weakref
+
+        try:
+            ref = weakref.ref(w_r)
+        except TypeError:
+            return wt, wp
+        if len(_TC_STAGE) > 16:
+            _TC_STAGE.clear()
+        _TC_STAGE[key] = (ref, w_r._version, w_r.data_ptr(), wt, wp)
+    return wt, wp
+
+
+def stage_router(w_r: torch.Tensor):
+    """Per-forward router-weight operands of the round-1 tcgen05 chain: (W_r^T padded,
+    W_r padded); (None, None) on the small-E and the small-N tensor-core paths (which stage
+    their own operands inside router_forward)."""
+    h, e = w_r.shape
+    if router_small(e, h) or (ROUTER_TC and 1 <= e <= 256 and h % 128 == 0 and h >= 128):
         return None, None
     return stage_router_weight(w_r)
 
@@ -92,10 +154,13 @@ def router_forward(x: torch.Tensor, w_r: torch.Tensor, top_k: int, score: str = 
     t, h = x.shape
     e = w_r.shape[1]
     dev = x.device
+    if router_tc(e, h, top_k):
+        return _router_forward_tc(x, w_r, top_k, score, selection_bias, coeff, want_scores)
     if w_r_t is None and router_small(e, h):
         return _router_forward_small(x, w_r, top_k, score, selection_bias, coeff, want_scores)
-    if w_r_t is None:
-        w_r_t, _ = stage_router_weight(w_r, want_pad=False)
+    w_pad = None
+    if w_r_t is None or w_r_t.shape[1] != ceil_to(e, ROUTER_NPAD):
+        w_r_t, w_pad = stage_router_weight(w_r)
     epad = w_r_t.shape[1]
     rows = max(ceil_to(t, ALIGN), ALIGN)
     nmb = torch.full((1,), rows // ALIGN, dtype=torch.int32, device=dev)
@@ -122,7 +187,84 @@ def router_forward(x: torch.Tensor, w_r: torch.Tensor, top_k: int, score: str = 
     _lib.call("moe_router_finalize", counts.data_ptr(), partials.data_ptr(), t, top_k, e,
               float(coeff), aux.data_ptr(), aux_grad.data_ptr(), mean_scores.data_ptr(), _stream())
     return RouterOut(logits, topk_idx, topk_prob, counts, aux, aux_grad, mean_scores, status,
-                     scores)
+                     scores, w_pad=w_pad)
+
+
+def _router_forward_tc(x, w_r, top_k, score, selection_bias, coeff, want_scores):
+    """route() + aux_loss() on the small-N tensor-core router: one GEMM launch whose epilogue
+    scores, selects and counts, then the finalize (moe_router_tc_fwd). No host sync."""
+    t, h = x.shape
+    e = w_r.shape[1]
+    dev = x.device
+    w_t, w_pad = stage_router_tc(w_r)
+    x = x.contiguous()
+    logits = torch.empty((t, e), dtype=torch.float32, device=dev)
+    topk_idx = torch.empty((t, top_k), dtype=torch.int32, device=dev)
+    topk_prob = torch.empty((t, top_k), dtype=torch.float32, device=dev)
+    counts = torch.empty((e,), dtype=torch.int32, device=dev)
+    ws = torch.empty((max(int(_lib.query("moe_router_tc_fwd_ws", t, h, e)), 1),),
+                     dtype=torch.float32, device=dev)
+    status = torch.empty((1,), dtype=torch.int32, device=dev)
+    scores = torch.empty((t, e), dtype=torch.float32, device=dev) if want_scores else None
+    bias = None
+    if selection_bias is not None:
+        bias = selection_bias.to(device=dev, dtype=torch.float32).contiguous()
+    aux = torch.empty((), dtype=torch.float32, device=dev)
+    aux_grad = torch.empty((e,), dtype=torch.float32, device=dev)
+    mean_scores = torch.empty((e,), dtype=torch.float32, device=dev)
+    _lib.call("moe_router_tc_fwd", x.data_ptr(), t, h, w_t.data_ptr(), e, top_k,
+              SCORE_FN[score], _p(bias), float(coeff), logits.data_ptr(), topk_idx.data_ptr(),
+              topk_prob.data_ptr(), _p(scores), counts.data_ptr(), ws.data_ptr(),
+              status.data_ptr(), aux.data_ptr(), aux_grad.data_ptr(), mean_scores.data_ptr(),
+              _stream())
+    return RouterOut(logits, topk_idx, topk_prob, counts, aux, aux_grad, mean_scores, status,
+                     scores, w_pad=w_pad, path="tc")
+
+
+def _router_backward_tc(x, r: RouterOut, dprob, score, aux_g, want_dx=True,
+                        num_splits: int = 8):
+    """Router backward of the tensor-core router: the score Jacobian (moe_router_bwd2 on the
+    compact logits), dW_r = x^T dl and the router dX = dl . W_r^T (expert GEMM engine, K =
+    tc_kpad(E)). dW_r runs on the small-N tile for E <= 32 (split-K, fixed-order sum); for
+    larger E the grouped-K split GEMM with N padded to 256 measured faster (Qwen3 shape
+    67 + 12 us vs 105 us, tools/router_bench.py), so that E uses it."""
+    t, h = x.shape
+    e = r.counts.shape[0]
+    k = r.topk_idx.shape[1]
+    dev = x.device
+    npad = int(_lib.query("moe_router_tc_npad", e))
+    kpad = r.w_pad.shape[2]
+    rows = max(ceil_to(t, ALIGN), ALIGN)
+    small = e <= 32
+    dl = (torch.empty((rows, kpad), dtype=torch.bfloat16, device=dev)
+          if (want_dx or not small) else None)
+    ldt = max(ceil_to(t, 8), 8)
+    dlt = torch.empty((npad, ldt), dtype=torch.bfloat16, device=dev) if small else None
+    _lib.call("moe_router_bwd2", r.logits.data_ptr(), e, t, e, k, SCORE_FN[score],
+              r.topk_idx.data_ptr(), dprob.data_ptr(), _p(aux_g), _p(dl), kpad,
+              _p(dlt), ldt, npad, _stream())
+    dw = torch.empty((h, e), dtype=torch.float32, device=dev)
+    if small:
+        ws = torch.empty((max(int(_lib.query("moe_router_tc_wgrad_ws", t, h, e)), 1),),
+                         dtype=torch.float32, device=dev)
+        _lib.call("moe_router_tc_wgrad", x.contiguous().data_ptr(), t, h, dlt.data_ptr(), ldt,
+                  e, ws.data_ptr(), dw.data_ptr(), _stream())
+    elif t > 0:
+        splits = max(1, min(num_splits, -(-t // 64)))
+        chunk = ceil_to(-(-t // splits), 64)
+        offs_t = (torch.arange(splits + 1, dtype=torch.int32, device=dev) * chunk).clamp_(
+            max=ceil_to(t, 64))
+        parts = gemm.wgrad_f32(x, dl, offs_t, splits, max_rows=t)
+        _lib.call("moe_reduce_groups_f32", parts.data_ptr(), splits, h, kpad, e, dw.data_ptr(),
+                  _stream())
+    else:
+        dw.zero_()
+    dx = None
+    if want_dx and t > 0:
+        nmb = torch.full((1,), rows // ALIGN, dtype=torch.int32, device=dev)
+        be = torch.zeros((rows // ALIGN,), dtype=torch.int32, device=dev)
+        dx = gemm.fc2_fwd(dl, r.w_pad, be, nmb)
+    return dw, dx
 
 
 def _router_forward_small(x, w_r, top_k, score, selection_bias, coeff, want_scores):
@@ -152,7 +294,7 @@ def _router_forward_small(x, w_r, top_k, score, selection_bias, coeff, want_scor
     _lib.call("moe_router_finalize", counts.data_ptr(), partials.data_ptr(), t, top_k, e,
               float(coeff), aux.data_ptr(), aux_grad.data_ptr(), mean_scores.data_ptr(), _stream())
     return RouterOut(logits, topk_idx, topk_prob, counts, aux, aux_grad, mean_scores, status,
-                     scores, w_r)
+                     scores, w_r, path="small")
 
 
 def _router_backward_small(x, r: RouterOut, dprob, score, aux_g, want_dx=True):
@@ -187,12 +329,16 @@ def router_backward(x: torch.Tensor, w_r_pad: torch.Tensor | None, r: RouterOut,
     w_r_pad: the staged [h, 256k] router weight of the tcgen05 path (None on the small-E path,
     which uses r.w_r).
     """
-    if r.w_r is not None:
+    if r.path in ("tc", "small"):
         aux_g = None
         if aux_scale is not None:
             aux_g = r.aux_grad if (isinstance(aux_scale, float) and aux_scale == 1.0) else (
                 r.aux_grad * aux_scale)
+        if r.path == "tc":
+            return _router_backward_tc(x, r, dprob, score, aux_g)
         return _router_backward_small(x, r, dprob, score, aux_g)
+    if w_r_pad is None:
+        w_r_pad = r.w_pad
     t, h = x.shape
     e = r.counts.shape[0]
     k = r.topk_idx.shape[1]

@@ -127,7 +127,8 @@ class ExpertParams:
 # ----------------------------------------------------------------------------- router
 
 def route(hidden, w_r, score: str = "softmax", top_k: int = 1, selection_bias=None):
-    """routing.py:71-108 on the device (tcgen05 logits GEMM + warp-per-token top-k)."""
+    """routing.py:71-108 on the device (small-N tcgen05 logits tile with the scoring, top-k
+    and counts in its epilogue; csrc/router_tc.cu)."""
     if score not in ops.SCORE_FN:
         raise ValueError(f"unknown score function {score!r}")
     np_io = _is_np(hidden)
@@ -137,7 +138,7 @@ def route(hidden, w_r, score: str = "softmax", top_k: int = 1, selection_bias=No
     e = w.shape[1]
     if top_k > e:
         raise ValueError(f"top_k={top_k} exceeds num_experts={e}")
-    hp = _ceil(max(h, 1), 64)
+    hp = _ceil(max(h, 1), 128)  # zero columns: same logits; h % 128 == 0 = small-N router
     x = _pad2(x, cols=hp)
     w = _pad2(w, rows=hp)
     bias = None if selection_bias is None else _t(selection_bias, torch.float32)

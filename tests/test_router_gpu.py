@@ -38,24 +38,33 @@ CASES = [  # (T, h, E, K, score, bias)
     (1, 256, 2, 2, "softmax", False),
     (777, 512, 32, 4, "sigmoid", False),      # E > 16: tcgen05 logits path
     (600, 512, 128, 8, "softmax", True),      # Qwen3-like E
+    (4096, 7168, 256, 8, "sigmoid", True),    # DeepSeek shape: small-N tiles split h over
+                                              # an 8-CTA cluster (32 token tiles)
+    (4096, 256, 8, 2, "softmax", False),      # BASELINE configs[0] router (h split in 4)
+    (2000, 2048, 64, 6, "softmax", False),    # NPAD 64, K between the KMAX variants
 ]
 
 
-@pytest.fixture(params=[False, True], ids=["tcgen05_path", "small_path"])
-def small_path(request, monkeypatch):
-    monkeypatch.setattr(ops, "ROUTER_SMALL", request.param)
+@pytest.fixture(params=["tc", "gemm", "small"],
+                ids=["small_n_tc_path", "tcgen05_256_path", "small_path"])
+def router_path(request, monkeypatch):
+    """tc: the default small-N tensor-core router (csrc/router_tc.cu); gemm: the round-1
+    chain (logits GEMM padded to 256 + warp-per-token top-k); small: CUDA-core E <= 16."""
+    monkeypatch.setattr(ops, "ROUTER_TC", request.param == "tc")
+    monkeypatch.setattr(ops, "ROUTER_SMALL", request.param == "small")
     return request.param
 
 
 @pytest.mark.parametrize("T,h,E,K,score,bias", CASES)
-def test_router_forward_backward(T, h, E, K, score, bias, dev, small_path):
+def test_router_forward_backward(T, h, E, K, score, bias, dev, router_path):
     g = torch.Generator(device=dev).manual_seed(T + E)
     x = torch.randn((T, h), device=dev, generator=g).to(torch.bfloat16)
     w_r = (torch.randn((h, E), device=dev, generator=g) * h ** -0.5).to(torch.bfloat16)
     sb = (torch.rand((E,), device=dev, generator=g) * 0.05) if bias else None
-    small = ops.router_small(E, h)
-    assert small == (small_path and E <= 16)
+    small = router_path == "small" and ops.router_small(E, h)
     r = ops.router_forward(x, w_r, K, score, sb, 1e-2, want_scores=True)
+    want = {"tc": "tc", "gemm": "gemm", "small": "small" if small else "gemm"}[router_path]
+    assert r.path == want
     torch.cuda.synchronize()
     logits = r.logits[:T, :E].double().cpu().numpy()
     xd, wd = x.double().cpu().numpy(), w_r.double().cpu().numpy()
@@ -73,7 +82,7 @@ def test_router_forward_backward(T, h, E, K, score, bias, dev, small_path):
     assert abs(float(r.aux) - R.aux_loss(dec, 1e-2)) <= 1e-5 * R.aux_loss(dec, 1e-2)
     # backward with a random upstream dprob and the aux term
     dprob = torch.randn((T, K), device=dev, generator=g)
-    w_r_pad = None if small else ops.stage_router_weight(w_r)[1]
+    w_r_pad = None if router_path != "gemm" else ops.stage_router_weight(w_r)[1]
     dw, dx = ops.router_backward(x, w_r_pad, r, dprob, score, aux_scale=1.0)
     torch.cuda.synchronize()
     # reference: ds = dprob at the selections + aux gradient, through the score Jacobian

@@ -264,7 +264,8 @@ def test_torch_in_torch_out():
 
 # -- edge cases of the top-k kernel (non-finite keys, fp64 score ties) ---------
 
-def test_nonfinite_rows_raise_and_select_valid_experts():
+@pytest.mark.parametrize("hp", [64, 128], ids=["gemm256_path", "small_n_tc_path"])
+def test_nonfinite_rows_raise_and_select_valid_experts(hp):
     """A NaN hidden row (and an inf one with a selection bias) makes route() raise the
     reference's ValueError; the kernel itself still writes K valid, distinct experts per
     token and leaves the counts consistent (no out-of-range index, no stray writes)."""
@@ -282,10 +283,11 @@ def test_nonfinite_rows_raise_and_select_valid_experts():
         G.route(inf_row, np.eye(E), score="sigmoid", top_k=K, selection_bias=bias)
     # kernel level: every row keeps K distinct in-range experts, counts sum to T*K
     x = torch.as_tensor(logits, dtype=torch.float32).to(torch.bfloat16).cuda()
-    x = torch.nn.functional.pad(x, (0, 64 - E))
-    w = torch.eye(64, E, dtype=torch.bfloat16, device="cuda")
+    x = torch.nn.functional.pad(x, (0, hp - E))
+    w = torch.eye(hp, E, dtype=torch.bfloat16, device="cuda")
     for bias_t in (None, torch.as_tensor(bias, dtype=torch.float32, device="cuda")):
         r = ops.router_forward(x, w, K, "softmax", bias_t)
+        assert r.path == ("tc" if hp == 128 else "gemm")
         idx = r.topk_idx.cpu().numpy()
         assert idx.min() >= 0 and idx.max() < E
         assert np.all(np.diff(idx, axis=1) > 0)

@@ -47,3 +47,24 @@ for name, (E, K, h, T) in {"mixtral": (8, 2, 4096, 16384), "qwen3": (128, 8, 409
         gbs = nbytes / (ms / 1e3) / 1e9
         print(f"{name:9s} {k:15s} {ms * 1e3:8.1f} us {nbytes / 1e6:8.1f} MB {gbs:7.0f} GB/s "
               f"({gbs / HBM:.2f} of measured HBM)", flush=True)
+
+# reference points for the write-heavy / read-heavy kernels above: torch's own write-only
+# (zero_), read-only (sum) and copy kernels over 2 GiB
+buf = torch.empty((1 << 30,), dtype=torch.bfloat16, device=dev)
+buf2 = torch.empty_like(buf)
+for k, (fn, nbytes) in {"write_only": (lambda: buf.zero_(), buf.numel() * 2),
+                        "read_only": (lambda: buf.sum(), buf.numel() * 2),
+                        "copy": (lambda: buf2.copy_(buf), buf.numel() * 4)}.items():
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / iters
+    gbs = nbytes / (ms / 1e3) / 1e9
+    print(f"torch     {k:15s} {ms * 1e3:8.1f} us {nbytes / 1e6:8.1f} MB {gbs:7.0f} GB/s "
+          f"({gbs / HBM:.2f} of measured HBM)", flush=True)

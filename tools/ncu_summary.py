@@ -61,6 +61,7 @@ def main():
         h, d = src[1], src[2:]
         cols = [i for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
         tot = {}
+        d = [r for r in d if len(r) == len(h)]  # (several kernels: header rows repeat)
         for r in d:
             for i in cols:
                 if r[i].isdigit():
@@ -76,6 +77,18 @@ def main():
         if waits:
             print("  mbarrier try_wait executions: " +
                   ", ".join(f"{a}:{n}" for a, n in sorted(waits, key=lambda w: -w[1])[:6]))
+        ntop = int(__import__("os").environ.get("NCU_TOP_SASS", "0"))
+        if ntop:
+            # hottest SASS instructions by warp-stall samples (all reasons)
+            per = []
+            for r in d:
+                n = sum(int(r[i]) for i in cols if r[i].isdigit())
+                if n:
+                    per.append((n, r[0], r[1][:90]))
+            per.sort(reverse=True)
+            print(f"  top {ntop} SASS lines by stall samples (share, address, instruction):")
+            for n, a, ins in per[:ntop]:
+                print(f"    {n / allv:6.3f}  {a}  {ins}")
 
 
 if __name__ == "__main__":

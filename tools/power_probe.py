@@ -12,7 +12,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import pynvml  # noqa: E402
 import torch  # noqa: E402
 
-sys.argv = [sys.argv[0], "mixtral", "none"]
+sys.argv = [sys.argv[0], os.environ.get("POWER_CONFIG", "mixtral"), "none"]
 import gemm_kinds as G  # noqa: E402  (tools/ on sys.path via the script dir)
 
 pynvml.nvmlInit()

@@ -1,5 +1,7 @@
 """Router chain timing (forward: logits + score/top-k + finalize; backward: score Jacobian +
-dW_r + router dX) on the small-E CUDA-core path and the tcgen05 path, per kernel.
+dW_r + router dX) per C-ABI call on three paths: "tc" (the default small-N tensor-core router,
+csrc/router_tc.cu), "gemm" (round-1: logits GEMM padded to 256 columns + warp-per-token top-k)
+and "small" (CUDA-core, E <= 16).
 
     python tools/router_probe.py
 """
@@ -17,7 +19,10 @@ SHAPES = {"mixtral": (16384, 4096, 8, 2), "mixtral_T32k": (32768, 4096, 8, 2),
           "deepseek": (4096, 7168, 256, 8)}
 
 
-def run(T, h, E, K, small, iters=20):
+def run(T, h, E, K, mode, iters=20):
+    ops.ROUTER_TC = mode == "tc"
+    ops.ROUTER_SMALL = mode == "small"
+    small = mode != "gemm"
     g = torch.Generator(device=dev).manual_seed(0)
     x = torch.randn((T, h), device=dev, generator=g).to(torch.bfloat16)
     w_r = (torch.randn((h, E), device=dev, generator=g) * h ** -0.5).to(torch.bfloat16)
@@ -44,13 +49,14 @@ def run(T, h, E, K, small, iters=20):
     xbytes = T * h * 2
     # compulsory HBM bytes of the chain: x read in the forward and in dW_r, dX written (bf16)
     alg = 2 * xbytes + xbytes
-    print(f"T={T} h={h} E={E} K={K} {'small' if small else 'tcgen05'}: {tot * 1e3:8.1f} us "
+    print(f"T={T} h={h} E={E} K={K} {mode}: {tot * 1e3:8.1f} us "
           f"(alg {alg / 1e6:.0f} MB -> {alg / (tot / 1e3) / 1e12:.2f} TB/s) "
           + " ".join(f"{k}={v * 1e3:.1f}" for k, v in sorted(per.items(), key=lambda kv: -kv[1])),
           flush=True)
 
 
 for name, (T, h, E, K) in SHAPES.items():
-    if ops.router_small(E, h):
-        run(T, h, E, K, True)
-    run(T, h, E, K, False)
+    run(T, h, E, K, "tc")
+    run(T, h, E, K, "gemm")
+    if E <= 16:
+        run(T, h, E, K, "small")
