@@ -73,7 +73,8 @@ int moe_router_bwd(const float* logits, int ld, int T, int E, int K, int score_f
  * routing.py:71-108 + aux_loss() :111-120 in one tcgen05 GEMM whose epilogue scores, selects
  * and counts (thread per token, logits read from TMEM) + the finalize: x[T,h] bf16,
  * w_t[moe_router_tc_npad(E), h] bf16 = W_r^T zero-padded; logits out compact [T, E] fp32;
- * ws: moe_router_tc_fwd_ws(T, h, E) floats (score partials first). K <= 8. */
+ * ws: moe_router_tc_fwd_ws(T, h, E) 4-byte words. K <= 8. Two launches (the GEMM with the
+ * selection epilogue, then the finalize), no memsets. */
 int moe_router_tc_npad(int E);
 long long moe_router_tc_fwd_ws(int T, int h, int E);
 int moe_router_tc_fwd(const void* x, int T, int h, const void* w_t, int E, int K, int score_fn,
@@ -83,6 +84,10 @@ int moe_router_tc_fwd(const void* x, int T, int h, const void* w_t, int E, int K
 int moe_router_finalize_p(const int* counts, const float* score_partials, int P, int T, int K,
                           int E, float coeff, float* aux_out, float* aux_grad,
                           float* mean_scores, void* stream);
+int moe_router_finalize_tiles(const int* tile_counts, const int* tile_status,
+                              const float* score_partials, int P, int T, int K, int E,
+                              float coeff, int* counts, int* status, float* aux_out,
+                              float* aux_grad, float* mean_scores, void* stream);
 /* Its backward: dl row-major bf16 [T, ldd] (dX GEMM operand) and/or dl^T bf16 [npad, ldt]
  * (moe_router_bwd semantics), and dW_r[h, E] fp32 = x^T dl on a small-N tcgen05 tile with a
  * fixed-order split-K sum (ws: moe_router_tc_wgrad_ws floats; h % 128 == 0). */

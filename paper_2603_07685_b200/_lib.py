@@ -41,6 +41,7 @@ SIGNATURES: dict[str, list] = {
     # small-N tensor-core router (csrc/router_tc.cu)
     "moe_router_tc_fwd": [P, I, I, P, I, I, I, P, F, P, P, P, P, P, P, P, P, P, P, P],
     "moe_router_finalize_p": [P, P, I, I, I, I, F, P, P, P, P],
+    "moe_router_finalize_tiles": [P, P, P, I, I, I, I, F, P, P, P, P, P, P],
     "moe_router_bwd2": [P, I, I, I, I, I, P, P, P, P, I, P, I, I, P],
     "moe_router_tc_wgrad": [P, I, I, P, I, I, P, P, P],
     "moe_router_bwd_f32": [P, I, I, I, I, I, P, P, P, P, P],

@@ -316,12 +316,31 @@ __global__ void __launch_bounds__(WARPS * 32) fused_small_kernel(
 // Thread (s, e) of the 1024-thread block sums score-partial rows b = s, s + S, ... of expert e
 // (S = 1024 / E subsets; consecutive threads read consecutive experts of a row: coalesced);
 // the S subset sums of each expert are then added in subset order (deterministic).
-__global__ void finalize_kernel(const int* __restrict__ counts,
+// tile_counts / tile_status (nullable): per-tile counts [P, E] and non-finite flags [P] of the
+// tensor-core router; summed here into counts[E] / OR-ed into *status (no memsets, no global
+// atomics in the producing kernel).
+__global__ void finalize_kernel(int* __restrict__ counts,
                                 const float* __restrict__ score_partials, int P, int T, int K,
                                 int E, float coeff, float* __restrict__ aux_out,
-                                float* __restrict__ aux_grad, float* __restrict__ mean_scores) {
+                                float* __restrict__ aux_grad, float* __restrict__ mean_scores,
+                                const int* __restrict__ tile_counts = nullptr,
+                                const int* __restrict__ tile_status = nullptr,
+                                int* __restrict__ status = nullptr) {
   __shared__ double sub[1024];
   __shared__ double fp[256];
+  if (tile_counts) {
+    for (int e2 = threadIdx.x; e2 < E; e2 += blockDim.x) {
+      int c = 0;
+      for (int b = 0; b < P; ++b) c += tile_counts[(long long)b * E + e2];
+      counts[e2] = c;
+    }
+    if (threadIdx.x == 0 && status) {
+      int st = 0;
+      for (int b = 0; b < P; ++b) st |= tile_status[b];
+      *status = st;
+    }
+    __syncthreads();
+  }
   const int S = blockDim.x / E;
   const int e = threadIdx.x % E, sidx = threadIdx.x / E;
   double ps = 0.0;
@@ -605,7 +624,8 @@ int moe_router_finalize(const int* counts, const float* score_partials, int T, i
                         void* stream) {
   const int P = moe_router_num_partials(T);
   finalize_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(
-      counts, score_partials, T == 0 ? 0 : P, T, K, E, coeff, aux_out, aux_grad, mean_scores);
+      const_cast<int*>(counts), score_partials, T == 0 ? 0 : P, T, K, E, coeff, aux_out,
+      aux_grad, mean_scores);
   MOE_LAUNCH_CHECK();
   return kOk;
 }
@@ -617,7 +637,22 @@ int moe_router_finalize_p(const int* counts, const float* score_partials, int P,
                           float* mean_scores, void* stream) {
   if (E < 1 || E > 256) return kErrInvalidArg;
   finalize_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(
-      counts, score_partials, T == 0 ? 0 : P, T, K, E, coeff, aux_out, aux_grad, mean_scores);
+      const_cast<int*>(counts), score_partials, T == 0 ? 0 : P, T, K, E, coeff, aux_out,
+      aux_grad, mean_scores);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+// moe_router_finalize_p with per-tile counts [P, E] and status flags [P] (summed / OR-ed into
+// counts[E] and status[1]).
+int moe_router_finalize_tiles(const int* tile_counts, const int* tile_status,
+                              const float* score_partials, int P, int T, int K, int E,
+                              float coeff, int* counts, int* status, float* aux_out,
+                              float* aux_grad, float* mean_scores, void* stream) {
+  if (E < 1 || E > 256) return kErrInvalidArg;
+  finalize_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(
+      counts, score_partials, T == 0 ? 0 : P, T, K, E, coeff, aux_out, aux_grad, mean_scores,
+      tile_counts, tile_status, status);
   MOE_LAUNCH_CHECK();
   return kOk;
 }

@@ -59,7 +59,7 @@ struct Cfg {
   static constexpr int STAGES = (RING_KB * 1024) / STAGE < 3 ? 3 : (RING_KB * 1024) / STAGE;
   static constexpr int TMEM_COLS = NPAD < 32 ? 32 : NPAD;
   static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/ +
-                              256 * 4 /*counts*/ + 256 * 4 /*selection bias*/;
+                              256 * 4 /*counts*/ + 256 * 4 /*selection bias*/ + 16 /*flag*/;
 };
 
 struct Params {
@@ -72,9 +72,10 @@ struct Params {
   int* topk_idx;         // [T, K]
   float* topk_prob;      // [T, K]
   float* scores_out;     // [T, E] or null
-  int* counts;           // [E] (zeroed before the launch)
+  int* tile_counts;      // [tiles * CS, E] per-slice expert counts
+  int* tile_status;      // [tiles * CS] per-slice non-finite flag
   float* score_partials; // [tiles, E]
-  int* status;           // bit 0: non-finite logits
+
   float* ws;             // route, CS > 1: [tiles, CS, NPAD, 128] fp32 partial logits
   float* part;           // wgrad: [splits, NPAD, h] fp32
   int debug_skip;        // probe only: stop after the logits (mainloop + copy-out)
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done_bar + 1);
   int* s_counts = reinterpret_cast<int*>(smem + C::STAGES * C::STAGE + 256);  // [256]
   float* s_bias = reinterpret_cast<float*>(s_counts + 256);                    // [256]
+  int* s_flag = reinterpret_cast<int*>(s_bias + 256);                          // [1]
 
   const int warp = warp_id(), lane = lane_id();
   const int crank = (MODE == MODE_ROUTE && p.CS > 1) ? static_cast<int>(cluster_rank_u32()) : 0;
@@ -150,6 +152,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
   }
   if (MODE == MODE_ROUTE) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) s_counts[i] = 0;
+    if (threadIdx.x == 0) s_flag[0] = 0;
     if (p.sel_bias)
       for (int i = threadIdx.x; i < p.E; i += blockDim.x)
         s_bias[i] = __ldg(p.sel_bias + i);
@@ -476,7 +479,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
           p.topk_prob[t * K + rank] = Lr[e] * inv;
           atomicAdd(&s_counts[e], 1);
         }
-        if (bad) atomicOr(p.status, 1);
+        if (bad) atomicOr(&s_flag[0], 1);
       }
       // pass 3: normalised scores s = sc * inv overwrite L (0 for rows past T) ->
       // scores_out and the slice's column sums (rows in fixed order: deterministic)
@@ -491,8 +494,9 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
 #pragma unroll 8
         for (int r = 0; r < RB; ++r) acc += L[r * LS + e];
         p.score_partials[prow * E + e] = acc;
-        if (s_counts[e]) atomicAdd(&p.counts[e], s_counts[e]);
+        p.tile_counts[prow * E + e] = s_counts[e];
       }
+      if (threadIdx.x == 0) p.tile_status[prow] = s_flag[0];
     }
   }
   tc_fence_before();
@@ -619,14 +623,16 @@ extern "C" {
 // Padded expert count of the small-N router tiles (W_r^T staging rows).
 int moe_router_tc_npad(int E) { return E >= 1 && E <= 256 ? npad_of(E) : -1; }
 
-// Workspace floats of moe_router_tc_fwd: score partials [tiles * CS, E] + split-h partial
-// logits [tiles, CS, NPAD, 128] (CS > 1 only).
+// Workspace of moe_router_tc_fwd in 4-byte words: score partials [P, E] fp32, slice counts
+// [P, E] int32, slice flags [P] int32 (P = tiles * CS, each 16-byte aligned), then the
+// split-h partial logits [tiles, CS, NPAD, 128] fp32 (CS > 1 only).
+static long long ws_a4(long long n) { return (n + 3) / 4 * 4; }
 long long moe_router_tc_fwd_ws(int T, int h, int E) {
   if (T <= 0) return E;
   const int tiles = ceil_div_i(T, BM);
   const int cs = route_cluster(T, h);
-  return (long long)ceil_div_i(tiles * cs * E, 4) * 4 +
-         (cs > 1 ? (long long)tiles * cs * BM * npad_of(E) : 0);
+  const long long P = (long long)tiles * cs;
+  return 2 * ws_a4(P * E) + ws_a4(P) + (cs > 1 ? (long long)tiles * cs * BM * npad_of(E) : 0);
 }
 
 // route() + aux_loss() (routing.py:71-120) in one GEMM-with-epilogue launch + finalize:
@@ -639,9 +645,10 @@ int moe_router_tc_fwd(const void* x, int T, int h, const void* w_t, int E, int K
   if (E < 1 || E > 256 || K < 1 || K > 8 || h < 8 || h % 8) return kErrInvalidArg;
   if (K > E) return kErrTopK;
   auto st = static_cast<cudaStream_t>(stream);
-  MOE_CUDA_CHECK(cudaMemsetAsync(counts, 0, sizeof(int) * E, st));
-  MOE_CUDA_CHECK(cudaMemsetAsync(status, 0, sizeof(int), st));
   const int tiles = T > 0 ? ceil_div_i(T, BM) : 0;
+  const long long P = T > 0 ? (long long)tiles * route_cluster(T, h) : 0;
+  int* tile_counts = reinterpret_cast<int*>(ws + ws_a4(P * E));
+  int* tile_status = tile_counts + ws_a4(P * E);
   if (T > 0) {
     const int np = npad_of(E);
     const int cs = route_cluster(T, h);
@@ -662,10 +669,10 @@ int moe_router_tc_fwd(const void* x, int T, int h, const void* w_t, int E, int K
     p.topk_idx = topk_idx;
     p.topk_prob = topk_prob;
     p.scores_out = scores_out;
-    p.counts = counts;
+    p.tile_counts = tile_counts;
+    p.tile_status = tile_status;
     p.score_partials = ws;
-    p.status = status;
-    p.ws = ws + (long long)ceil_div_i(tiles * cs * E, 4) * 4;  // 16-byte aligned
+    p.ws = ws + 2 * ws_a4(P * E) + ws_a4(P);  // 16-byte aligned
     {
       static int dbg = -1;
       if (dbg < 0) {
@@ -682,9 +689,9 @@ int moe_router_tc_fwd(const void* x, int T, int h, const void* w_t, int E, int K
     }
     if (r) return r;
   }
-  const int prows = T > 0 ? tiles * route_cluster(T, h) : 0;  // one per (tile, cluster rank)
-  return moe_router_finalize_p(counts, ws, prows, T, K, E, coeff, aux_out, aux_grad, mean_scores,
-                               stream);
+  // (T == 0: P == 0, the finalize writes zero counts, a clear status and a zero aux loss)
+  return moe_router_finalize_tiles(tile_counts, tile_status, ws, (int)P, T, K, E, coeff, counts,
+                                   status, aux_out, aux_grad, mean_scores, stream);
 }
 
 // Workspace floats of moe_router_tc_wgrad: part [splits, NPAD, h].

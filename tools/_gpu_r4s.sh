@@ -1,0 +1,4 @@
+timeout 300 python -m pytest tests/test_router_gpu.py tests/test_routing_api_gpu.py tests/test_layer_gpu.py -x -q -p no:cacheprovider 2>&1 | tail -2
+python tools/router_bench.py tc
+python tools/router_bench.py gemm
+timeout 200 python tools/router_probe.py 2>&1 | grep -v small
