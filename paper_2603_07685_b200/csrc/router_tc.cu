@@ -51,10 +51,20 @@ constexpr int MODE_WGRAD = 1;
 #endif
 constexpr int RING_KB = MOE_ROUTER_RING_KB;  // operand ring per CTA (A/B: 96 vs 160 measured)
 
-template <int NPAD>
+// 64-column sub-blocks per ring stage of the route kernel: each stage reads SUBK * 128
+// contiguous bytes of every x row (longer DRAM bursts per row than one 128-byte box)
+#ifndef MOE_ROUTER_SUBK
+#define MOE_ROUTER_SUBK 2
+#endif
+// (NPAD >= 128: the W^T box alone is 16-32 KB per sub-block; one sub-block per stage)
+template <int MODE, int NPAD>
+constexpr int subk_of() { return MODE == 0 && NPAD <= 64 ? MOE_ROUTER_SUBK : 1; }
+static int subk_route(int npad) { return npad <= 64 ? MOE_ROUTER_SUBK : 1; }
+
+template <int NPAD, int SUBK = 1>
 struct Cfg {
-  static constexpr int A_STAGE = BM * BK * 2;    // 16 KB
-  static constexpr int B_STAGE = NPAD * BK * 2;  // NPAD rows x 128 B (multiple of 1 KB)
+  static constexpr int A_STAGE = SUBK * BM * BK * 2;    // SUBK x 16 KB
+  static constexpr int B_STAGE = SUBK * NPAD * BK * 2;  // SUBK x NPAD rows x 128 B
   static constexpr int STAGE = A_STAGE + B_STAGE;
   static constexpr int STAGES = (RING_KB * 1024) / STAGE < 3 ? 3 : (RING_KB * 1024) / STAGE;
   static constexpr int TMEM_COLS = NPAD < 32 ? 32 : NPAD;
@@ -108,7 +118,9 @@ template <int NPAD, int MODE, int KMAX>
 __global__ void __launch_bounds__(threads_of<MODE>(), 1)
     router_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
                      const __grid_constant__ CUtensorMap tmap_b, const Params p) {
-  using C = Cfg<NPAD>;
+  constexpr int SUBK = subk_of<MODE, NPAD>();
+  constexpr int KB = SUBK * BK;  // columns per ring stage
+  using C = Cfg<NPAD, SUBK>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -129,16 +141,16 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
   if constexpr (MODE == MODE_ROUTE) {
     tile = blockIdx.x / p.CS;
     m0 = tile * BM;
-    k0 = crank * p.num_kb * BK;
+    k0 = crank * p.num_kb * KB;
   } else {
     tile = blockIdx.x % p.m_tiles;
     m0 = tile * BM;
-    k0 = (blockIdx.x / p.m_tiles) * p.num_kb * BK;
+    k0 = (blockIdx.x / p.m_tiles) * p.num_kb * KB;
   }
   // k-blocks this CTA owns (the last range may be short; TMA zero-fills past the end)
   const int kdim = MODE == MODE_ROUTE ? p.h : p.T;
   int nkb = p.num_kb;
-  if (k0 + nkb * BK > kdim) nkb = k0 < kdim ? (kdim - k0 + BK - 1) / BK : 0;
+  if (k0 + nkb * KB > kdim) nkb = k0 < kdim ? (kdim - k0 + KB - 1) / KB : 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
@@ -171,16 +183,21 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty_bar[s], ph ^ 1);
         mbar_arrive_expect_tx(&full_bar[s], C::STAGE);
-        const int k = k0 + kb * BK;
+        const int k = k0 + kb * KB;
         uint8_t* sa = smem_a + s * C::A_STAGE;
         if constexpr (MODE == MODE_ROUTE) {
-          tma_load_2d(sa, &tmap_a, &full_bar[s], k, m0);  // x rows m0.., columns k..
+#pragma unroll
+          for (int sb = 0; sb < SUBK; ++sb)  // x rows m0.., columns k + 64 sb ..
+            tma_load_2d(sa + sb * (BM * BK * 2), &tmap_a, &full_bar[s], k + sb * BK, m0);
         } else {
           // x^T tile, MN-major: two 64(h) x 64(token) boxes
           tma_load_2d(sa, &tmap_a, &full_bar[s], m0, k);
           tma_load_2d(sa + 64 * BK * 2, &tmap_a, &full_bar[s], m0 + 64, k);
         }
-        tma_load_2d(smem_b + s * C::B_STAGE, &tmap_b, &full_bar[s], k, 0);
+#pragma unroll
+        for (int sb = 0; sb < SUBK; ++sb)
+          tma_load_2d(smem_b + s * C::B_STAGE + sb * (NPAD * BK * 2), &tmap_b, &full_bar[s],
+                      k + sb * BK, 0);
         if (++s == C::STAGES) {
           s = 0;
           ph ^= 1;
@@ -199,13 +216,16 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         const uint32_t a_base = smem_u32(smem_a + s * C::A_STAGE);
         const uint32_t b_base = smem_u32(smem_b + s * C::B_STAGE);
 #pragma unroll
-        for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-          const uint64_t adesc =
-              MODE == MODE_WGRAD ? make_sdesc_sw128(a_base + kk * (UMMA_K * 128), 64 * BK * 2, 1024)
-                                 : make_sdesc_sw128(a_base + kk * (UMMA_K * 2), 16, 1024);
-          const uint64_t bdesc = make_sdesc_sw128(b_base + kk * (UMMA_K * 2), 16, 1024);
-          umma_bf16(tmem_base, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
-        }
+        for (int sb = 0; sb < SUBK; ++sb)
+#pragma unroll
+          for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+            const uint32_t ab = a_base + sb * (BM * BK * 2), bb = b_base + sb * (NPAD * BK * 2);
+            const uint64_t adesc =
+                MODE == MODE_WGRAD ? make_sdesc_sw128(ab + kk * (UMMA_K * 128), 64 * BK * 2, 1024)
+                                   : make_sdesc_sw128(ab + kk * (UMMA_K * 2), 16, 1024);
+            const uint64_t bdesc = make_sdesc_sw128(bb + kk * (UMMA_K * 2), 16, 1024);
+            umma_bf16(tmem_base, adesc, bdesc, idesc, (kb | sb | kk) != 0 ? 1u : 0u);
+          }
         umma_commit(&empty_bar[s]);
         if (++s == C::STAGES) {
           s = 0;
@@ -569,11 +589,12 @@ template <int NPAD, int MODE, int KMAX>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid,
                   int cs, cudaStream_t st) {
   auto kern = router_tc_kernel<NPAD, MODE, KMAX>;
-  MOE_CUDA_CHECK(ensure_dyn_smem(reinterpret_cast<const void*>(kern), Cfg<NPAD>::SMEM));
+  constexpr int SMEM = Cfg<NPAD, subk_of<MODE, NPAD>()>::SMEM;
+  MOE_CUDA_CHECK(ensure_dyn_smem(reinterpret_cast<const void*>(kern), SMEM));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads_of<MODE>());
-  cfg.dynamicSmemBytes = Cfg<NPAD>::SMEM;
+  cfg.dynamicSmemBytes = SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -663,7 +684,7 @@ int moe_router_tc_fwd(const void* x, int T, int h, const void* w_t, int E, int K
     p.K = K;
     p.score_fn = score_fn;
     p.CS = cs;
-    p.num_kb = ceil_div_i(ceil_div_i(h, BK), cs);
+    p.num_kb = ceil_div_i(ceil_div_i(h, BK * subk_route(np)), cs);  // ring stages
     p.sel_bias = sel_bias;
     p.logits = logits;
     p.topk_idx = topk_idx;
