@@ -32,6 +32,9 @@ for name, (E, K, h, T) in {"mixtral": (8, 2, 4096, 16384), "qwen3": (128, 8, 409
         "combine": (lambda: ops.combine(o, plan, r.topk_prob, out=y), R * h * w + T * h * w),
         "combine_bwd": (lambda: ops.combine_backward(dy, plan, o, r.topk_prob, d_rows=d_rows),
                         T * h * w + 2 * R * h * w),
+        # the dX combine: unweighted row sum + the router dX (`extra`), as in the backward
+        "combine_dx": (lambda: ops.combine(o, plan, None, extra=dy, out=y),
+                       R * h * w + 2 * T * h * w),
     }
     for k, (fn, nbytes) in cases.items():
         for _ in range(3):
