@@ -328,21 +328,26 @@ __global__ void finalize_kernel(int* __restrict__ counts,
                                 int* __restrict__ status = nullptr) {
   __shared__ double sub[1024];
   __shared__ double fp[256];
-  if (tile_counts) {
-    for (int e2 = threadIdx.x; e2 < E; e2 += blockDim.x) {
-      int c = 0;
-      for (int b = 0; b < P; ++b) c += tile_counts[(long long)b * E + e2];
-      counts[e2] = c;
-    }
-    if (threadIdx.x == 0 && status) {
-      int st = 0;
-      for (int b = 0; b < P; ++b) st |= tile_status[b];
-      *status = st;
-    }
-    __syncthreads();
-  }
+  __shared__ int isub[1024];
   const int S = blockDim.x / E;
   const int e = threadIdx.x % E, sidx = threadIdx.x / E;
+  if (tile_counts) {
+    // same subset split as the score partials below: coalesced, then a fixed-order combine
+    int c = 0;
+    if (sidx < S)
+      for (int b = sidx; b < P; b += S) c += tile_counts[(long long)b * E + e];
+    isub[threadIdx.x] = c;
+    int st = 0;
+    for (int b = threadIdx.x; b < P; b += blockDim.x) st |= tile_status[b];
+    st = __syncthreads_or(st);
+    if (threadIdx.x < E) {
+      int tot = 0;
+      for (int q = 0; q < S; ++q) tot += isub[q * E + threadIdx.x];
+      counts[threadIdx.x] = tot;
+    }
+    if (threadIdx.x == 0 && status) *status = st;
+    __syncthreads();
+  }
   double ps = 0.0;
   if (sidx < S)
     for (int b = sidx; b < P; b += S) ps += score_partials[(long long)b * E + e];

@@ -42,8 +42,10 @@ def main():
     ours = [d for d in launches.values() if "moe::" in d["name"] or "grouped_gemm" in d["name"]
             or any(k in d["name"] for k in ("router", "perm", "combine", "gather", "topk",
                                             "finalize", "bwd_kernel", "zero_pad", "reduce"))]
-    # the last of the 4 steps: its launches start at the last stage_router_weight / router
-    starts = [i for i, d in enumerate(ours) if "stage_router_weight" in d["name"]]
+    # the last of the 4 steps: its launches start at the last router forward (the small-N
+    # router kernel, or the round-1 chain's weight staging)
+    starts = [i for i, d in enumerate(ours) if "stage_router_weight" in d["name"]
+              or ("router_tc_kernel<" in d["name"] and ", 0, " in d["name"])]
     step = ours[starts[-1]:] if starts else ours[-len(ours) // 4:]
     s = SHAPES[cfg]
     E, K, h, m, T, ms = s["E"], s["K"], s["h"], s["m"], s["T"], s["ms"]
