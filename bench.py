@@ -729,7 +729,16 @@ def run_gpu(args, c) -> None:
                 "frac": round(gemm_tflops / peak_tf, 4) if gemm_tflops else None,
                 "frac_vs": ({"sustained_measured": round(gemm_tflops / peak_tf, 4),
                              "burst_measured": round(gemm_tflops / burst_tf, 4),
-                             "datasheet_dense_2250": round(gemm_tflops / 2250.0, 4)}
+                             "datasheet_dense_2250": round(gemm_tflops / 2250.0, 4),
+                             # the dense bf16 tensor pipe at the SM clock the run actually
+                             # held under the 1 kW cap: 8192 FLOP/clk/SM x 148 SMs x the
+                             # median sampled clock (2.25 PF corresponds to ~1.86 GHz)
+                             "clock_adjusted_dense": (
+                                 round(gemm_tflops / (8192 * 148 * clk["sm_mhz"] * 1e6 / 1e12), 4)
+                                 if clk and clk.get("sm_mhz") else None),
+                             "clock_adjusted_peak_tflops": (
+                                 round(8192 * 148 * clk["sm_mhz"] * 1e6 / 1e12, 1)
+                                 if clk and clk.get("sm_mhz") else None)}
                             if gemm_tflops else None),
                 "traffic": traffic["bytes"] if traffic else None,
                 "traffic_detail": traffic,
