@@ -217,7 +217,14 @@ __device__ __forceinline__ void decode_tile(const Params& p, int t, int num_unit
                                             Tile& tl) {
   const int nb_count = p.N / BN;
   if constexpr (!GROUPED_K) {
-    const int bm = p.band_m;
+    // band_m <= 0: one expert's M units per band (clamped to [4, 16]); measured on B200
+    // (profiles/r02_band_ab.txt): Qwen3 (8 units per expert) band 8 beats 16 by 3.7% over
+    // the four grouped-M kinds, Mixtral (16 units per expert) band 16 beats 8
+    int bm = p.band_m;
+    if (bm <= 0) {
+      bm = num_units / (p.num_experts > 0 ? p.num_experts : 1);
+      bm = bm < 4 ? 4 : (bm > BAND_M ? BAND_M : bm);
+    }
     const int band = t / (bm * nb_count);
     const int rem = t - band * bm * nb_count;
     const int u0 = band * bm;
@@ -1030,13 +1037,13 @@ static int run(const void* a, uint64_t a_inner, uint64_t a_outer, const void* b,
                cudaStream_t stream) {
   p.stream_stores = stream_stores_default();
   {
-    static int bm = -1;
+    static int bm = -1;  // MOE_B200_BAND forces a band; else auto (pair) / BAND_M (1-CTA)
     if (bm < 0) {
       const char* e = getenv("MOE_B200_BAND");
-      bm = e ? atoi(e) : BAND_M;
-      if (bm < 1) bm = BAND_M;
+      bm = e ? atoi(e) : 0;
+      if (bm < 0) bm = 0;
     }
-    p.band_m = bm;
+    p.band_m = bm > 0 ? bm : (pair ? 0 : BAND_M);
   }
   {
     // grouped-K with few token rows per expert (avg <= 512: DeepSeek-shape EP=1 has 128) is

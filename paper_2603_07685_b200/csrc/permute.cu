@@ -325,16 +325,26 @@ __global__ void __launch_bounds__(GT_WARPS * 32) gather_tokens_tma_kernel(
 }
 
 // Zero the rows whose source is -1 (padding / phantom) among the first meta[0]*128 rows.
+// Each warp checks 32 rows per step with 32 independent loads (lane l: row w + l * nwarps,
+// so the padding rows, which sit together at the end of each expert block, spread over all
+// warps), a ballot picks the padding rows, and the warp zeroes them: the scan is not a chain
+// of one dependent 4-byte load per row (Qwen3 shape: ~270k rows).
 __global__ void zero_pad_rows_kernel(const int* __restrict__ meta, const int* __restrict__ row_src,
                                      int hv, int4* __restrict__ out) {
   const int rows = meta[0] * ALIGN;
+  const int lane = lane_id();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int4 z = make_int4(0, 0, 0, 0);
-  for (int r = warp; r < rows; r += nwarps) {
-    if (__ldg(row_src + r) >= 0) continue;
-    int4* o = out + (long long)r * hv;
-    for (int c = lane_id(); c < hv; c += 32) st_na_v4(o + c, z);
+  for (long long base = warp; base < rows; base += 32LL * nwarps) {
+    const long long r = base + (long long)lane * nwarps;
+    unsigned m = __ballot_sync(0xffffffffu, r < rows && __ldg(row_src + r) < 0);
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      int4* o = out + (base + (long long)j * nwarps) * hv;
+      for (int c = lane; c < hv; c += 32) st_na_v4(o + c, z);
+    }
   }
 }
 
