@@ -135,6 +135,13 @@ int moe_ep_plan_device(const float* gathered, int ldg, int n, int E, int me, int
 int moe_ep_row_dst(const int* table, int n, int el, int rows_pad, const int* dst_off,
                    const unsigned long long* peers, long long row_bytes,
                    unsigned long long* row_dst, void* stream);
+/* Split units for the grouped GEMMs' kFlagSplit (flags bit 1, with the pair bit 0): from a
+ * 128-row aligned padded plan, each expert's blocks as 256-row pairs (CTA-pair engine) and
+ * at most one single 128-row block (1-CTA engine): halves the padding of a 256-row plan.
+ * U [2 + 2 * cap] int32: U[0] pairs, U[1] singles, U[2..2+cap) pair start blocks,
+ * U[2+cap..2+2cap) single blocks; pass U as the GEMMs' num_m_blocks with flags = 3. */
+int moe_split_units(const int* meta, const int* block_expert, const int* off_pad, int cap,
+                    int* U, void* stream);
 int moe_permute_compact_map(const int* meta, const int* off_c, const int* off_pad, int E,
                             const int* row_src, long long* row_id_map, int* compact_to_pad,
                             int max_compact, void* stream);

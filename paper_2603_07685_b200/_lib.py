@@ -54,6 +54,7 @@ SIGNATURES: dict[str, list] = {
     "moe_ep_plan_device": [P, I, I, I, I, I, I, I, I, I, F, I, P, P, P, P, I, P, P, P, P, P, P],
     "moe_ep_row_dst": [P, I, I, I, P, P, L, P, P],
     "moe_permute_compact_map": [P, P, P, I, P, P, P, I, P],
+    "moe_split_units": [P, P, P, I, P, P],
     "moe_permute_gather": [P, I, I, I, P, P, P, P, P],
     "moe_zero_pad_rows": [P, P, I, P, P],
     "moe_gather_rows": [P, I, P, P, I, P, P],

@@ -165,6 +165,9 @@ struct Params {
   int sync_slot;
   int sync_kb;
   int sync_lag;  // a producer at sync point g waits for every CTA to reach g - sync_lag
+  // split units (grouped-M, kFlagSplit): unit u starts at 128-row block unit_block[u] and
+  // *num_m_blocks counts UNITS (pairs for CG = 2, single blocks for CG = 1)
+  const int* unit_block;
 };
 
 // per-(device, stream) wave-sync counters (common.cuh wave_sync_slot)
@@ -232,8 +235,14 @@ __device__ __forceinline__ void decode_tile(const Params& p, int t, int num_unit
     const int nb = rem / rows;
     int u = u0 + (rem - nb * rows);
     if (p.unit_order) u = __ldg(p.unit_order + u);
-    tl.expert = __ldg(p.block_expert + u * CG);
-    tl.m0 = u * (BM * CG) + rank * BM;
+    if (p.unit_block) {
+      const int blk = __ldg(p.unit_block + u);
+      tl.expert = __ldg(p.block_expert + blk);
+      tl.m0 = blk * BM + rank * BM;
+    } else {
+      tl.expert = __ldg(p.block_expert + u * CG);
+      tl.m0 = u * (BM * CG) + rank * BM;
+    }
     tl.n0 = nb * BN;
     tl.k_begin = 0;
     tl.num_kb = p.K / BK;
@@ -416,7 +425,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
   int num_tiles;
   int num_units = 0;
   if constexpr (!GROUPED_K) {
-    num_units = *p.num_m_blocks / CG;
+    num_units = p.unit_block ? *p.num_m_blocks : *p.num_m_blocks / CG;
     num_tiles = num_units * (p.N / BN);
   } else {
     num_tiles = p.num_experts * (p.M / (BM * CG)) * (p.N / BN);
@@ -1019,6 +1028,10 @@ static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtenso
 
 // flags bit 0: CTA-pair engine (grouped-M: expert blocks 256-row aligned).
 constexpr int kFlagPair = 1;
+// flags bit 1: split units (with bit 0): num_m_blocks is the unit table of moe_split_units
+// over a 128-row aligned plan; pairs run on the CTA-pair engine, single blocks on the 1-CTA
+// engine (two launches). Not with the EP source waits.
+constexpr int kFlagSplit = 2;
 
 // Builds tensor maps for the chosen engine and launches. a_inner/a_outer/b_* describe the
 // 2-D global views; a/b K-major (box {64, rows}) or MN-major (box {64, 64}).
@@ -1034,7 +1047,7 @@ static int stream_stores_default() {
 template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI>
 static int run(const void* a, uint64_t a_inner, uint64_t a_outer, const void* b,
                uint64_t b_inner, uint64_t b_outer, Params p, int units_m, int pair,
-               cudaStream_t stream) {
+               cudaStream_t stream, int split = 0) {
   p.stream_stores = stream_stores_default();
   {
     static int bm = -1;  // MOE_B200_BAND forces a band; else auto (pair) / BAND_M (1-CTA)
@@ -1130,6 +1143,30 @@ static int run(const void* a, uint64_t a_inner, uint64_t a_outer, const void* b,
                         CU_TENSOR_MAP_SWIZZLE_64B)))
       return st;
   }
+  if constexpr (!GROUPED_K) {
+    if (split) {
+      // kFlagSplit: num_m_blocks points at the unit table U of moe_split_units (a 128-row
+      // aligned plan): U[0] pairs, U[1] singles, U[2..2+cap) pair start blocks,
+      // U[2+cap..2+2cap) single blocks. The 256-row pairs run on the CTA-pair engine, each
+      // expert's odd last block on the 1-CTA engine (half the padding of a 256-row plan).
+      const int* U = p.num_m_blocks;
+      const int cap = p.max_m_blocks;
+      Params pp = p;
+      pp.unit_block = U + 2;
+      pp.num_m_blocks = U;
+      int st2 = launch_cg<A_MN, B_MN, GROUPED_K, EPI, 2, false>(ta, tb, tc, td, pp,
+                                                                 (cap / 2) * nb, stream);
+      if (st2) return st2;
+      CUtensorMap tb1 = tb;  // the 1-CTA engine stages all 256 B rows
+      if (!B_MN && (st2 = make_tmap(&tb1, b, b_inner, b_outer, b_inner, 64, BN))) return st2;
+      Params ps = p;
+      ps.unit_block = U + 2 + cap;
+      ps.num_m_blocks = U + 1;
+      const int singles = p.num_experts < cap ? p.num_experts : cap;
+      return launch_cg<A_MN, B_MN, GROUPED_K, EPI, 1, false>(ta, tb1, tc, td, ps, singles * nb,
+                                                             stream);
+    }
+  }
   if (pair)
     return launch_cg<A_MN, B_MN, GROUPED_K, EPI, 2, false>(ta, tb, tc, td, p,
                                                            (units_m / 2) * nb, stream);
@@ -1171,7 +1208,9 @@ static int fc1_fwd_impl(const void* xp, const void* w1, int a_rows, int max_rows
                         const float* row_prob, void* preact, void* act, int flags,
                         const SourceWait* w, void* stream) {
   const int pair = flags & kFlagPair;
-  if (h % BK || (2 * m) % BN || max_rows % (BM * (pair ? 2 : 1)) || a_rows > max_rows)
+  const int split = (flags & kFlagSplit) && pair;
+  if (h % BK || (2 * m) % BN || max_rows % (BM * (pair && !split ? 2 : 1)) ||
+      a_rows > max_rows || (split && w))
     return kErrInvalidArg;
   Params p{};
   set_wait(p, w);
@@ -1188,7 +1227,7 @@ static int fc1_fwd_impl(const void* xp, const void* w1, int a_rows, int max_rows
   p.row_scale = row_prob;
   return run<false, false, false, EPI_SWIGLU>(xp, h, a_rows, w1, h, (uint64_t)num_experts * 2 * m,
                                               p, p.max_m_blocks, pair,
-                                              static_cast<cudaStream_t>(stream));
+                                              static_cast<cudaStream_t>(stream), split);
 }
 
 int moe_gg_fc1_fwd(const void* xp, const void* w1, int a_rows, int max_rows, int h, int m,
@@ -1218,7 +1257,8 @@ static int fc2_fwd_impl(const void* act, const void* w2, int a_rows, int max_row
                         const int* num_m_blocks, void* out, const unsigned long long* row_dst,
                         int flags, void* stream) {
   const int pair = flags & kFlagPair;
-  if (m % BK || h % BN || max_rows % (BM * (pair ? 2 : 1)) || a_rows > max_rows)
+  const int split = (flags & kFlagSplit) && pair;
+  if (m % BK || h % BN || max_rows % (BM * (pair && !split ? 2 : 1)) || a_rows > max_rows)
     return kErrInvalidArg;
   Params p{};
   p.row_dst = row_dst;
@@ -1232,7 +1272,7 @@ static int fc2_fwd_impl(const void* act, const void* w2, int a_rows, int max_row
   p.ldo = h;
   return run<false, false, false, EPI_BF16>(act, m, a_rows, w2, m, (uint64_t)num_experts * h, p,
                                             p.max_m_blocks, pair,
-                                            static_cast<cudaStream_t>(stream));
+                                            static_cast<cudaStream_t>(stream), split);
 }
 
 // fc2 forward: out[rows, h] = act[rows, m] * w2_e^T, w2[E, h, m].
@@ -1265,7 +1305,9 @@ static int fc2_dgrad_impl(const void* dout, const void* w2, const void* preact, 
                           float* dprob_partial, int flags, const SourceWait* w,
                           void* stream) {
   const int pair = flags & kFlagPair;
-  if (h % BK || m % BN || max_rows % (BM * (pair ? 2 : 1)) || a_rows > max_rows)
+  const int split = (flags & kFlagSplit) && pair;
+  if (h % BK || m % BN || max_rows % (BM * (pair && !split ? 2 : 1)) || a_rows > max_rows ||
+      (split && w))
     return kErrInvalidArg;
   Params p{};
   set_wait(p, w);
@@ -1284,7 +1326,7 @@ static int fc2_dgrad_impl(const void* dout, const void* w2, const void* preact, 
   p.ld_partial = (m / BN) * DSW_HALVES;  // one partial per (n-tile, epilogue half)
   return run<false, true, false, EPI_DSWIGLU>(dout, h, a_rows, w2, m, (uint64_t)num_experts * h,
                                               p, p.max_m_blocks, pair,
-                                              static_cast<cudaStream_t>(stream));
+                                              static_cast<cudaStream_t>(stream), split);
 }
 
 int moe_gg_dprob_partials(int m) { return (m / BN) * DSW_HALVES; }
@@ -1315,7 +1357,8 @@ static int fc1_dgrad_impl(const void* d_preact, const void* w1, int a_rows, int 
                           const int* num_m_blocks, void* dxp,
                           const unsigned long long* row_dst, int flags, void* stream) {
   const int pair = flags & kFlagPair;
-  if ((2 * m) % BK || h % BN || max_rows % (BM * (pair ? 2 : 1)) || a_rows > max_rows)
+  const int split = (flags & kFlagSplit) && pair;
+  if ((2 * m) % BK || h % BN || max_rows % (BM * (pair && !split ? 2 : 1)) || a_rows > max_rows)
     return kErrInvalidArg;
   Params p{};
   p.row_dst = row_dst;
@@ -1329,7 +1372,7 @@ static int fc1_dgrad_impl(const void* d_preact, const void* w1, int a_rows, int 
   p.ldo = h;
   return run<false, true, false, EPI_BF16>(d_preact, 2 * m, a_rows, w1, h,
                                            (uint64_t)num_experts * 2 * m, p, p.max_m_blocks,
-                                           pair, static_cast<cudaStream_t>(stream));
+                                           pair, static_cast<cudaStream_t>(stream), split);
 }
 
 // fc1 data-gradient: dxp[rows, h] = d_preact[rows, 2m] * w1_e  (w1[E, 2m, h] read MN-major).

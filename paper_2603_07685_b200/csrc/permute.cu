@@ -180,6 +180,54 @@ __global__ void pad_rows_kernel(const int* __restrict__ meta, const int* __restr
   }
 }
 
+// Split units of a 128-row aligned padded plan (the grouped GEMMs' kFlagSplit): expert e's
+// blocks [off_pad[e] / 128, off_pad[e+1] / 128) become floor(n_e / 2) 256-row pairs and, when
+// n_e is odd, one single 128-row block (its last). One block of 1024 threads; block order is
+// preserved in both lists. U[0] = pairs, U[1] = singles, U[2 .. 2+cap) = pair start blocks,
+// U[2+cap .. 2+2cap) = single blocks.
+__global__ void split_units_kernel(const int* __restrict__ meta,
+                                   const int* __restrict__ block_expert,
+                                   const int* __restrict__ off_pad, int cap, int* __restrict__ U) {
+  __shared__ int s_pair[1024], s_single[1024];
+  const int nb = min(meta[0], cap);
+  const int per = (cap + blockDim.x - 1) / blockDim.x;
+  const int b0 = threadIdx.x * per, b1 = min(nb, b0 + per);
+  auto kind = [&](int b) {  // 1 = pair start, 2 = single, 0 = neither
+    const int e = __ldg(block_expert + b);
+    const int first = __ldg(off_pad + e) / ALIGN, end = __ldg(off_pad + e + 1) / ALIGN;
+    if ((b - first) & 1) return 0;
+    return b + 1 < end ? 1 : 2;
+  };
+  int np = 0, ns = 0;
+  for (int b = b0; b < b1; ++b) {
+    const int k = kind(b);
+    np += k == 1;
+    ns += k == 2;
+  }
+  s_pair[threadIdx.x] = np;
+  s_single[threadIdx.x] = ns;
+  __syncthreads();
+  // exclusive scans (Hillis-Steele over 1024 entries)
+  for (int off = 1; off < blockDim.x; off <<= 1) {
+    const int a = threadIdx.x >= off ? s_pair[threadIdx.x - off] : 0;
+    const int c = threadIdx.x >= off ? s_single[threadIdx.x - off] : 0;
+    __syncthreads();
+    s_pair[threadIdx.x] += a;
+    s_single[threadIdx.x] += c;
+    __syncthreads();
+  }
+  int ip = s_pair[threadIdx.x] - np, is = s_single[threadIdx.x] - ns;
+  for (int b = b0; b < b1; ++b) {
+    const int k = kind(b);
+    if (k == 1) U[2 + ip++] = b;
+    if (k == 2) U[2 + cap + is++] = b;
+  }
+  if (threadIdx.x == blockDim.x - 1) {
+    U[0] = s_pair[threadIdx.x];
+    U[1] = s_single[threadIdx.x];
+  }
+}
+
 // compact (oracle-layout) map: compact row j of expert e = padded row off_pad[e] + (j - off_c[e])
 __global__ void compact_map_kernel(const int* __restrict__ meta, const int* __restrict__ off_c,
                                    const int* __restrict__ off_pad, int E,
@@ -845,6 +893,17 @@ int moe_ep_row_dst(const int* table, int n, int el, int rows_pad, const int* dst
 }
 
 // Oracle-layout (compact) row_id_map (int64, -1 phantom) and compact->padded row index.
+// Unit table of a 128-row aligned padded plan for the grouped GEMMs' split mode (kFlagSplit):
+// U [2 + 2 * cap] int32, cap = the plan's max_rows / 128.
+int moe_split_units(const int* meta, const int* block_expert, const int* off_pad, int cap,
+                    int* U, void* stream) {
+  if (cap < 1) return kErrInvalidArg;
+  split_units_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(meta, block_expert,
+                                                                        off_pad, cap, U);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
 int moe_permute_compact_map(const int* meta, const int* off_c, const int* off_pad, int E,
                             const int* row_src, long long* row_id_map, int* compact_to_pad,
                             int max_compact, void* stream) {

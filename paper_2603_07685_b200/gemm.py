@@ -68,8 +68,16 @@ def _wait_args(wait):
     return (flag.data_ptr(), epoch.data_ptr(), need.data_ptr(), _ptr(order), _ptr(status))
 
 
+def _blocks(num_m_blocks, pair, units):
+    """(num_m_blocks-or-unit-table pointer, flags) of a grouped-M call: with a split-unit
+    table (ops.Plan.units) the table stands in for num_m_blocks and flags = pair | split."""
+    if units is not None:
+        return units.data_ptr(), 3
+    return num_m_blocks.data_ptr(), int(pair)
+
+
 def fc1_fwd(xp, w1, block_expert, num_m_blocks, row_prob=None, preact=None, act=None,
-            max_rows=None, pair=False, wait=None):
+            max_rows=None, pair=False, wait=None, units=None):
     a_rows, h = xp.shape
     rows = a_rows if max_rows is None else max_rows
     e, m2, _ = w1.shape
@@ -78,9 +86,9 @@ def fc1_fwd(xp, w1, block_expert, num_m_blocks, row_prob=None, preact=None, act=
         preact = torch.empty((rows, m2), dtype=torch.bfloat16, device=xp.device)
     if act is None:
         act = torch.empty((rows, m), dtype=torch.bfloat16, device=xp.device)
+    nmb, flags = _blocks(num_m_blocks, pair, units)
     args = (xp.data_ptr(), w1.data_ptr(), a_rows, rows, h, m, e, block_expert.data_ptr(),
-            num_m_blocks.data_ptr(), _ptr(row_prob), preact.data_ptr(), act.data_ptr(),
-            int(pair))
+            nmb, _ptr(row_prob), preact.data_ptr(), act.data_ptr(), flags)
     if wait is None:
         _lib.call("moe_gg_fc1_fwd", *args, _stream())
     else:
@@ -88,15 +96,16 @@ def fc1_fwd(xp, w1, block_expert, num_m_blocks, row_prob=None, preact=None, act=
     return preact, act
 
 
-def fc2_fwd(act, w2, block_expert, num_m_blocks, out=None, max_rows=None, pair=False):
+def fc2_fwd(act, w2, block_expert, num_m_blocks, out=None, max_rows=None, pair=False,
+            units=None):
     a_rows, m = act.shape
     rows = a_rows if max_rows is None else max_rows
     e, h, _ = w2.shape
     if out is None:
         out = torch.empty((rows, h), dtype=torch.bfloat16, device=act.device)
+    nmb, flags = _blocks(num_m_blocks, pair, units)
     _lib.call("moe_gg_fc2_fwd", act.data_ptr(), w2.data_ptr(), a_rows, rows, m, h, e,
-              block_expert.data_ptr(), num_m_blocks.data_ptr(), out.data_ptr(), int(pair),
-              _stream())
+              block_expert.data_ptr(), nmb, out.data_ptr(), flags, _stream())
     return out
 
 
@@ -121,7 +130,7 @@ def fc1_dgrad_scatter(d_preact, w1, block_expert, num_m_blocks, row_dst, max_row
 
 
 def fc2_dgrad(dout, w2, preact, block_expert, num_m_blocks, row_prob=None, want_dprob=False,
-              d_preact=None, max_rows=None, pair=False, part=None, wait=None):
+              d_preact=None, max_rows=None, pair=False, part=None, wait=None, units=None):
     """part: optional preallocated [rows, m/256] fp32 dprob partials (implies want_dprob)."""
     a_rows, h = dout.shape
     rows = a_rows if max_rows is None else max_rows
@@ -130,9 +139,10 @@ def fc2_dgrad(dout, w2, preact, block_expert, num_m_blocks, row_prob=None, want_
         d_preact = torch.empty((rows, 2 * m), dtype=torch.bfloat16, device=dout.device)
     if want_dprob and part is None:
         part = torch.empty((rows, dprob_partials(m)), dtype=torch.float32, device=dout.device)
+    nmb, flags = _blocks(num_m_blocks, pair, units)
     args = (dout.data_ptr(), w2.data_ptr(), preact.data_ptr(), a_rows, rows, h, m, e,
-            block_expert.data_ptr(), num_m_blocks.data_ptr(), _ptr(row_prob),
-            d_preact.data_ptr(), _ptr(part), int(pair))
+            block_expert.data_ptr(), nmb, _ptr(row_prob), d_preact.data_ptr(), _ptr(part),
+            flags)
     if wait is None:
         _lib.call("moe_gg_fc2_dgrad", *args, _stream())
     else:
@@ -140,15 +150,16 @@ def fc2_dgrad(dout, w2, preact, block_expert, num_m_blocks, row_prob=None, want_
     return d_preact, part
 
 
-def fc1_dgrad(d_preact, w1, block_expert, num_m_blocks, out=None, max_rows=None, pair=False):
+def fc1_dgrad(d_preact, w1, block_expert, num_m_blocks, out=None, max_rows=None, pair=False,
+              units=None):
     a_rows, m2 = d_preact.shape
     rows = a_rows if max_rows is None else max_rows
     e, _, h = w1.shape
     if out is None:
         out = torch.empty((rows, h), dtype=torch.bfloat16, device=d_preact.device)
+    nmb, flags = _blocks(num_m_blocks, pair, units)
     _lib.call("moe_gg_fc1_dgrad", d_preact.data_ptr(), w1.data_ptr(), a_rows, rows, m2 // 2, h, e,
-              block_expert.data_ptr(), num_m_blocks.data_ptr(), out.data_ptr(), int(pair),
-              _stream())
+              block_expert.data_ptr(), nmb, out.data_ptr(), flags, _stream())
     return out
 
 

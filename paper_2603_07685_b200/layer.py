@@ -64,7 +64,8 @@ class _MoEFunction(torch.autograd.Function):
             raise ValueError("router logits are not finite")
         cap = cfg.capacity(t)
         plan = ops.build_plan(r.topk_idx, r.topk_prob, e, cap, cfg.pad_to_capacity,
-                              align=ops.pick_align(t, cfg.top_k, e))
+                              align=ops.pick_align(t, cfg.top_k, e),
+                              split=cfg.precision == "bf16")
         xp = ops.permute_gather(x, plan)
         row_prob = plan.row_prob if cfg.mem_efficient else None
         act_t = None
@@ -74,8 +75,9 @@ class _MoEFunction(torch.autograd.Function):
             act = None  # the weight gradient reads the token-row quantised copy
         else:
             preact, act = gemm.fc1_fwd(xp, w1, plan.block_expert, plan.num_m_blocks, row_prob,
-                                       pair=plan.pair)
-            o = gemm.fc2_fwd(act, w2, plan.block_expert, plan.num_m_blocks, pair=plan.pair)
+                                       pair=plan.pair, units=plan.units)
+            o = gemm.fc2_fwd(act, w2, plan.block_expert, plan.num_m_blocks, pair=plan.pair,
+                             units=plan.units)
         shared = shared_expert_forward(x, w1s, w2s) if w1s is not None else None
         y = ops.combine(o, plan, None if cfg.mem_efficient else r.topk_prob,
                         resid=x if cap >= 0 else None,
@@ -98,13 +100,13 @@ class _MoEFunction(torch.autograd.Function):
             d_o, _ = ops.combine_backward(dy, plan, None, None)
             d_pre, part = gemm.fc2_dgrad(d_o, w2, preact, plan.block_expert, plan.num_m_blocks,
                                          row_prob=plan.row_prob, want_dprob=True,
-                                         pair=plan.pair)
+                                         pair=plan.pair, units=plan.units)
             dprob = ops.dprob_from_partials(plan, part)
         else:
             d_o, dprob = ops.combine_backward(dy, plan, o, r.topk_prob)
             if cfg.precision != "mxfp8":
                 d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, plan.block_expert,
-                                          plan.num_m_blocks, pair=plan.pair)
+                                          plan.num_m_blocks, pair=plan.pair, units=plan.units)
         if cfg.precision == "mxfp8":
             dxp, dw1, dw2 = gemm.mxfp8_experts_bwd(d_o, xp, w1, w2, preact, ctx.act_t,
                                                    plan.block_expert, plan.num_m_blocks,
@@ -112,7 +114,7 @@ class _MoEFunction(torch.autograd.Function):
         else:
             dw2 = gemm.wgrad(d_o, act, plan.off_pad, e)
             dxp = gemm.fc1_dgrad(d_pre, w1, plan.block_expert, plan.num_m_blocks,
-                                 pair=plan.pair)
+                                 pair=plan.pair, units=plan.units)
             dw1 = gemm.wgrad(d_pre, xp, plan.off_pad, e)
         aux_scale = None if daux is None else daux.float()
         dw_r, dx_router = ops.router_backward(x, w_r_pad, r, dprob, cfg.score,

@@ -396,6 +396,10 @@ class Plan:
     row_prob: torch.Tensor      # [max_rows] fp32
     status: torch.Tensor        # [1] bit1 = overflow of max_rows
     align: int = ALIGN          # expert block alignment (256: CTA-pair GEMM engine)
+    # split units (build_plan(split=True)): a 128-row aligned plan whose grouped GEMMs run
+    # each expert's 256-row pairs on the CTA-pair engine and its odd last 128-row block on
+    # the 1-CTA engine (moe_split_units table, passed as the GEMMs' `units`)
+    units: torch.Tensor | None = None
 
     @property
     def num_m_blocks(self) -> torch.Tensor:
@@ -403,7 +407,7 @@ class Plan:
 
     @property
     def pair(self) -> bool:
-        return self.align == 2 * ALIGN
+        return self.align == 2 * ALIGN or self.units is not None
 
 
 def plan_max_rows(T: int, K: int, E: int, capacity: int = -1, pad: bool = False,
@@ -428,16 +432,31 @@ def pick_align(T: int, K: int, E: int) -> int:
     return 2 * ALIGN if T * K >= 8 * 2 * ALIGN * E else ALIGN
 
 
+# Split units for the pair engine (Plan.units): on by default; MOE_B200_SPLIT_UNITS=0 keeps
+# the 256-row aligned plan (A/B)
+SPLIT_UNITS = os.environ.get("MOE_B200_SPLIT_UNITS", "1") != "0"
+
+
 def build_plan(topk_idx: torch.Tensor, topk_prob: torch.Tensor | None, E: int,
                capacity: int = -1, pad: bool = False, max_rows: int | None = None,
                phantom: torch.Tensor | None = None, phantom_max: int = 0,
                cap_e: torch.Tensor | None = None, compact: bool = False,
-               align: int = ALIGN) -> Plan:
+               align: int = ALIGN, split: bool = False) -> Plan:
     """phantom: optional device int32 [E] extra zero rows per expert (routing_map_pad);
     phantom_max bounds it for buffer sizing. cap_e: optional device int32 [E] per-expert
-    capacity (EP global-position drops). compact: no 128-row alignment (EP send layout)."""
+    capacity (EP global-position drops). compact: no 128-row alignment (EP send layout).
+    split (with align 256, bf16 expert GEMMs only): build the 128-row aligned plan plus the
+    split-unit table instead (half the padding; Plan.units)."""
     t, k = topk_idx.shape
     dev = topk_idx.device
+    # measured (profiles/r02_split_units_ab.txt, alternating runs on one box): Mixtral
+    # (~4096 rows per expert) 30.85 -> 30.26 ms per step; Qwen3 (~2048 rows per expert, 128
+    # experts: ~64 one-block tails per GEMM on the 1-CTA engine) 31.0 -> 31.2 ms. Split
+    # where experts hold >= 16 pair units.
+    split = (split and SPLIT_UNITS and align == 2 * ALIGN and not compact
+             and t * k >= 16 * 2 * ALIGN * E)
+    if split:
+        align = ALIGN
     if max_rows is None:
         if compact:
             max_rows = max(t * k, 1)
@@ -463,9 +482,15 @@ def build_plan(topk_idx: torch.Tensor, topk_prob: torch.Tensor | None, E: int,
               eff.data_ptr(), counts.data_ptr(), _p(block_expert), inv_map.data_ptr(),
               row_src.data_ptr(), row_prob.data_ptr(), ws.data_ptr(), status.data_ptr(),
               _stream())
+    units = None
+    if split:
+        cap = max_rows // ALIGN
+        units = torch.empty((2 + 2 * cap,), **i32)
+        _lib.call("moe_split_units", meta.data_ptr(), block_expert.data_ptr(), off_pad.data_ptr(),
+                  cap, units.data_ptr(), _stream())
     return Plan(t, k, E, int(capacity), bool(pad), max_rows, meta, off_pad, off_c, kept, eff,
                 counts, block_expert, inv_map, row_src, row_prob, status,
-                1 if compact else align)
+                1 if compact else align, units)
 
 
 def compact_row_id_map(plan: Plan, n_compact: int | None = None):

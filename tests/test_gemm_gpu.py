@@ -179,3 +179,61 @@ def test_gemm_f32_large_k(dev):
     for e, c in enumerate(counts):
         sl = slice(oh[e], oh[e] + c)
         assert _relerr(out[sl], a[sl].float() @ b[e].float().T) < 1e-4
+
+
+def test_split_units_all_grouped_m_gemms(dev):
+    """Split units (ops.Plan.units, flags pair | split): a 128-row aligned plan whose experts
+    run as 256-row pairs on the CTA-pair engine plus an odd last 128-row block on the 1-CTA
+    engine. Odd and even block counts, an empty expert and enough pairs for several waves;
+    every grouped-M GEMM against torch fp32, and the unit table against its definition."""
+    from paper_2603_07685_b200 import _lib
+
+    g = torch.Generator().manual_seed(7)
+    counts = [200, 0, 333, 128, 1, 2500, 640, 129]
+    E, m, h = len(counts), 256, 512
+    global ALIGN
+    ALIGN = 128
+    offs, be, nmb, rows, max_rows = _layout(counts, dev)
+    oh = offs.tolist()
+    cap = max_rows // 128
+    meta = torch.tensor([rows // 128, rows, 0], dtype=torch.int32, device=dev)
+    units = torch.full((2 + 2 * cap,), -7, dtype=torch.int32, device=dev)
+    _lib.call("moe_split_units", meta.data_ptr(), be.data_ptr(), offs.data_ptr(), cap,
+              units.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    u = units.cpu().tolist()
+    pairs, singles = [], []
+    for e in range(E):
+        b0, b1 = oh[e] // 128, oh[e + 1] // 128
+        pairs += list(range(b0, b1 - 1, 2))
+        if (b1 - b0) % 2:
+            singles.append(b1 - 1)
+    assert u[0] == len(pairs) and u[1] == len(singles)
+    assert u[2: 2 + u[0]] == pairs and u[2 + cap: 2 + cap + u[1]] == singles
+
+    xp = _rows(counts, oh, h, dev, g)
+    w1 = (torch.randn((E, 2 * m, h), generator=g) / h ** 0.5).to(dev, torch.bfloat16)
+    w2 = (torch.randn((E, h, m), generator=g) / m ** 0.5).to(dev, torch.bfloat16)
+    kw = dict(pair=True, units=units)
+    preact, act = gemm.fc1_fwd(xp, w1, be, nmb, **kw)
+    o = gemm.fc2_fwd(act, w2, be, nmb, **kw)
+    dout = _rows(counts, oh, h, dev, g)
+    d_pre, _ = gemm.fc2_dgrad(dout, w2, preact, be, nmb, **kw)
+    dxp = gemm.fc1_dgrad(d_pre, w1, be, nmb, **kw)
+    torch.cuda.synchronize()
+    for e, c in enumerate(counts):
+        if not c:
+            continue
+        sl = slice(oh[e], oh[e] + c)
+        pre_ref = xp[sl].float() @ w1[e].float().T
+        assert _relerr(preact[sl], pre_ref) < 1e-2, ("fc1", e)
+        gate, up = gemm.deinterleave_cols(preact[sl].float())
+        a_ref = torch.nn.functional.silu(gate) * up
+        assert _relerr(act[sl], a_ref) < 1e-2, ("act", e)
+        assert _relerr(o[sl], act[sl].float() @ w2[e].float().T) < 1e-2, ("fc2", e)
+        da = dout[sl].float() @ w2[e].float()
+        s = torch.sigmoid(gate)
+        dg_ref = da * up * s * (1 + gate * (1 - s))
+        du_ref = da * gate * s
+        dg, du = gemm.deinterleave_cols(d_pre[sl].float())
+        assert _relerr(dg, dg_ref) < 2e-2 and _relerr(du, du_ref) < 2e-2, ("fc2 dgrad", e)
+        assert _relerr(dxp[sl], d_pre[sl].float() @ w1[e].float()) < 1e-2, ("fc1 dgrad", e)
