@@ -46,7 +46,25 @@ def _join_all(procs):
             p.join(timeout=10)
 
 
+def _worker_diag(rank, port, transport):
+    """MOE_TEST_WORKER_LOG=dir: this worker's stderr goes to dir/ep_<port>_<transport>_r<rank>.log
+    and a hung worker dumps every thread's Python stack there shortly before the test's queue
+    timeout (diagnosing a rank that never reports)."""
+    d = os.environ.get("MOE_TEST_WORKER_LOG")
+    if not d:
+        return
+    import faulthandler
+
+    os.makedirs(d, exist_ok=True)
+    f = open(os.path.join(d, f"ep_{port}_{transport}_r{rank}.log"), "w")
+    os.dup2(f.fileno(), 2)
+    faulthandler.enable(file=f)
+    faulthandler.dump_traceback_later(
+        max(int(os.environ.get("MOE_TEST_TIMEOUT", "300")) - 20, 10), exit=False, file=f)
+
+
 def _worker(rank, world, port, case, q, transport):
+    _worker_diag(rank, port, transport)
     try:
         import torch.distributed as dist
 
