@@ -106,7 +106,11 @@ def test_ep_pair_engine_matches_global_oracle(name, transport):
     _run(PAIR_CASES[name], transport)
 
 
-def _run(case, transport):
+def _run(case, transport, attempt=0):
+    """One EP group of spawned ranks on the box's GPUs. A group in which no rank reported
+    anything (no error, no result: a process-group start-up that never completed; seen twice
+    in ~200 four-GPU runs, not reproducible on a re-run) is retried once on a fresh port; a
+    rank that reports an error fails the test at once."""
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
     # the whole EP group of the box (all visible GPUs: EP=8 on an 8-GPU box);
@@ -123,13 +127,25 @@ def _run(case, transport):
              for r in range(world)]
     for p in procs:
         p.start()
+    import queue as _queue
+
+    res = []
     try:
-        res = [q.get(timeout=int(os.environ.get("MOE_TEST_TIMEOUT", "300")))
-               for _ in range(world)]
+        for _ in range(world):
+            res.append(q.get(timeout=int(os.environ.get("MOE_TEST_TIMEOUT", "300"))))
+    except _queue.Empty:
+        pass
     finally:
         _join_all(procs)
+    # a rank that failed reports first; the others then wait on it in a collective
     for rank, msg in res:
         assert msg == "ok", f"rank {rank}: {msg}"
+    if not res and attempt == 0:
+        import warnings
+
+        warnings.warn(f"EP group {case} / {transport}: no rank reported; retrying once")
+        return _run(case, transport, attempt=1)
+    assert len(res) == world, f"only ranks {[r for r, _ in res]} of {world} reported"
 
 
 def _stash_worker(rank, world, port, q):
@@ -216,10 +232,17 @@ def test_ep_paged_stash_two_layers():
     procs = [ctx.Process(target=_stash_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
+    import queue as _queue
+
+    res = []
     try:
-        res = [q.get(timeout=int(os.environ.get("MOE_TEST_TIMEOUT", "300")))
-               for _ in range(world)]
+        for _ in range(world):
+            res.append(q.get(timeout=int(os.environ.get("MOE_TEST_TIMEOUT", "300"))))
+    except _queue.Empty:
+        pass
     finally:
         _join_all(procs)
+    # a rank that failed reports first; the others then wait on it in a collective
     for rank, msg in res:
         assert msg == "ok", f"rank {rank}: {msg}"
+    assert len(res) == world, f"only ranks {[r for r, _ in res]} of {world} reported"
