@@ -430,6 +430,9 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
   } else {
     num_tiles = p.num_experts * (p.M / (BM * CG)) * (p.N / BN);
   }
+  // Allow a programmatic-dependent launch queued behind this grid (the split-unit tail
+  // launch, which touches disjoint rows) to take SMs as soon as this grid's CTAs retire.
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int first = blockIdx.x / CG;
   const int stride = gridDim.x / CG;
 
@@ -963,6 +966,9 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
                    : "memory");
     }
   }
+  // A programmatic-dependent grid (the split-unit tail) completes only after the grid it
+  // overlapped, so work queued behind it sees both. No-op for a normal launch.
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ host side
@@ -1003,7 +1009,7 @@ static int num_sms() { return device_sms(); }
 template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI, int CG, bool SK>
 static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                      const CUtensorMap& td, const Params& p, int max_tiles,
-                     cudaStream_t stream) {
+                     cudaStream_t stream, bool pdl = false) {
   auto kern = grouped_gemm_kernel<A_MN, B_MN, GROUPED_K, EPI, CG, SK>;
   MOE_CUDA_CHECK(ensure_dyn_smem(reinterpret_cast<const void*>(kern),
                                  smem_bytes<EPI, GROUPED_K, CG, SK>()));
@@ -1015,13 +1021,15 @@ static int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtenso
   cfg.blockDim = dim3(64 + 32 * epi_warps<GROUPED_K, EPI>());
   cfg.dynamicSmemBytes = smem_bytes<EPI, GROUPED_K, CG, SK>();
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   MOE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, td, p));
   return kOk;
 }
@@ -1163,8 +1171,20 @@ static int run(const void* a, uint64_t a_inner, uint64_t a_outer, const void* b,
       ps.unit_block = U + 2 + cap;
       ps.num_m_blocks = U + 1;
       const int singles = p.num_experts < cap ? p.num_experts : cap;
+      // programmatic dependent launch: the tail tiles take the SMs the pair grid's last
+      // wave leaves idle (disjoint rows, no data dependency; the next launch on the stream
+      // still waits for both). Its own wave sync would share the stream's counter: off.
+      static int pdl = -1;
+      if (pdl < 0) {
+        const char* e = getenv("MOE_B200_SPLIT_PDL");
+        pdl = (e && e[0] == '0') ? 0 : 1;
+      }
+      if (pdl) {
+        ps.sync_on = 0;
+        ps.sync_slot = -1;
+      }
       return launch_cg<A_MN, B_MN, GROUPED_K, EPI, 1, false>(ta, tb1, tc, td, ps, singles * nb,
-                                                             stream);
+                                                             stream, pdl != 0);
     }
   }
   if (pair)
