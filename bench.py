@@ -425,6 +425,13 @@ def run_gpu(args, c) -> None:
         t_wait = time.time()
         while not clocks.lines and time.time() - t_wait < 10:
             time.sleep(0.05)
+    # Python's cyclic GC can pause the host long enough to drain the GPU queue in the
+    # middle of a timed step (seen as isolated 34-43 ms steps in A/B runs whose GEMM time
+    # was unchanged): collect once now, keep it off through warm-up and every timed region
+    import gc
+
+    gc.collect()
+    gc.disable()
     if not args.graph:
         for _ in range(args.warmup):
             step(x, dy)
@@ -774,6 +781,7 @@ def run_gpu(args, c) -> None:
             cb = cpu_baseline(c, args.cpu_sample_tokens, thr)
             out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         emit(out)
+    gc.enable()
     if n > 1:
         dist.barrier()
         dist.destroy_process_group()

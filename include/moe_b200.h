@@ -303,6 +303,11 @@ int moe_gg_fc1_dgrad(const void* d_preact, const void* w1, int a_rows, int max_r
                      void* dxp, int flags, void* stream);
 int moe_gg_wgrad(const void* a, const void* b, int max_rows, int M, int N, int num_experts,
                  const int* expert_offsets, void* dw, void* stream);
+/* moe_gg_wgrad with flags: bit 0 = programmatic dependent launch (the caller asserts the
+ * gradient reads nothing the previous launch on the stream writes; it fills that launch's
+ * last wave and completes after it). */
+int moe_gg_wgrad_ex(const void* a, const void* b, int max_rows, int M, int N, int num_experts,
+                    const int* expert_offsets, void* dw, int flags, void* stream);
 int moe_gg_wgrad_f32(const void* a, const void* b, int max_rows, int M, int N,
                      int num_groups, const int* offsets, float* dw, void* stream);
 int moe_gg_gemm_f32(const void* a, const void* b, int a_rows, int max_rows, int K, int N,

@@ -102,6 +102,7 @@ SIGNATURES: dict[str, list] = {
     "moe_gg_fc2_dgrad": [P, P, P, I, I, I, I, I, P, P, P, P, P, I, P],
     "moe_gg_fc1_dgrad": [P, P, I, I, I, I, I, P, P, P, I, P],
     "moe_gg_wgrad": [P, P, I, I, I, I, P, P, P],
+    "moe_gg_wgrad_ex": [P, P, I, I, I, I, P, P, I, P],
     "moe_gg_wgrad_f32": [P, P, I, I, I, I, P, P, P],
     "moe_gg_gemm_f32": [P, P, I, I, I, I, I, P, P, P, P],
 }

@@ -1055,7 +1055,7 @@ static int stream_stores_default() {
 template <bool A_MN, bool B_MN, bool GROUPED_K, int EPI>
 static int run(const void* a, uint64_t a_inner, uint64_t a_outer, const void* b,
                uint64_t b_inner, uint64_t b_outer, Params p, int units_m, int pair,
-               cudaStream_t stream, int split = 0) {
+               cudaStream_t stream, int split = 0, int pdl_launch = 0) {
   p.stream_stores = stream_stores_default();
   {
     static int bm = -1;  // MOE_B200_BAND forces a band; else auto (pair) / BAND_M (1-CTA)
@@ -1128,8 +1128,9 @@ static int run(const void* a, uint64_t a_inner, uint64_t a_outer, const void* b,
         return st;
       if (pair)
         return launch_cg<A_MN, B_MN, true, EPI, 2, true>(ta, tb, tc, tc, p, (units_m / 2) * nb,
-                                                         stream);
-      return launch_cg<A_MN, B_MN, true, EPI, 1, true>(ta, tb, tc, tc, p, units_m * nb, stream);
+                                                         stream, pdl_launch != 0);
+      return launch_cg<A_MN, B_MN, true, EPI, 1, true>(ta, tb, tc, tc, p, units_m * nb, stream,
+                                                       pdl_launch != 0);
     }
   }
   tc = tb;  // unused by the other variants
@@ -1189,9 +1190,10 @@ static int run(const void* a, uint64_t a_inner, uint64_t a_outer, const void* b,
   }
   if (pair)
     return launch_cg<A_MN, B_MN, GROUPED_K, EPI, 2, false>(ta, tb, tc, td, p,
-                                                           (units_m / 2) * nb, stream);
+                                                           (units_m / 2) * nb, stream,
+                                                           pdl_launch != 0);
   return launch_cg<A_MN, B_MN, GROUPED_K, EPI, 1, false>(ta, tb, tc, td, p, units_m * nb,
-                                                         stream);
+                                                         stream, pdl_launch != 0);
 }
 
 }  // namespace gg
@@ -1420,6 +1422,15 @@ int moe_gg_fc1_dgrad_scatter(const void* d_preact, const void* w1, int a_rows, i
 // read as zero. Uses the CTA-pair engine whenever M % 256 == 0.
 int moe_gg_wgrad(const void* a, const void* b, int max_rows, int M, int N, int num_experts,
                  const int* expert_offsets, void* dw, void* stream) {
+  return moe_gg_wgrad_ex(a, b, max_rows, M, N, num_experts, expert_offsets, dw, 0, stream);
+}
+
+// moe_gg_wgrad with flags: bit 0 = programmatic dependent launch. The caller asserts the
+// weight gradient does not read what the previous launch on the stream writes (e.g. dW2
+// after the fc2 data-gradient: both only read d_O), so it may take the SMs that launch's
+// last wave leaves idle; it completes after that launch.
+int moe_gg_wgrad_ex(const void* a, const void* b, int max_rows, int M, int N, int num_experts,
+                    const int* expert_offsets, void* dw, int flags, void* stream) {
   if (M % BM || N % BN) return kErrInvalidArg;
   Params p{};
   p.expert_offsets = expert_offsets;
@@ -1432,7 +1443,7 @@ int moe_gg_wgrad(const void* a, const void* b, int max_rows, int M, int N, int n
   const int pair = (M % (2 * BM)) == 0;
   return run<true, true, true, EPI_BF16>(a, M, max_rows, b, N, max_rows, p,
                                          num_experts * (M / BM), pair,
-                                         static_cast<cudaStream_t>(stream));
+                                         static_cast<cudaStream_t>(stream), 0, flags & 1);
 }
 
 // Same as moe_gg_wgrad with fp32 output (split-K partials of the router weight gradient:

@@ -163,18 +163,20 @@ def fc1_dgrad(d_preact, w1, block_expert, num_m_blocks, out=None, max_rows=None,
     return out
 
 
-def wgrad(a, b, expert_offsets, num_experts, out=None, max_rows=None):
+def wgrad(a, b, expert_offsets, num_experts, out=None, max_rows=None, overlap_prev=False):
     """out[e] = a[rows_e]^T @ b[rows_e] for each expert's padded row range.
 
-    max_rows bounds the rows TMA reads from both operands (beyond it: zeros)."""
+    max_rows bounds the rows TMA reads from both operands (beyond it: zeros).
+    overlap_prev: programmatic dependent launch; the caller asserts a and b are not written
+    by the previous launch on the stream (it then fills that launch's last wave)."""
     rows, M = a.shape
     if max_rows is not None:
         rows = max_rows
     _, N = b.shape
     if out is None:
         out = torch.empty((num_experts, M, N), dtype=torch.bfloat16, device=a.device)
-    _lib.call("moe_gg_wgrad", a.data_ptr(), b.data_ptr(), rows, M, N, num_experts,
-              expert_offsets.data_ptr(), out.data_ptr(), _stream())
+    _lib.call("moe_gg_wgrad_ex", a.data_ptr(), b.data_ptr(), rows, M, N, num_experts,
+              expert_offsets.data_ptr(), out.data_ptr(), 1 if overlap_prev else 0, _stream())
     return out
 
 

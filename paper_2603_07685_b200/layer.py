@@ -15,11 +15,16 @@ No host synchronisation happens in forward or backward at EP = 1.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import torch
 
 from . import gemm, ops
+
+# weight gradients as programmatic dependent launches behind the data-gradient GEMMs
+# (MOE_B200_WGRAD_PDL=0: plain launches, for A/B)
+OVERLAP_WGRAD = os.environ.get("MOE_B200_WGRAD_PDL", "1") != "0"
 
 
 @dataclass(frozen=True)
@@ -112,10 +117,13 @@ class _MoEFunction(torch.autograd.Function):
                                                    plan.block_expert, plan.num_m_blocks,
                                                    plan.off_pad, plan.pair)
         else:
-            dw2 = gemm.wgrad(d_o, act, plan.off_pad, e)
+            # each weight gradient reads nothing the data-gradient GEMM launched just before
+            # it writes (dW2: d_O, act; dW1: d_pre, xp), so it is launched to overlap that
+            # GEMM's last wave (programmatic dependent launch)
+            dw2 = gemm.wgrad(d_o, act, plan.off_pad, e, overlap_prev=OVERLAP_WGRAD)
             dxp = gemm.fc1_dgrad(d_pre, w1, plan.block_expert, plan.num_m_blocks,
                                  pair=plan.pair, units=plan.units)
-            dw1 = gemm.wgrad(d_pre, xp, plan.off_pad, e)
+            dw1 = gemm.wgrad(d_pre, xp, plan.off_pad, e, overlap_prev=OVERLAP_WGRAD)
         aux_scale = None if daux is None else daux.float()
         dw_r, dx_router = ops.router_backward(x, w_r_pad, r, dprob, cfg.score,
                                               aux_scale=aux_scale)

@@ -435,6 +435,7 @@ def pick_align(T: int, K: int, E: int) -> int:
 # Split units for the pair engine (Plan.units): on by default; MOE_B200_SPLIT_UNITS=0 keeps
 # the 256-row aligned plan (A/B)
 SPLIT_UNITS = os.environ.get("MOE_B200_SPLIT_UNITS", "1") != "0"
+SPLIT_FORCE = os.environ.get("MOE_B200_SPLIT_UNITS", "1") == "2"  # (A/B: ignore the size rule)
 
 
 def build_plan(topk_idx: torch.Tensor, topk_prob: torch.Tensor | None, E: int,
@@ -454,7 +455,7 @@ def build_plan(topk_idx: torch.Tensor, topk_prob: torch.Tensor | None, E: int,
     # experts: ~64 one-block tails per GEMM on the 1-CTA engine) 31.0 -> 31.2 ms. Split
     # where experts hold >= 16 pair units.
     split = (split and SPLIT_UNITS and align == 2 * ALIGN and not compact
-             and t * k >= 16 * 2 * ALIGN * E)
+             and (SPLIT_FORCE or t * k >= 16 * 2 * ALIGN * E))
     if split:
         align = ALIGN
     if max_rows is None:
