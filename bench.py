@@ -439,37 +439,73 @@ def run_gpu(args, c) -> None:
 
     run = step
     graph_launches = None
+    graph_error = None
+    graph_events = None
     if args.graph:
         # whole fwd+bwd step (router, EP planning on the device, exchanges, GEMMs, NCCL
         # all-gather / barriers) captured once and replayed: no host work per step
         # warm-up on a side stream only: eager steps on the legacy default stream before
         # the capture make it fail (cudaErrorStreamCaptureImplicit, measured at EP=1)
-        sx, sdy = x.clone(), dy.clone()
-        side = torch.cuda.Stream(device=dev)
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
-            for _ in range(max(args.warmup, 2)):
-                step(sx, sdy)
-        torch.cuda.current_stream().wait_stream(side)
-        barrier()
-        graph = torch.cuda.CUDAGraph()
-        l0 = _lib.stats.launches
-        with torch.cuda.graph(graph):
-            g_out = step(sx, sdy)
-        graph_launches = _lib.stats.launches - l0
-        barrier()
+        try:
+            sx, sdy = x.clone(), dy.clone()
+            side = torch.cuda.Stream(device=dev)
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                for _ in range(max(args.warmup, 2)):
+                    step(sx, sdy)
+            torch.cuda.current_stream().wait_stream(side)
+            barrier()
+            graph = torch.cuda.CUDAGraph()
+            l0 = _lib.stats.launches
+            # per-call CUDA events (roofline) captured into the graph as event-record nodes:
+            # every replay re-records them, so after the timed region they hold the last
+            # timed step's per-kernel durations, measured live
+            graph_events = None
+            if os.environ.get("MOE_BENCH_KERNEL_EVENTS", "1") != "0":
+                _lib.stats.prepare(128, external=True)
+                _lib.stats.events = []
+                _lib.stats.timing = True
+            try:
+                with torch.cuda.graph(graph):
+                    g_out = step(sx, sdy)
+                graph_events = list(_lib.stats.events) if _lib.stats.timing else None
+            except Exception:  # noqa: BLE001  (capture again without the event nodes)
+                if not _lib.stats.timing:
+                    raise
+                _lib.stats.timing = False
+                torch.cuda.synchronize()
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph):
+                    g_out = step(sx, sdy)
+            _lib.stats.timing = False
+            _lib.stats.events = []
+            graph_launches = _lib.stats.launches - l0
+            barrier()
 
-        def run(xx, dyy):
-            if xx is not sx:
-                sx.copy_(xx, non_blocking=True)
-                sdy.copy_(dyy, non_blocking=True)
-            graph.replay()
-            return g_out
+            def run(xx, dyy):
+                if xx is not sx:
+                    sx.copy_(xx, non_blocking=True)
+                    sdy.copy_(dyy, non_blocking=True)
+                graph.replay()
+                return g_out
 
-        x, dy = sx, sdy
-        for _ in range(2):
-            run(x, dy)
-        barrier()
+            x, dy = sx, sdy
+            for _ in range(2):
+                run(x, dy)
+            barrier()
+        except Exception as exc:  # noqa: BLE001  (a capture failure falls back to eager)
+            if n > 1:
+                raise
+            graph_error = f"{type(exc).__name__}: {exc}"[:200]
+            print(f"bench: CUDA-graph capture failed ({graph_error}); timing eager steps",
+                  file=sys.stderr)
+            args.graph = False
+            run = step
+            graph_launches = None
+            torch.cuda.synchronize()
+            for _ in range(args.warmup):
+                step(x, dy)
+            barrier()
 
     # ---- timed region: device-resident inputs ------------------------------------
     if rank == 0:
@@ -493,15 +529,23 @@ def run_gpu(args, c) -> None:
     clocks.window(False)
     launches = _lib.stats.launches if graph_launches is None else graph_launches * args.steps
     ms_total = t_start.elapsed_time(t_end)
-    if args.graph or not live_events:
-        # per-kernel timings (roofline) from eager instrumented steps outside the timed region
-        _lib.stats.prepare(64 * args.steps)
-        _lib.stats.timing = True
-        for _ in range(args.steps):
-            step(x, dy)
-        barrier()
+    ev_steps = args.steps  # timed steps the per-kernel events cover
+    kernel_events = "live, every timed step"
+    if args.graph and graph_events:
+        ev = graph_events
+        ev_steps = 1
+        kernel_events = "live, the last timed step (event-record nodes in the replayed graph)"
+    else:
+        if args.graph or not live_events:
+            # per-kernel timings (roofline) from eager instrumented steps after the timed region
+            _lib.stats.prepare(64 * args.steps)
+            _lib.stats.timing = True
+            for _ in range(args.steps):
+                step(x, dy)
+            barrier()
+            kernel_events = "eager instrumented steps after the timed region"
+        ev = _lib.stats.events
     _lib.stats.timing = False
-    ev = _lib.stats.events
     gemm_ms = sum(s.elapsed_time(e) for nm, s, e in ev if nm.startswith("moe_gg_"))
     per_kernel: dict[str, list] = {}
     for nm, s, e in ev:
@@ -515,6 +559,18 @@ def run_gpu(args, c) -> None:
     ms_step = ms_total / args.steps
     tokens = T * n
     value = tokens / (ms_step / 1e3)
+
+    if args.graph and graph_launches is not None:
+        # the e2e region runs the eager public API: release the graph and its private memory
+        # pool first (kept alive, it leaves the eager steps short of cached blocks; DeepSeek
+        # shape measured 25 ms eager steps instead of 19)
+        run = step
+        for p_ in params:  # (the captured backward's gradients live in the graph's pool)
+            p_.grad = None
+        del graph, g_out
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
 
     # ---- e2e: host buffers through the public API ----------------------------------
     # Each step's x and dY come from pinned host memory (H2D on a copy stream, double
@@ -550,9 +606,8 @@ def run_gpu(args, c) -> None:
             if i + 1 < steps:
                 h2d(1 - slot)
             main.wait_event(landed[slot])
-            if args.graph:  # the replay overwrites the graph's static y: previous D2H first
-                main.wait_stream(d2h_stream)
-            y, aux = run(*bufs[slot])
+            # the public API, eagerly (as a user calls it), whatever the timed region used
+            y, aux = step(*bufs[slot])
             released[slot].record(main)
             ev = torch.cuda.Event()
             ev.record(main)
@@ -641,7 +696,7 @@ def run_gpu(args, c) -> None:
         ex_names = ("moe_ep_dispatch_push", "moe_ep_combine_pull", "moe_ep_combine_bwd_push",
                     "moe_gather_rows", "moe_ep_dispatch_dedup", "moe_ep_expand_grad",
                     "moe_ep_dispatch_push_dest", "moe_ep_combine_bwd_push_dest")
-        ex_ms = sum(sum(v) for k_, v in per_kernel.items() if k_ in ex_names) / args.steps
+        ex_ms = sum(sum(v) for k_, v in per_kernel.items() if k_ in ex_names) / ev_steps
         # per step: 4 one-way transfers of this rank's remote rows (x, O, dO, dX); with
         # balanced routing each direction of the NVLink port carries ~4 x sent bytes
         out_bytes = 2 * last_exchange["bytes_sent_remote"] + 2 * last_exchange["bytes_recv_remote"]
@@ -689,11 +744,11 @@ def run_gpu(args, c) -> None:
         hbm_gbs = peaks.get("hbm_gbs", 6650.0)
         traffic = gemm_traffic(args.config, n)
         write_gbs = measure_write_gbs()
-        hbm = hbm_kernels(c, per_kernel, args.steps, hbm_gbs, write_gbs)
+        hbm = hbm_kernels(c, per_kernel, ev_steps, hbm_gbs, write_gbs)
         hbm["_peaks"] = {"copy_GBps": hbm_gbs, "write_only_GBps": round(write_gbs, 1),
                          "copy_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
                          "write_source": "measured in this run (torch zero_ over 2 GiB)"}
-        gemm_tflops = gemm_flops_step * args.steps / (gemm_ms / 1e3) / 1e12 if gemm_ms else None
+        gemm_tflops = gemm_flops_step * ev_steps / (gemm_ms / 1e3) / 1e12 if gemm_ms else None
         gemm_launches = sum(len(v) for k_, v in per_kernel.items() if k_.startswith("moe_gg_"))
         out = {
             "metric": METRIC,
@@ -720,6 +775,7 @@ def run_gpu(args, c) -> None:
                 "parallelism": f"ep{n}",
                 "ep_transport": args.ep_transport if n > 1 else None,
                 "cuda_graph": bool(args.graph),
+                "cuda_graph_error": graph_error,
                 "sync_free": bool(args.sync_free or args.graph) if n > 1 else None,
                 "l2": "inputs larger than L2 (x alone is "
                       f"{T * h * 2 / 1e6:.0f} MB; expert weights {E * 3 * h * m * 2 / 1e9:.2f} GB)",
@@ -751,7 +807,8 @@ def run_gpu(args, c) -> None:
                 "traffic_detail": traffic,
                 "algorithmic": f"18*K*h*m FLOP/token = {gemm_flops_per_token(c) / 1e9:.3f} "
                                "GFLOP/token (fwd 6, dgrad 6, wgrad 6)",
-                "gemm_share_of_step": round(gemm_ms / args.steps / ms_step, 4) if gemm_ms else None,
+                "gemm_share_of_step": round(gemm_ms / ev_steps / ms_step, 4) if gemm_ms else None,
+                "kernel_events": kernel_events,
             },
             "hbm_kernels": hbm,
             "e2e": {
@@ -762,11 +819,13 @@ def run_gpu(args, c) -> None:
                 "d2h_bytes_per_step": int(x.numel() * 2 + 4),
                 "copies": "x, dY pinned H2D (copy stream, prefetched one step ahead); y and "
                           "the aux loss D2H to pinned host (second copy stream)",
+                "api": "eager moe_forward + autograd backward (the public layer API) every "
+                       "step, also when the device-resident timed region replays a graph",
             },
             "gpu_launches": launches,
             "gpu_launches_per_step": launches / args.steps,
             "gemm_launches": gemm_launches,
-            "kernel_ms_per_step": {k_: round(sum(v) / args.steps, 4) for k_, v in
+            "kernel_ms_per_step": {k_: round(sum(v) / ev_steps, 4) for k_, v in
                                    sorted(per_kernel.items(), key=lambda kv: -sum(kv[1]))},
             "clocks": clk,
             "routing": routing_stats,
@@ -848,9 +907,11 @@ def main():
     ap.add_argument("--sync-free", action=argparse.BooleanOptionalAction, default=True,
                     help="EP: plan the exchange on the device (no host read of the counts; "
                          "worst-case static buffers). Default on: +2%% at EP=4 (measured)")
-    ap.add_argument("--graph", action="store_true",
-                    help="capture the whole fwd+bwd step in a CUDA graph (EP: implies "
-                         "--sync-free)")
+    ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=None,
+                    help="capture the whole fwd+bwd step in a CUDA graph and replay it in the "
+                         "timed region (EP: implies --sync-free). Default: on at N=1 (no host "
+                         "work per step: immune to host pauses that drain the GPU queue), "
+                         "off under EP (measured 1%% slower at EP=4)")
     ap.add_argument("--echo-slots", type=int, default=0,
                     help="ECHO hot-expert clone slots per rank (EP, dropless)")
     ap.add_argument("--skew", type=float, default=None,
@@ -858,6 +919,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.graph is None:
+        args.graph = int(os.environ.get("WORLD_SIZE", str(args.gpus))) == 1 and args.gpus == 1
     c = CONFIGS[args.config]
     # stdout carries exactly one JSON line: everything else (NCCL's version banner, library
     # chatter) is routed to stderr at the fd level; the JSON goes to the saved stdout fd.

@@ -183,10 +183,13 @@ class _Stats:
     events: list = []  # (name, start_event, end_event)
     pool: list = []    # pre-created event pairs (prepare()): no event creation while timing
 
-    def prepare(self, n: int) -> None:
+    def prepare(self, n: int, external: bool = False) -> None:
+        """n pre-created event pairs. external=True: events whose record() inside a CUDA-graph
+        capture becomes an event-record node of the graph (each replay re-records them)."""
         import torch
 
-        self.pool = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        self.pool = [(torch.cuda.Event(enable_timing=True, external=external),
+                      torch.cuda.Event(enable_timing=True, external=external))
                      for _ in range(n)]
 
 
