@@ -57,6 +57,12 @@ constexpr int RING_KB = MOE_ROUTER_RING_KB;  // operand ring per CTA (A/B: 96 vs
 #define MOE_ROUTER_SUBK 2
 #endif
 // (NPAD >= 128: the W^T box alone is 16-32 KB per sub-block; one sub-block per stage)
+// rows per x box of the route kernel (A/B: 128 = one box per 64-column sub-block)
+#ifndef MOE_ROUTER_BOX_ROWS
+#define MOE_ROUTER_BOX_ROWS 64
+#endif
+constexpr int ROUTE_BOX_ROWS = MOE_ROUTER_BOX_ROWS;
+
 template <int MODE, int NPAD>
 constexpr int subk_of() { return MODE == 0 && NPAD <= 64 ? MOE_ROUTER_SUBK : 1; }
 static int subk_route(int npad) { return npad <= 64 ? MOE_ROUTER_SUBK : 1; }
@@ -188,7 +194,10 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         if constexpr (MODE == MODE_ROUTE) {
 #pragma unroll
           for (int sb = 0; sb < SUBK; ++sb)  // x rows m0.., columns k + 64 sb ..
-            tma_load_2d(sa + sb * (BM * BK * 2), &tmap_a, &full_bar[s], k + sb * BK, m0);
+#pragma unroll
+            for (int hb = 0; hb < BM / ROUTE_BOX_ROWS; ++hb)  // (same smem image as one box)
+              tma_load_2d(sa + sb * (BM * BK * 2) + hb * (ROUTE_BOX_ROWS * BK * 2), &tmap_a,
+                          &full_bar[s], k + sb * BK, m0 + hb * ROUTE_BOX_ROWS);
         } else {
           // x^T tile, MN-major: two 64(h) x 64(token) boxes
           tma_load_2d(sa, &tmap_a, &full_bar[s], m0, k);
@@ -675,7 +684,7 @@ int moe_router_tc_fwd(const void* x, int T, int h, const void* w_t, int E, int K
     const int cs = route_cluster(T, h);
     CUtensorMap ta, tb;
     int s;
-    if ((s = make_tmap(&ta, x, h, T, h, BK, BM))) return s;
+    if ((s = make_tmap(&ta, x, h, T, h, BK, ROUTE_BOX_ROWS))) return s;
     if ((s = make_tmap(&tb, w_t, h, np, h, BK, np))) return s;
     Params p{};
     p.T = T;
