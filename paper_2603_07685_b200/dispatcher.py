@@ -32,7 +32,7 @@ import torch.distributed as dist
 
 from . import _lib, gemm, ops
 from . import echo as echo_mod
-from .layer import MoEConfig, shared_expert_backward, shared_expert_forward
+from .layer import OVERLAP_WGRAD, MoEConfig, shared_expert_backward, shared_expert_forward
 
 
 class EPGroup:
@@ -309,9 +309,9 @@ class _MoEEPFunction(torch.autograd.Function):
         else:
             d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, xc.block_expert, xc.num_m_blocks,
                                       pair=ctx.pair)
-        dw2 = gemm.wgrad(d_o, act, xc.off_pad, el)
+        dw2 = gemm.wgrad(d_o, act, xc.off_pad, el, overlap_prev=OVERLAP_WGRAD)
         dxp = gemm.fc1_dgrad(d_pre, w1, xc.block_expert, xc.num_m_blocks, pair=ctx.pair)
-        dw1 = gemm.wgrad(d_pre, xp, xc.off_pad, el)
+        dw1 = gemm.wgrad(d_pre, xp, xc.off_pad, el, overlap_prev=OVERLAP_WGRAD)
         dxp_local = xc.a2a(xc.from_padded(dxp), False, ep)
         aux_scale = None if daux is None else daux.float()
         dw_r, dx_router = ops.router_backward(x, w_r_pad, r, dprob, cfg.score,
@@ -901,7 +901,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
         if ctx.overlap:
             main.wait_stream(pool.comm)
         if not mx:
-            dw2 = gemm.wgrad(d_o, act, off_pad_d, el)
+            dw2 = gemm.wgrad(d_o, act, off_pad_d, el, overlap_prev=OVERLAP_WGRAD)
         if ctx.scatter:  # dX rows return from fc1_dgrad's epilogue into the source ranks
             if mx:
                 _lib.call("moe_ep_scatter_rows", dxp_mx.data_ptr(), ctx.rows_bound, h,
@@ -916,7 +916,7 @@ class _MoEEPP2PFunction(torch.autograd.Function):
             else:
                 gemm.fc1_dgrad(d_pre, w1, be_d, nmb, out=dxp, pair=ctx.pair)
         if not mx:
-            dw1 = gemm.wgrad(d_pre, xp, off_pad_d, el)
+            dw1 = gemm.wgrad(d_pre, xp, off_pad_d, el, overlap_prev=OVERLAP_WGRAD)
         # also orders every rank's reads of its symmetric buffers (xp, d_o) before any
         # peer's next write into them
         pool.barrier()
@@ -1142,9 +1142,9 @@ class _MoEEPDedupFunction(torch.autograd.Function):
                                       pair=ctx.pair, part=part)
         else:
             d_pre, _ = gemm.fc2_dgrad(d_o, w2, preact, be_d, nmb, pair=ctx.pair)
-        dw2 = gemm.wgrad(d_o, act, off_pad_d, el)
+        dw2 = gemm.wgrad(d_o, act, off_pad_d, el, overlap_prev=OVERLAP_WGRAD)
         dxp = gemm.fc1_dgrad(d_pre, w1, be_d, nmb, pair=ctx.pair)
-        dw1 = gemm.wgrad(d_pre, xp, off_pad_d, el)
+        dw1 = gemm.wgrad(d_pre, xp, off_pad_d, el, overlap_prev=OVERLAP_WGRAD)
         if tok_recv:
             _lib.call("moe_combine", dxp.data_ptr(), tok_recv, K, h, srows.data_ptr(), None,
                       None, None, None, partial.data_ptr(), stream)
