@@ -671,7 +671,9 @@ int moe_router_bwd2(const float* logits, int ld, int T, int E, int K, int score_
   if (E < 1 || E > 256 || K > 32 || (dlogits && ldd < E) || (dlt && (ldt < T || npad < E)))
     return kErrInvalidArg;
   if (T == 0) return kOk;
-  const int blocks = moe_router_num_partials(T);
+  // one token per warp: the per-token chain (logits load, max, exp, sum, Jacobian) is
+  // latency-bound, so every token gets its own warp (T / 8 blocks, no partial-row cap)
+  const int blocks = ceil_div_i(T, WARPS);
   auto st = static_cast<cudaStream_t>(stream);
   auto out = static_cast<__nv_bfloat16*>(dlogits);
   auto ot = static_cast<__nv_bfloat16*>(dlt);
