@@ -24,3 +24,36 @@ def test_reference_arm_json_line():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
     assert d["config"]["workload"]
+
+
+def test_gpu_bench_json_line():
+    """The GPU arm on the tiny config: one JSON line with the contract's keys, the whole-step
+    CUDA graph in the timed region (N=1 default), per-kernel events captured in the graph,
+    the eager e2e with its host<->device bytes, our kernels counted."""
+    import pytest
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--config", "tiny", "--steps",
+                        "3", "--warmup", "3", "--no-cpu-baseline", "--no-dropin"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "roofline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 3
+    assert d["config"]["cuda_graph"] is True and d["config"]["cuda_graph_error"] is None
+    for k in ("bound", "achieved", "peak", "unit", "frac"):
+        assert k in d["roofline"], k
+    assert d["roofline"]["kernel_events"].startswith("live")
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+    assert d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0 and any(k.startswith("moe_gg") for k in d["kernel_ms_per_step"])
+
+
+test_gpu_bench_json_line = __import__("pytest").mark.gpu(test_gpu_bench_json_line)
