@@ -274,6 +274,56 @@ def gemm_traffic(config: str, n: int):
                       "one step of tools/layer_step.py)"}
 
 
+def gemm_floor_model(c, n: int, per_kernel: dict, steps: int, peak_tf: float, hbm_gbs: float):
+    """Per-GEMM roofline floor of one step: each expert GEMM kind's time floor is
+    max(FLOPs / sustained tensor peak, compulsory bytes / copy bandwidth), with the compulsory
+    bytes of SURVEY §8(d) (operands read once, outputs written once, bf16; routed experts E/n
+    per rank with T*K rows, plus the shared expert as one T-row group). Decides the GEMM set's
+    bound: Mixtral/Qwen3 are tensor-bound, DeepSeek's 128-row-per-expert GEMMs stream
+    15 GB of fc1 weights per pass and are HBM-bound at EP=1."""
+    w = 2
+    groups = [(c["E"] // n, c["T"] * c["K"], c["m"])]
+    if c.get("shared"):
+        groups.append((1, c["T"], c["shared"]))
+    h = c["h"]
+    kinds = {}
+    for el, r, m in groups:
+        per = {  # (flops, bytes)
+            "fc1_fwd": (4.0 * r * h * m, r * h * w + el * 2 * m * h * w + r * 3 * m * w),
+            "fc2_fwd": (2.0 * r * h * m, r * m * w + el * h * m * w + r * h * w),
+            "fc2_dgrad": (2.0 * r * h * m, r * h * w + el * h * m * w + r * 4 * m * w),
+            "fc1_dgrad": (4.0 * r * h * m, r * 2 * m * w + el * 2 * m * h * w + r * h * w),
+            "wgrad": (6.0 * r * h * m, el * 3 * h * m * w + 2 * r * h * w + 3 * r * m * w),
+        }
+        for k, (f, b) in per.items():
+            a = kinds.setdefault(k, [0.0, 0.0, 0.0])
+            a[0] += f
+            a[1] += b
+            a[2] += max(f / (peak_tf * 1e12), b / (hbm_gbs * 1e9)) * 1e3
+    out, floor_ms, meas_ms, t_ms, m_ms = {}, 0.0, 0.0, 0.0, 0.0
+    for k, (f, b, fl) in kinds.items():
+        ms = sum(sum(v) for nm, v in per_kernel.items()
+                 if k in nm and nm.startswith("moe_gg_") and not nm.endswith("_f32")) / steps
+        tt, tm = f / (peak_tf * 1e12) * 1e3, b / (hbm_gbs * 1e9) * 1e3
+        out[k] = {"TFLOP": round(f / 1e12, 3), "GB": round(b / 1e9, 3),
+                  "tensor_ms": round(tt, 3), "hbm_ms": round(tm, 3),
+                  "bound": "tensor" if tt >= tm else "hbm", "floor_ms": round(fl, 3),
+                  "measured_ms": round(ms, 4) if ms else None,
+                  "frac_of_floor": round(fl / ms, 3) if ms else None}
+        floor_ms += fl
+        meas_ms += ms
+        t_ms += tt
+        m_ms += tm
+    return {"per_gemm": out, "floor_ms": round(floor_ms, 3),
+            "measured_ms": round(meas_ms, 4) if meas_ms else None,
+            "frac_of_floor": round(floor_ms / meas_ms, 3) if meas_ms else None,
+            "bound": "tensor" if t_ms >= m_ms else "hbm",
+            "tflop": sum(v[0] for v in kinds.values()) / 1e12,
+            "bytes": sum(v[1] for v in kinds.values()),
+            "assumes": f"tensor peak {peak_tf} TF/s sustained, copy {hbm_gbs} GB/s; "
+                       f"{c['E'] // n} routed experts x {c['T'] * c['K']} rows per rank"}
+
+
 def measure_write_gbs(nbytes: int = 1 << 31, iters: int = 10) -> float:
     """HBM write-only bandwidth of this GPU (torch zero_ over 2 GiB, CUDA events, best of
     `iters`): the bound of write-dominated kernels, which B200 serves well below the copy
@@ -550,10 +600,25 @@ def run_gpu(args, c) -> None:
             kernel_events = "eager instrumented steps after the timed region"
         ev = _lib.stats.events
     _lib.stats.timing = False
-    gemm_ms = sum(s.elapsed_time(e) for nm, s, e in ev if nm.startswith("moe_gg_"))
     per_kernel: dict[str, list] = {}
     for nm, s, e in ev:
         per_kernel.setdefault(nm, []).append(s.elapsed_time(e))
+    # GEMM busy time: programmatic dependent launches (the split-unit tail, the weight
+    # gradients) start while the GEMM before them drains, so their event spans overlap it.
+    # Each GEMM interval is clipped at the end of the ones before it (the union of the GEMM
+    # intervals, the overlap attributed to the earlier launch): per-kind exclusive times
+    gemm_excl: dict[str, list] = {}
+    gemm_ms = 0.0
+    if ev:
+        ref = ev[0][1]
+        iv = sorted((ref.elapsed_time(s), ref.elapsed_time(e), nm) for nm, s, e in ev
+                    if nm.startswith("moe_gg_"))
+        cur = float("-inf")
+        for t0_, t1_, nm in iv:
+            span = max(0.0, t1_ - max(t0_, cur))
+            gemm_excl.setdefault(nm, []).append(span)
+            gemm_ms += span
+            cur = max(cur, t1_)
     clk = clocks.stop() if rank == 0 else None
 
     t_tensor = torch.tensor([ms_total, gemm_ms], dtype=torch.float64, device=dev)
@@ -754,6 +819,11 @@ def run_gpu(args, c) -> None:
                          "write_source": "measured in this run (best of torch zero_ / fill_ / "
                                          "broadcast copy over 2 GiB)"}
         gemm_tflops = gemm_flops_step * ev_steps / (gemm_ms / 1e3) / 1e12 if gemm_ms else None
+        floor = gemm_floor_model(c, n, gemm_excl, ev_steps, peak_tf, hbm_gbs)
+        # an HBM-bound GEMM set (DeepSeek at EP=1) reports compulsory bytes over its time
+        hbm_ach = (floor.pop("bytes") / (floor["measured_ms"] / 1e3) / 1e9
+                   if floor["measured_ms"] else None)
+        floor.pop("tflop")
         gemm_launches = sum(len(v) for k_, v in per_kernel.items() if k_.startswith("moe_gg_"))
         out = {
             "metric": METRIC,
@@ -788,13 +858,19 @@ def run_gpu(args, c) -> None:
             "grouped_gemm_tflops": round(gemm_tflops, 1) if gemm_tflops else None,
             "layer_tflops": round(flops_per_token(c) * tokens / (ms_step / 1e3) / 1e12 / n, 1),
             "roofline": {
-                "bound": "tensor",
+                "bound": floor["bound"],
                 "kernel": "grouped GEMM (all tcgen05 launches: fc1/fc2 fwd, dgrad, wgrad)",
-                "achieved": round(gemm_tflops, 1) if gemm_tflops else None,
-                "peak": peak_tf,
-                "peak_source": peak_src,
-                "unit": "TFLOP/s",
-                "frac": round(gemm_tflops / peak_tf, 4) if gemm_tflops else None,
+                **({"achieved": round(gemm_tflops, 1) if gemm_tflops else None,
+                    "peak": peak_tf, "peak_source": peak_src, "unit": "TFLOP/s",
+                    "frac": round(gemm_tflops / peak_tf, 4) if gemm_tflops else None}
+                   if floor["bound"] == "tensor" or not hbm_ach else
+                   {"achieved": round(hbm_ach, 1), "peak": hbm_gbs,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if peaks else "fallback",
+                    "unit": "GB/s", "frac": round(hbm_ach / hbm_gbs, 4),
+                    "tensor": {"achieved": round(gemm_tflops, 1) if gemm_tflops else None,
+                               "peak": peak_tf, "unit": "TFLOP/s",
+                               "frac": round(gemm_tflops / peak_tf, 4) if gemm_tflops else None}}),
+                "floor_model": floor,
                 "frac_vs": ({"sustained_measured": round(gemm_tflops / peak_tf, 4),
                              "burst_measured": round(gemm_tflops / burst_tf, 4),
                              "datasheet_dense_2250": round(gemm_tflops / 2250.0, 4),
@@ -813,6 +889,9 @@ def run_gpu(args, c) -> None:
                 "algorithmic": f"18*K*h*m FLOP/token = {gemm_flops_per_token(c) / 1e9:.3f} "
                                "GFLOP/token (fwd 6, dgrad 6, wgrad 6)",
                 "gemm_share_of_step": round(gemm_ms / ev_steps / ms_step, 4) if gemm_ms else None,
+                "gemm_ms_per_step": round(gemm_ms / ev_steps, 4) if gemm_ms else None,
+                "gemm_time": "union of the GEMM launches' event spans (a programmatic dependent "
+                             "launch's overlap with the GEMM before it counted once)",
                 "kernel_events": kernel_events,
             },
             "hbm_kernels": hbm,
@@ -830,6 +909,8 @@ def run_gpu(args, c) -> None:
             "gpu_launches": launches,
             "gpu_launches_per_step": launches / args.steps,
             "gemm_launches": gemm_launches,
+            "gemm_exclusive_ms_per_step": {k_: round(sum(v) / ev_steps, 4) for k_, v in
+                                           gemm_excl.items()},
             "kernel_ms_per_step": {k_: round(sum(v) / ev_steps, 4) for k_, v in
                                    sorted(per_kernel.items(), key=lambda kv: -sum(kv[1]))},
             "clocks": clk,
