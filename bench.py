@@ -334,9 +334,23 @@ def measure_write_gbs(nbytes: int = 1 << 31, iters: int = 10) -> float:
     src = torch.ones((1,), dtype=torch.bfloat16, device="cuda").expand(nbytes // 2)
     buf.zero_()
     best = None
-    # the best of three write-only kernels (fill with 0, fill with 1, broadcast copy): torch's
-    # fill kernel alone measured 2.97-3.95 TB/s on different boxes
-    for fn in (lambda: buf.zero_(), lambda: buf.fill_(1.0), lambda: buf.copy_(src)):
+    # the best of six write-only kernels: torch's fill with 0 / fill with 1 / broadcast copy
+    # (fill alone measured 2.88-3.95 TB/s on different boxes) and the library's probes
+    # (16-byte stores, streaming stores, TMA bulk stores of a zeroed smem chunk)
+    from paper_2603_07685_b200 import _lib
+
+    lib = _lib.load()
+
+    def probe(mode):
+        st = lib.moe_hbm_write_probe(buf.data_ptr(), nbytes, mode,
+                                     torch.cuda.current_stream().cuda_stream)
+        _lib.check(st, "moe_hbm_write_probe")
+
+    methods = {"torch_zero": lambda: buf.zero_(), "torch_fill": lambda: buf.fill_(1.0),
+               "torch_broadcast_copy": lambda: buf.copy_(src), "probe_st16": lambda: probe(0),
+               "probe_st16_cs": lambda: probe(1), "probe_tma_bulk": lambda: probe(2)}
+    per = {}
+    for nm, fn in methods.items():
         for _ in range(iters):
             s, e = torch.cuda.Event(True), torch.cuda.Event(True)
             s.record()
@@ -345,7 +359,9 @@ def measure_write_gbs(nbytes: int = 1 << 31, iters: int = 10) -> float:
             e.synchronize()
             ms = s.elapsed_time(e)
             best = ms if best is None else min(best, ms)
+            per[nm] = min(per.get(nm, ms), ms)
     del buf
+    measure_write_gbs.per_method = {k: round(nbytes / (v / 1e3) / 1e9, 1) for k, v in per.items()}
     return nbytes / (best / 1e3) / 1e9
 
 
@@ -817,7 +833,9 @@ def run_gpu(args, c) -> None:
         hbm["_peaks"] = {"copy_GBps": hbm_gbs, "write_only_GBps": round(write_gbs, 1),
                          "copy_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
                          "write_source": "measured in this run (best of torch zero_ / fill_ / "
-                                         "broadcast copy over 2 GiB)"}
+                                         "broadcast copy and moe_hbm_write_probe's 16-byte, "
+                                         "streaming and TMA bulk stores, over 2 GiB)",
+                         "write_GBps_by_method": getattr(measure_write_gbs, "per_method", None)}
         gemm_tflops = gemm_flops_step * ev_steps / (gemm_ms / 1e3) / 1e12 if gemm_ms else None
         floor = gemm_floor_model(c, n, gemm_excl, ev_steps, peak_tf, hbm_gbs)
         # an HBM-bound GEMM set (DeepSeek at EP=1) reports compulsory bytes over its time

@@ -102,6 +102,10 @@ int moe_stage_router_weight(const void* w, int h, int E, int Epad, void* wt_pad,
                             void* stream);
 int moe_reduce_groups_f32(const float* in, int G, int rows, int cols_in, int cols_out,
                           float* out, void* stream);
+/* measurement only (no reference counterpart): HBM write-only bandwidth probe, zeros `bytes`
+ * (multiple of 16) at dst; mode 0 16-byte stores, 1 streaming (.cs) stores, 2 TMA bulk stores.
+ * bench.py's write bound for write-dominated kernels. */
+int moe_hbm_write_probe(void* dst, long long bytes, int mode, void* stream);
 
 /* ------------------------------------------------------------------ permutation
  * replaces permute() routing.py:149-168, _expert_slices() :180-186, effective_counts()

@@ -37,6 +37,7 @@ SIGNATURES: dict[str, list] = {
     "moe_router_bwd": [P, I, I, I, I, I, P, P, P, P, I, P],
     "moe_stage_router_weight": [P, I, I, I, P, P, P],
     "moe_reduce_groups_f32": [P, I, I, I, I, P, P],
+    "moe_hbm_write_probe": [P, L, I, P],
     "moe_router_fused": [P, I, I, P, I, I, I, P, P, P, P, P, P, P, P, P],
     # small-N tensor-core router (csrc/router_tc.cu)
     "moe_router_tc_fwd": [P, I, I, P, I, I, I, P, F, P, P, P, P, P, P, P, P, P, P, P],

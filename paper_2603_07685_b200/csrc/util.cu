@@ -36,6 +36,51 @@ __global__ void reduce_groups_kernel(const float* __restrict__ in, int G, int ro
   }
 }
 
+// HBM write-only probes (bench.py's write bound for write-dominated kernels). Zeros written
+// over `bytes` (a multiple of 16). mode 0: 16-byte stores, 4 in flight per thread; mode 1:
+// the same with .cs (streaming) stores; mode 2: TMA bulk stores of a zeroed 32 KB smem chunk
+// (one issuing thread per CTA, up to 8 groups in flight).
+constexpr int kProbeChunk = 32768;
+
+template <bool CS>
+__global__ void __launch_bounds__(512) write_probe_st_kernel(uint4* __restrict__ dst,
+                                                             long long n16) {
+  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if constexpr (CS) __stcs(dst + i + u * stride, z);
+      else dst[i + u * stride] = z;
+    }
+  }
+  for (; i < n16; i += stride) dst[i] = z;
+}
+
+__global__ void __launch_bounds__(32) write_probe_bulk_kernel(char* __restrict__ dst,
+                                                              long long bytes) {
+  extern __shared__ __align__(128) uint4 zbuf[];
+  for (int i = threadIdx.x; i < kProbeChunk / 16; i += blockDim.x)
+    zbuf[i] = make_uint4(0u, 0u, 0u, 0u);
+  fence_async_shared();
+  __syncwarp();
+  if (threadIdx.x != 0) return;
+  const long long chunks = bytes / kProbeChunk;
+  int inflight = 0;
+  for (long long c = blockIdx.x; c < chunks; c += gridDim.x) {
+    bulk_store_s2g(dst + c * kProbeChunk, zbuf, kProbeChunk);
+    bulk_commit();
+    if (++inflight >= 8) asm volatile("cp.async.bulk.wait_group.read 7;" ::: "memory");
+  }
+  const long long tail = bytes - chunks * kProbeChunk;  // multiple of 16
+  if (blockIdx.x == 0 && tail > 0) {
+    bulk_store_s2g(dst + chunks * kProbeChunk, zbuf, (uint32_t)tail);
+    bulk_commit();
+  }
+  bulk_wait_all();
+}
+
 }  // namespace util
 }  // namespace moe
 
@@ -57,6 +102,26 @@ int moe_reduce_groups_f32(const float* in, int G, int rows, int cols_in, int col
                           void* stream) {
   util::reduce_groups_kernel<<<1024, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       in, G, rows, cols_in, cols_out, out);
+  MOE_LAUNCH_CHECK();
+  return kOk;
+}
+
+// bench.py's HBM write-only bandwidth probe: zeros `bytes` (multiple of 16) at dst.
+int moe_hbm_write_probe(void* dst, long long bytes, int mode, void* stream) {
+  if (!dst || bytes <= 0 || (bytes & 15) || ((uintptr_t)dst & 15) || mode < 0 || mode > 2)
+    return kErrInvalidArg;
+  auto st = static_cast<cudaStream_t>(stream);
+  const int sms = device_sms();
+  if (mode == 2) {
+    util::write_probe_bulk_kernel<<<sms * 4, 32, util::kProbeChunk, st>>>(
+        static_cast<char*>(dst), bytes);
+  } else if (mode == 1) {
+    util::write_probe_st_kernel<true><<<sms * 4, 512, 0, st>>>(static_cast<uint4*>(dst),
+                                                                bytes / 16);
+  } else {
+    util::write_probe_st_kernel<false><<<sms * 4, 512, 0, st>>>(static_cast<uint4*>(dst),
+                                                                 bytes / 16);
+  }
   MOE_LAUNCH_CHECK();
   return kOk;
 }
