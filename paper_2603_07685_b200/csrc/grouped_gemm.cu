@@ -158,6 +158,8 @@ struct Params {
   int stream_stores;
   int band_m;  // raster band: M units that sweep each n-block together (L2 reuse)
   int bulk_out;  // grouped-K EPI_BF16: the SK variant (TMA tensor stores of staged boxes)
+  int debug_skip;  // SK diagnostics (MOE_B200_DEBUG_SKIP): 1 no epilogue work, 2 no output
+                   // stores, 4 no MMAs (commits only); results are wrong when set
   int gk_mu_fast;  // grouped-K raster: M units fastest (when M < N), else n-blocks fastest
   // wave sync of the TMA producers (common.cuh wave_sync): off when sync_on == 0; sync points
   // at every tile start and, grouped-M only, every sync_kb k-blocks inside a tile (0 = none)
@@ -534,6 +536,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
             const uint64_t bdesc =
                 B_MN ? make_sdesc_sw128(b_base + kk * (UMMA_K * 128), 64 * BK * 2, 1024)
                      : make_sdesc_sw128(b_base + kk * (UMMA_K * 2), 16, 1024);
+            if (SK && (p.debug_skip & 4)) continue;
             if constexpr (CG == 1)
               umma_bf16(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
             else
@@ -645,7 +648,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
         // boxes alternate so a store drains while the next piece is staged. Both 32-column
         // TMEM loads of a piece are in flight before the single wait.
 #pragma unroll 1
-        for (int pc = 0; pc < EC / 64; ++pc) {
+        for (int pc = 0; pc < (p.debug_skip & 1 ? 0 : EC / 64); ++pc) {
           const int col = cb + pc * 64;
           uint32_t r[2][32];
           tmem_ld_32x32b_x32(t_base + col, r[0]);
@@ -666,7 +669,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<GROUPED_K, EPI>(), 1)
           }
           fence_async_shared();
           __syncwarp();
-          if (lane == 0) {
+          if (lane == 0 && !(p.debug_skip & 2)) {
             if (MOE_EPI_EVICT_FIRST)
               tma_store_2d_hint(&tmap_c, box, tl.n0 + col, tl.expert * p.M + tl.m0 + q * 32,
                                 epi_pol);
@@ -1440,7 +1443,20 @@ int moe_gg_wgrad_ex(const void* a, const void* b, int max_rows, int M, int N, in
   p.out = dw;
   p.ldo = N;
   p.out_expert_stride = (long long)M * N;
-  const int pair = (M % (2 * BM)) == 0;
+  static int force_single = -1;  // MOE_B200_WGRAD_PAIR=0: the 1-CTA engine (A/B)
+  if (force_single < 0) {
+    const char* e = getenv("MOE_B200_WGRAD_PAIR");
+    force_single = (e && e[0] == '0') ? 1 : 0;
+  }
+  const int pair = !force_single && (M % (2 * BM)) == 0;
+  {
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* e = getenv("MOE_B200_DEBUG_SKIP");
+      dbg = e ? atoi(e) : 0;
+    }
+    p.debug_skip = dbg;
+  }
   return run<true, true, true, EPI_BF16>(a, M, max_rows, b, N, max_rows, p,
                                          num_experts * (M / BM), pair,
                                          static_cast<cudaStream_t>(stream), 0, flags & 1);

@@ -24,6 +24,12 @@ R = T * K
 align = ops.pick_align(T, K, E)
 pair = align == 256
 counts = [R // E] * E
+if os.environ.get("GEMM_KINDS_COUNTS") == "random":
+    # per-expert counts of seeded uniform top-K routing (K distinct experts per token), as
+    # the bench step sees them (DeepSeek: 128 +- 11 rows; 128-row padding doubles about half)
+    gen = torch.Generator().manual_seed(0)
+    sel = torch.rand((T, E), generator=gen).topk(K, dim=1).indices
+    counts = torch.bincount(sel.flatten(), minlength=E).tolist()
 offs, be = [0], []
 for e, c in enumerate(counts):
     nb = (c + align - 1) // align * (align // 128)
