@@ -78,3 +78,24 @@ def test_ctypes_signatures_match_header_arity():
         assert len(argtypes) == arity[name], (name, len(argtypes), arity[name])
     for name, (argtypes, _) in _lib.QUERIES.items():
         assert len(argtypes) == arity[name], (name, len(argtypes), arity[name])
+
+
+@pytest.mark.gpu
+def test_hbm_write_probe_zeros_exactly_the_range():
+    """moe_hbm_write_probe (bench.py's write bound): every mode zeros [dst, dst + bytes) and
+    nothing past it, including a non-multiple of the 32 KB bulk chunk; bad arguments fail."""
+    import torch
+
+    lib = _lib.load()
+    st = torch.cuda.current_stream().cuda_stream
+    for mode in (0, 1, 2):
+        for nbytes in (16, 4096, 3 * 32768 + 48, (1 << 22) + 16 * 7):
+            buf = torch.full((nbytes // 2 + 64,), 7, dtype=torch.int16, device="cuda")
+            assert lib.moe_hbm_write_probe(buf.data_ptr(), nbytes, mode, st) == 0
+            torch.cuda.synchronize()
+            assert int(buf[: nbytes // 2].abs().sum()) == 0, (mode, nbytes)
+            assert bool((buf[nbytes // 2:] == 7).all()), (mode, nbytes)
+    buf = torch.zeros((64,), dtype=torch.int16, device="cuda")
+    assert lib.moe_hbm_write_probe(buf.data_ptr(), 24, 0, st) != 0      # not a multiple of 16
+    assert lib.moe_hbm_write_probe(buf.data_ptr(), 32, 3, st) != 0      # unknown mode
+    assert lib.moe_hbm_write_probe(buf.data_ptr() + 8, 32, 0, st) != 0  # misaligned
