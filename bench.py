@@ -993,7 +993,9 @@ def run_reference(args, c) -> None:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    # 60 steps (~1.7 s at Mixtral): the 1 kW power limiter needs ~1 s to settle, and 20-step
+    # windows read ~3.5% fast (profiles/r02_power_window.txt)
+    ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
