@@ -995,7 +995,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     # 60 steps (~1.7 s at Mixtral): the 1 kW power limiter needs ~1 s to settle, and 20-step
     # windows read ~3.5% fast (profiles/r02_power_window.txt)
-    ap.add_argument("--steps", type=int, default=60)
+    # (the reference arm's CPU steps take ~3 s each: it defaults to 10)
+    ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -1023,6 +1024,8 @@ def main():
     ap.add_argument("--skew", type=float, default=None,
                     help="router logit skew alpha (config 5 sweep: 0, 0.5, 1, 2)")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 10 if args.impl == "reference" else 60
     if args.warmup < 3:
         args.warmup = 3
     if args.graph is None:
