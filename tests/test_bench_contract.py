@@ -57,3 +57,34 @@ def test_gpu_bench_json_line():
 
 
 test_gpu_bench_json_line = __import__("pytest").mark.gpu(test_gpu_bench_json_line)
+
+
+def test_gemm_floor_model_bounds():
+    """The per-GEMM roofline floor (bench.gemm_floor_model): Mixtral is tensor-bound in every
+    kind, DeepSeek at EP=1 HBM-bound in every kind (fc1 streams E*2*m*h bf16 weights for
+    ~128 rows per expert) and tensor-bound at EP=2 (twice the rows per expert); the floor
+    is the sum of per-kind max(compute, bytes) and frac_of_floor = floor / measured."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    peak_tf, hbm = 1379.5, 6547.8
+    kinds = ("fc1_fwd", "fc2_fwd", "fc2_dgrad", "fc1_dgrad", "wgrad")
+    mx = bench.gemm_floor_model(bench.CONFIGS["mixtral"], 1, {}, 1, peak_tf, hbm)
+    assert mx["bound"] == "tensor" and all(mx["per_gemm"][k]["bound"] == "tensor" for k in kinds)
+    # 18*K*h*m*T FLOP at the sustained peak
+    c = bench.CONFIGS["mixtral"]
+    t_ms = 18.0 * c["K"] * c["h"] * c["m"] * c["T"] / (peak_tf * 1e12) * 1e3
+    assert abs(mx["floor_ms"] - t_ms) < 1e-2 and mx["measured_ms"] is None
+    ds = bench.gemm_floor_model(bench.CONFIGS["deepseek"], 1, {}, 1, peak_tf, hbm)
+    assert ds["bound"] == "hbm" and all(ds["per_gemm"][k]["bound"] == "hbm" for k in kinds)
+    w1 = 256 * 2 * 2048 * 7168 * 2  # the routed fc1 weights, bytes
+    assert ds["per_gemm"]["fc1_fwd"]["GB"] * 1e9 > w1
+    assert bench.gemm_floor_model(bench.CONFIGS["deepseek"], 2, {}, 1, peak_tf, hbm)["bound"] \
+        == "tensor"
+    # measured per-kind exclusive times (ms lists per launch name) -> frac_of_floor
+    per = {"moe_gg_fc1_fwd": [2 * mx["per_gemm"]["fc1_fwd"]["floor_ms"]],
+           "moe_gg_wgrad_ex": [mx["per_gemm"]["wgrad"]["floor_ms"]],
+           "moe_gg_wgrad_f32": [100.0]}  # the router's fp32 split-K GEMM is not an expert kind
+    f = bench.gemm_floor_model(c, 1, per, 1, peak_tf, hbm)
+    assert f["per_gemm"]["fc1_fwd"]["frac_of_floor"] == 0.5
+    assert f["per_gemm"]["wgrad"]["frac_of_floor"] == 1.0
