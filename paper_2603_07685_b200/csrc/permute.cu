@@ -281,6 +281,59 @@ __global__ void gather_tokens_kernel(const int4* __restrict__ x, int T, int K, i
   }
 }
 
+// Token-driven gather with the destination rows held in registers (K <= KMAX) and the next
+// chunk of x loaded while the current one is stored K times (one load always in flight).
+template <int VPL, int KMAX>
+__global__ void gather_tokens_pf_kernel(const int4* __restrict__ x, int T, int K, int hv,
+                                        const int* __restrict__ inv_map,
+                                        int4* __restrict__ out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = lane_id();
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  constexpr int CH = 32 * VPL;
+  for (int t = warp; t < T; t += nwarps) {
+    int d[KMAX];
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      d[k] = k < K ? __ldg(inv_map + (long long)t * K + k) : -1;
+      any |= d[k] >= 0;
+    }
+    if (!any) continue;
+    const int4* src = x + (long long)t * hv;
+    int4 cur[VPL], nxt[VPL];
+#pragma unroll
+    for (int u = 0; u < VPL; ++u) {
+      const int c = u * 32 + lane;
+      if (c < hv) cur[u] = ld_nc_v4(src + c);
+    }
+    for (int c0 = 0; c0 < hv; c0 += CH) {
+      const bool more = c0 + CH < hv;
+      if (more) {
+#pragma unroll
+        for (int u = 0; u < VPL; ++u) {
+          const int c = c0 + CH + u * 32 + lane;
+          if (c < hv) nxt[u] = ld_nc_v4(src + c);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        if (d[k] < 0) continue;
+        int4* o = out + (long long)d[k] * hv;
+#pragma unroll
+        for (int u = 0; u < VPL; ++u) {
+          const int c = c0 + u * 32 + lane;
+          if (c < hv) st_na_v4(o + c, cur[u]);
+        }
+      }
+      if (more) {
+#pragma unroll
+        for (int u = 0; u < VPL; ++u) cur[u] = nxt[u];
+      }
+    }
+  }
+}
+
 // Token-driven gather over (token, chunk) work items: a chunk is 32 lanes x VPL 16-byte
 // vectors of one x row, read once and stored to each kept destination row. Splitting rows
 // into chunks keeps every SM busy when T is small (DeepSeek shape: 4096 tokens of 14 KB).
@@ -927,7 +980,8 @@ int moe_permute_gather(const void* x, int T, int K, int h, const int* inv_map, c
   static int mode = -1;
   if (mode < 0) {
     const char* e = getenv("MOE_B200_GATHER");
-    mode = !e ? 2 : (e[0] == 't' && e[1] == 'm') ? 1 : (e[0] == 'c') ? 0 : 2;
+    mode = !e ? 2 : (e[0] == 't' && e[1] == 'm') ? 1 : (e[0] == 'c') ? 0
+                 : (e[0] == 'p' && e[1] == 'f') ? 3 : 2;
   }
   const int use_tma = mode == 1;
   const int row_bytes = h * 2;
@@ -941,7 +995,11 @@ int moe_permute_gather(const void* x, int T, int K, int h, const int* inv_map, c
     gather_tokens_tma_kernel<<<grid, GT_WARPS * 32, smem, st>>>(
         static_cast<const uint8_t*>(x), T, K, row_bytes, inv_map, static_cast<uint8_t*>(xp));
     MOE_LAUNCH_CHECK();
-  } else if (T > 0 && mode == 2) {
+  } else if (T > 0 && mode == 3 && K <= 8) {
+    gather_tokens_pf_kernel<4, 8><<<warp_grid(T), 256, 0, st>>>(
+        static_cast<const int4*>(x), T, K, hv, inv_map, static_cast<int4*>(xp));
+    MOE_LAUNCH_CHECK();
+  } else if (T > 0 && (mode == 2 || mode == 3)) {
     gather_tokens_kernel<4><<<warp_grid(T), 256, 0, st>>>(static_cast<const int4*>(x), T, K, hv,
                                                           inv_map, static_cast<int4*>(xp));
     MOE_LAUNCH_CHECK();
