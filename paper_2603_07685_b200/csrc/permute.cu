@@ -977,6 +977,8 @@ int moe_permute_gather(const void* x, int T, int K, int h, const int* inv_map, c
   // 0.84 of HBM). MOE_B200_GATHER=chunks: (token, chunk) work items (Qwen3 0.79);
   // =tma: bulk-copy variant (Mixtral 0.75, Qwen3 0.79). DeepSeek's 0.55 is the zero fill of
   // the padding rows (experts of ~128 rows padded to 128-row blocks), not counted here.
+  // =pf: destination rows in registers, next chunk prefetched (standalone +1-7%, in-step
+  // neutral; profiles/r02_gather_pf_ab.txt).
   static int mode = -1;
   if (mode < 0) {
     const char* e = getenv("MOE_B200_GATHER");
